@@ -1,0 +1,474 @@
+"""fp64 CPU oracle of the memory step -- TEST INFRASTRUCTURE ONLY.
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s ``cpu_baseline`` /
+``--impl reference`` legs may import this module.  It shares no code with the CUDA
+path (``paper_2403_16161_b200``) and never receives a value produced by it.
+
+It is a plain, slow, obviously-correct restatement of what the paper's "Memory" model
+(§3.4, Eq. 3) computes, with the readings listed in DESIGN.md
+("Readings of the paper").  Citations: ``P:n`` = /root/reference/PAPER.md line n.
+
+Structure (deliberately different from the GPU path):
+  * the memory caches each frame's *block input representation* per transformer
+    block, exactly as the paper describes ("save in memory the successive outputs of
+    these transformers for each predicted frame"; "each frame is saved in the
+    memory as much times as there are transformers", P:99 / Fig. 2 caption) and
+    re-projects K/V from it every step; the GPU caches projected K/V instead;
+  * attention is computed per head with explicit score and probability matrices over
+    keys in temporal (frame-id) order; the GPU walks the ring-buffer slot order;
+  * everything is float64; inputs are whatever the caller passes (the bf16 path's
+    tests pass bf16-representable values, see vi_synth.round_bf16).
+
+Pinned by tests/test_oracle_*.py (torch library routines, closed forms, SPEC worked
+examples, the memory-equivalence invariants I1/I2 and brute force).  Every function
+here has at least one pin; none is "parity unpinned".
+"""
+from __future__ import annotations
+
+import math
+from typing import Dict, List, Optional, Sequence, Tuple
+
+import numpy as np
+from scipy.special import erf
+
+# status codes of the C-ABI (include/vi.h), restated here for the bookkeeping model
+VI_OK = 0
+VI_NOT_RESIDENT = 1
+VI_E_ARG = -1
+VI_E_PROTOCOL = -4
+
+LN_EPS = 1e-5  # SURVEY Q1 / SPEC S:61
+
+
+# ----------------------------------------------------------------------------------
+# Patch geometry: soft split / soft composite (FuseFormer overlapping patches)
+# P:53 "the idea of having the patches overlapping"; "cut into patches";
+# P:166 FuseFormer patches "blended together".  Reading Q6: nn.Unfold semantics
+# (symmetric zero padding), patch vector ordered (ky, kx, c), tokens row-major (oy, ox).
+# ----------------------------------------------------------------------------------
+
+def out_size(n: int, k: int, s: int, p: int) -> int:
+    """Number of window positions along one side: (n + 2p - k) // s + 1."""
+    return (n + 2 * p - k) // s + 1
+
+
+def soft_split(F: np.ndarray, kh: int, kw: int, sh: int, sw: int, ph: int, pw: int) -> np.ndarray:
+    """Overlapping unfold of channels-last maps F[T,H,W,C] -> tokens [T, oh*ow, kh*kw*C].
+
+    Tp[t, oy*ow+ox, (ky*kw+kx)*C + c] = F[t, oy*sh-ph+ky, ox*sw-pw+kx, c], 0 outside.
+    """
+    F = np.asarray(F, dtype=np.float64)
+    T, H, W, C = F.shape
+    oh, ow = out_size(H, kh, sh, ph), out_size(W, kw, sw, pw)
+    out = np.zeros((T, oh * ow, kh * kw * C), dtype=np.float64)
+    for oy in range(oh):
+        for ox in range(ow):
+            tok = oy * ow + ox
+            for ky in range(kh):
+                y = oy * sh - ph + ky
+                if y < 0 or y >= H:
+                    continue
+                for kx in range(kw):
+                    x = ox * sw - pw + kx
+                    if x < 0 or x >= W:
+                        continue
+                    j = (ky * kw + kx) * C
+                    out[:, tok, j:j + C] = F[:, y, x, :]
+    return out
+
+
+def coverage(H: int, W: int, kh: int, kw: int, sh: int, sw: int, ph: int, pw: int) -> np.ndarray:
+    """How many (token, ky, kx) windows cover each cell: the composite's divisor."""
+    oh, ow = out_size(H, kh, sh, ph), out_size(W, kw, sw, pw)
+    cnt = np.zeros((H, W), dtype=np.int64)
+    for oy in range(oh):
+        for ox in range(ow):
+            for ky in range(kh):
+                y = oy * sh - ph + ky
+                if y < 0 or y >= H:
+                    continue
+                for kx in range(kw):
+                    x = ox * sw - pw + kx
+                    if 0 <= x < W:
+                        cnt[y, x] += 1
+    return cnt
+
+
+def soft_composite(Yp: np.ndarray, H: int, W: int, C: int, kh: int, kw: int, sh: int, sw: int,
+                   ph: int, pw: int) -> np.ndarray:
+    """Overlap-add of patch vectors back onto the map, divided by the cover count.
+
+    out[t,y,x,c] = (sum over (tok,ky,kx) landing on (y,x) of Yp[t,tok,(ky*kw+kx)*C+c]) / cnt[y,x].
+    Padding positions are discarded.  A cell no window covers is a configuration error.
+    """
+    Yp = np.asarray(Yp, dtype=np.float64)
+    T = Yp.shape[0]
+    oh, ow = out_size(H, kh, sh, ph), out_size(W, kw, sw, pw)
+    assert Yp.shape[1] == oh * ow and Yp.shape[2] == kh * kw * C, Yp.shape
+    acc = np.zeros((T, H, W, C), dtype=np.float64)
+    cnt = np.zeros((H, W), dtype=np.int64)
+    for oy in range(oh):
+        for ox in range(ow):
+            tok = oy * ow + ox
+            for ky in range(kh):
+                y = oy * sh - ph + ky
+                if y < 0 or y >= H:
+                    continue
+                for kx in range(kw):
+                    x = ox * sw - pw + kx
+                    if x < 0 or x >= W:
+                        continue
+                    j = (ky * kw + kx) * C
+                    acc[:, y, x, :] += Yp[:, tok, j:j + C]
+                    cnt[y, x] += 1
+    if (cnt == 0).any():
+        raise ValueError("soft_composite: a cell is covered by no window (config error)")
+    return acc / cnt[None, :, :, None]
+
+
+# ----------------------------------------------------------------------------------
+# Transformer block pieces ("same general pipeline as the original vision
+# transformer"; readings Q1-Q5: pre-norm, biases, 1/sqrt(d) scale, exact-erf GELU,
+# FuseFormer Fusion-FFN = FFN1 -> fold/count -> unfold -> GELU -> FFN2).
+# ----------------------------------------------------------------------------------
+
+def layer_norm(x: np.ndarray, g: np.ndarray, b: np.ndarray, eps: float = LN_EPS) -> np.ndarray:
+    x = np.asarray(x, dtype=np.float64)
+    mu = x.mean(axis=-1, keepdims=True)
+    var = ((x - mu) ** 2).mean(axis=-1, keepdims=True)
+    return (x - mu) / np.sqrt(var + eps) * np.asarray(g, np.float64) + np.asarray(b, np.float64)
+
+
+def gelu(x: np.ndarray) -> np.ndarray:
+    x = np.asarray(x, dtype=np.float64)
+    return 0.5 * x * (1.0 + erf(x / math.sqrt(2.0)))
+
+
+def linear(x: np.ndarray, w: np.ndarray, b: Optional[np.ndarray]) -> np.ndarray:
+    """nn.Linear convention: y = x W^T + b, W stored [out, in]."""
+    y = np.asarray(x, np.float64) @ np.asarray(w, np.float64).T
+    if b is not None:
+        y = y + np.asarray(b, np.float64)
+    return y
+
+
+def softmax_rows(S: np.ndarray) -> np.ndarray:
+    """Row softmax with max subtraction."""
+    S = np.asarray(S, dtype=np.float64)
+    E = np.exp(S - S.max(axis=-1, keepdims=True))
+    return E / E.sum(axis=-1, keepdims=True)
+
+
+def attention(Q: np.ndarray, K: np.ndarray, V: np.ndarray, heads: int,
+              allowed: Optional[np.ndarray] = None, row_chunk: int = 1024,
+              return_lse: bool = False):
+    """Multi-head softmax(Q_h K_h^T / sqrt(d)) V_h, one explicit head at a time.
+
+    Q [nq, D], K/V [nk, D]; ``allowed`` optional boolean [nq, nk] (True = key visible).
+    Returns O [nq, D] (and lse [heads, nq] = log sum exp of the scaled scores).
+    P:121 "the query vector ... only contain patches from this last frame", "the key and
+    value vectors must still represent all the frames selected".
+    """
+    Q = np.asarray(Q, np.float64); K = np.asarray(K, np.float64); V = np.asarray(V, np.float64)
+    nq, D = Q.shape
+    d = D // heads
+    O = np.zeros((nq, D), dtype=np.float64)
+    lse = np.zeros((heads, nq), dtype=np.float64)
+    scale = 1.0 / math.sqrt(d)
+    for h in range(heads):
+        cols = slice(h * d, (h + 1) * d)
+        kh, vh = K[:, cols], V[:, cols]
+        for r0 in range(0, nq, row_chunk):
+            r1 = min(nq, r0 + row_chunk)
+            S = (Q[r0:r1, cols] @ kh.T) * scale
+            if allowed is not None:
+                S = np.where(allowed[r0:r1], S, -np.inf)
+            m = S.max(axis=-1, keepdims=True)
+            E = np.exp(S - m)
+            l = E.sum(axis=-1, keepdims=True)
+            O[r0:r1, cols] = (E / l) @ vh
+            lse[h, r0:r1] = (m + np.log(l))[:, 0]
+    return (O, lse) if return_lse else O
+
+
+def f3n_mix(u: np.ndarray, cfg) -> np.ndarray:
+    """FuseFormer Fusion-FFN hidden mixing (reading Q5): per frame, view the hidden
+    vector of each token as (ky, kx, c) with c = F / (kh*kw), fold onto the feature map
+    with overlap-count normalisation, then unfold again with the same geometry."""
+    T = u.shape[0]
+    F = u.shape[-1]
+    cf = F // (cfg.kh * cfg.kw)
+    assert cf * cfg.kh * cfg.kw == F
+    g = (cfg.kh, cfg.kw, cfg.sh, cfg.sw, cfg.ph, cfg.pw)
+    folded = soft_composite(u.reshape(T, -1, F), cfg.feat_h, cfg.feat_w, cf, *g)
+    return soft_split(folded, *g)
+
+
+def ffn(h2: np.ndarray, w: Dict[str, np.ndarray], l: int, cfg, n_frames: int) -> Tuple[np.ndarray, np.ndarray]:
+    """FFN of block l on LN2 output h2 [n*P, D]; returns (u, g) and the caller adds W2."""
+    u = linear(h2, w["w1"][l], w["b1"][l])
+    if cfg.ffn_kind == 1:
+        g = gelu(f3n_mix(u.reshape(n_frames, cfg.tokens, -1), cfg).reshape(u.shape))
+    else:
+        g = gelu(u)
+    return u, g
+
+
+def embed(feats: np.ndarray, w: Dict[str, np.ndarray], cfg) -> Tuple[np.ndarray, np.ndarray]:
+    """Soft split + patch embedding: X0 = SoftSplit(F) We^T + be (+ pos)."""
+    Tp = soft_split(feats, cfg.kh, cfg.kw, cfg.sh, cfg.sw, cfg.ph, cfg.pw)
+    n = Tp.shape[0]
+    X = linear(Tp.reshape(n * cfg.tokens, -1), w["embed_w"], w["embed_b"])
+    if w.get("pos") is not None:
+        X = X + np.tile(np.asarray(w["pos"], np.float64), (n, 1))
+    return Tp, X
+
+
+def compose(X: np.ndarray, w: Dict[str, np.ndarray], cfg, n_frames: int) -> Tuple[np.ndarray, np.ndarray]:
+    """Back-projection + soft composite to the feature map [n, H, W, C]."""
+    Yp = linear(X, w["back_w"], w["back_b"]).reshape(n_frames, cfg.tokens, -1)
+    out = soft_composite(Yp, cfg.feat_h, cfg.feat_w, cfg.feat_c,
+                         cfg.kh, cfg.kw, cfg.sh, cfg.sw, cfg.ph, cfg.pw)
+    return Yp, out
+
+
+def qkv(x: np.ndarray, w, l: int, cfg):
+    h = layer_norm(x, w["ln1_g"][l], w["ln1_b"][l])
+    D = cfg.d_model
+    y = linear(h, w["wqkv"][l], w["bqkv"][l])
+    return h, y[:, :D], y[:, D:2 * D], y[:, 2 * D:]
+
+
+# ----------------------------------------------------------------------------------
+# One transformer block of the Memory model (Eq. 3): queries = the new frames only,
+# keys/values = memory frames (span s) + the new frames.
+# ----------------------------------------------------------------------------------
+
+def block_memory(x: np.ndarray, mem_kv: Sequence[Tuple[np.ndarray, np.ndarray]], w, l: int, cfg,
+                 n_frames: int, chunk_causal: bool = False) -> Tuple[np.ndarray, Dict[str, np.ndarray]]:
+    """x [n*P, D] = block-l input of the chunk; mem_kv = [(K_j, V_j)] in frame-id order."""
+    P = cfg.tokens
+    h1, Q, Kc, Vc = qkv(x, w, l, cfg)
+    K = np.concatenate([k for k, _ in mem_kv] + [Kc], axis=0)
+    V = np.concatenate([v for _, v in mem_kv] + [Vc], axis=0)
+    allowed = None
+    if chunk_causal and n_frames > 1:
+        nm = len(mem_kv) * P
+        qf = np.repeat(np.arange(n_frames), P)
+        kf = np.concatenate([np.full(nm, -1), np.repeat(np.arange(n_frames), P)])
+        allowed = kf[None, :] <= qf[:, None]
+    O, lse = attention(Q, K, V, cfg.heads, allowed=allowed, return_lse=True)
+    xa = x + linear(O, w["wo"][l], w["bo"][l])
+    h2 = layer_norm(xa, w["ln2_g"][l], w["ln2_b"][l])
+    u, g = ffn(h2, w, l, cfg, n_frames)
+    xo = xa + linear(g, w["w2"][l], w["b2"][l])
+    st = dict(h1=h1, q=Q, k=Kc, v=Vc, o=O, lse=lse, x_attn=xa, h2=h2, u=u, g=g, x=xo)
+    return xo, st
+
+
+def joint_forward(feats: np.ndarray, w, cfg, mode: str = "causal") -> Dict[str, object]:
+    """Eq. 1/2-style joint pass over a window of frames, all predicted together.
+
+    mode "causal": frame i's queries see frames j <= i (frame-level block-causal mask);
+    mode "full": bidirectional (the offline/refiner window of Eq. 1).
+    Returns per-layer K/V [L][n, P, D] and the composite output [n, H, W, C].
+    """
+    n = feats.shape[0]
+    P, D = cfg.tokens, cfg.d_model
+    Tp, X = embed(feats, w, cfg)
+    fr = np.repeat(np.arange(n), P)
+    allowed = (fr[None, :] <= fr[:, None]) if mode == "causal" else None
+    ks, vs, xs = [], [], [X]
+    for l in range(cfg.layers):
+        h1, Q, K, V = qkv(X, w, l, cfg)
+        ks.append(K.reshape(n, P, D)); vs.append(V.reshape(n, P, D))
+        O = attention(Q, K, V, cfg.heads, allowed=allowed)
+        X = X + linear(O, w["wo"][l], w["bo"][l])
+        h2 = layer_norm(X, w["ln2_g"][l], w["ln2_b"][l])
+        _, g = ffn(h2, w, l, cfg, n)
+        X = X + linear(g, w["w2"][l], w["b2"][l])
+        xs.append(X)
+    Yp, out = compose(X, w, cfg, n)
+    return dict(k=ks, v=vs, x=xs, yp=Yp, out=out)
+
+
+# ----------------------------------------------------------------------------------
+# The memory itself (set model).  Reading Q11: the memory of Eq. 3 keeps frames
+# f-s .. f-1 (span s = M); older frames are removed ("removing information
+# from ancient frames").  Reading Q13: refined entries (Eq. 4)
+# overwrite online ones and are applied at the next frame boundary.
+# ----------------------------------------------------------------------------------
+
+class OracleMemory:
+    """Resident-set bookkeeping + per-(layer, frame) cache, no slots, no arrays of slots."""
+
+    def __init__(self, mem_frames: int, max_new: int):
+        self.M = mem_frames
+        self.T_max = max_new
+        self.next_id = 0
+        self.cur_first = 0     # first id of the chunk pushed last
+        self.cur_n = 0
+        self.resident: set = set()
+        self.refined: set = set()
+        self.pending: Dict[int, object] = {}
+        self.stepped = False   # has the chunk pushed last gone through all blocks?
+
+    def mark_stepped(self):
+        self.stepped = True
+
+    @property
+    def slots(self) -> int:
+        return self.M + self.T_max
+
+    def push(self, n: int, on_evict=None, on_commit=None) -> Tuple[int, List[int]]:
+        if n < 1 or n > self.T_max:
+            raise ValueError("push: n out of range")
+        f = self.next_id
+        evicted = sorted(j for j in self.resident if j < f - self.M)
+        for j in evicted:
+            self.resident.discard(j)
+            self.refined.discard(j)
+            if on_evict:
+                on_evict(j)
+        for j in sorted(self.pending):
+            if j in self.resident:
+                self.refined.add(j)
+                if on_commit:
+                    on_commit(j, self.pending[j])
+        self.pending.clear()
+        for j in range(f, f + n):
+            self.resident.add(j)
+        self.next_id = f + n
+        self.cur_first, self.cur_n = f, n
+        self.stepped = False
+        return f, evicted
+
+    def _check_past(self, fid: int) -> int:
+        if fid < 0:
+            return VI_E_ARG
+        if fid >= self.next_id or (fid >= self.cur_first and not self.stepped):
+            # a future frame, or a frame of the chunk whose step has not completed yet
+            # ("t >= f -> protocol error"; reading Q13: never tear a frame)
+            return VI_E_PROTOCOL
+        if fid not in self.resident:
+            return VI_NOT_RESIDENT
+        return VI_OK
+
+    def evict(self, fid: int, on_evict=None) -> int:
+        st = self._check_past(fid)
+        if st == VI_OK:
+            self.resident.discard(fid)
+            self.refined.discard(fid)
+            self.pending.pop(fid, None)
+            if on_evict:
+                on_evict(fid)
+        return st
+
+    def commit(self, fid: int, payload) -> int:
+        st = self._check_past(fid)
+        if st == VI_OK:
+            self.pending[fid] = payload
+        return st
+
+    def window(self) -> List[int]:
+        """Memory frames the current chunk attends to, in temporal order."""
+        return sorted(j for j in self.resident if j < self.cur_first)
+
+    def state(self) -> Tuple[List[int], List[int], int]:
+        """(slot_id[S], refined[S], valid mask) under slot = id mod S."""
+        S = self.slots
+        slot_id, ref, mask = [-1] * S, [0] * S, 0
+        for j in self.resident:
+            s = j % S
+            assert slot_id[s] == -1, "two resident frames share a slot"
+            slot_id[s] = j
+            ref[s] = int(j in self.refined)
+            mask |= 1 << s
+        return slot_id, ref, mask
+
+
+class OracleStream:
+    """A live stream through the Memory model (Eq. 3), one chunk of n new frames per step."""
+
+    def __init__(self, cfg, w: Dict[str, np.ndarray], chunk_causal: bool = False):
+        self.cfg = cfg
+        self.w = w
+        self.mem = OracleMemory(cfg.mem_frames, cfg.t_new)
+        self.chunk_causal = chunk_causal
+        # (layer, frame id) -> ("x", block input [P, D]) or ("kv", K [P, D], V [P, D])
+        self.entries: Dict[Tuple[int, int], tuple] = {}
+
+    # -- bookkeeping -------------------------------------------------------------
+    def push(self, n: int):
+        def drop(j):
+            for l in range(self.cfg.layers):
+                self.entries.pop((l, j), None)
+
+        def apply(j, payload):
+            K, V = payload
+            for l in range(self.cfg.layers):
+                self.entries[(l, j)] = ("kv", np.asarray(K[l], np.float64), np.asarray(V[l], np.float64))
+        return self.mem.push(n, on_evict=drop, on_commit=apply)
+
+    def evict(self, fid: int) -> int:
+        def drop(j):
+            for l in range(self.cfg.layers):
+                self.entries.pop((l, j), None)
+        return self.mem.evict(fid, on_evict=drop)
+
+    def commit(self, fid: int, K: np.ndarray, V: np.ndarray) -> int:
+        return self.mem.commit(fid, (np.array(K, np.float64), np.array(V, np.float64)))
+
+    def memory_kv(self, l: int) -> List[Tuple[np.ndarray, np.ndarray]]:
+        out = []
+        for j in self.mem.window():
+            e = self.entries[(l, j)]
+            if e[0] == "kv":
+                out.append((e[1], e[2]))
+            else:
+                _, _, K, V = qkv(e[1], self.w, l, self.cfg)
+                out.append((K, V))
+        return out
+
+    # -- one memory step ---------------------------------------------------------------
+    def step(self, feats: np.ndarray) -> Tuple[np.ndarray, Dict[str, object]]:
+        """Process the chunk pushed last: feats [n, H, W, C] -> output maps [n, H, W, C]."""
+        cfg = self.cfg
+        n = feats.shape[0]
+        assert n == self.mem.cur_n, "step() must follow push(n)"
+        P = cfg.tokens
+        Tp, X = embed(feats, self.w, cfg)
+        stages: Dict[str, object] = dict(tp=Tp, x0=X.copy(), layers=[])
+        for l in range(cfg.layers):
+            mem = self.memory_kv(l)
+            for i in range(n):   # cache this block's input for the chunk's frames
+                self.entries[(l, self.mem.cur_first + i)] = ("x", X[i * P:(i + 1) * P].copy())
+            X, st = block_memory(X, mem, self.w, l, cfg, n, self.chunk_causal)
+            stages["layers"].append(st)
+        Yp, out = compose(X, self.w, cfg, n)
+        stages["x"] = X
+        stages["yp"] = Yp
+        stages["out"] = out
+        self.mem.mark_stepped()
+        return out, stages
+
+    def frame_kv(self, l: int, fid: int) -> Tuple[np.ndarray, np.ndarray]:
+        """K/V of a resident frame at block l as the oracle would attend to them."""
+        e = self.entries[(l, fid)]
+        if e[0] == "kv":
+            return e[1], e[2]
+        _, _, K, V = qkv(e[1], self.w, l, self.cfg)
+        return K, V
+
+
+def mac_counts(P: int, n_mem: int, n_new: int, D: int) -> int:
+    """Score MACs of one memory-step block: Nq * Nk * D."""
+    return (n_new * P) * ((n_mem + n_new) * P) * D
+
+
+def rel_err(got: np.ndarray, ref: np.ndarray) -> float:
+    """Tolerance metric (reading Q18): max_i |g_i - o_i| / max(|o_i|, rms(o))."""
+    got = np.asarray(got, np.float64); ref = np.asarray(ref, np.float64)
+    rms = math.sqrt(float(np.mean(ref * ref))) if ref.size else 0.0
+    den = np.maximum(np.abs(ref), rms if rms > 0 else 1e-300)
+    return float(np.max(np.abs(got - ref) / den)) if ref.size else 0.0
