@@ -1,0 +1,285 @@
+#!/usr/bin/env python
+"""Benchmark of the memory step (BASELINE.json metric: "memory-step frames/s per stream at
+720-tok/frame shape; attn % bf16 peak") on the FuseFormer-shaped config (configs[2]).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--config C3|C3T1]
+
+One step = vi_memory_push(5) + soft split/embedding + 8 memory blocks (3600 queries over
+the 10800 keys of a full 15-slot ring per block) + back-projection/composite, on 5 new
+frames, through libvi.so.  N GPUs = N independent live streams, one per GPU (weak
+scaling, no data-path collective: the streams are independent problems).  Inputs are
+resident in HBM; L2 is flushed (256 MiB write) between timed steps.  Rank 0 prints one
+JSON line.  --impl reference times the fp64 CPU oracle (oracle/) on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "memory-step frames/s per stream at 720-tok/frame shape; attn % bf16 peak"
+UNIT = "frames/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["bf16_tflops"]), float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+def workload_config(cfg):
+    return {"workload": f"{cfg.name}: FuseFormer-shaped memory step (BASELINE.json configs[2])",
+            "layers": cfg.layers, "heads": cfg.heads, "d_model": cfg.d_model, "tokens_per_frame": cfg.tokens,
+            "new_frames_per_step": cfg.t_new, "mem_frames": cfg.mem_frames,
+            "keys_per_block": cfg.slots * cfg.tokens, "queries_per_block": cfg.t_new * cfg.tokens,
+            "feature_map": [cfg.feat_h, cfg.feat_w, cfg.feat_c], "ffn": "F3N 1960",
+            "l2": "flushed between timed steps (256 MiB write)", "streams_per_gpu": 1}
+
+
+class ClockSampler:
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                                       "-lms", "100", "-i", str(self.device)], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if not self.p:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, smax, reasons = [], None, set()
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                s, m = float(f[1]), float(f[2])
+            except ValueError:
+                continue
+            smax = m
+            sm.append(s)
+            names = ("hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap")
+            for name, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(name)
+        load = [s for s in sm if smax and s > 0.3 * smax] or sm
+        return {"sm_mhz": statistics.median(load) if load else None, "sm_max_mhz": smax,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def cpu_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] or [1])
+    except Exception:
+        return len(os.sched_getaffinity(0))
+
+
+def oracle_sample(cfg, seed=0):
+    """Time the fp64 oracle on a bounded sample of one step: split+embed of the 5-frame
+    chunk, ONE of the 8 blocks against a full 10-frame memory, composite.  Returns the
+    extrapolated seconds per step (embed + L * block + composite) and the sample time."""
+    import numpy as np
+    from oracle import vi_oracle as O
+    from vi_synth import make_features, make_weights, rng_for
+    w = make_weights(cfg, seed=seed)
+    feats = make_features(cfg, cfg.t_new, first_frame=cfg.mem_frames, seed=seed)
+    rng = rng_for(seed, "oracle-mem")
+    mem = []
+    for j in range(cfg.mem_frames):          # K/V of the resident frames of block 0
+        _, _, K, V = O.qkv(rng.standard_normal((cfg.tokens, cfg.d_model)), w, 0, cfg)
+        mem.append((K, V))
+    t0 = time.perf_counter()
+    _, X = O.embed(feats, w, cfg)
+    t1 = time.perf_counter()
+    X, _ = O.block_memory(X, mem, w, 0, cfg, cfg.t_new)
+    t2 = time.perf_counter()
+    O.compose(X, w, cfg, cfg.t_new)
+    t3 = time.perf_counter()
+    step = (t1 - t0) + cfg.layers * (t2 - t1) + (t3 - t2)
+    return step, t3 - t0
+
+
+def run_reference(args, cfg):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    for _ in range(args.warmup):
+        oracle_sample(cfg)
+    steps = []
+    for _ in range(args.steps):
+        s, _ = oracle_sample(cfg)
+        steps.append(s)
+    total = sum(steps)
+    value = args.steps * cfg.t_new / total
+    cores = cpu_threads()
+    sample = (f"per step: soft split + embedding of {cfg.t_new} frames, 1 of {cfg.layers} blocks against a full "
+              f"{cfg.mem_frames}-frame memory, composite; block time x{cfg.layers} (extrapolated)")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": workload_config(cfg), "impl": "reference",
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args, cfg):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    from paper_2403_16161_b200 import vi
+    from vi_synth import make_features, make_weights
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    T, P, D = cfg.t_new, cfg.tokens, cfg.d_model
+    ctx = vi.Context.from_synth(cfg, device=local)
+    ctx.set_weights(make_weights(cfg, seed=0))
+    stream = torch.cuda.ExternalStream(ctx.stream())
+    dt = torch.bfloat16
+    nchunks = 4
+    feats = [torch.from_numpy(make_features(cfg, T, first_frame=(rank * nchunks + i) * T, seed=0)).to(dt).cuda()
+             for i in range(nchunks)]
+    out = torch.empty_like(feats[0])
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    torch.cuda.synchronize()
+
+    warm = max(args.warmup, math.ceil(cfg.mem_frames / T) + 1)   # the memory is full from here on
+    for i in range(warm):
+        ctx.run_step(feats[i % nchunks], T, out)
+    ctx.sync()
+
+    clocks = ClockSampler(local)
+    clocks.start()
+    time.sleep(0.3)
+    starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ctx.profile(1)                                  # attention kernels timed with events
+    l0 = ctx.launches()
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    for k in range(args.steps):
+        with torch.cuda.stream(stream):
+            flush.fill_(float(k))                   # untimed L2 flush
+            starts[k].record(stream)
+        ctx.run_step(feats[k % nchunks], T, out)
+        ends[k].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    launches = ctx.launches() - l0
+    prof = ctx.profile_read()
+    ctx.profile(0)
+    step_ms = [s.elapsed_time(e) for s, e in zip(starts, ends)]
+    total_ms = sum(step_ms)
+
+    # end to end through the public API with host (pinned) buffers, copies inside
+    host_in = [f.cpu().pin_memory() for f in feats]
+    host_out = torch.empty(out.shape, dtype=dt).pin_memory()
+    e2e_steps = max(3, min(args.steps, 50))
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    for k in range(e2e_steps):
+        ctx.run_step(host_in[k % nchunks], T, host_out)     # returns after the D2H landed
+    e2e_s = time.perf_counter() - t0
+    clk = clocks.stop()
+
+    tmax = torch.tensor([total_ms, e2e_s], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(tmax, op=dist.ReduceOp.MAX)
+    total_ms, e2e_s = float(tmax[0]), float(tmax[1])
+
+    frames = world * T * args.steps
+    value = frames / (total_ms / 1e3)
+    e2e_value = world * T * e2e_steps / e2e_s
+    bf16_peak, hbm_peak, peak_src = peaks()
+    attn_ms, attn_recs = prof["attention"]
+    per_block_ms = attn_ms / (args.steps * cfg.layers)
+    nq, nk = T * P, cfg.slots * P
+    attn_flop = 4.0 * nq * nk * D
+    achieved = attn_flop / (per_block_ms * 1e-3) / 1e12
+    traffic = None
+    try:
+        with open(os.path.join(ROOT, "profiles", "attention_traffic.json")) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    except Exception:
+        pass
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": warm, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) features, N(0,0.02) weights)",
+        "config": workload_config(cfg),
+        "fps_per_stream": value / world,
+        "step_latency_ms": {"p50": statistics.median(step_ms), "p5": sorted(step_ms)[int(0.05 * len(step_ms))],
+                            "p95": sorted(step_ms)[min(len(step_ms) - 1, int(0.95 * len(step_ms)))]},
+        "roofline": {"kernel": "memory attention (attn_tc_kernel + split combine), per block",
+                     "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
+                     "frac": achieved / bf16_peak, "traffic": traffic,
+                     "flop_per_launch": attn_flop, "avg_launch_ms": per_block_ms,
+                     "peak_source": f"{peak_src} bf16 dense (burst)",
+                     "share_of_step": attn_ms / total_ms},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_in[0].numel() * 2,
+                "d2h_bytes_per_step": host_out.numel() * 2, "api": "vi_run_step (host buffers)"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        s, sample_s = oracle_sample(cfg)
+        line["cpu_baseline"] = {"value": T / s, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+                                "sample": f"1 of {cfg.layers} blocks + split/embed + composite of one {T}-frame "
+                                          f"step ({sample_s:.1f} s of CPU work), block time x{cfg.layers}"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=100)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C3", choices=["C3", "C3T1"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    from vi_synth import CONFIGS
+    cfg = CONFIGS[args.config]
+    if args.impl == "reference":
+        run_reference(args, cfg)
+    else:
+        run_ours(args, cfg)
+
+
+if __name__ == "__main__":
+    main()

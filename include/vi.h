@@ -1,0 +1,237 @@
+/*
+ * vi.h -- C-ABI of the B200 memory-step engine (libvi.so).
+ *
+ * What it computes: the per-frame memory step of an online video-inpainting
+ * transformer, the "Memory" model of arXiv 2403.16161 (§3.4, Eq. 3,
+ * P:119-132) and the refined-memory hand-off of the "Refined" model (§3.5, Eq. 4,
+ * P:142-154).  Citations: P:n = /root/reference/PAPER.md line n.  Readings Qn are
+ * listed in DESIGN.md ("Readings of the paper").
+ *
+ * One step of n new frames (1 <= n <= max_new_frames) is, in this order:
+ *   1. vi_memory_push(n)               frame ids f..f+n-1 enter the ring memory,
+ *                                      frames older than f-M leave it (Eq. 3 span s=M);
+ *   2. vi_soft_split(project=1)        overlapping unfold + patch embedding;
+ *   3. vi_memory_step(l), l = 0..L-1   block l: queries = the new frames only,
+ *                                      keys/values = the new frames + the memory,
+ *                                      the new frames' K/V written into the memory of
+ *                                      block l ("after each transformer, the new result is
+ *                                      saved for later", Fig. 2);
+ *   4. vi_soft_composite(project=1)    back-projection + overlapping fold with
+ *                                      overlap-count normalisation ("blended").
+ * vi_run_step() does 1-4 in one call.
+ *
+ * Conventions
+ *   - Status: 0 = VI_OK, 1 = VI_NOT_RESIDENT (informational, nothing done), < 0 error.
+ *   - Arguments, shapes and protocol are validated synchronously BEFORE any side
+ *     effect: a call that returns an error changed nothing.
+ *   - Device work is enqueued on the context's CUDA stream; calls return after
+ *     enqueue (vi_sync waits).  CUDA errors are sticky: the context is poisoned and
+ *     every later call returns VI_E_CUDA (vi_last_error tells why).
+ *   - Buffers ("device" below) are caller-owned, contiguous, 16-byte aligned device
+ *     pointers unless a function says host pointers are accepted.  The context owns
+ *     its weights, K/V memory slabs and workspaces; nothing returned must be freed
+ *     except the context itself (vi_destroy).
+ *   - Element type "ctx dtype" = bf16 (dtype 0, tensor-core path) or fp32 (dtype 1,
+ *     SIMT path).  The residual stream x is always fp32.
+ *   - Layouts: feature maps [n][H][W][C] channels-last; tokens [n][P][k*k*C] with the
+ *     patch vector ordered (ky, kx, c) and tokens row-major (oy, ox) (reading Q6);
+ *     x [n][P][D]; weights in nn.Linear layout [out][in].
+ *   - Not thread-safe per context, except vi_refine_commit, which may be called from
+ *     another (refiner) thread.
+ */
+#ifndef VI_H_
+#define VI_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t vi_status;
+#define VI_OK            0
+#define VI_NOT_RESIDENT  1   /* evict/commit of a frame no longer in memory: no-op */
+#define VI_E_ARG        -1   /* bad argument value (NULL, negative id, n out of range) */
+#define VI_E_SHAPE      -2   /* inconsistent shapes */
+#define VI_E_CONFIG     -3   /* unsupported configuration */
+#define VI_E_PROTOCOL   -4   /* call out of protocol order (see each function) */
+#define VI_E_CUDA       -5   /* CUDA failure (sticky) or no usable sm_100 device */
+#define VI_E_OOM        -6   /* device allocation failed */
+#define VI_E_NCCL       -7   /* collective failure */
+
+#define VI_DTYPE_BF16 0
+#define VI_DTYPE_FP32 1
+#define VI_FFN_MLP    0     /* FFN1 -> GELU -> FFN2 */
+#define VI_FFN_F3N    1     /* FuseFormer Fusion-FFN: FFN1 -> fold/count -> unfold -> GELU -> FFN2 */
+
+typedef struct vi_ctx vi_ctx;
+
+typedef struct vi_config {
+  int layers;            /* L transformer blocks ("8 consecutive transformer blocks") */
+  int heads;             /* H attention heads */
+  int d_model;           /* D hidden width; head dim d = D/H (16..128, multiple of 16 on bf16) */
+  int tokens_per_frame;  /* P; must equal oh*ow of the split geometry below */
+  int mem_frames;        /* M = memory span s of Eq. 3 (frames f-M..f-1 are attended) */
+  int max_new_frames;    /* T_max frames per step; ring slots S = M + T_max <= 64 */
+  int feat_h, feat_w, feat_c;   /* feature map H x W x C */
+  int kh, kw, sh, sw, ph, pw;   /* soft split kernel / stride / symmetric zero padding */
+  int ffn_hidden;        /* F; F3N requires F % (kh*kw) == 0 */
+  int ffn_kind;          /* VI_FFN_MLP or VI_FFN_F3N */
+  int dtype;             /* VI_DTYPE_BF16 or VI_DTYPE_FP32 */
+  int pos_embed;         /* 0 none, 1 additive [P][D] table given in vi_weights.pos */
+  int device;            /* CUDA device ordinal */
+  void* stream;          /* cudaStream_t to enqueue on (NULL = the context creates one) */
+} vi_config;
+
+/* Weights, host fp32 pointers in nn.Linear layout (y = x W^T + b); converted to the
+ * ctx dtype (round-to-nearest-even) and copied into ctx-owned device buffers.
+ * Biases and LayerNorm parameters stay fp32 on the device. */
+typedef struct vi_weights {
+  const float* embed_w;  /* [D][kh*kw*C] */
+  const float* embed_b;  /* [D] */
+  const float* pos;      /* [P][D] or NULL (only read when pos_embed = 1) */
+  const float* ln1_g;    /* [L][D] */
+  const float* ln1_b;    /* [L][D] */
+  const float* wqkv;     /* [L][3D][D]  rows 0..D-1 = Wq, D..2D-1 = Wk, 2D..3D-1 = Wv */
+  const float* bqkv;     /* [L][3D] */
+  const float* wo;       /* [L][D][D] */
+  const float* bo;       /* [L][D] */
+  const float* ln2_g;    /* [L][D] */
+  const float* ln2_b;    /* [L][D] */
+  const float* w1;       /* [L][F][D] */
+  const float* b1;       /* [L][F] */
+  const float* w2;       /* [L][D][F] */
+  const float* b2;       /* [L][D] */
+  const float* back_w;   /* [kh*kw*C][D] */
+  const float* back_b;   /* [kh*kw*C] */
+} vi_weights;
+
+/* Fill *cfg with the FuseFormer-shaped defaults (BASELINE.json configs[2]): L=8, H=4,
+ * D=512, P=720, M=10, T_max=5, 60x108x128 map, 7x7 s3 p3, F3N 1960, bf16, device 0. */
+vi_status vi_config_default(vi_config* cfg);
+
+/* Create a context: the short form of BASELINE.json's north_star
+ * (vi_create(layers, heads, d_model, tokens_per_frame, mem_frames)); every other field
+ * takes vi_config_default's value.  tokens_per_frame must match the default geometry
+ * (720).  VI_E_CUDA if no sm_100 device is present.  *out is NULL on error. */
+vi_status vi_create(vi_ctx** out, int layers, int heads, int d_model, int tokens_per_frame,
+                    int mem_frames);
+vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg);
+vi_status vi_destroy(vi_ctx* ctx);
+
+/* Upload weights (see vi_weights).  Must precede any compute call (else VI_E_PROTOCOL).
+ * Synchronous: the host arrays may be freed on return. */
+vi_status vi_set_weights(vi_ctx* ctx, const vi_weights* w);
+
+/* Ring memory, push: frames f..f+n-1 (f = next id, ids are consecutive from 0) enter
+ * the memory at slots id mod S; resident frames with id < f-M leave it (Eq. 3 span,
+ * P:127-130; "removing information from ancient frames"), reported in
+ * evicted[0..*n_evicted) (capacity S, may be NULL).  Refine commits queued since the
+ * last push are applied now, for frames still resident (reading Q13).
+ * VI_E_ARG if n < 1 or n > max_new_frames.  first_id may be NULL. */
+vi_status vi_memory_push(vi_ctx* ctx, int n, int64_t* first_id, int64_t* evicted, int* n_evicted);
+
+/* Explicit eviction of a past frame.  VI_E_PROTOCOL for a future frame or a frame of
+ * the current chunk whose step has not finished; VI_NOT_RESIDENT if already gone. */
+vi_status vi_memory_evict(vi_ctx* ctx, int64_t frame_id);
+
+/* Soft split of n feature maps feat [n][H][W][C] (device, ctx dtype).
+ * project = 0: out = raw tokens [n][P][kh*kw*C] (ctx dtype), any 1 <= n <= T_max;
+ * project = 1: out = x0 [n][P][D] fp32 = tokens We^T + be (+pos).  Bit-exact copies
+ * for project = 0 (padding positions are 0). */
+vi_status vi_soft_split(vi_ctx* ctx, const void* feat, int n, void* out, int project);
+
+/* Block `layer` of the memory step for the chunk pushed last (n frames):
+ *   h = LN1(x); Q,K,V = h Wqkv^T + bqkv; K,V rows -> memory slab of block `layer`;
+ *   O = softmax(Q K^T / sqrt(d)) V over the keys of every valid slot (the chunk +
+ *   resident frames f-M..f-1), per head; x += O Wo^T + bo; x += FFN(LN2(x)).
+ * x_in / x_out: device fp32 [n][P][D]; x_in == x_out allowed.
+ * VI_E_PROTOCOL unless called after a push with layer = 0, 1, ..., L-1 in order. */
+vi_status vi_memory_step(vi_ctx* ctx, int layer, const float* x_in, float* x_out);
+
+/* Soft composite of n frames into feat [n][H][W][C] (device, ctx dtype).
+ * project = 0: in = raw tokens [n][P][kh*kw*C] (ctx dtype);
+ * project = 1: in = x [n][P][D] fp32, back-projected with back_w / back_b first.
+ * out[y][x][c] = sum of the patch entries landing on (y,x) / cover count (IEEE div). */
+vi_status vi_soft_composite(vi_ctx* ctx, const void* in, int n, void* feat, int project);
+
+/* Refine commit (Eq. 4's refined memory M-bar): overwrite the memory
+ * entries of a past, resident frame for every block with k, v = [L][P][D] (host or
+ * device, ctx dtype).  Queued and applied at the next vi_memory_push, so a frame is
+ * never torn across blocks; a later commit for the same frame replaces an earlier one.
+ * The payload is copied before return (buffers may be reused).  Thread-safe w.r.t.
+ * the context's other calls.  VI_E_PROTOCOL / VI_NOT_RESIDENT as vi_memory_evict. */
+vi_status vi_refine_commit(vi_ctx* ctx, int64_t frame_id, const void* k, const void* v);
+
+/* Host snapshot of the ring: slot_id[S] (-1 = empty), refined[S] (0/1), valid bitmask
+ * (bit s = slot s holds a resident frame).  Any pointer may be NULL. */
+vi_status vi_memory_state(vi_ctx* ctx, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask);
+
+/* One whole step: push(n) + split(project=1) + L blocks + composite(project=1).
+ * feat / out may be HOST or device pointers ([n][H][W][C], ctx dtype); host buffers
+ * are staged through ctx-owned device buffers on the ctx stream (the call then
+ * returns after the output has landed in host memory). */
+vi_status vi_run_step(vi_ctx* ctx, const void* feat, int n, void* out, int64_t* first_id);
+
+/* Wait for all work enqueued on the context stream. */
+vi_status vi_sync(vi_ctx* ctx);
+/* Last error message of this context (static storage inside the ctx; never NULL). */
+const char* vi_last_error(const vi_ctx* ctx);
+/* Number of kernels this context has launched so far (test / bench evidence). */
+int64_t vi_kernel_launches(const vi_ctx* ctx);
+/* Ring slot count S and the ctx stream (cudaStream_t). */
+int vi_num_slots(const vi_ctx* ctx);
+void* vi_stream(const vi_ctx* ctx);
+
+/* Device-side timing of the context's own kernels with CUDA events on its stream.
+ * mode 0 = off, 1 = memory attention only (attention kernel + split combine),
+ * 2 = every category.  vi_profile_read waits for the stream, then returns per category
+ * the summed milliseconds and the number of timed launches and resets the counters.
+ * Categories: VI_PROF_ATTN, VI_PROF_GEMM (all tensor-core / SIMT GEMMs),
+ * VI_PROF_PATCH (soft split / composite / F3N fold-unfold), VI_PROF_ROW (LN, casts). */
+#define VI_PROF_ATTN  0
+#define VI_PROF_GEMM  1
+#define VI_PROF_PATCH 2
+#define VI_PROF_ROW   3
+#define VI_PROF_N     4
+vi_status vi_profile(vi_ctx* ctx, int mode);
+vi_status vi_profile_read(vi_ctx* ctx, double* ms /*[VI_PROF_N]*/, int64_t* launches /*[VI_PROF_N]*/);
+
+/* Test hook: copy an internal buffer to dst (host or device), `bytes` must match.
+ *   VI_DBG_TOKENS  raw split tokens of the last split       [n][P][kh*kw*C] ctx dtype
+ *   VI_DBG_H       LN output last written                    [n][P][D] ctx dtype
+ *   VI_DBG_Q       queries of the last block                 [n][P][D] ctx dtype
+ *   VI_DBG_O       attention output of the last block        [n][P][D] ctx dtype
+ *   VI_DBG_U       FFN1 output of the last block             [n][P][F] ctx dtype
+ *   VI_DBG_G       GELU(F3N(u)) of the last block            [n][P][F] ctx dtype
+ *   VI_DBG_K, VI_DBG_V   memory rows of (layer, slot)        [P][D] ctx dtype
+ * `n` is the chunk size of the last push. */
+#define VI_DBG_TOKENS 0
+#define VI_DBG_H      1
+#define VI_DBG_Q      2
+#define VI_DBG_O      3
+#define VI_DBG_U      4
+#define VI_DBG_G      5
+#define VI_DBG_K      6
+#define VI_DBG_V      7
+vi_status vi_debug_read(vi_ctx* ctx, int what, int layer, int slot, void* dst, size_t bytes);
+
+/* ---- Ring bookkeeping alone (CUDA-free; the same code every context uses) ---------
+ * For tests of the integer bookkeeping on machines without a GPU. */
+typedef struct vi_ring vi_ring;
+vi_status vi_ring_create(vi_ring** out, int mem_frames, int max_new_frames);
+vi_status vi_ring_destroy(vi_ring* r);
+vi_status vi_ring_push(vi_ring* r, int n, int64_t* first_id, int64_t* evicted, int* n_evicted);
+vi_status vi_ring_evict(vi_ring* r, int64_t frame_id);
+vi_status vi_ring_commit(vi_ring* r, int64_t frame_id);     /* bookkeeping of a commit only */
+vi_status vi_ring_mark_stepped(vi_ring* r);                  /* the chunk went through all blocks */
+vi_status vi_ring_state(const vi_ring* r, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask);
+
+/* Library version string. */
+const char* vi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VI_H_ */

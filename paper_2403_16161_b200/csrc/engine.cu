@@ -1,0 +1,812 @@
+// libvi.so engine: the vi_* C-ABI (include/vi.h) over the sm_100a kernels.
+//
+// Per context (one live stream on one GPU) the engine owns, in HBM:
+//   weights  (bf16 matrices / fp32 biases + LN params; nn.Linear [out][in] layout,
+//             the per-block matrices of all L blocks stacked so one TMA map covers them)
+//   memory   K slab [L][S*P][D] and V slab stored TRANSPOSED [L][D][S*P] (ctx dtype);
+//            slot s of block l holds rows s*P .. s*P+P-1 (reading Q11, slot = id mod S)
+//   workspaces for one chunk of up to T_max frames (tokens, h, Q, O, u, g, F3N fold map,
+//            KV-split partials) plus host-buffer staging for vi_run_step.
+// Every step of the path runs in the kernels of kernels/*.cu; the host only validates,
+// keeps the integer ring bookkeeping (ring.cpp) and enqueues launches.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "kernels/kernels.h"
+#include "ring.h"
+#include "vi.h"
+
+using namespace vi;
+
+namespace {
+
+typedef CUresult (*PFN_encodeTiled_t)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                      const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                      CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+PFN_encodeTiled_t encode_fn() {
+  static PFN_encodeTiled_t fn = nullptr;
+  if (!fn) {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_encodeTiled_t>(p);
+  }
+  return fn;
+}
+
+// 2-D bf16 tensor [outer][inner] (row pitch = inner elements), box {box_inner, box_outer},
+// 128-byte swizzle, zero fill out of bounds.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint32_t box_inner,
+               uint32_t box_outer) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {inner * 2};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t es[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, es,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+uint16_t f2bf(float f) {  // round to nearest even
+  uint32_t u;
+  std::memcpy(&u, &f, 4);
+  if ((u & 0x7fffffffu) > 0x7f800000u) return 0x7fc0;
+  u += 0x7fffu + ((u >> 16) & 1u);
+  return uint16_t(u >> 16);
+}
+
+bool is_host_ptr(const void* p) {
+  cudaPointerAttributes at;
+  if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+    cudaGetLastError();
+    return true;
+  }
+  return at.type == cudaMemoryTypeHost || at.type == cudaMemoryTypeUnregistered;
+}
+
+constexpr int kMaxSplit = 16;
+
+}  // namespace
+
+struct vi_ctx {
+  vi_config cfg{};
+  Geom g{}, gf{};          // split geometry (C = feat_c) and F3N geometry (C = F / (kh*kw))
+  int L = 0, H = 0, D = 0, hd = 0, P = 0, M = 0, Tmax = 0, S = 0, F = 0, Pd = 0, es = 2;
+  bool bf16 = true;
+  cudaStream_t stream = nullptr, copy_stream = nullptr;
+  bool own_stream = false;
+  std::string err = "ok";
+  bool poisoned = false;
+  int64_t launches = 0;
+  Ring ring{0, 1};
+  std::mutex mu;
+  bool have_weights = false;
+  int next_layer = -1;     // expected layer of the next vi_memory_step (-1: no push yet)
+
+  // weights
+  void *w_embed = nullptr, *w_qkv = nullptr, *w_o = nullptr, *w_1 = nullptr, *w_2 = nullptr, *w_back = nullptr;
+  float *b_embed = nullptr, *pos = nullptr, *ln1_g = nullptr, *ln1_b = nullptr, *b_qkv = nullptr, *b_o = nullptr;
+  float *ln2_g = nullptr, *ln2_b = nullptr, *b_1 = nullptr, *b_2 = nullptr, *b_back = nullptr;
+  // memory
+  void *kslab = nullptr, *vtslab = nullptr;
+  // workspaces
+  void *tokens = nullptr, *h = nullptr, *q = nullptr, *o = nullptr, *u = nullptr, *gbuf = nullptr, *xb = nullptr;
+  float *x_ws = nullptr, *fold_ws = nullptr, *opart = nullptr, *lse = nullptr;
+  void *feat_in = nullptr, *feat_out = nullptr;
+  std::vector<void*> allocs;
+  std::map<int64_t, std::pair<void*, void*>> pending_kv;  // queued refine commits (device copies)
+  std::vector<std::pair<void*, void*>> free_kv;
+
+  // tensor maps (bf16 path)
+  CUtensorMap tm_tokens, tm_wembed, tm_h, tm_wqkv, tm_o, tm_wo, tm_w1, tm_g, tm_w2, tm_xb, tm_wback;
+  CUtensorMap tm_q, tm_k, tm_vt;
+  int bn_embed = 128, bn_qkv = 128, bn_o = 64, bn_1 = 128, bn_2 = 64, bn_back = 128;
+
+  // profiling (vi_profile)
+  int prof_mode = 0;
+  struct Rec { int cat; cudaEvent_t a, b; };
+  std::vector<Rec> prof_recs;
+  std::vector<cudaEvent_t> ev_pool;
+  cudaEvent_t prof_ev() {
+    if (ev_pool.empty()) {
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      return e;
+    }
+    cudaEvent_t e = ev_pool.back();
+    ev_pool.pop_back();
+    return e;
+  }
+
+  ~vi_ctx();
+  vi_status fail(vi_status st, const std::string& m) {
+    err = m;
+    return st;
+  }
+  vi_status cuda_fail(cudaError_t e, const char* where) {
+    poisoned = true;
+    err = std::string("CUDA error in ") + where + ": " + cudaGetErrorString(e);
+    return VI_E_CUDA;
+  }
+  void* dalloc(size_t bytes, bool zero = true) {
+    void* p = nullptr;
+    if (cudaMalloc(&p, bytes ? bytes : 16) != cudaSuccess) {
+      cudaGetLastError();
+      return nullptr;
+    }
+    if (zero) cudaMemset(p, 0, bytes ? bytes : 16);
+    allocs.push_back(p);
+    return p;
+  }
+};
+
+vi_ctx::~vi_ctx() {
+  if (stream) cudaStreamSynchronize(stream);
+  for (auto& r : prof_recs) {
+    cudaEventDestroy(r.a);
+    cudaEventDestroy(r.b);
+  }
+  for (auto e : ev_pool) cudaEventDestroy(e);
+  for (auto& kv : pending_kv) free_kv.push_back(kv.second);
+  for (auto& kv : free_kv) {
+    cudaFree(kv.first);
+    cudaFree(kv.second);
+  }
+  for (void* p : allocs) cudaFree(p);
+  if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (own_stream && stream) cudaStreamDestroy(stream);
+}
+
+#define CK(call, where)                                 \
+  do {                                                  \
+    cudaError_t e_ = (call);                            \
+    if (e_ != cudaSuccess) return c->cuda_fail(e_, where); \
+  } while (0)
+#define LAUNCH(call, where)        \
+  do {                             \
+    ++c->launches;                 \
+    CK((call), where);             \
+  } while (0)
+#define PLAUNCH(cat, call, where) \
+  do {                             \
+    Prof p_(c, cat);               \
+    LAUNCH(call, where);           \
+  } while (0)
+#define LIVE(c)                                                      \
+  do {                                                               \
+    if (!(c)) return VI_E_ARG;                                       \
+    if ((c)->poisoned) return VI_E_CUDA;                             \
+  } while (0)
+
+// Scoped event pair around the launches of one category (vi_profile).
+struct Prof {
+  vi_ctx* c;
+  int cat;
+  cudaEvent_t b = nullptr;
+  Prof(vi_ctx* c_, int cat_) : c(c_), cat(cat_) {
+    if (c->prof_mode == 2 || (c->prof_mode == 1 && cat == VI_PROF_ATTN)) {
+      cudaEvent_t a = c->prof_ev();
+      b = c->prof_ev();
+      cudaEventRecord(a, c->stream);
+      c->prof_recs.push_back({cat, a, b});
+    }
+  }
+  ~Prof() {
+    if (b) cudaEventRecord(b, c->stream);
+  }
+};
+
+// ------------------------------------------------------------------------------ setup
+
+static vi_status validate(const vi_config* k, std::string* why) {
+  auto bad = [&](const char* m) {
+    *why = m;
+    return VI_E_CONFIG;
+  };
+  if (k->layers < 1 || k->heads < 1 || k->d_model < 1 || k->mem_frames < 0 || k->max_new_frames < 1)
+    return bad("layers, heads, d_model, max_new_frames must be >= 1 and mem_frames >= 0");
+  if (k->mem_frames + k->max_new_frames > 64) return bad("mem_frames + max_new_frames must be <= 64");
+  if (k->d_model % k->heads) return bad("d_model must be divisible by heads");
+  const int hd = k->d_model / k->heads;
+  if (k->dtype != VI_DTYPE_BF16 && k->dtype != VI_DTYPE_FP32) return bad("dtype must be 0 (bf16) or 1 (fp32)");
+  if (k->kh < 1 || k->kw < 1 || k->sh < 1 || k->sw < 1 || k->ph < 0 || k->pw < 0) return bad("bad split geometry");
+  const int oh = (k->feat_h + 2 * k->ph - k->kh) / k->sh + 1, ow = (k->feat_w + 2 * k->pw - k->kw) / k->sw + 1;
+  if (oh < 1 || ow < 1 || oh * ow != k->tokens_per_frame) return bad("tokens_per_frame != oh*ow of the split geometry");
+  // every cell must be covered by a window (the composite divides by the count)
+  if (k->kh < k->sh || k->kw < k->sw || (oh - 1) * k->sh - k->ph + k->kh < k->feat_h ||
+      (ow - 1) * k->sw - k->pw + k->kw < k->feat_w || k->ph >= k->kh || k->pw >= k->kw)
+    return bad("split geometry leaves feature cells uncovered");
+  const int vec = k->dtype == VI_DTYPE_BF16 ? 8 : 4;
+  if (k->feat_c % vec) return bad("feat_c must be a multiple of 8 (bf16) / 4 (fp32)");
+  if (k->ffn_hidden < 1 || (k->ffn_kind != VI_FFN_MLP && k->ffn_kind != VI_FFN_F3N)) return bad("bad ffn");
+  if (k->ffn_kind == VI_FFN_F3N) {
+    if (k->ffn_hidden % (k->kh * k->kw)) return bad("F3N needs ffn_hidden % (kh*kw) == 0");
+    if ((k->ffn_hidden / (k->kh * k->kw)) % vec) return bad("F3N hidden channels must be a multiple of 8/4");
+  }
+  if (k->dtype == VI_DTYPE_BF16) {
+    if (hd != 64 && hd != 128) return bad("bf16 path: head dim must be 64 or 128");
+    if (k->d_model % 64 || k->ffn_hidden % 8) return bad("bf16 path: d_model % 64 and ffn_hidden % 8 required");
+    if ((k->kh * k->kw * k->feat_c) % 64) return bad("bf16 path: patch dim must be a multiple of 64");
+  } else {
+    if (hd % 32 || hd > 128) return bad("fp32 path: head dim must be a multiple of 32, <= 128");
+    if (k->d_model > 1024) return bad("d_model <= 1024");
+  }
+  if (k->d_model > 1024) return bad("d_model <= 1024 (LayerNorm kernel)");
+  return VI_OK;
+}
+
+extern "C" vi_status vi_config_default(vi_config* k) {
+  if (!k) return VI_E_ARG;
+  std::memset(k, 0, sizeof(*k));
+  k->layers = 8; k->heads = 4; k->d_model = 512; k->tokens_per_frame = 720; k->mem_frames = 10;
+  k->max_new_frames = 5; k->feat_h = 60; k->feat_w = 108; k->feat_c = 128; k->kh = k->kw = 7;
+  k->sh = k->sw = 3; k->ph = k->pw = 3; k->ffn_hidden = 1960; k->ffn_kind = VI_FFN_F3N;
+  k->dtype = VI_DTYPE_BF16; k->pos_embed = 0; k->device = 0; k->stream = nullptr;
+  return VI_OK;
+}
+
+static vi_status build_maps(vi_ctx* c) {
+  const int rows = c->Tmax * c->P;
+  bool ok = true;
+  ok &= make_tmap(&c->tm_tokens, c->tokens, c->Pd, rows, 64, 128);
+  ok &= make_tmap(&c->tm_wembed, c->w_embed, c->Pd, c->D, 64, c->bn_embed);
+  ok &= make_tmap(&c->tm_h, c->h, c->D, rows, 64, 128);
+  ok &= make_tmap(&c->tm_wqkv, c->w_qkv, c->D, (uint64_t)c->L * 3 * c->D, 64, c->bn_qkv);
+  ok &= make_tmap(&c->tm_o, c->o, c->D, rows, 64, 128);
+  ok &= make_tmap(&c->tm_wo, c->w_o, c->D, (uint64_t)c->L * c->D, 64, c->bn_o);
+  ok &= make_tmap(&c->tm_w1, c->w_1, c->D, (uint64_t)c->L * c->F, 64, c->bn_1);
+  ok &= make_tmap(&c->tm_g, c->gbuf, c->F, rows, 64, 128);
+  ok &= make_tmap(&c->tm_w2, c->w_2, c->F, (uint64_t)c->L * c->D, 64, c->bn_2);
+  ok &= make_tmap(&c->tm_xb, c->xb, c->D, rows, 64, 128);
+  ok &= make_tmap(&c->tm_wback, c->w_back, c->D, c->Pd, 64, c->bn_back);
+  ok &= make_tmap(&c->tm_q, c->q, c->D, rows, 64, 128);
+  ok &= make_tmap(&c->tm_k, c->kslab, c->D, (uint64_t)c->L * c->S * c->P, 64, 128);
+  ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->S * c->P, (uint64_t)c->L * c->D, 64, c->hd);
+  return ok ? VI_OK : c->fail(VI_E_CUDA, "cuTensorMapEncodeTiled failed");
+}
+
+extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
+  if (!out || !cfg) return VI_E_ARG;
+  *out = nullptr;
+  std::string why;
+  vi_status st = validate(cfg, &why);
+  if (st != VI_OK) return st;
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || cfg->device < 0 || cfg->device >= ndev) {
+    cudaGetLastError();
+    return VI_E_CUDA;
+  }
+  cudaDeviceProp prop;
+  if (cudaGetDeviceProperties(&prop, cfg->device) != cudaSuccess || prop.major != 10) return VI_E_CUDA;
+  if (cudaSetDevice(cfg->device) != cudaSuccess) return VI_E_CUDA;
+
+  vi_ctx* c = new (std::nothrow) vi_ctx();
+  if (!c) return VI_E_OOM;
+  c->cfg = *cfg;
+  c->L = cfg->layers; c->H = cfg->heads; c->D = cfg->d_model; c->hd = c->D / c->H;
+  c->P = cfg->tokens_per_frame; c->M = cfg->mem_frames; c->Tmax = cfg->max_new_frames; c->S = c->M + c->Tmax;
+  c->F = cfg->ffn_hidden; c->Pd = cfg->kh * cfg->kw * cfg->feat_c;
+  c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
+  c->ring = Ring(c->M, c->Tmax);
+  const int oh = (cfg->feat_h + 2 * cfg->ph - cfg->kh) / cfg->sh + 1;
+  const int ow = (cfg->feat_w + 2 * cfg->pw - cfg->kw) / cfg->sw + 1;
+  c->g = Geom{cfg->feat_h, cfg->feat_w, cfg->feat_c, cfg->kh, cfg->kw, cfg->sh, cfg->sw, cfg->ph, cfg->pw, oh, ow};
+  c->gf = c->g;
+  c->gf.C = cfg->ffn_kind == VI_FFN_F3N ? c->F / (cfg->kh * cfg->kw) : 0;
+  if (cfg->stream) {
+    c->stream = static_cast<cudaStream_t>(cfg->stream);
+  } else {
+    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete c;
+      return VI_E_CUDA;
+    }
+    c->own_stream = true;
+  }
+  if (cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    delete c;
+    return VI_E_CUDA;
+  }
+  const size_t es = c->es, L = c->L, D = c->D, F = c->F, Pd = c->Pd, S = c->S, P = c->P;
+  const size_t rows = (size_t)c->Tmax * P;
+  const size_t fmap = (size_t)c->Tmax * cfg->feat_h * cfg->feat_w * cfg->feat_c;
+  bool ok = true;
+  auto A = [&](size_t bytes) {
+    void* p = c->dalloc(bytes);
+    ok &= p != nullptr;
+    return p;
+  };
+  c->w_embed = A(D * Pd * es); c->b_embed = (float*)A(D * 4); c->pos = (float*)A(P * D * 4);
+  c->ln1_g = (float*)A(L * D * 4); c->ln1_b = (float*)A(L * D * 4);
+  c->w_qkv = A(L * 3 * D * D * es); c->b_qkv = (float*)A(L * 3 * D * 4);
+  c->w_o = A(L * D * D * es); c->b_o = (float*)A(L * D * 4);
+  c->ln2_g = (float*)A(L * D * 4); c->ln2_b = (float*)A(L * D * 4);
+  c->w_1 = A(L * F * D * es); c->b_1 = (float*)A(L * F * 4);
+  c->w_2 = A(L * D * F * es); c->b_2 = (float*)A(L * D * 4);
+  c->w_back = A(Pd * D * es); c->b_back = (float*)A(Pd * 4);
+  c->kslab = A(L * S * P * D * es); c->vtslab = A(L * S * P * D * es);
+  c->tokens = A(rows * Pd * es); c->h = A(rows * D * es); c->q = A(rows * D * es); c->o = A(rows * D * es);
+  c->u = A(rows * F * es); c->gbuf = A(rows * F * es); c->xb = A(rows * D * es);
+  c->x_ws = (float*)A(rows * D * 4);
+  c->fold_ws = (float*)A((size_t)c->Tmax * cfg->feat_h * cfg->feat_w * std::max(c->gf.C, 1) * 4);
+  if (c->bf16) {
+    c->opart = (float*)A((size_t)kMaxSplit * rows * D * 4);
+    c->lse = (float*)A((size_t)kMaxSplit * c->H * rows * 4);
+  }
+  c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);
+  if (!ok) {
+    delete c;
+    return VI_E_OOM;
+  }
+  if (cudaDeviceSynchronize() != cudaSuccess) {
+    delete c;
+    return VI_E_CUDA;
+  }
+  if (c->bf16) {
+    if (c->D % 128) c->bn_o = c->bn_2 = 64;
+    if (build_maps(c) != VI_OK) {
+      delete c;
+      return VI_E_CUDA;
+    }
+  }
+  *out = c;
+  return VI_OK;
+}
+
+extern "C" vi_status vi_create(vi_ctx** out, int layers, int heads, int d_model, int tokens_per_frame,
+                               int mem_frames) {
+  vi_config k;
+  vi_config_default(&k);
+  k.layers = layers; k.heads = heads; k.d_model = d_model; k.tokens_per_frame = tokens_per_frame;
+  k.mem_frames = mem_frames;
+  return vi_create_ex(out, &k);
+}
+
+extern "C" vi_status vi_destroy(vi_ctx* c) {
+  delete c;
+  return VI_OK;
+}
+
+static vi_status upload_mat(vi_ctx* c, void* dst, const float* src, size_t n) {
+  if (c->bf16) {
+    std::vector<uint16_t> tmp(n);
+    for (size_t i = 0; i < n; ++i) tmp[i] = f2bf(src[i]);
+    CK(cudaMemcpy(dst, tmp.data(), n * 2, cudaMemcpyHostToDevice), "upload");
+  } else {
+    CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice), "upload");
+  }
+  return VI_OK;
+}
+static vi_status upload_f32(vi_ctx* c, float* dst, const float* src, size_t n) {
+  CK(cudaMemcpy(dst, src, n * 4, cudaMemcpyHostToDevice), "upload");
+  return VI_OK;
+}
+
+extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
+  LIVE(c);
+  if (!w || !w->embed_w || !w->embed_b || !w->ln1_g || !w->ln1_b || !w->wqkv || !w->bqkv || !w->wo || !w->bo ||
+      !w->ln2_g || !w->ln2_b || !w->w1 || !w->b1 || !w->w2 || !w->b2 || !w->back_w || !w->back_b)
+    return c->fail(VI_E_ARG, "vi_set_weights: NULL weight pointer");
+  if (c->cfg.pos_embed && !w->pos) return c->fail(VI_E_ARG, "vi_set_weights: pos_embed=1 needs pos");
+  CK(cudaStreamSynchronize(c->stream), "set_weights sync");
+  const size_t L = c->L, D = c->D, F = c->F, Pd = c->Pd;
+  vi_status st = VI_OK;
+  auto U = [&](vi_status s) {
+    if (s != VI_OK) st = s;
+  };
+  U(upload_mat(c, c->w_embed, w->embed_w, D * Pd));
+  U(upload_f32(c, c->b_embed, w->embed_b, D));
+  if (c->cfg.pos_embed) U(upload_f32(c, c->pos, w->pos, (size_t)c->P * D));
+  U(upload_f32(c, c->ln1_g, w->ln1_g, L * D));
+  U(upload_f32(c, c->ln1_b, w->ln1_b, L * D));
+  U(upload_mat(c, c->w_qkv, w->wqkv, L * 3 * D * D));
+  U(upload_f32(c, c->b_qkv, w->bqkv, L * 3 * D));
+  U(upload_mat(c, c->w_o, w->wo, L * D * D));
+  U(upload_f32(c, c->b_o, w->bo, L * D));
+  U(upload_f32(c, c->ln2_g, w->ln2_g, L * D));
+  U(upload_f32(c, c->ln2_b, w->ln2_b, L * D));
+  U(upload_mat(c, c->w_1, w->w1, L * F * D));
+  U(upload_f32(c, c->b_1, w->b1, L * F));
+  U(upload_mat(c, c->w_2, w->w2, L * D * F));
+  U(upload_f32(c, c->b_2, w->b2, L * D));
+  U(upload_mat(c, c->w_back, w->back_w, Pd * D));
+  U(upload_f32(c, c->b_back, w->back_b, Pd));
+  if (st == VI_OK) c->have_weights = true;
+  return st;
+}
+
+// ------------------------------------------------------------------------------ ring
+
+static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
+  const size_t es = c->es, P = c->P, D = c->D, SP = (size_t)c->S * c->P;
+  for (int64_t id : ids) {
+    auto it = c->pending_kv.find(id);
+    if (it == c->pending_kv.end()) continue;
+    const int slot = int(id % c->S);
+    for (int l = 0; l < c->L; ++l) {
+      const uint8_t* ksrc = static_cast<const uint8_t*>(it->second.first) + (size_t)l * P * D * es;
+      const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.second) + (size_t)l * P * D * es;
+      uint8_t* kdst = static_cast<uint8_t*>(c->kslab) + ((size_t)l * SP + (size_t)slot * P) * D * es;
+      CK(cudaMemcpyAsync(kdst, ksrc, P * D * es, cudaMemcpyDeviceToDevice, c->stream), "commit K");
+      uint8_t* vt = static_cast<uint8_t*>(c->vtslab) + (size_t)l * D * SP * es;
+      PLAUNCH(VI_PROF_ROW, launch_transpose_to_slab(vsrc, vt, c->P, c->D, SP, (size_t)slot * P, c->bf16 ? 0 : 1, c->stream),
+             "commit V");
+    }
+  }
+  return VI_OK;
+}
+
+extern "C" vi_status vi_memory_push(vi_ctx* c, int n, int64_t* first_id, int64_t* evicted, int* n_evicted) {
+  LIVE(c);
+  if (n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_memory_push: n out of [1, max_new_frames]");
+  std::lock_guard<std::mutex> lk(c->mu);
+  std::vector<int64_t> ev, apply;
+  const int64_t f = c->ring.push(n, &ev, &apply);
+  vi_status st = apply_commits(c, apply);
+  // all queued payloads are consumed (applied, or dropped because the frame left)
+  for (auto& kv : c->pending_kv) c->free_kv.push_back(kv.second);
+  c->pending_kv.clear();
+  if (st != VI_OK) return st;
+  c->next_layer = 0;
+  if (first_id) *first_id = f;
+  if (evicted)
+    for (size_t i = 0; i < ev.size(); ++i) evicted[i] = ev[i];
+  if (n_evicted) *n_evicted = int(ev.size());
+  return VI_OK;
+}
+
+extern "C" vi_status vi_memory_evict(vi_ctx* c, int64_t frame_id) {
+  LIVE(c);
+  std::lock_guard<std::mutex> lk(c->mu);
+  const vi_status st = c->ring.evict(frame_id);
+  if (st == VI_OK) {
+    auto it = c->pending_kv.find(frame_id);
+    if (it != c->pending_kv.end()) {
+      c->free_kv.push_back(it->second);
+      c->pending_kv.erase(it);
+    }
+  }
+  return st;
+}
+
+extern "C" vi_status vi_refine_commit(vi_ctx* c, int64_t frame_id, const void* k, const void* v) {
+  LIVE(c);
+  if (!k || !v) return VI_E_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  const vi_status st = c->ring.commit(frame_id);
+  if (st != VI_OK) return st;
+  const size_t bytes = (size_t)c->L * c->P * c->D * c->es;
+  auto it = c->pending_kv.find(frame_id);
+  std::pair<void*, void*> buf;
+  if (it != c->pending_kv.end()) {
+    buf = it->second;
+  } else if (!c->free_kv.empty()) {
+    buf = c->free_kv.back();
+    c->free_kv.pop_back();
+  } else {
+    if (cudaMalloc(&buf.first, bytes) != cudaSuccess || cudaMalloc(&buf.second, bytes) != cudaSuccess) {
+      cudaGetLastError();
+      return c->fail(VI_E_OOM, "vi_refine_commit: staging allocation failed");
+    }
+  }
+  const cudaMemcpyKind kk = is_host_ptr(k) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  const cudaMemcpyKind kv = is_host_ptr(v) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+  // the online stream may still read an older payload of this buffer? no: payloads are
+  // consumed at push (stream-ordered) -- order the copy after the ctx stream's work.
+  cudaEvent_t ev;
+  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "commit event");
+  CK(cudaEventRecord(ev, c->stream), "commit event");
+  CK(cudaStreamWaitEvent(c->copy_stream, ev, 0), "commit wait");
+  CK(cudaMemcpyAsync(buf.first, k, bytes, kk, c->copy_stream), "commit copy K");
+  CK(cudaMemcpyAsync(buf.second, v, bytes, kv, c->copy_stream), "commit copy V");
+  CK(cudaStreamSynchronize(c->copy_stream), "commit sync");
+  cudaEventDestroy(ev);
+  c->pending_kv[frame_id] = buf;
+  return VI_OK;
+}
+
+extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask) {
+  if (!c) return VI_E_ARG;
+  std::lock_guard<std::mutex> lk(c->mu);
+  for (int s = 0; s < c->S; ++s) {
+    if (slot_id) slot_id[s] = c->ring.slot_id[s];
+    if (refined) refined[s] = c->ring.refined[s];
+  }
+  if (valid_mask) *valid_mask = c->ring.valid_mask();
+  return VI_OK;
+}
+
+// ------------------------------------------------------------------------------ compute
+
+static Epi epi_base(int kind, int M, int N, const float* bias) {
+  Epi e;
+  std::memset(&e, 0, sizeof(e));
+  e.kind = kind; e.M = M; e.N = N; e.bias = bias; e.P = 1; e.S = 1;
+  return e;
+}
+
+extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out, int project) {
+  LIVE(c);
+  if (!feat || !out || n < 1 || n > c->Tmax || (project != 0 && project != 1))
+    return c->fail(VI_E_ARG, "vi_soft_split: bad argument");
+  if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_split: weights not set");
+  const int dt = c->bf16 ? 0 : 1;
+  void* tok = project ? c->tokens : out;
+  PLAUNCH(VI_PROF_PATCH, launch_unfold(feat, tok, n, c->g, dt, c->stream), "unfold");
+  if (project) {
+    const int M = n * c->P;
+    Epi e = epi_base(EPI_STORE, M, c->D, c->b_embed);
+    e.out = out; e.ldo = c->D; e.out_f32 = 1; e.pos = c->cfg.pos_embed ? c->pos : nullptr; e.P = c->P;
+    if (c->bf16)
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, c->bn_embed, e, c->stream), "embed gemm");
+    else
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->tokens, (const float*)c->w_embed, M, c->D, c->Pd, e, c->stream),
+             "embed gemm");
+  }
+  return VI_OK;
+}
+
+static void choose_split(int units, int ntiles, int* nsplit, int* tps) {
+  double best = 1e30;
+  *nsplit = 1;
+  *tps = ntiles;
+  for (int s = 1; s <= kMaxSplit && s <= ntiles; ++s) {
+    const int t = (ntiles + s - 1) / s;
+    const int waves = (units * s + 147) / 148;
+    const double cost = double(waves) * t + (s > 1 ? 2.0 + 0.15 * s : 0.0);
+    if (cost < best - 1e-9) {
+      best = cost;
+      *nsplit = s;
+      *tps = t;
+    }
+  }
+}
+
+static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
+  KeySegs k;
+  std::memset(&k, 0, sizeof(k));
+  int s = 0;
+  while (s < c->S) {
+    if (!((valid >> s) & 1)) {
+      ++s;
+      continue;
+    }
+    int e = s;
+    while (e + 1 < c->S && ((valid >> (e + 1)) & 1)) ++e;
+    k.row0[k.n] = s * c->P;
+    k.len[k.n] = (e - s + 1) * c->P;
+    k.tile0[k.n + 1] = k.tile0[k.n] + (k.len[k.n] + 127) / 128;
+    ++k.n;
+    s = e + 1;
+  }
+  return k;
+}
+
+extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, float* x_out) {
+  LIVE(c);
+  if (!x_in || !x_out) return c->fail(VI_E_ARG, "vi_memory_step: NULL x");
+  if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_memory_step: weights not set");
+  if (c->next_layer < 0 || layer != c->next_layer || layer >= c->L)
+    return c->fail(VI_E_PROTOCOL, "vi_memory_step: needs a push, then layers 0..L-1 in order");
+  const int l = layer, n = c->ring.cur_n, M = n * c->P, D = c->D, F = c->F;
+  const int dt = c->bf16 ? 0 : 1;
+  const size_t es = c->es, SP = (size_t)c->S * c->P;
+  void* kl = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * D * es;
+  void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * SP * D * es;
+  const uint64_t valid = c->ring.valid_mask();
+
+  // a3: LN1
+  PLAUNCH(VI_PROF_ROW, launch_layernorm(x_in, c->ln1_g + (size_t)l * D, c->ln1_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln1");
+  // a4: QKV projection + memory write
+  Epi eq = epi_base(EPI_QKV, M, 3 * D, c->b_qkv + (size_t)l * 3 * D);
+  eq.D = D; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
+  eq.S = c->S; eq.P = c->P;
+  if (c->bf16)
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * D, M, 3 * D, D, c->bn_qkv, eq, c->stream), "qkv gemm");
+  else
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_qkv + (size_t)l * 3 * D * D, M, 3 * D, D, eq,
+                                c->stream),
+           "qkv gemm");
+  // a5: memory attention over every valid slot
+  const float scale_log2 = float(1.4426950408889634 / std::sqrt(double(c->hd)));
+  if (c->bf16) {
+    AttnTC a;
+    std::memset(&a, 0, sizeof(a));
+    a.Nq = M; a.hd = c->hd; a.D = D; a.H = c->H; a.krow_base = int(l * SP); a.vrow_base = l * D;
+    a.scale_log2 = scale_log2; a.segs = make_segs(c, valid);
+    const int ntiles = a.segs.tile0[a.segs.n];
+    choose_split(((M + 127) / 128) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
+    a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
+    a.o = static_cast<bf16*>(c->o); a.opart = c->opart; a.lse = c->lse;
+    PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
+    if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
+  } else {
+    AttnArgs a;
+    a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->S; a.valid = valid;
+    a.scale_log2 = scale_log2; a.q = c->q; a.kslab = kl; a.vtslab = vl; a.o = c->o;
+    PLAUNCH(VI_PROF_ATTN, launch_attn_simt_f32(a, c->stream), "attention");
+  }
+  // a7: output projection + residual
+  Epi eo = epi_base(EPI_RESID, M, D, c->b_o + (size_t)l * D);
+  eo.x_in = x_in; eo.x_out = x_out;
+  if (c->bf16)
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream), "o gemm");
+  else
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->o, (const float*)c->w_o + (size_t)l * D * D, M, D, D, eo, c->stream),
+           "o gemm");
+  // a8: LN2
+  PLAUNCH(VI_PROF_ROW, launch_layernorm(x_out, c->ln2_g + (size_t)l * D, c->ln2_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln2");
+  // a9 / a10: FFN1 (+ F3N fold/unfold) + GELU
+  const bool f3n = c->cfg.ffn_kind == VI_FFN_F3N;
+  Epi e1 = epi_base(f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
+  e1.out = f3n ? c->u : c->gbuf; e1.ldo = F;
+  if (c->bf16)
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream), "ffn1 gemm");
+  else
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_1 + (size_t)l * F * D, M, F, D, e1, c->stream),
+           "ffn1 gemm");
+  if (f3n) {
+    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, dt, c->fold_ws, 1, n, c->gf, c->stream), "f3n fold");
+    PLAUNCH(VI_PROF_PATCH, launch_unfold_gelu(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream), "f3n unfold");
+  }
+  // a11: FFN2 + residual
+  Epi e2 = epi_base(EPI_RESID, M, D, c->b_2 + (size_t)l * D);
+  e2.x_in = x_out; e2.x_out = x_out;
+  if (c->bf16)
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, c->tm_w2, l * D, M, D, F, c->bn_2, e2, c->stream), "ffn2 gemm");
+  else
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->gbuf, (const float*)c->w_2 + (size_t)l * D * F, M, D, F, e2,
+                                c->stream),
+           "ffn2 gemm");
+  c->next_layer = layer + 1;
+  if (c->next_layer == c->L) {
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->ring.mark_stepped();
+  }
+  return VI_OK;
+}
+
+extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* feat, int project) {
+  LIVE(c);
+  if (!in || !feat || n < 1 || n > c->Tmax || (project != 0 && project != 1))
+    return c->fail(VI_E_ARG, "vi_soft_composite: bad argument");
+  if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_composite: weights not set");
+  const int dt = c->bf16 ? 0 : 1;
+  const void* tok = in;
+  if (project) {
+    const int M = n * c->P;
+    Epi e = epi_base(EPI_STORE, M, c->Pd, c->b_back);
+    e.out = c->tokens; e.ldo = c->Pd;
+    if (c->bf16) {
+      PLAUNCH(VI_PROF_ROW, launch_cast_bf16((const float*)in, c->xb, (size_t)M * c->D, c->stream), "cast");
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_xb, c->tm_wback, 0, M, c->Pd, c->D, c->bn_back, e, c->stream), "back gemm");
+    } else {
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)in, (const float*)c->w_back, M, c->Pd, c->D, e, c->stream),
+             "back gemm");
+    }
+    tok = c->tokens;
+  }
+  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, dt, feat, dt, n, c->g, c->stream), "fold");
+  return VI_OK;
+}
+
+extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, int64_t* first_id) {
+  LIVE(c);
+  if (!feat || !out || n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_run_step: bad argument");
+  if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_run_step: weights not set");
+  const size_t fbytes = (size_t)n * c->g.H * c->g.W * c->g.C * c->es;
+  const bool hin = is_host_ptr(feat), hout = is_host_ptr(out);
+  const void* fin = feat;
+  if (hin) {
+    CK(cudaMemcpyAsync(c->feat_in, feat, fbytes, cudaMemcpyHostToDevice, c->stream), "run_step h2d");
+    fin = c->feat_in;
+  }
+  vi_status st = vi_memory_push(c, n, first_id, nullptr, nullptr);
+  if (st != VI_OK) return st;
+  if ((st = vi_soft_split(c, fin, n, c->x_ws, 1)) != VI_OK) return st;
+  for (int l = 0; l < c->L; ++l)
+    if ((st = vi_memory_step(c, l, c->x_ws, c->x_ws)) != VI_OK) return st;
+  void* fout = hout ? c->feat_out : out;
+  if ((st = vi_soft_composite(c, c->x_ws, n, fout, 1)) != VI_OK) return st;
+  if (hout) {
+    CK(cudaMemcpyAsync(out, c->feat_out, fbytes, cudaMemcpyDeviceToHost, c->stream), "run_step d2h");
+    CK(cudaStreamSynchronize(c->stream), "run_step sync");
+  }
+  return VI_OK;
+}
+
+extern "C" vi_status vi_sync(vi_ctx* c) {
+  LIVE(c);
+  CK(cudaStreamSynchronize(c->stream), "vi_sync");
+  return VI_OK;
+}
+
+extern "C" vi_status vi_profile(vi_ctx* c, int mode) {
+  LIVE(c);
+  if (mode < 0 || mode > 2) return VI_E_ARG;
+  c->prof_mode = mode;
+  return VI_OK;
+}
+
+extern "C" vi_status vi_profile_read(vi_ctx* c, double* ms, int64_t* launches) {
+  LIVE(c);
+  CK(cudaStreamSynchronize(c->stream), "profile sync");
+  double acc[VI_PROF_N] = {0, 0, 0, 0};
+  int64_t cnt[VI_PROF_N] = {0, 0, 0, 0};
+  for (auto& r : c->prof_recs) {
+    float t = 0.f;
+    if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {
+      acc[r.cat] += t;
+      cnt[r.cat] += 1;
+    } else {
+      cudaGetLastError();
+    }
+    c->ev_pool.push_back(r.a);
+    c->ev_pool.push_back(r.b);
+  }
+  c->prof_recs.clear();
+  for (int i = 0; i < VI_PROF_N; ++i) {
+    if (ms) ms[i] = acc[i];
+    if (launches) launches[i] = cnt[i];
+  }
+  return VI_OK;
+}
+
+extern "C" const char* vi_last_error(const vi_ctx* c) { return c ? c->err.c_str() : "null context"; }
+extern "C" int64_t vi_kernel_launches(const vi_ctx* c) { return c ? c->launches : 0; }
+extern "C" int vi_num_slots(const vi_ctx* c) { return c ? c->S : 0; }
+extern "C" void* vi_stream(const vi_ctx* c) { return c ? (void*)c->stream : nullptr; }
+extern "C" const char* vi_version(void) { return "vi-memstep 0.1 (sm_100a)"; }
+
+extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, void* dst, size_t bytes) {
+  LIVE(c);
+  if (!dst) return VI_E_ARG;
+  const int n = std::max(c->ring.cur_n, 1);
+  const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, SP = (size_t)c->S * c->P;
+  const void* src = nullptr;
+  size_t need = 0;
+  switch (what) {
+    case VI_DBG_TOKENS: src = c->tokens; need = rows * c->Pd * es; break;
+    case VI_DBG_H: src = c->h; need = rows * D * es; break;
+    case VI_DBG_Q: src = c->q; need = rows * D * es; break;
+    case VI_DBG_O: src = c->o; need = rows * D * es; break;
+    case VI_DBG_U: src = c->cfg.ffn_kind == VI_FFN_F3N ? c->u : c->gbuf; need = rows * c->F * es; break;
+    case VI_DBG_G: src = c->gbuf; need = rows * c->F * es; break;
+    case VI_DBG_K:
+    case VI_DBG_V: need = (size_t)c->P * D * es; break;
+    default: return VI_E_ARG;
+  }
+  if (bytes != need) return c->fail(VI_E_SHAPE, "vi_debug_read: byte count mismatch");
+  if ((what == VI_DBG_K || what == VI_DBG_V) && (layer < 0 || layer >= c->L || slot < 0 || slot >= c->S))
+    return VI_E_ARG;
+  CK(cudaStreamSynchronize(c->stream), "debug sync");
+  if (what == VI_DBG_K) {
+    src = static_cast<const uint8_t*>(c->kslab) + ((size_t)layer * SP + (size_t)slot * c->P) * D * es;
+    CK(cudaMemcpy(dst, src, need, cudaMemcpyDefault), "debug copy");
+  } else if (what == VI_DBG_V) {
+    // Vt [D][S*P] columns slot*P.. -> [P][D]
+    std::vector<uint8_t> tmp(need);
+    const uint8_t* base = static_cast<const uint8_t*>(c->vtslab) + ((size_t)layer * D * SP + (size_t)slot * c->P) * es;
+    CK(cudaMemcpy2D(tmp.data(), c->P * es, base, SP * es, c->P * es, D, cudaMemcpyDeviceToHost), "debug copy V");
+    std::vector<uint8_t> tr(need);
+    for (size_t d = 0; d < D; ++d)
+      for (int p = 0; p < c->P; ++p) std::memcpy(&tr[((size_t)p * D + d) * es], &tmp[(d * c->P + p) * es], es);
+    CK(cudaMemcpy(dst, tr.data(), need, cudaMemcpyDefault), "debug copy V");
+  } else {
+    CK(cudaMemcpy(dst, src, need, cudaMemcpyDefault), "debug copy");
+  }
+  return VI_OK;
+}

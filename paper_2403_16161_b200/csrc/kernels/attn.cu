@@ -1,0 +1,382 @@
+// Memory attention: per head h,
+//   O_h = softmax(Q_h K_h^T / sqrt(d)) V_h
+// where the queries are the new frames only and the keys/values are the rows
+// of every VALID slot of the layer's ring-buffer memory: the chunk itself plus the
+// resident frames f-M .. f-1 (Eq. 3).  Softmax is exact (max-subtracted,
+// online over key tiles; reading Q14), key order = slot order (permutation invariant).
+//
+// attn_tc_kernel (bf16, sm_100a tensor cores), one CTA = (128-query tile, head, KV split):
+//   warp 0 lane 0 : TMA producer -- Q tile once, then K tiles [128 keys][d] and
+//                   transposed-V tiles [d][128 keys] through a 2-stage ring
+//   warp 1 lane 0 : MMA issuer -- S_b = Q K^T (tcgen05, M=128 N=128, TMEM, double-
+//                   buffered b = 0/1) and O += P V (M=128, N=d, TMEM)
+//   warp 2        : TMEM allocator (512 columns: S0 | S1 | O)
+//   warps 4..7    : softmax -- thread i owns query row i (TMEM lane i): tcgen05.ld of
+//                   its S row, mask, running max / sum in the log2 domain (ex2), P to
+//                   shared memory in the 128B-swizzled K-major layout the MMA reads,
+//                   O rescale in TMEM when the running max grows, final 1/l epilogue.
+// QK^T of tile j+1 runs on the tensor core while the softmax of tile j runs.
+// KV splits write normalised fp32 partials + log2-sum-exp; attn_combine_kernel merges
+// them in a fixed order (deterministic, no atomics).
+#include "kernels.h"
+
+namespace vi {
+
+// ------------------------------------------------------------------ SIMT fp32 path
+__global__ void attn_simt_f32_kernel(AttnArgs a) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= a.Nq * a.H) return;
+  const int q = warp / a.H, h = warp - q * a.H;
+  const int R = a.hd / 32;                    // hd % 32 == 0, hd <= 128
+  const float* Q = reinterpret_cast<const float*>(a.q) + (size_t)q * a.D + h * a.hd;
+  const float* K = reinterpret_cast<const float*>(a.kslab);
+  const float* Vt = reinterpret_cast<const float*>(a.vtslab);
+  const size_t ld = (size_t)a.S * a.P;
+  float qv[4], acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int i = 0; i < R; ++i) qv[i] = Q[lane + 32 * i];
+  float m = -INFINITY, l = 0.f;
+  for (int s = 0; s < a.S; ++s) {
+    if (!((a.valid >> s) & 1ull)) continue;
+    for (int p = 0; p < a.P; ++p) {
+      const size_t row = (size_t)s * a.P + p;
+      const float* kr = K + row * a.D + h * a.hd;
+      float dot = 0.f;
+      for (int i = 0; i < R; ++i) dot = fmaf(qv[i], kr[lane + 32 * i], dot);
+#pragma unroll
+      for (int o = 16; o; o >>= 1) dot += __shfl_xor_sync(0xffffffffu, dot, o);
+      const float sc = dot * a.scale_log2;
+      const float mn = fmaxf(m, sc);
+      const float alpha = exp2f(m - mn), pe = exp2f(sc - mn);
+      l = l * alpha + pe;
+      for (int i = 0; i < R; ++i) acc[i] = acc[i] * alpha + pe * Vt[(size_t)(h * a.hd + lane + 32 * i) * ld + row];
+      m = mn;
+    }
+  }
+  float* O = reinterpret_cast<float*>(a.o) + (size_t)q * a.D + h * a.hd;
+  for (int i = 0; i < R; ++i) O[lane + 32 * i] = acc[i] / l;
+}
+
+cudaError_t launch_attn_simt_f32(const AttnArgs& a, cudaStream_t st) {
+  const int warps = a.Nq * a.H;
+  attn_simt_f32_kernel<<<(warps * 32 + 255) / 256, 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+// ------------------------------------------------------------------ tcgen05 bf16 path
+template <int HD>
+struct AttnSmem {
+  static constexpr int ST = 2;
+  static constexpr int QB = 128 * HD * 2;       // Q tile: HD/64 atoms of [128 rows][128 B]
+  static constexpr int KB = 128 * HD * 2;       // K tile: same layout (128 key rows)
+  static constexpr int VB = HD * 128 * 2;       // Vt tile: 2 atoms (keys 0-63 | 64-127) of [HD rows][128 B]
+  static constexpr int PB = 128 * 128 * 2;      // P tile: 2 atoms of [128 rows][128 B]
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = QB;
+  static constexpr int V_OFF = K_OFF + ST * KB;
+  static constexpr int P_OFF = V_OFF + ST * VB;
+  static constexpr int BAR_OFF = P_OFF + PB;
+  static constexpr int NBAR = 1 + 2 * ST + 2 * ST + 2 + 2 + 1 + 1;
+  static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
+};
+
+__device__ __forceinline__ void key_tile(const KeySegs& s, int g, int& row0, int& nvalid) {
+  int i = 0;
+  while (i + 1 < s.n && g >= s.tile0[i + 1]) ++i;
+  const int off = (g - s.tile0[i]) * 128;
+  row0 = s.row0[i] + off;
+  const int rem = s.len[i] - off;
+  nvalid = rem < 128 ? rem : 128;
+}
+
+template <int HD>
+__global__ void __launch_bounds__(256, 1)
+attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+               const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
+  using L = AttnSmem<HD>;
+  constexpr int ST = L::ST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + ST;
+  uint64_t* v_full = k_empty + ST;
+  uint64_t* v_empty = v_full + ST;
+  uint64_t* s_full = v_empty + ST;
+  uint64_t* s_empty = s_full + 2;
+  uint64_t* p_full = s_empty + 2;
+  uint64_t* o_done = p_full + 1;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = blockIdx.x * 128, h = blockIdx.y, z = blockIdx.z;
+  const int ntiles = a.segs.tile0[a.segs.n];
+  const int t_begin = z * a.tiles_per_split;
+  int t_end = t_begin + a.tiles_per_split;
+  if (t_end > ntiles) t_end = ntiles;
+  const int n = t_end > t_begin ? t_end - t_begin : 0;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tq);
+    tma_prefetch(&tk);
+    tma_prefetch(&tvt);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&s_full[b], 1);
+      mbar_init(&s_empty[b], 128);
+    }
+    mbar_init(p_full, 128);
+    mbar_init(o_done, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t TM_S = tmem, TM_O = tmem + 256;
+
+  if (warp == 0) {
+    if (lane == 0 && n > 0) {
+      uint8_t* sq = smem + L::Q_OFF;
+      mbar_arrive_expect_tx(q_full, L::QB);
+#pragma unroll
+      for (int at = 0; at < HD / 64; ++at) tma_load_2d(sq + at * 16384, &tq, q_full, h * HD + at * 64, q0);
+      for (int jj = 0; jj < n; ++jj) {
+        int row0, nv;
+        key_tile(a.segs, t_begin + jj, row0, nv);
+        const int st = jj % ST;
+        const uint32_t par = ((jj / ST) & 1) ^ 1;
+        if (jj >= ST) mbar_wait(&k_empty[st], par);
+        uint8_t* sk = smem + L::K_OFF + st * L::KB;
+        mbar_arrive_expect_tx(&k_full[st], L::KB);
+#pragma unroll
+        for (int at = 0; at < HD / 64; ++at)
+          tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + row0);
+        if (jj >= ST) mbar_wait(&v_empty[st], par);
+        uint8_t* sv = smem + L::V_OFF + st * L::VB;
+        mbar_arrive_expect_tx(&v_full[st], L::VB);
+#pragma unroll
+        for (int at = 0; at < 2; ++at)
+          tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], row0 + at * 64, a.vrow_base + h * HD);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0 && n > 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD);
+      const uint32_t sq = smem_u32(smem + L::Q_OFF);
+      const uint32_t sp = smem_u32(smem + L::P_OFF);
+      mbar_wait(q_full, 0);
+      auto issue_qk = [&](int t) {
+        const int st = t % ST, b = t & 1;
+        mbar_wait(&k_full[st], (t / ST) & 1);
+        if (t >= 2) mbar_wait(&s_empty[b], ((t >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t sk = smem_u32(smem + L::K_OFF + st * L::KB);
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16_ss(TM_S + b * 128, sdesc_k_sw128(sq + off), sdesc_k_sw128(sk + off), idesc_s, kk > 0);
+        }
+        umma_commit(&k_empty[st]);
+        umma_commit(&s_full[b]);
+      };
+      issue_qk(0);
+      for (int jj = 0; jj < n; ++jj) {
+        if (jj + 1 < n) issue_qk(jj + 1);
+        const int st = jj % ST;
+        mbar_wait(p_full, jj & 1);
+        mbar_wait(&v_full[st], (jj / ST) & 1);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + L::V_OFF + st * L::VB);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t offp = (kk >> 2) * 16384 + (kk & 3) * 32;
+          const uint32_t offv = (kk >> 2) * (HD * 128) + (kk & 3) * 32;
+          umma_bf16_ss(TM_O, sdesc_k_sw128(sp + offp), sdesc_k_sw128(sv + offv), idesc_o, (jj | kk) != 0);
+        }
+        umma_commit(&v_empty[st]);
+        umma_commit(o_done);
+      }
+    }
+  } else if (warp >= 4) {
+    const int qd = warp - 4;
+    const int row = qd * 32 + lane;                 // query row inside the tile == TMEM lane
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    uint8_t* sp = smem + L::P_OFF;
+    float m = -INFINITY, l = 0.f;
+    for (int jj = 0; jj < n; ++jj) {
+      const int b = jj & 1;
+      int row0, nv;
+      key_tile(a.segs, t_begin + jj, row0, nv);
+      mbar_wait(&s_full[b], (jj >> 1) & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(TM_S + lane_off + b * 128 + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(&s_empty[b]);
+      float mx = -INFINITY;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        if (i >= nv) s[i] = -INFINITY;
+        mx = fmaxf(mx, s[i]);
+      }
+      const float m_new = fmaxf(m, mx * a.scale_log2);
+      const float alpha = ex2(m - m_new);
+      float sum = 0.f;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        const float p = ex2(fmaf(s[i], a.scale_log2, -m_new));
+        s[i] = p;
+        sum += p;
+      }
+      l = l * alpha + sum;
+      if (jj > 0) {
+        mbar_wait(o_done, (jj - 1) & 1);              // PV(jj-1) done: O stable, P buffer free
+        tc_fence_after();
+        if (alpha < 1.f) {
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 16) {
+            uint32_t r[16];
+            tmem_ld16(TM_O + lane_off + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st16(TM_O + lane_off + c, r);
+          }
+          tmem_wait_st();
+        }
+      }
+      // P row -> smem, K-major, 128-byte swizzle: 16-byte chunk c of row r sits at c ^ (r & 7)
+#pragma unroll
+      for (int at = 0; at < 2; ++at) {
+        uint8_t* base = sp + at * 16384 + row * 128;
+#pragma unroll
+        for (int c = 0; c < 8; ++c) {
+          const float* p = s + at * 64 + c * 8;
+          *reinterpret_cast<uint4*>(base + ((c ^ (row & 7)) << 4)) =
+              make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
+        }
+      }
+      fence_proxy_async_smem();
+      tc_fence_before();
+      mbar_arrive(p_full);
+      m = m_new;
+    }
+    // epilogue
+    const int q = q0 + row;
+    if (n > 0) {
+      mbar_wait(o_done, (n - 1) & 1);
+      tc_fence_after();
+    }
+    const float inv = n > 0 ? 1.f / l : 0.f;
+    if (a.nsplit == 1) {
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 16) {
+        uint32_t r[16];
+        tmem_ld16(TM_O + lane_off + c, r);
+        tmem_wait_ld();
+        if (q < a.Nq) {
+          float* f = reinterpret_cast<float*>(r);
+          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.D + h * HD + c);
+          dst[0] = make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
+                              pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
+          dst[1] = make_uint4(pack_bf16(f[8] * inv, f[9] * inv), pack_bf16(f[10] * inv, f[11] * inv),
+                              pack_bf16(f[12] * inv, f[13] * inv), pack_bf16(f[14] * inv, f[15] * inv));
+        }
+      }
+    } else {
+      float* op = a.opart + ((size_t)z * a.Nq + q) * a.D + h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 16) {
+        uint32_t r[16];
+        if (n > 0) {
+          tmem_ld16(TM_O + lane_off + c, r);
+          tmem_wait_ld();
+        }
+        if (q < a.Nq) {
+          float4* dst = reinterpret_cast<float4*>(op + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = n > 0 ? make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                         __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (q < a.Nq) a.lse[((size_t)z * a.H + h) * a.Nq + q] = n > 0 ? m + __log2f(l) : -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int HD>
+static cudaError_t launch_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                             cudaStream_t st) {
+  using L = AttnSmem<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((a.Nq + 127) / 128, a.H, a.nsplit);
+  attn_tc_kernel<HD><<<grid, 256, L::TOTAL, st>>>(tq, tk, tvt, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                           cudaStream_t st) {
+  if (a.hd == 128) return launch_hd<128>(tq, tk, tvt, a, st);
+  if (a.hd == 64) return launch_hd<64>(tq, tk, tvt, a, st);
+  return cudaErrorInvalidValue;
+}
+
+// Merge KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), fixed order.
+__global__ void attn_combine_kernel(const AttnTC a) {
+  const int hd4 = a.hd / 4;
+  const size_t total = (size_t)a.Nq * a.H * hd4;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    const int c4 = int(i % hd4);
+    const size_t r = i / hd4;
+    const int h = int(r % a.H);
+    const int q = int(r / a.H);
+    float mx = -INFINITY;
+    for (int z = 0; z < a.nsplit; ++z) mx = fmaxf(mx, a.lse[((size_t)z * a.H + h) * a.Nq + q]);
+    float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+    for (int z = 0; z < a.nsplit; ++z) {
+      const float lz = a.lse[((size_t)z * a.H + h) * a.Nq + q];
+      if (lz == -INFINITY) continue;
+      const float w = exp2f(lz - mx);
+      wsum += w;
+      const float4 v = *reinterpret_cast<const float4*>(a.opart + ((size_t)z * a.Nq + q) * a.D + h * a.hd + c4 * 4);
+      acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
+    }
+    const float inv = 1.f / wsum;
+    uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)q * a.D + h * a.hd + c4 * 4);
+    *dst = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+  }
+}
+
+cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st) {
+  const size_t total = (size_t)a.Nq * a.H * (a.hd / 4);
+  size_t blocks = (total + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  attn_combine_kernel<<<unsigned(blocks ? blocks : 1), 256, 0, st>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace vi

@@ -1,0 +1,137 @@
+// GEMM epilogues of the memory step.
+// C[m][n] = sum_k A[m][k] * W[n][k]  (fp32 accumulate), then one of:
+//   EPI_STORE   out[m][n] = C + bias[n] (+ pos[m % P][n])        -> T_out (bf16 or fp32)
+//   EPI_GELU    out[m][n] = GELU_erf(C + bias[n])                -> T_out
+//   EPI_RESID   x_out[m][n] = x_in[m][n] + C + bias[n]           (fp32 residual stream)
+//   EPI_QKV     n <  D : Q[m][n] = C + b
+//               n < 2D : K slab row (slot(t)*P + p), col n-D     (the memory write)
+//               else   : Vt slab [D][S*P] column (slot(t)*P + p) (V stored transposed)
+//               with m = t*P + p, slot(t) = (first_slot + t) % S.
+#pragma once
+#include "common.cuh"
+
+namespace vi {
+
+enum EpiKind : int { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_QKV = 3 };
+
+struct Epi {
+  int kind;
+  int M, N;
+  const float* bias;      // [N]
+  void* out;              // EPI_STORE / EPI_GELU
+  int ldo;
+  int out_f32;            // EPI_STORE: 1 = write fp32 (the residual stream x0), 0 = ctx dtype
+  const float* pos;       // EPI_STORE optional, [P][N]
+  int P;
+  const float* x_in;      // EPI_RESID
+  float* x_out;
+  int D;                  // EPI_QKV
+  void* q;                // [M][D]
+  void* kslab;            // [S*P][D] (this layer)
+  void* vtslab;           // [D][S*P] (this layer)
+  int first_slot, S;
+};
+
+template <typename T>
+__device__ __forceinline__ void epi_one(const Epi& e, int m, int n, float acc) {
+  float v = acc + (e.bias ? e.bias[n] : 0.f);
+  switch (e.kind) {
+    case EPI_STORE:
+      if (e.pos) v += e.pos[(size_t)(m % e.P) * e.N + n];
+      if (e.out_f32)
+        reinterpret_cast<float*>(e.out)[(size_t)m * e.ldo + n] = v;
+      else
+        reinterpret_cast<T*>(e.out)[(size_t)m * e.ldo + n] = from_f<T>(v);
+      break;
+    case EPI_GELU:
+      reinterpret_cast<T*>(e.out)[(size_t)m * e.ldo + n] = from_f<T>(gelu_erf(v));
+      break;
+    case EPI_RESID:
+      e.x_out[(size_t)m * e.N + n] = e.x_in[(size_t)m * e.N + n] + v;
+      break;
+    default: {
+      const int t = m / e.P, p = m - t * e.P;
+      const size_t row = (size_t)((e.first_slot + t) % e.S) * e.P + p;
+      if (n < e.D) {
+        reinterpret_cast<T*>(e.q)[(size_t)m * e.D + n] = from_f<T>(v);
+      } else if (n < 2 * e.D) {
+        reinterpret_cast<T*>(e.kslab)[row * e.D + (n - e.D)] = from_f<T>(v);
+      } else {
+        reinterpret_cast<T*>(e.vtslab)[(size_t)(n - 2 * e.D) * ((size_t)e.S * e.P) + row] = from_f<T>(v);
+      }
+    }
+  }
+}
+
+// 32 consecutive columns n0..n0+31 of row m (tensor-core epilogue; one thread per row).
+__device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, float* v) {
+  if (m >= e.M) return;
+  const bool full = (n0 + 32 <= e.N);
+  if (!full) {
+    for (int i = 0; i < 32 && n0 + i < e.N; ++i) epi_one<bf16>(e, m, n0 + i, v[i]);
+    return;
+  }
+  if (e.bias) {
+    const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      float4 b = __ldg(b4 + i);
+      v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
+    }
+  }
+  switch (e.kind) {
+    case EPI_STORE:
+    case EPI_GELU: {
+      if (e.kind == EPI_GELU) {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+      } else if (e.pos) {
+        const float* pr = e.pos + (size_t)(m % e.P) * e.N + n0;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] += pr[i];
+      }
+      if (e.out_f32) {
+        float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)m * e.ldo + n0);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) d4[i] = make_float4(v[4 * i], v[4 * i + 1], v[4 * i + 2], v[4 * i + 3]);
+        break;
+      }
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<bf16*>(e.out) + (size_t)m * e.ldo + n0);
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                            pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+      break;
+    }
+    case EPI_RESID: {
+      const float4* xi = reinterpret_cast<const float4*>(e.x_in + (size_t)m * e.N + n0);
+      float4* xo = reinterpret_cast<float4*>(e.x_out + (size_t)m * e.N + n0);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        float4 a = xi[i];
+        xo[i] = make_float4(a.x + v[4 * i], a.y + v[4 * i + 1], a.z + v[4 * i + 2], a.w + v[4 * i + 3]);
+      }
+      break;
+    }
+    default: {  // EPI_QKV; a 32-column group never straddles Q/K/V (D % 32 == 0)
+      const int t = m / e.P, p = m - t * e.P;
+      const size_t row = (size_t)((e.first_slot + t) % e.S) * e.P + p;
+      if (n0 < 2 * e.D) {
+        bf16* base = (n0 < e.D) ? reinterpret_cast<bf16*>(e.q) + (size_t)m * e.D + n0
+                                : reinterpret_cast<bf16*>(e.kslab) + row * e.D + (n0 - e.D);
+        uint4* dst = reinterpret_cast<uint4*>(base);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(v[8 * i], v[8 * i + 1]), pack_bf16(v[8 * i + 2], v[8 * i + 3]),
+                              pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
+      } else {
+        bf16* vt = reinterpret_cast<bf16*>(e.vtslab);
+        const size_t ld = (size_t)e.S * e.P;
+#pragma unroll
+        for (int i = 0; i < 32; ++i) vt[(size_t)(n0 - 2 * e.D + i) * ld + row] = __float2bfloat16_rn(v[i]);
+      }
+    }
+  }
+}
+
+}  // namespace vi

@@ -1,0 +1,131 @@
+// tcgen05 GEMM with fused epilogues: C[M][N] = A[M][K] * W[N][K]^T (bf16 in, fp32 acc).
+//
+// One CTA computes a 128 x BN tile.  Warp roles (256 threads):
+//   warp 0, lane 0 : TMA producer  (A box 64x128, W box 64xBN, 128-byte swizzle)
+//   warp 1, lane 0 : MMA issuer    (tcgen05.mma kind::f16, M=128, N=BN, K=16 per instr)
+//   warp 2         : TMEM allocator (BN fp32 columns)
+//   warps 4..7     : epilogue      (tcgen05.ld 32x32b, thread = accumulator row)
+// An STAGES-deep smem ring with full/empty mbarriers decouples TMA from the MMAs;
+// tcgen05.commit releases a stage when the MMAs that read it are done.
+#include "epilogue.cuh"
+#include "kernels.h"
+
+namespace vi {
+
+template <int BN, int STAGES>
+struct GemmSmem {
+  static constexpr int A_BYTES = 128 * 64 * 2;
+  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
+  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
+  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 1) * 8 + 16 + 1024;  // +1024 alignment slack
+};
+
+template <int BN, int STAGES>
+__global__ void __launch_bounds__(256, 1)
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int brow0, Epi epi) {
+  using L = GemmSmem<BN, STAGES>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* empty = full + STAGES;
+  uint64_t* tmem_full = empty + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tmem_full + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * 128, n0 = blockIdx.y * BN;
+  const int nk = (K + 63) / 64;
+  constexpr uint32_t TMEM_COLS = BN < 32 ? 32 : BN;
+
+  if (warp == 0 && lane == 0) {
+    tma_prefetch(&tmA);
+    tma_prefetch(&tmB);
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(tmem_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        if (kb >= STAGES) mbar_wait(&empty[s], ((kb / STAGES) & 1) ^ 1);
+        uint8_t* sa = smem + s * L::STAGE_BYTES;
+        mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+        tma_load_2d(sa, &tmA, &full[s], kb * 64, m0);
+        tma_load_2d(sa + L::A_BYTES, &tmB, &full[s], kb * 64, brow0 + n0);
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+      for (int kb = 0; kb < nk; ++kb) {
+        const int s = kb % STAGES;
+        mbar_wait(&full[s], (kb / STAGES) & 1);
+        tc_fence_after();
+        const uint32_t a = smem_u32(smem + s * L::STAGE_BYTES);
+        const uint32_t b = a + L::A_BYTES;
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          umma_bf16_ss(tmem, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
+        umma_commit(&empty[s]);
+      }
+      umma_commit(tmem_full);
+    }
+  } else if (warp >= 4) {
+    const int q = warp - 4;                      // TMEM lane quadrant of this warp
+    mbar_wait(tmem_full, 0);
+    tc_fence_after();
+    const int m = m0 + q * 32 + lane;
+#pragma unroll 1
+    for (int c = 0; c < BN; c += 32) {
+      if (n0 + c >= epi.N) break;
+      uint32_t r[32];
+      tmem_ld32(tmem + (uint32_t(q * 32) << 16) + c, r);
+      tmem_wait_ld();
+      epi_row32_bf16(epi, m, n0 + c, reinterpret_cast<float*>(r));
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    tc_fence_after();
+    tmem_dealloc(tmem, TMEM_COLS);
+  }
+}
+
+template <int BN, int STAGES>
+static cudaError_t launch_bn(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
+                             const Epi& e, cudaStream_t st) {
+  using L = GemmSmem<BN, STAGES>;
+  auto kfn = gemm_tc_kernel<BN, STAGES>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (err != cudaSuccess) return err;
+    configured = true;
+  }
+  dim3 grid((M + 127) / 128, (N + BN - 1) / BN);
+  kfn<<<grid, 256, L::TOTAL, st>>>(a, b, K, brow0, e);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K, int bn,
+                           const Epi& e, cudaStream_t st) {
+  switch (bn) {
+    case 64: return launch_bn<64, 6>(a, b, brow0, M, N, K, e, st);
+    case 128: return launch_bn<128, 4>(a, b, brow0, M, N, K, e, st);
+    case 256: return launch_bn<256, 3>(a, b, brow0, M, N, K, e, st);
+    default: return cudaErrorInvalidValue;
+  }
+}
+
+}  // namespace vi

@@ -1,0 +1,74 @@
+// Host-side launchers of the sm_100a kernels (internal to libvi.so).
+#pragma once
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include "epilogue.cuh"
+
+namespace vi {
+
+struct Geom {
+  int H, W, C, kh, kw, sh, sw, ph, pw, oh, ow;
+};
+
+// ---- patch gather kernels (HBM-bound) -------------------
+// soft split: in [n][H][W][C] -> out [n][P][kh*kw*C]; dtype 0 = bf16, 1 = fp32.
+cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st);
+// F3N second half: folded fp32 [n][H][W][Cf] -> GELU(unfold) bf16/fp32 [n][P][kh*kw*Cf]
+cudaError_t launch_unfold_gelu(const float* in, void* out, int n, const Geom& g, int out_dtype, cudaStream_t st);
+// fold with cover-count division: in [n][P][kh*kw*C] (in_dtype) -> out [n][H][W][C] (out_dtype)
+cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g,
+                        cudaStream_t st);
+
+// ---- row kernels -------------------------------------------------------------------
+// LayerNorm over D (eps 1e-5), fp32 in, out dtype 0 bf16 / 1 fp32.
+cudaError_t launch_layernorm(const float* x, const float* g, const float* b, void* out, int out_dtype, int rows,
+                             int D, cudaStream_t st);
+cudaError_t launch_cast_bf16(const float* x, void* out, size_t n, cudaStream_t st);
+cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D, size_t ld, size_t col0, int dtype,
+                                     cudaStream_t st);
+
+// ---- GEMMs ---------------------------------------------------------------------------
+// tensor cores (bf16): A [M][K] and W [N][K] described by 2-D TMA maps with 64 x 128 /
+// 64 x BN boxes and 128-byte swizzle.
+// brow0: row offset of this layer's weight block inside the stacked W map.
+cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& w, int brow0, int M, int N, int K, int bn,
+                           const Epi& e, cudaStream_t st);
+// SIMT (fp32 path): A [M][K], W [N][K] row-major fp32, FFMA accumulate.
+cudaError_t launch_gemm_simt_f32(const float* A, const float* W, int M, int N, int K, const Epi& e, cudaStream_t st);
+
+// ---- attention -----------------------------------------------------------------------
+struct KeySegs {            // contiguous runs of valid ring slots, as slab row ranges
+  int n;
+  int row0[32];
+  int len[32];
+  int tile0[33];            // prefix count of 128-key tiles per segment
+};
+
+struct AttnArgs {
+  int Nq, D, H, hd, P, S;
+  uint64_t valid;           // slot validity mask
+  float scale_log2;         // log2(e) / sqrt(hd)
+  const void* q;            // [Nq][D]
+  const void* kslab;        // [S*P][D]        (this layer)
+  const void* vtslab;       // [D][S*P]        (this layer)
+  void* o;                  // [Nq][D]
+};
+cudaError_t launch_attn_simt_f32(const AttnArgs& a, cudaStream_t st);
+
+struct AttnTC {
+  int Nq, hd, D, krow_base, vrow_base;   // row offsets of this layer inside the 2-D slab maps
+  int nsplit, tiles_per_split;
+  float scale_log2;
+  KeySegs segs;
+  bf16* o;                  // [Nq][D] final (nsplit == 1)
+  float* opart;             // [nsplit][Nq][D] normalised partial outputs (nsplit > 1)
+  float* lse;               // [nsplit][H][Nq] log2-sum-exp of the partials
+  int H;
+};
+cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                           cudaStream_t st);
+cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st);
+
+}  // namespace vi

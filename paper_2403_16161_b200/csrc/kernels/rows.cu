@@ -1,0 +1,102 @@
+// Row kernels: pre-norm LayerNorm (reading Q1, eps 1e-5), fp32 -> bf16 cast, and the
+// V transpose used by refine commits (the memory stores V transposed, [D][S*P]).
+#include "kernels.h"
+
+namespace vi {
+
+// One warp per row; D <= 1024 and D % 32 == 0.  Two-pass mean / variance in registers.
+template <typename Tout, int PER>
+__global__ void layernorm_kernel(const float* __restrict__ x, const float* __restrict__ g,
+                                 const float* __restrict__ b, Tout* __restrict__ out, int rows, int D) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float* xr = x + (size_t)warp * D;
+  float v[PER];
+  float s = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = i * 32 + lane;
+    v[i] = c < D ? xr[c] : 0.f;
+    s += v[i];
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  const float mu = s / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = i * 32 + lane;
+    const float d = c < D ? v[i] - mu : 0.f;
+    q += d * d;
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / D + 1e-5f);
+  Tout* orow = out + (size_t)warp * D;
+#pragma unroll
+  for (int i = 0; i < PER; ++i) {
+    const int c = i * 32 + lane;
+    if (c < D) orow[c] = from_f<Tout>((v[i] - mu) * rstd * g[c] + b[c]);
+  }
+}
+
+cudaError_t launch_layernorm(const float* x, const float* g, const float* b, void* out, int out_dtype, int rows,
+                             int D, cudaStream_t st) {
+  const int blocks = (rows * 32 + 255) / 256;
+#define LN_CASE(PER)                                                                                   \
+  if (D <= PER * 32) {                                                                                 \
+    if (out_dtype == 0)                                                                                \
+      layernorm_kernel<bf16, PER><<<blocks, 256, 0, st>>>(x, g, b, (bf16*)out, rows, D);               \
+    else                                                                                               \
+      layernorm_kernel<float, PER><<<blocks, 256, 0, st>>>(x, g, b, (float*)out, rows, D);             \
+    return cudaGetLastError();                                                                         \
+  }
+  LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(16) LN_CASE(32)
+#undef LN_CASE
+  return cudaErrorInvalidValue;
+}
+
+__global__ void cast_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ out, size_t n4) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
+    float4 v = x[i];
+    out[i] = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+  }
+}
+
+cudaError_t launch_cast_bf16(const float* x, void* out, size_t n, cudaStream_t st) {
+  const size_t n4 = n / 4;
+  size_t blocks = (n4 + 255) / 256;
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  if (!blocks) blocks = 1;
+  cast_bf16_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<uint2*>(out),
+                                                     n4);
+  return cudaGetLastError();
+}
+
+// v [P][D] -> vt[d][col0 + p] (row pitch ld elements), 32x32 smem tiles.
+template <typename T>
+__global__ void transpose_kernel(const T* __restrict__ v, T* __restrict__ vt, int P, int D, size_t ld, size_t col0) {
+  __shared__ T tile[32][33];
+  const int p0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int p = p0 + i, d = d0 + threadIdx.x;
+    if (p < P && d < D) tile[i][threadIdx.x] = v[(size_t)p * D + d];
+  }
+  __syncthreads();
+  for (int i = threadIdx.y; i < 32; i += 8) {
+    const int d = d0 + i, p = p0 + threadIdx.x;
+    if (p < P && d < D) vt[(size_t)d * ld + col0 + p] = tile[threadIdx.x][i];
+  }
+}
+
+cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D, size_t ld, size_t col0, int dtype,
+                                     cudaStream_t st) {
+  dim3 grid((P + 31) / 32, (D + 31) / 32), block(32, 8);
+  if (dtype == 0)
+    transpose_kernel<bf16><<<grid, block, 0, st>>>((const bf16*)v, (bf16*)vt_slab, P, D, ld, col0);
+  else
+    transpose_kernel<float><<<grid, block, 0, st>>>((const float*)v, (float*)vt_slab, P, D, ld, col0);
+  return cudaGetLastError();
+}
+
+}  // namespace vi

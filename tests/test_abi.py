@@ -1,0 +1,116 @@
+"""C-ABI checks that need no GPU: libvi.so loads, exports every symbol include/vi.h
+declares, and its integer ring bookkeeping matches the oracle's set model bit-exactly."""
+import json
+import os
+import random
+import re
+import subprocess
+
+import pytest
+
+from oracle import vi_oracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.fixture(scope="module")
+def V():
+    from paper_2403_16161_b200 import build
+    build.build()
+    from paper_2403_16161_b200 import vi
+    return vi
+
+
+def header_symbols():
+    src = open(os.path.join(ROOT, "include", "vi.h")).read()
+    return sorted(set(re.findall(r"^\s*(?:vi_status|const char\*|int64_t|int|void\*)\s+(vi_\w+)\s*\(", src, re.M)))
+
+
+def test_library_exports_every_header_symbol(V):
+    syms = header_symbols()
+    assert len(syms) >= 25, syms
+    out = subprocess.run(["nm", "-D", "--defined-only", V.LIB_PATH], capture_output=True, text=True).stdout
+    exported = set(re.findall(r"\bT (vi_\w+)", out))
+    missing = [s for s in syms if s not in exported]
+    assert not missing, missing
+    assert set(V.EXPORTS) == set(syms)
+    assert "sm_100a" in V.version()
+
+
+def test_library_is_sm100a_tensor_core_code(V):
+    sass = subprocess.run(["/usr/local/cuda/bin/cuobjdump", "-sass", V.LIB_PATH], capture_output=True,
+                          text=True).stdout
+    assert "UTCHMMA" in sass          # tcgen05.mma
+    assert "UTMALDG" in sass          # TMA tensor loads
+    assert "LDTM" in sass             # tcgen05.ld (TMEM -> registers)
+    assert "HMMA" not in sass.replace("UTCHMMA", "")   # no legacy mma.sync path
+
+
+def test_ring_goldens_through_abi(V):
+    g = json.load(open(os.path.join(ROOT, "tests", "golden", "ring_trace.json")))
+    r = V.Ring(g["M"], g["T_max"])
+    S = g["M"] + g["T_max"]
+    for op in g["ops"]:
+        if op["op"] == "push":
+            first, ev = r.push(op["n"])
+            assert (first, ev) == (op["first"], op["evicted"])
+            _, ref, mask = r.state()
+            assert mask == int(op["mask"], 16)
+            if "refined_slots" in op:
+                assert [i for i in range(S) if ref[i]] == op["refined_slots"]
+        elif op["op"] == "commit":
+            assert r.commit(op["id"]) == op["status"]
+        else:
+            assert r.evict(op["id"]) == op["status"]
+
+
+def test_ring_matches_oracle_set_model_random_traces(V):
+    rnd = random.Random(1234)
+    for trial in range(400):
+        M, T = rnd.randint(0, 20), rnd.randint(1, 8)
+        r, m = V.Ring(M, T), O.OracleMemory(M, T)
+        for step in range(60):
+            x = rnd.random()
+            if x < 0.45:
+                n = rnd.randint(1, T)
+                assert r.push(n) == m.push(n)
+            elif x < 0.6:
+                r.mark_stepped(); m.mark_stepped()
+            elif x < 0.8:
+                fid = rnd.randint(-1, m.next_id + 1)
+                assert r.evict(fid) == m.evict(fid), (trial, step, fid)
+            else:
+                fid = rnd.randint(-1, m.next_id + 1)
+                assert r.commit(fid) == m.commit(fid, None), (trial, step, fid)
+            assert r.state() == tuple(list(x) if isinstance(x, list) else x for x in m.state())
+
+
+def test_ring_rejects_bad_arguments(V):
+    with pytest.raises(V.ViError):
+        V.Ring(60, 5)                  # S > 64
+    r = V.Ring(3, 2)
+    with pytest.raises(V.ViError):
+        r.push(3)
+    with pytest.raises(V.ViError):
+        r.push(0)
+
+
+def test_create_without_gpu_fails_loudly(V):
+    import torch
+    if torch.cuda.is_available():
+        pytest.skip("a GPU is present")
+    with pytest.raises(V.ViError) as e:
+        V.Context(layers=1)
+    assert e.value.status == V.VI_E_CUDA
+
+
+def test_create_validates_config_before_touching_the_gpu(V):
+    with pytest.raises(V.ViError) as e:
+        V.Context(tokens_per_frame=719)
+    assert e.value.status == V.VI_E_CONFIG
+    with pytest.raises(V.ViError) as e:
+        V.Context(mem_frames=60)
+    assert e.value.status == V.VI_E_CONFIG
+    with pytest.raises(V.ViError) as e:
+        V.Context(sh=9, kh=7, feat_h=60, tokens_per_frame=7 * 36)   # stride > kernel: uncovered cells
+    assert e.value.status == V.VI_E_CONFIG

@@ -1,0 +1,299 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the fp64 oracle on the same
+seeded inputs.  Bars (BASELINE.json north_star; metric = reading Q18, oracle.rel_err):
+  * soft-split indexing and ring bookkeeping: bit-exact;
+  * fp32 SIMT path: rel_err <= 1e-4 on every stage and output;
+  * bf16 tensor-core path: rel_err <= 2e-2 on every stage and output.
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import vi_oracle as O
+from vi_synth import CONFIGS, make_features, make_kv, make_weights, round_bf16, rng_for
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-4, "bf16": 2e-2}
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2403_16161_b200 import build
+    build.build()
+
+
+def H():
+    from tests import gpu_harness
+    return gpu_harness
+
+
+def assert_close(got, ref, tol, what):
+    got = got.float().cpu().numpy() if isinstance(got, torch.Tensor) else got
+    e = O.rel_err(got, ref)
+    assert np.isfinite(got).all(), f"{what}: non-finite values"
+    assert e <= tol, f"{what}: rel_err {e:.3e} > {tol}"
+    return e
+
+
+def compare_step(cfg, ost, gst, tol, tag=""):
+    n = ost["tp"].shape[0]
+    errs = {}
+    if "tp" in gst:
+        assert np.array_equal(gst["tp"].float().cpu().numpy().astype(np.float64), ost["tp"]), "soft split not bit-exact"
+    errs["x0"] = assert_close(gst["x0"], ost["x0"], tol, tag + "x0")
+    for l, (ol, gl) in enumerate(zip(ost["layers"], gst["layers"])):
+        for k in ("q", "o", "u", "g"):
+            errs[f"{k}{l}"] = assert_close(gl[k], ol[k], tol, f"{tag}layer {l} {k}")
+        errs[f"x{l}"] = assert_close(gl["x"], ol["x"], tol, f"{tag}layer {l} x")
+    errs["out"] = assert_close(gst["out"], ost["out"], tol, tag + "out")
+    return errs
+
+
+def run_pair(cfg, w, steps, ns=None, seed=0, masked=False):
+    """Free-running oracle and GPU streams over the same frames; compare every step."""
+    g = H().GpuStream(cfg, w)
+    o = O.OracleStream(cfg, w)
+    fid = 0
+    worst = 0.0
+    for i in range(steps):
+        n = ns[i] if ns else cfg.t_new
+        feats = make_features(cfg, n, first_frame=fid, seed=seed, masked=masked)
+        fid += n
+        f_o, ev_o = o.push(n)
+        _, ost = o.step(feats)
+        _, gst = g.step(feats)
+        assert (gst["first"], gst["evicted"]) == (f_o, ev_o)
+        assert g.ctx.state() == tuple(o.mem.state()), "ring state differs"
+        errs = compare_step(cfg, ost, gst, TOL[cfg.dtype], tag=f"step {i}: ")
+        worst = max(worst, max(errs.values()))
+    return g, o, worst
+
+
+# ---------------------------------------------------------------- soft split / composite
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C2"])
+def test_soft_split_bit_exact(name):
+    from paper_2403_16161_b200 import vi
+    cfg = CONFIGS[name]
+    ctx = vi.Context.from_synth(cfg)
+    n = cfg.t_new
+    feats = make_features(cfg, n, seed=11)
+    f = H().tdev(feats, cfg.dtype)
+    out = torch.empty(n, cfg.tokens, cfg.patch_dim, dtype=H().tdtype(cfg), device="cuda")
+    ctx.soft_split(f, n, out, 0)
+    ctx.sync()
+    ref = O.soft_split(feats, cfg.kh, cfg.kw, cfg.sh, cfg.sw, cfg.ph, cfg.pw)
+    assert np.array_equal(out.float().cpu().numpy().astype(np.float64), ref)
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "C2"])
+def test_soft_composite_and_identity(name):
+    from paper_2403_16161_b200 import vi
+    cfg = CONFIGS[name]
+    ctx = vi.Context.from_synth(cfg)
+    n = cfg.t_new
+    dt = H().tdtype(cfg)
+    g = (cfg.kh, cfg.kw, cfg.sh, cfg.sw, cfg.ph, cfg.pw)
+    yp = rng_for(3, "yp").standard_normal((n, cfg.tokens, cfg.patch_dim)).astype(np.float32)
+    yp = round_bf16(yp) if cfg.dtype == "bf16" else yp
+    out = torch.empty(n, cfg.feat_h, cfg.feat_w, cfg.feat_c, dtype=dt, device="cuda")
+    ctx.soft_composite(H().tdev(yp, cfg.dtype), n, out, 0)
+    ctx.sync()
+    ref = O.soft_composite(yp, cfg.feat_h, cfg.feat_w, cfg.feat_c, *g)
+    assert_close(out, ref, 2 ** -8 if cfg.dtype == "bf16" else 1e-6, "composite")
+    # identity: composite(split(x)) == x bit-exactly (<= 9 exact copies, exact division)
+    feats = make_features(cfg, n, seed=12)
+    f = H().tdev(feats, cfg.dtype)
+    tok = torch.empty(n, cfg.tokens, cfg.patch_dim, dtype=dt, device="cuda")
+    ctx.soft_split(f, n, tok, 0)
+    ctx.soft_composite(tok, n, out, 0)
+    ctx.sync()
+    if cfg.dtype == "bf16":
+        assert torch.equal(out, f)
+    else:
+        np.testing.assert_allclose(out.cpu().numpy(), feats, rtol=2.5e-7, atol=0)
+
+
+# ---------------------------------------------------------------- fp32 path (configs[0])
+
+def test_c1_fp32_stream_per_stage():
+    """BASELINE configs[0]: 1 block, 24 tokens/frame, 1 new frame + 3-frame memory,
+    fp32 end to end; 7 steps wrap the 4-slot ring twice."""
+    cfg = CONFIGS["C1"]
+    w = make_weights(cfg, seed=0)
+    _, _, worst = run_pair(cfg, w, steps=7)
+    assert worst <= 1e-4
+
+
+def test_c1_fp32_sensitive_two_layers():
+    cfg = CONFIGS["C1"].replace(layers=2)
+    w = make_weights(cfg, seed=1, variant="sensitive")
+    run_pair(cfg, w, steps=5)
+
+
+def test_c1_f3n_fp32():
+    cfg = CONFIGS["C1"].replace(ffn_kind=1, ffn_hidden=49 * 4, layers=2)
+    w = make_weights(cfg, seed=2, variant="sensitive")
+    run_pair(cfg, w, steps=4)
+
+
+def test_I1_causal_replay_through_abi():
+    """T=1 steps from an empty memory == one block-causal joint pass (north_star check)."""
+    cfg = CONFIGS["C1"].replace(layers=2, mem_frames=5)
+    w = make_weights(cfg, seed=3, variant="sensitive")
+    feats = make_features(cfg, 5, seed=3)
+    joint = O.joint_forward(feats, w, cfg, mode="causal")
+    g = H().GpuStream(cfg, w)
+    for i in range(5):
+        out, _ = g.step(feats[i:i + 1], stages=False)
+        assert_close(out[0], joint["out"][i], 1e-4, f"I1 frame {i}")
+
+
+def test_I2_refine_commit_through_abi():
+    """Committing a bidirectional joint pass's K/V for t-M..t-1 makes the memory step on
+    frame t reproduce that pass's frame-t output (vi_refine_commit path, Eq. 4)."""
+    cfg = CONFIGS["C1"].replace(layers=2, mem_frames=3)
+    w = make_weights(cfg, seed=4, variant="sensitive")
+    feats = make_features(cfg, 4, seed=4)
+    joint = O.joint_forward(feats, w, cfg, mode="full")
+    g = H().GpuStream(cfg, w)
+    for i in range(3):
+        g.step(feats[i:i + 1], stages=False)
+    for i in range(3):
+        K = np.stack([joint["k"][l][i] for l in range(cfg.layers)]).astype(np.float32)
+        V = np.stack([joint["v"][l][i] for l in range(cfg.layers)]).astype(np.float32)
+        assert g.ctx.commit(i, K, V) == 0                       # host payload
+    out, _ = g.step(feats[3:4], stages=False)
+    _, ref, _ = g.ctx.state()
+    assert sum(ref) == 3
+    assert_close(out[0], joint["out"][3], 1e-4, "I2")
+
+
+def test_commit_rows_land_in_slab_and_device_payload():
+    cfg = CONFIGS["C1"].replace(mem_frames=3)
+    w = make_weights(cfg, seed=5)
+    g = H().GpuStream(cfg, w)
+    for i in range(3):
+        g.step(make_features(cfg, 1, first_frame=i, seed=5), stages=False)
+    k, v = make_kv(cfg, 9, 1)
+    kd, vd = torch.from_numpy(k).cuda(), torch.from_numpy(v).cuda()
+    assert g.ctx.commit(1, kd, vd) == 0                            # device payload
+    assert g.ctx.commit(2, kd, vd) == g.vi.VI_OK
+    assert g.ctx.evict(2) == 0                                     # evicted before apply: dropped
+    g.step(make_features(cfg, 1, first_frame=3, seed=5), stages=False)
+    gk, gv = g.kv(0, 1 % g.ctx.S)
+    assert torch.equal(gk.cpu(), torch.from_numpy(k[0])) and torch.equal(gv.cpu(), torch.from_numpy(v[0]))
+    sid, ref, mask = g.ctx.state()
+    assert ref[1] == 1 and sid[2] == -1
+
+
+def test_kv_memory_rows_match_oracle():
+    cfg = CONFIGS["C1"].replace(layers=2)
+    w = make_weights(cfg, seed=6, variant="sensitive")
+    g, o, _ = run_pair(cfg, w, steps=5)
+    for fid in o.mem.window() + [o.mem.cur_first]:
+        for l in range(cfg.layers):
+            K, V = o.frame_kv(l, fid)
+            gk, gv = g.kv(l, fid % g.ctx.S)
+            assert_close(gk, K, 1e-4, f"K l{l} f{fid}")
+            assert_close(gv, V, 1e-4, f"V l{l} f{fid}")
+
+
+def test_protocol_errors():
+    from paper_2403_16161_b200 import vi
+    cfg = CONFIGS["C1"]
+    g = H().GpuStream(cfg, make_weights(cfg))
+    x = g.x
+    with pytest.raises(vi.ViError) as e:
+        g.ctx.memory_step(0, x, x)                  # no push yet
+    assert e.value.status == vi.VI_E_PROTOCOL
+    g.ctx.push(1)
+    with pytest.raises(vi.ViError) as e:
+        g.ctx.memory_step(1, x, x)                  # out of order
+    assert e.value.status == vi.VI_E_PROTOCOL
+    assert g.ctx.evict(0) == vi.VI_E_PROTOCOL        # current chunk, step not finished
+    assert g.ctx.commit(5, np.zeros(1, np.float32), np.zeros(1, np.float32)) == vi.VI_E_PROTOCOL
+    with pytest.raises(vi.ViError) as e:
+        g.ctx.push(2)                               # n > max_new_frames
+    assert e.value.status == vi.VI_E_ARG
+
+
+# ---------------------------------------------------------------- bf16 tensor-core path
+
+def test_c3s_bf16_stream_per_stage():
+    """Reduced FuseFormer shape (2 blocks, 180 tokens/frame, T=2, M=3): several 128-row
+    tiles with ragged tails, F3N, split-KV attention; 5 steps wrap the 5-slot ring."""
+    cfg = CONFIGS["C3S"]
+    w = make_weights(cfg, seed=0)
+    _, _, worst = run_pair(cfg, w, steps=5)
+    assert worst <= 2e-2
+
+
+def test_c3s_bf16_sensitive_and_ragged_chunks():
+    cfg = CONFIGS["C3S"].replace(t_new=3)
+    w = make_weights(cfg, seed=1, variant="sensitive")
+    run_pair(cfg, w, steps=5, ns=[3, 1, 2, 3, 1])
+
+
+def test_c3s_bf16_sharp_logits_online_softmax():
+    cfg = CONFIGS["C3S"].replace(layers=1)
+    w = make_weights(cfg, seed=2, variant="sharp")
+    run_pair(cfg, w, steps=4)
+
+
+def test_c2_shape_headdim64_mlp():
+    cfg = CONFIGS["C2"].replace(layers=1, mem_frames=2, t_new=2, feat_h=30, feat_w=54)
+    w = make_weights(cfg, seed=3, variant="sensitive")
+    run_pair(cfg, w, steps=3)
+
+
+def test_bf16_kv_rows_and_determinism():
+    cfg = CONFIGS["C3S"].replace(layers=1)
+    w = make_weights(cfg, seed=4, variant="sensitive")
+    g1, o, _ = run_pair(cfg, w, steps=3)
+    for fid in o.mem.window() + list(range(o.mem.cur_first, o.mem.next_id)):
+        K, V = o.frame_kv(0, fid)
+        gk, gv = g1.kv(0, fid % g1.ctx.S)
+        assert_close(gk, K, 2e-2, f"K f{fid}")
+        assert_close(gv, V, 2e-2, f"V f{fid}")
+    # two contexts on the same inputs are bitwise identical (no atomics)
+    g1b, g2 = H().GpuStream(cfg, w), H().GpuStream(cfg, w)
+    for i in range(3):
+        feats = make_features(cfg, cfg.t_new, first_frame=i * cfg.t_new, seed=0)
+        a, _ = g1b.step(feats, stages=False)
+        b, _ = g2.step(feats, stages=False)
+        assert torch.equal(a, b)
+
+
+def test_run_step_host_buffers_equal_device_path():
+    cfg = CONFIGS["C3S"].replace(layers=1)
+    w = make_weights(cfg, seed=5)
+    g = H().GpuStream(cfg, w)
+    from paper_2403_16161_b200 import vi
+    c2 = vi.Context.from_synth(cfg)
+    c2.set_weights(w)
+    for i in range(3):
+        feats = make_features(cfg, cfg.t_new, first_frame=i * cfg.t_new, seed=7)
+        ref, _ = g.step(feats, stages=False)
+        host_in = torch.from_numpy(feats).to(torch.bfloat16).contiguous()
+        host_out = torch.empty_like(host_in)
+        c2.run_step(host_in, cfg.t_new, host_out)
+        assert torch.equal(host_out, ref.cpu())
+
+
+def test_c3_full_shape_step():
+    """The metric config (BASELINE configs[2]) at full size: 3 steps of 5 frames fill the
+    10-frame memory, the 4th step (3600 queries x 10800 keys) is compared stage by stage."""
+    cfg = CONFIGS["C3"].replace(layers=2)
+    w = make_weights(cfg, seed=0)
+    g = H().GpuStream(cfg, w)
+    o = O.OracleStream(cfg, w)
+    for i in range(4):
+        feats = make_features(cfg, 5, first_frame=5 * i, seed=0)
+        o.push(5)
+        _, ost = o.step(feats)
+        _, gst = g.step(feats, stages=(i == 3))
+    assert g.ctx.state()[2] == (1 << 15) - 1
+    compare_step(cfg, ost, gst, 2e-2)
