@@ -203,7 +203,7 @@ vi_status vi_profile_read(vi_ctx* ctx, double* ms /*[VI_PROF_N]*/, int64_t* laun
  *   VI_DBG_H       LN output last written                    [n][P][D] ctx dtype
  *   VI_DBG_Q       queries of the last block                 [n][P][D] ctx dtype
  *   VI_DBG_O       attention output of the last block        [n][P][D] ctx dtype
- *   VI_DBG_U       FFN1 output of the last block             [n][P][F] ctx dtype
+ *   VI_DBG_U       FFN1 output of the last block (F3N only)  [n][P][F] fp32
  *   VI_DBG_G       GELU(F3N(u)) of the last block            [n][P][F] ctx dtype
  *   VI_DBG_K, VI_DBG_V   memory rows of (layer, slot)        [P][D] ctx dtype
  * `n` is the chunk size of the last push. */

@@ -22,6 +22,8 @@
 #include <string>
 #include <vector>
 
+#include <unistd.h>
+
 #include "kernels/kernels.h"
 #include "ring.h"
 #include "vi.h"
@@ -86,6 +88,7 @@ struct vi_ctx {
   vi_config cfg{};
   Geom g{}, gf{};          // split geometry (C = feat_c) and F3N geometry (C = F / (kh*kw))
   int L = 0, H = 0, D = 0, hd = 0, P = 0, M = 0, Tmax = 0, S = 0, F = 0, Pd = 0, es = 2;
+  int vt_ld = 0;           // row pitch of the transposed V slab: S*P rounded up to 64 (TMA: 16-B pitch)
   bool bf16 = true;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
   bool own_stream = false;
@@ -104,7 +107,7 @@ struct vi_ctx {
   // memory
   void *kslab = nullptr, *vtslab = nullptr;
   // workspaces
-  void *tokens = nullptr, *h = nullptr, *q = nullptr, *o = nullptr, *u = nullptr, *gbuf = nullptr, *xb = nullptr;
+  void *tokens = nullptr, *yp32 = nullptr, *w_back2 = nullptr, *h = nullptr, *q = nullptr, *o = nullptr, *u = nullptr, *gbuf = nullptr, *xb = nullptr;
   float *x_ws = nullptr, *fold_ws = nullptr, *opart = nullptr, *lse = nullptr;
   void *feat_in = nullptr, *feat_out = nullptr;
   std::vector<void*> allocs;
@@ -171,6 +174,27 @@ vi_ctx::~vi_ctx() {
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
+// VI_DEBUG_SYNC=1: wait for every launch (poll, 20 s limit) and name a kernel that hangs.
+static const bool g_debug_sync = [] {
+  const char* e = getenv("VI_DEBUG_SYNC");
+  return e && e[0] == '1';
+}();
+static void debug_wait(vi_ctx* c, const char* where) {
+  for (int i = 0; i < 20000; ++i) {
+    cudaError_t e = cudaStreamQuery(c->stream);
+    if (e == cudaSuccess) return;
+    if (e != cudaErrorNotReady) {
+      fprintf(stderr, "[vi debug] kernel '%s' failed: %s\n", where, cudaGetErrorString(e));
+      fflush(stderr);
+      _exit(3);
+    }
+    usleep(1000);
+  }
+  fprintf(stderr, "[vi debug] kernel '%s' did not finish within 20 s\n", where);
+  fflush(stderr);
+  _exit(4);
+}
+
 #define CK(call, where)                                 \
   do {                                                  \
     cudaError_t e_ = (call);                            \
@@ -180,6 +204,7 @@ vi_ctx::~vi_ctx() {
   do {                             \
     ++c->launches;                 \
     CK((call), where);             \
+    if (g_debug_sync) debug_wait(c, where); \
   } while (0)
 #define PLAUNCH(cat, call, where) \
   do {                             \
@@ -271,11 +296,11 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_w1, c->w_1, c->D, (uint64_t)c->L * c->F, 64, c->bn_1);
   ok &= make_tmap(&c->tm_g, c->gbuf, c->F, rows, 64, 128);
   ok &= make_tmap(&c->tm_w2, c->w_2, c->F, (uint64_t)c->L * c->D, 64, c->bn_2);
-  ok &= make_tmap(&c->tm_xb, c->xb, c->D, rows, 64, 128);
-  ok &= make_tmap(&c->tm_wback, c->w_back, c->D, c->Pd, 64, c->bn_back);
+  ok &= make_tmap(&c->tm_xb, c->xb, 2 * c->D, rows, 64, 128);
+  ok &= make_tmap(&c->tm_wback, c->w_back2, 2 * c->D, c->Pd, 64, c->bn_back);
   ok &= make_tmap(&c->tm_q, c->q, c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_k, c->kslab, c->D, (uint64_t)c->L * c->S * c->P, 64, 128);
-  ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->S * c->P, (uint64_t)c->L * c->D, 64, c->hd);
+  ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->D, 64, c->hd);
   return ok ? VI_OK : c->fail(VI_E_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
@@ -300,6 +325,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->L = cfg->layers; c->H = cfg->heads; c->D = cfg->d_model; c->hd = c->D / c->H;
   c->P = cfg->tokens_per_frame; c->M = cfg->mem_frames; c->Tmax = cfg->max_new_frames; c->S = c->M + c->Tmax;
   c->F = cfg->ffn_hidden; c->Pd = cfg->kh * cfg->kw * cfg->feat_c;
+  c->vt_ld = (c->S * c->P + 63) / 64 * 64;
   c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
   c->ring = Ring(c->M, c->Tmax);
   const int oh = (cfg->feat_h + 2 * cfg->ph - cfg->kh) / cfg->sh + 1;
@@ -337,9 +363,14 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->w_1 = A(L * F * D * es); c->b_1 = (float*)A(L * F * 4);
   c->w_2 = A(L * D * F * es); c->b_2 = (float*)A(L * D * 4);
   c->w_back = A(Pd * D * es); c->b_back = (float*)A(Pd * 4);
-  c->kslab = A(L * S * P * D * es); c->vtslab = A(L * S * P * D * es);
+  c->kslab = A(L * S * P * D * es); c->vtslab = A(L * D * (size_t)c->vt_ld * es);
   c->tokens = A(rows * Pd * es); c->h = A(rows * D * es); c->q = A(rows * D * es); c->o = A(rows * D * es);
-  c->u = A(rows * F * es); c->gbuf = A(rows * F * es); c->xb = A(rows * D * es);
+  c->u = A(rows * F * 4);   // FFN1 output kept fp32 for the F3N fold (one rounding less)
+  c->gbuf = A(rows * F * es); c->xb = A(rows * 2 * D * es);
+  if (c->bf16) {
+    c->yp32 = A(rows * Pd * 4);          // back-projection output kept fp32 for the fold
+    c->w_back2 = A(Pd * 2 * D * es);     // [Wb | Wb] for the hi/lo split of x
+  }
   c->x_ws = (float*)A(rows * D * 4);
   c->fold_ws = (float*)A((size_t)c->Tmax * cfg->feat_h * cfg->feat_w * std::max(c->gf.C, 1) * 4);
   if (c->bf16) {
@@ -423,6 +454,14 @@ extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
   U(upload_mat(c, c->w_2, w->w2, L * D * F));
   U(upload_f32(c, c->b_2, w->b2, L * D));
   U(upload_mat(c, c->w_back, w->back_w, Pd * D));
+  if (c->bf16) {   // [Wb | Wb]: row r = (Wb[r], Wb[r])
+    std::vector<float> w2(Pd * 2 * D);
+    for (size_t r = 0; r < Pd; ++r) {
+      std::memcpy(&w2[r * 2 * D], w->back_w + r * D, D * 4);
+      std::memcpy(&w2[r * 2 * D + D], w->back_w + r * D, D * 4);
+    }
+    U(upload_mat(c, c->w_back2, w2.data(), Pd * 2 * D));
+  }
   U(upload_f32(c, c->b_back, w->back_b, Pd));
   if (st == VI_OK) c->have_weights = true;
   return st;
@@ -441,8 +480,8 @@ static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
       const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.second) + (size_t)l * P * D * es;
       uint8_t* kdst = static_cast<uint8_t*>(c->kslab) + ((size_t)l * SP + (size_t)slot * P) * D * es;
       CK(cudaMemcpyAsync(kdst, ksrc, P * D * es, cudaMemcpyDeviceToDevice, c->stream), "commit K");
-      uint8_t* vt = static_cast<uint8_t*>(c->vtslab) + (size_t)l * D * SP * es;
-      PLAUNCH(VI_PROF_ROW, launch_transpose_to_slab(vsrc, vt, c->P, c->D, SP, (size_t)slot * P, c->bf16 ? 0 : 1, c->stream),
+      uint8_t* vt = static_cast<uint8_t*>(c->vtslab) + (size_t)l * D * c->vt_ld * es;
+      PLAUNCH(VI_PROF_ROW, launch_transpose_to_slab(vsrc, vt, c->P, c->D, c->vt_ld, (size_t)slot * P, c->bf16 ? 0 : 1, c->stream),
              "commit V");
     }
   }
@@ -586,8 +625,10 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
     }
     int e = s;
     while (e + 1 < c->S && ((valid >> (e + 1)) & 1)) ++e;
-    k.row0[k.n] = s * c->P;
-    k.len[k.n] = (e - s + 1) * c->P;
+    const int r0 = s * c->P;
+    k.row0[k.n] = r0 & ~7;
+    k.lead[k.n] = r0 & 7;
+    k.len[k.n] = (e - s + 1) * c->P + k.lead[k.n];
     k.tile0[k.n + 1] = k.tile0[k.n] + (k.len[k.n] + 127) / 128;
     ++k.n;
     s = e + 1;
@@ -605,7 +646,7 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
   const int dt = c->bf16 ? 0 : 1;
   const size_t es = c->es, SP = (size_t)c->S * c->P;
   void* kl = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * D * es;
-  void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * SP * D * es;
+  void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * c->vt_ld * D * es;
   const uint64_t valid = c->ring.valid_mask();
 
   // a3: LN1
@@ -613,7 +654,7 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
   // a4: QKV projection + memory write
   Epi eq = epi_base(EPI_QKV, M, 3 * D, c->b_qkv + (size_t)l * 3 * D);
   eq.D = D; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
-  eq.S = c->S; eq.P = c->P;
+  eq.S = c->S; eq.P = c->P; eq.vt_ld = c->vt_ld;
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * D, M, 3 * D, D, c->bn_qkv, eq, c->stream), "qkv gemm");
   else
@@ -635,7 +676,7 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
   } else {
     AttnArgs a;
-    a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->S; a.valid = valid;
+    a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->S; a.vt_ld = c->vt_ld; a.valid = valid;
     a.scale_log2 = scale_log2; a.q = c->q; a.kslab = kl; a.vtslab = vl; a.o = c->o;
     PLAUNCH(VI_PROF_ATTN, launch_attn_simt_f32(a, c->stream), "attention");
   }
@@ -652,14 +693,14 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
   // a9 / a10: FFN1 (+ F3N fold/unfold) + GELU
   const bool f3n = c->cfg.ffn_kind == VI_FFN_F3N;
   Epi e1 = epi_base(f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
-  e1.out = f3n ? c->u : c->gbuf; e1.ldo = F;
+  e1.out = f3n ? c->u : c->gbuf; e1.ldo = F; e1.out_f32 = f3n ? 1 : 0;
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream), "ffn1 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_1 + (size_t)l * F * D, M, F, D, e1, c->stream),
            "ffn1 gemm");
   if (f3n) {
-    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, dt, c->fold_ws, 1, n, c->gf, c->stream), "f3n fold");
+    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, 1, n, c->gf, c->stream), "f3n fold");
     PLAUNCH(VI_PROF_PATCH, launch_unfold_gelu(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream), "f3n unfold");
   }
   // a11: FFN2 + residual
@@ -691,15 +732,19 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
     Epi e = epi_base(EPI_STORE, M, c->Pd, c->b_back);
     e.out = c->tokens; e.ldo = c->Pd;
     if (c->bf16) {
-      PLAUNCH(VI_PROF_ROW, launch_cast_bf16((const float*)in, c->xb, (size_t)M * c->D, c->stream), "cast");
-      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_xb, c->tm_wback, 0, M, c->Pd, c->D, c->bn_back, e, c->stream), "back gemm");
+      // x enters the GEMM as bf16 hi + lo (K = 2D against [Wb | Wb]) and Yp leaves it in
+      // fp32: the back projection adds no bf16 rounding of its own
+      e.out = c->yp32; e.out_f32 = 1;
+      PLAUNCH(VI_PROF_ROW, launch_split_bf16((const float*)in, c->xb, M, c->D, c->stream), "cast");
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_xb, c->tm_wback, 0, M, c->Pd, 2 * c->D, c->bn_back, e, c->stream),
+              "back gemm");
     } else {
       PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)in, (const float*)c->w_back, M, c->Pd, c->D, e, c->stream),
              "back gemm");
     }
-    tok = c->tokens;
+    tok = c->bf16 ? c->yp32 : c->tokens;
   }
-  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, dt, feat, dt, n, c->g, c->stream), "fold");
+  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, (project && c->bf16) ? 1 : dt, feat, dt, n, c->g, c->stream), "fold");
   return VI_OK;
 }
 
@@ -783,7 +828,9 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
     case VI_DBG_H: src = c->h; need = rows * D * es; break;
     case VI_DBG_Q: src = c->q; need = rows * D * es; break;
     case VI_DBG_O: src = c->o; need = rows * D * es; break;
-    case VI_DBG_U: src = c->cfg.ffn_kind == VI_FFN_F3N ? c->u : c->gbuf; need = rows * c->F * es; break;
+    case VI_DBG_U:
+      if (c->cfg.ffn_kind != VI_FFN_F3N) return c->fail(VI_E_CONFIG, "vi_debug_read: u exists for F3N only");
+      src = c->u; need = rows * c->F * 4; break;
     case VI_DBG_G: src = c->gbuf; need = rows * c->F * es; break;
     case VI_DBG_K:
     case VI_DBG_V: need = (size_t)c->P * D * es; break;
@@ -799,8 +846,10 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
   } else if (what == VI_DBG_V) {
     // Vt [D][S*P] columns slot*P.. -> [P][D]
     std::vector<uint8_t> tmp(need);
-    const uint8_t* base = static_cast<const uint8_t*>(c->vtslab) + ((size_t)layer * D * SP + (size_t)slot * c->P) * es;
-    CK(cudaMemcpy2D(tmp.data(), c->P * es, base, SP * es, c->P * es, D, cudaMemcpyDeviceToHost), "debug copy V");
+    const uint8_t* base =
+        static_cast<const uint8_t*>(c->vtslab) + ((size_t)layer * D * c->vt_ld + (size_t)slot * c->P) * es;
+    CK(cudaMemcpy2D(tmp.data(), c->P * es, base, (size_t)c->vt_ld * es, c->P * es, D, cudaMemcpyDeviceToHost),
+       "debug copy V");
     std::vector<uint8_t> tr(need);
     for (size_t d = 0; d < D; ++d)
       for (int p = 0; p < c->P; ++p) std::memcpy(&tr[((size_t)p * D + d) * es], &tmp[(d * c->P + p) * es], es);

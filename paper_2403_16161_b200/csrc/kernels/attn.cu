@@ -31,7 +31,7 @@ __global__ void attn_simt_f32_kernel(AttnArgs a) {
   const float* Q = reinterpret_cast<const float*>(a.q) + (size_t)q * a.D + h * a.hd;
   const float* K = reinterpret_cast<const float*>(a.kslab);
   const float* Vt = reinterpret_cast<const float*>(a.vtslab);
-  const size_t ld = (size_t)a.S * a.P;
+  const size_t ld = (size_t)a.vt_ld;
   float qv[4], acc[4] = {0.f, 0.f, 0.f, 0.f};
   for (int i = 0; i < R; ++i) qv[i] = Q[lane + 32 * i];
   float m = -INFINITY, l = 0.f;
@@ -79,13 +79,16 @@ struct AttnSmem {
   static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
 };
 
-__device__ __forceinline__ void key_tile(const KeySegs& s, int g, int& row0, int& nvalid) {
+// Tile g of the valid key space: keys row0 .. row0+127 of the slab, of which
+// [nskip, nvalid) belong to valid slots (the rest is masked to -inf).
+__device__ __forceinline__ void key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
   int i = 0;
   while (i + 1 < s.n && g >= s.tile0[i + 1]) ++i;
   const int off = (g - s.tile0[i]) * 128;
   row0 = s.row0[i] + off;
   const int rem = s.len[i] - off;
   nvalid = rem < 128 ? rem : 128;
+  nskip = off == 0 ? s.lead[i] : 0;
 }
 
 template <int HD>
@@ -149,8 +152,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
 #pragma unroll
       for (int at = 0; at < HD / 64; ++at) tma_load_2d(sq + at * 16384, &tq, q_full, h * HD + at * 64, q0);
       for (int jj = 0; jj < n; ++jj) {
-        int row0, nv;
-        key_tile(a.segs, t_begin + jj, row0, nv);
+        int row0, nv, nskip;
+        key_tile(a.segs, t_begin + jj, row0, nv, nskip);
         const int st = jj % ST;
         const uint32_t par = ((jj / ST) & 1) ^ 1;
         if (jj >= ST) mbar_wait(&k_empty[st], par);
@@ -214,8 +217,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
     float m = -INFINITY, l = 0.f;
     for (int jj = 0; jj < n; ++jj) {
       const int b = jj & 1;
-      int row0, nv;
-      key_tile(a.segs, t_begin + jj, row0, nv);
+      int row0, nv, nskip;
+      key_tile(a.segs, t_begin + jj, row0, nv, nskip);
       mbar_wait(&s_full[b], (jj >> 1) & 1);
       tc_fence_after();
       float s[128];
@@ -227,15 +230,16 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
       float mx = -INFINITY;
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
-        if (i >= nv) s[i] = -INFINITY;
+        if (i >= nv || i < nskip) s[i] = -INFINITY;
         mx = fmaxf(mx, s[i]);
       }
       const float m_new = fmaxf(m, mx * a.scale_log2);
       const float alpha = ex2(m - m_new);
+      // the row sum is taken over the bf16-rounded P the PV MMA actually multiplies
       float sum = 0.f;
 #pragma unroll
       for (int i = 0; i < 128; ++i) {
-        const float p = ex2(fmaf(s[i], a.scale_log2, -m_new));
+        const float p = __bfloat162float(__float2bfloat16_rn(ex2(fmaf(s[i], a.scale_log2, -m_new))));
         s[i] = p;
         sum += p;
       }
@@ -243,7 +247,8 @@ attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
       if (jj > 0) {
         mbar_wait(o_done, (jj - 1) & 1);              // PV(jj-1) done: O stable, P buffer free
         tc_fence_after();
-        if (alpha < 1.f) {
+        // tcgen05.ld/st are warp-collective: rescale if any row of this warp needs it
+        if (__any_sync(0xffffffffu, alpha < 1.f)) {
 #pragma unroll 1
           for (int c = 0; c < HD; c += 16) {
             uint32_t r[16];

@@ -5,7 +5,7 @@
 //   EPI_RESID   x_out[m][n] = x_in[m][n] + C + bias[n]           (fp32 residual stream)
 //   EPI_QKV     n <  D : Q[m][n] = C + b
 //               n < 2D : K slab row (slot(t)*P + p), col n-D     (the memory write)
-//               else   : Vt slab [D][S*P] column (slot(t)*P + p) (V stored transposed)
+//               else   : Vt slab [D][vt_ld] column (slot(t)*P + p) (V stored transposed)
 //               with m = t*P + p, slot(t) = (first_slot + t) % S.
 #pragma once
 #include "common.cuh"
@@ -30,6 +30,7 @@ struct Epi {
   void* kslab;            // [S*P][D] (this layer)
   void* vtslab;           // [D][S*P] (this layer)
   int first_slot, S;
+  int vt_ld;              // row pitch (elements) of the Vt slab, >= S*P, multiple of 64
 };
 
 template <typename T>
@@ -57,7 +58,7 @@ __device__ __forceinline__ void epi_one(const Epi& e, int m, int n, float acc) {
       } else if (n < 2 * e.D) {
         reinterpret_cast<T*>(e.kslab)[row * e.D + (n - e.D)] = from_f<T>(v);
       } else {
-        reinterpret_cast<T*>(e.vtslab)[(size_t)(n - 2 * e.D) * ((size_t)e.S * e.P) + row] = from_f<T>(v);
+        reinterpret_cast<T*>(e.vtslab)[(size_t)(n - 2 * e.D) * (size_t)e.vt_ld + row] = from_f<T>(v);
       }
     }
   }
@@ -126,7 +127,7 @@ __device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, floa
                               pack_bf16(v[8 * i + 4], v[8 * i + 5]), pack_bf16(v[8 * i + 6], v[8 * i + 7]));
       } else {
         bf16* vt = reinterpret_cast<bf16*>(e.vtslab);
-        const size_t ld = (size_t)e.S * e.P;
+        const size_t ld = (size_t)e.vt_ld;
 #pragma unroll
         for (int i = 0; i < 32; ++i) vt[(size_t)(n0 - 2 * e.D + i) * ld + row] = __float2bfloat16_rn(v[i]);
       }

@@ -25,7 +25,8 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
 // LayerNorm over D (eps 1e-5), fp32 in, out dtype 0 bf16 / 1 fp32.
 cudaError_t launch_layernorm(const float* x, const float* g, const float* b, void* out, int out_dtype, int rows,
                              int D, cudaStream_t st);
-cudaError_t launch_cast_bf16(const float* x, void* out, size_t n, cudaStream_t st);
+// x fp32 [rows][D] -> [rows][2D] bf16 (hi | lo) for the extended-precision back projection
+cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaStream_t st);
 cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D, size_t ld, size_t col0, int dtype,
                                      cudaStream_t st);
 
@@ -41,18 +42,19 @@ cudaError_t launch_gemm_simt_f32(const float* A, const float* W, int M, int N, i
 // ---- attention -----------------------------------------------------------------------
 struct KeySegs {            // contiguous runs of valid ring slots, as slab row ranges
   int n;
-  int row0[32];
-  int len[32];
+  int row0[32];             // first row, aligned DOWN to a multiple of 8 (TMA: 16-byte start)
+  int lead[32];             // rows row0 .. row0+lead-1 precede the segment: masked
+  int len[32];              // lead + valid rows
   int tile0[33];            // prefix count of 128-key tiles per segment
 };
 
 struct AttnArgs {
-  int Nq, D, H, hd, P, S;
+  int Nq, D, H, hd, P, S, vt_ld;
   uint64_t valid;           // slot validity mask
   float scale_log2;         // log2(e) / sqrt(hd)
   const void* q;            // [Nq][D]
   const void* kslab;        // [S*P][D]        (this layer)
-  const void* vtslab;       // [D][S*P]        (this layer)
+  const void* vtslab;       // [D][vt_ld]      (this layer)
   void* o;                  // [Nq][D]
 };
 cudaError_t launch_attn_simt_f32(const AttnArgs& a, cudaStream_t st);

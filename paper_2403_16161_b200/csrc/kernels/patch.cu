@@ -182,10 +182,12 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
       fold_kernel<bf16, bf16, 8><<<grid_for(total), 256, 0, st>>>((const bf16*)in, (bf16*)out, n, g);
     else
       fold_kernel<bf16, float, 8><<<grid_for(total), 256, 0, st>>>((const bf16*)in, (float*)out, n, g);
-  } else {
+  } else if (out_dtype == 1) {
     const size_t total = (size_t)n * g.H * g.W * (g.C / 4);
-    if (out_dtype != 1) return cudaErrorInvalidValue;
     fold_kernel<float, float, 4><<<grid_for(total), 256, 0, st>>>((const float*)in, (float*)out, n, g);
+  } else {
+    const size_t total = (size_t)n * g.H * g.W * (g.C / 8);
+    fold_kernel<float, bf16, 8><<<grid_for(total), 256, 0, st>>>((const float*)in, (bf16*)out, n, g);
   }
   return cudaGetLastError();
 }

@@ -56,20 +56,27 @@ cudaError_t launch_layernorm(const float* x, const float* g, const float* b, voi
   return cudaErrorInvalidValue;
 }
 
-__global__ void cast_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ out, size_t n4) {
+// x [rows][D] fp32 -> [rows][2D] bf16 with hi = bf16(x) in columns 0..D-1 and
+// lo = bf16(x - hi) in D..2D-1: a K = 2D GEMM against [W | W] then sees x to ~2^-17.
+__global__ void split_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ out, int rows, int D4) {
+  const size_t n4 = (size_t)rows * D4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
-    float4 v = x[i];
-    out[i] = make_uint2(pack_bf16(v.x, v.y), pack_bf16(v.z, v.w));
+    const size_t r = i / D4, c = i - r * D4;
+    const float4 v = x[i];
+    const __nv_bfloat162 h01 = __floats2bfloat162_rn(v.x, v.y), h23 = __floats2bfloat162_rn(v.z, v.w);
+    const float2 f01 = __bfloat1622float2(h01), f23 = __bfloat1622float2(h23);
+    out[r * 2 * D4 + c] = make_uint2(*reinterpret_cast<const uint32_t*>(&h01), *reinterpret_cast<const uint32_t*>(&h23));
+    out[r * 2 * D4 + D4 + c] = make_uint2(pack_bf16(v.x - f01.x, v.y - f01.y), pack_bf16(v.z - f23.x, v.w - f23.y));
   }
 }
 
-cudaError_t launch_cast_bf16(const float* x, void* out, size_t n, cudaStream_t st) {
-  const size_t n4 = n / 4;
+cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaStream_t st) {
+  const size_t n4 = (size_t)rows * D / 4;
   size_t blocks = (n4 + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (!blocks) blocks = 1;
-  cast_bf16_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<uint2*>(out),
-                                                     n4);
+  split_bf16_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<uint2*>(out),
+                                                      rows, D / 4);
   return cudaGetLastError();
 }
 

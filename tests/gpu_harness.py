@@ -53,9 +53,11 @@ class GpuStream:
             ctx.memory_step(l, x, x)
             if stages:
                 d = {}
-                for name, width in (("q", cfg.d_model), ("o", cfg.d_model), ("u", cfg.ffn_hidden),
-                                    ("g", cfg.ffn_hidden)):
-                    buf = torch.empty(n * cfg.tokens, width, dtype=dt, device="cuda")
+                names = [("q", cfg.d_model, dt), ("o", cfg.d_model, dt), ("g", cfg.ffn_hidden, dt)]
+                if cfg.ffn_kind == 1:
+                    names.append(("u", cfg.ffn_hidden, torch.float32))
+                for name, width, bdt in names:
+                    buf = torch.empty(n * cfg.tokens, width, dtype=bdt, device="cuda")
                     ctx.debug_read(name, buf)
                     d[name] = buf
                 ctx.sync()
