@@ -179,6 +179,11 @@ static const bool g_debug_sync = [] {
   const char* e = getenv("VI_DEBUG_SYNC");
   return e && e[0] == '1';
 }();
+// VI_ATTN_V1=1 selects the one-Q-tile attention kernel (A/B comparisons).
+static const bool g_attn_v1 = [] {
+  const char* e = getenv("VI_ATTN_V1");
+  return e && e[0] == '1';
+}();
 static void debug_wait(vi_ctx* c, const char* where) {
   for (int i = 0; i < 20000; ++i) {
     cudaError_t e = cudaStreamQuery(c->stream);
@@ -669,10 +674,14 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     a.Nq = M; a.hd = c->hd; a.D = D; a.H = c->H; a.krow_base = int(l * SP); a.vrow_base = l * D;
     a.scale_log2 = scale_log2; a.segs = make_segs(c, valid);
     const int ntiles = a.segs.tile0[a.segs.n];
-    choose_split(((M + 127) / 128) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
+    const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
+    choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
     a.o = static_cast<bf16*>(c->o); a.opart = c->opart; a.lse = c->lse;
-    PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
+    if (g_attn_v1)
+      PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
+    else
+      PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
     if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
   } else {
     AttnArgs a;

@@ -350,6 +350,297 @@ cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const C
   return cudaErrorInvalidValue;
 }
 
+// ------------------------------------------------------------------ v2: two Q tiles per CTA
+// attn_tc2_kernel: one CTA = (pair of 128-query tiles, head, KV split), 384 threads:
+//   warps 0-3 : softmax of Q tile 0 (thread = query row = TMEM lane)
+//   warps 4-7 : softmax of Q tile 1
+//   warp 8    : TMA producer (Q tiles once; K / transposed-V tiles, 2-stage ring)
+//   warp 9    : MMA issuer
+//   warp 10   : TMEM allocator (512 cols: S0/P0 | S1/P1 | O0 | O1)
+// Each K/V tile fetched once serves 256 queries.  P is written back into the TMEM
+// columns of its own S tile (bf16 pairs) and is the A operand (from TMEM) of O += P V.
+// Tensor-core order per KV tile j:  PV(0,j-1) QK(0,j) PV(1,j-1) QK(1,j), so while one
+// softmax warpgroup works on tile j the tensor core runs the other tile's MMAs.
+// tcgen05 ops of one thread complete in order, so the commit of QK(t,j) also proves
+// PV(t,j-1) finished: the softmax may then overwrite P(t) and rescale O(t) safely.
+// Running max update is lazy (only when it grows by > 8 in log2 units), exact either way.
+template <int HD>
+struct Attn2Smem {
+  static constexpr int ST = 2;
+  static constexpr int QB = 128 * HD * 2;
+  static constexpr int KB = 128 * HD * 2;
+  static constexpr int VB = HD * 128 * 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = 2 * QB;
+  static constexpr int V_OFF = K_OFF + ST * KB;
+  static constexpr int BAR_OFF = V_OFF + ST * VB;
+  static constexpr int NBAR = 1 + 4 * ST + 2 + 2 + 2;
+  static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
+};
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+                const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
+  using L = Attn2Smem<HD>;
+  constexpr int ST = L::ST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* k_full = bars + 1;
+  uint64_t* k_empty = k_full + ST;
+  uint64_t* v_full = k_empty + ST;
+  uint64_t* v_empty = v_full + ST;
+  uint64_t* s_full = v_empty + ST;    // [2] per Q tile
+  uint64_t* p_full = s_full + 2;      // [2]
+  uint64_t* o_final = p_full + 2;     // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int q0 = blockIdx.x * 256, h = blockIdx.y, z = blockIdx.z;
+  const int ntiles = a.segs.tile0[a.segs.n];
+  const int t_begin = z * a.tiles_per_split;
+  int t_end = t_begin + a.tiles_per_split;
+  if (t_end > ntiles) t_end = ntiles;
+  const int n = t_end > t_begin ? t_end - t_begin : 0;
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tq);
+    tma_prefetch(&tk);
+    tma_prefetch(&tvt);
+    mbar_init(q_full, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[t], 128);
+      mbar_init(&o_final[t], 1);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 10) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 8) {
+    if (lane == 0 && n > 0) {
+      mbar_arrive_expect_tx(q_full, 2 * L::QB);
+#pragma unroll
+      for (int t = 0; t < 2; ++t)
+#pragma unroll
+        for (int at = 0; at < HD / 64; ++at)
+          tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, q0 + t * 128);
+      for (int jj = 0; jj < n; ++jj) {
+        int row0, nv, nskip;
+        key_tile(a.segs, t_begin + jj, row0, nv, nskip);
+        const int st = jj % ST;
+        const uint32_t par = ((jj / ST) & 1) ^ 1;
+        if (jj >= ST) mbar_wait(&k_empty[st], par);
+        uint8_t* sk = smem + L::K_OFF + st * L::KB;
+        mbar_arrive_expect_tx(&k_full[st], L::KB);
+#pragma unroll
+        for (int at = 0; at < HD / 64; ++at)
+          tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + row0);
+        if (jj >= ST) mbar_wait(&v_empty[st], par);
+        uint8_t* sv = smem + L::V_OFF + st * L::VB;
+        mbar_arrive_expect_tx(&v_full[st], L::VB);
+#pragma unroll
+        for (int at = 0; at < 2; ++at)
+          tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], row0 + at * 64, a.vrow_base + h * HD);
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0 && n > 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD);
+      const uint32_t sq = smem_u32(smem + L::Q_OFF);
+      mbar_wait(q_full, 0);
+      auto issue_pv = [&](int t, int j) {            // O_t (+)= P_t(j) V(j)
+        const int st = j % ST;
+        mbar_wait(&p_full[t], j & 1);
+        if (t == 0) mbar_wait(&v_full[st], (j / ST) & 1);
+        tc_fence_after();
+        const uint32_t sv = smem_u32(smem + L::V_OFF + st * L::VB);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t offv = (kk >> 2) * (HD * 128) + (kk & 3) * 32;
+          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_k_sw128(sv + offv), idesc_o,
+                       (j | kk) != 0);
+        }
+        if (t == 1) umma_commit(&v_empty[st]);
+      };
+      auto issue_qk = [&](int t, int j) {            // S_t = Q_t K(j)^T
+        const int st = j % ST;
+        if (t == 0) {
+          mbar_wait(&k_full[st], (j / ST) & 1);
+          tc_fence_after();
+        }
+        const uint32_t sk = smem_u32(smem + L::K_OFF + st * L::KB);
+        const uint32_t sqt = sq + t * L::QB;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+          umma_bf16_ss(tmem + t * 128, sdesc_k_sw128(sqt + off), sdesc_k_sw128(sk + off), idesc_s, kk > 0);
+        }
+        umma_commit(&s_full[t]);
+        if (t == 1) umma_commit(&k_empty[st]);
+      };
+      for (int j = 0; j < n; ++j) {
+        for (int t = 0; t < 2; ++t) {
+          if (j > 0) issue_pv(t, j - 1);
+          issue_qk(t, j);
+        }
+      }
+      for (int t = 0; t < 2; ++t) {
+        issue_pv(t, n - 1);
+        umma_commit(&o_final[t]);
+      }
+    }
+  } else if (warp < 8) {
+    const int t = warp >> 2;                          // Q tile of this warpgroup
+    const int qd = warp & 3;                          // TMEM lane quadrant
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t TS = tmem + t * 128 + lane_off, TO = tmem + 256 + t * 128 + lane_off;
+    float m_use = -INFINITY, l = 0.f;
+    for (int jj = 0; jj < n; ++jj) {
+      int row0, nv, nskip;
+      key_tile(a.segs, t_begin + jj, row0, nv, nskip);
+      mbar_wait(&s_full[t], jj & 1);
+      tc_fence_after();
+      float s[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) tmem_ld32(TS + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
+      tmem_wait_ld();
+      float mx[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
+      if (nv < 128 || nskip > 0) {
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (i >= nv || i < nskip) s[i] = -INFINITY;
+      }
+#pragma unroll
+      for (int i = 0; i < 128; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
+      const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * a.scale_log2;
+      // lazy rescale: keep the old reference max unless the row max grew by > 8 (x256)
+      const bool grow = rmax > m_use + 8.f;
+      float alpha = 1.f;
+      if (grow) {
+        alpha = ex2(m_use - rmax);
+        m_use = rmax;
+      }
+      if (__any_sync(0xffffffffu, grow) && jj > 0) {  // O(t) is idle here (see above)
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          uint32_t r[32];
+          tmem_ld32(TO + c, r);
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+          tmem_st32(TO + c, r);
+        }
+      }
+      float sum[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) sum[i] = 0.f;
+      uint32_t pk[64];
+#pragma unroll
+      for (int i = 0; i < 64; ++i) {
+        const float p0 = ex2(fmaf(s[2 * i], a.scale_log2, -m_use));
+        const float p1 = ex2(fmaf(s[2 * i + 1], a.scale_log2, -m_use));
+        __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
+        pk[i] = *reinterpret_cast<uint32_t*>(&b);
+        const float2 r = __bfloat1622float2(b);       // the row sum uses the rounded P
+        sum[i & 7] += r.x + r.y;
+      }
+      l = l * alpha + (((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7])));
+#pragma unroll
+      for (int c = 0; c < 2; ++c) tmem_st32(TS + c * 32, pk + c * 32);
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(&p_full[t]);
+    }
+    // epilogue
+    const int q = q0 + t * 128 + qd * 32 + lane;
+    if (n > 0) {
+      mbar_wait(&o_final[t], 0);
+      tc_fence_after();
+    }
+    const float inv = n > 0 ? 1.f / l : 0.f;
+    if (a.nsplit == 1) {
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t r[32];
+        tmem_ld32(TO + c, r);
+        tmem_wait_ld();
+        if (q < a.Nq) {
+          const float* f = reinterpret_cast<const float*>(r);
+          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.D + h * HD + c);
+#pragma unroll
+          for (int i = 0; i < 4; ++i)
+            dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv), pack_bf16(f[8 * i + 2] * inv, f[8 * i + 3] * inv),
+                                pack_bf16(f[8 * i + 4] * inv, f[8 * i + 5] * inv), pack_bf16(f[8 * i + 6] * inv, f[8 * i + 7] * inv));
+        }
+      }
+    } else {
+      float* op = a.opart + ((size_t)z * a.Nq + q) * a.D + h * HD;
+#pragma unroll 1
+      for (int c = 0; c < HD; c += 32) {
+        uint32_t r[32];
+        if (n > 0) {
+          tmem_ld32(TO + c, r);
+          tmem_wait_ld();
+        }
+        if (q < a.Nq) {
+          float4* dst = reinterpret_cast<float4*>(op + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i)
+            dst[i] = n > 0 ? make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
+                                         __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv)
+                           : make_float4(0.f, 0.f, 0.f, 0.f);
+        }
+      }
+      if (q < a.Nq) a.lse[((size_t)z * a.H + h) * a.Nq + q] = n > 0 ? m_use + __log2f(l) : -INFINITY;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 10) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int HD>
+static cudaError_t launch2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                              cudaStream_t st) {
+  using L = Attn2Smem<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  dim3 grid((a.Nq + 255) / 256, a.H, a.nsplit);
+  attn_tc2_kernel<HD><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                            cudaStream_t st) {
+  if (a.hd == 128) return launch2_hd<128>(tq, tk, tvt, a, st);
+  if (a.hd == 64) return launch2_hd<64>(tq, tk, tvt, a, st);
+  return cudaErrorInvalidValue;
+}
+
 // Merge KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), fixed order.
 __global__ void attn_combine_kernel(const AttnTC a) {
   const int hd4 = a.hd / 4;

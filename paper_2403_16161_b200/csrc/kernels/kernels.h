@@ -71,6 +71,9 @@ struct AttnTC {
 };
 cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            cudaStream_t st);
+// two 128-query tiles per CTA, P kept in TMEM (see attn.cu)
+cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                            cudaStream_t st);
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st);
 
 }  // namespace vi
