@@ -183,7 +183,7 @@ def run_ours(args, cfg):
     time.sleep(0.3)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ctx.profile(1)                                  # attention kernels timed with events
+    ctx.profile(int(os.environ.get("VI_PROFILE_MODE", "1")))   # attention kernels timed with events
     l0 = ctx.launches()
     if world > 1:
         dist.barrier()
@@ -253,6 +253,9 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    if os.environ.get("VI_PROFILE_MODE") == "2":
+        line["profile_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}
+        line["profile_launches_per_step"] = {k: v[1] / args.steps for k, v in prof.items()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         s, sample_s = oracle_sample(cfg)
         line["cpu_baseline"] = {"value": T / s, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",

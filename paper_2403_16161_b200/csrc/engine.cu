@@ -117,10 +117,22 @@ struct vi_ctx {
   // tensor maps (bf16 path)
   CUtensorMap tm_tokens, tm_wembed, tm_h, tm_wqkv, tm_o, tm_wo, tm_w1, tm_g, tm_w2, tm_xb, tm_wback;
   CUtensorMap tm_q, tm_k, tm_vt;
-  int bn_embed = 128, bn_qkv = 128, bn_o = 64, bn_1 = 128, bn_2 = 64, bn_back = 128;
+  // N-tile per GEMM (persistent kernel: ~1-3 tiles per SM at M = 3600; N=64 MMAs run at 2/3 rate)
+  int bn_embed = 128, bn_qkv = 128, bn_o = 128, bn_1 = 128, bn_2 = 128, bn_back = 256;
 
   // profiling (vi_profile)
   int prof_mode = 0;
+  unsigned long long* attn_timing = nullptr;   // KernelTiming (device), used in profile mode 1
+  // CUDA graphs of whole steps (vi_run_step), keyed by everything baked into the launches
+  struct GraphEntry {
+    std::vector<uint64_t> key;
+    cudaGraphExec_t exec;
+    int64_t launches;
+    int64_t last_use;
+  };
+  std::vector<GraphEntry> graphs;
+  int64_t graph_clock = 0, weights_gen = 0;
+  bool use_graphs = true;
   struct Rec { int cat; cudaEvent_t a, b; };
   std::vector<Rec> prof_recs;
   std::vector<cudaEvent_t> ev_pool;
@@ -159,6 +171,7 @@ struct vi_ctx {
 
 vi_ctx::~vi_ctx() {
   if (stream) cudaStreamSynchronize(stream);
+  for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   for (auto& r : prof_recs) {
     cudaEventDestroy(r.a);
     cudaEventDestroy(r.b);
@@ -182,6 +195,11 @@ static const bool g_debug_sync = [] {
 // VI_ATTN_V1=1 selects the one-Q-tile attention kernel (A/B comparisons).
 static const bool g_attn_v1 = [] {
   const char* e = getenv("VI_ATTN_V1");
+  return e && e[0] == '1';
+}();
+// VI_ATTN_COLSPLIT=1: attention v2 with the column-split softmax (A/B experiments).
+static const bool g_attn_colsplit = [] {
+  const char* e = getenv("VI_ATTN_COLSPLIT");
   return e && e[0] == '1';
 }();
 static void debug_wait(vi_ctx* c, const char* where) {
@@ -228,7 +246,7 @@ struct Prof {
   int cat;
   cudaEvent_t b = nullptr;
   Prof(vi_ctx* c_, int cat_) : c(c_), cat(cat_) {
-    if (c->prof_mode == 2 || (c->prof_mode == 1 && cat == VI_PROF_ATTN)) {
+    if (c->prof_mode == 2) {
       cudaEvent_t a = c->prof_ev();
       b = c->prof_ev();
       cudaEventRecord(a, c->stream);
@@ -383,6 +401,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     c->lse = (float*)A((size_t)kMaxSplit * c->H * rows * 4);
   }
   c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);
+  c->attn_timing = (unsigned long long*)A(sizeof(KernelTiming));
   if (!ok) {
     delete c;
     return VI_E_OOM;
@@ -390,6 +409,17 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   if (cudaDeviceSynchronize() != cudaSuccess) {
     delete c;
     return VI_E_CUDA;
+  }
+  {
+    KernelTiming kt;
+    std::memset(&kt, 0, sizeof(kt));
+    kt.tmin = ~0ull;
+    if (cudaMemcpy(c->attn_timing, &kt, sizeof(kt), cudaMemcpyHostToDevice) != cudaSuccess) {
+      delete c;
+      return VI_E_CUDA;
+    }
+    const char* ng = getenv("VI_NO_GRAPH");
+    c->use_graphs = !(ng && ng[0] == '1') && c->own_stream;
   }
   if (c->bf16) {
     if (c->D % 128) c->bn_o = c->bn_2 = 64;
@@ -469,6 +499,7 @@ extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
   }
   U(upload_f32(c, c->b_back, w->back_b, Pd));
   if (st == VI_OK) c->have_weights = true;
+  ++c->weights_gen;
   return st;
 }
 
@@ -610,7 +641,8 @@ static void choose_split(int units, int ntiles, int* nsplit, int* tps) {
   for (int s = 1; s <= kMaxSplit && s <= ntiles; ++s) {
     const int t = (ntiles + s - 1) / s;
     const int waves = (units * s + 147) / 148;
-    const double cost = double(waves) * t + (s > 1 ? 2.0 + 0.15 * s : 0.0);
+    // per-CTA fixed cost (TMEM alloc, Q load, pipeline fill, partial epilogue) ~ 4 tiles
+    const double cost = double(waves) * (t + 4.0) + (s > 1 ? 1.0 + 0.3 * s : 0.0);
     if (cost < best - 1e-9) {
       best = cost;
       *nsplit = s;
@@ -678,11 +710,31 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
     a.o = static_cast<bf16*>(c->o); a.opart = c->opart; a.lse = c->lse;
+    a.timing = c->prof_mode == 1 ? c->attn_timing : nullptr;
+    static long long* trace_buf = nullptr;
+    static int trace_calls = 0;
+    if (getenv("VI_ATTN_TRACE") && !trace_buf) cudaMalloc(&trace_buf, 32 * 32 * sizeof(long long));
+    if (trace_buf && l == 0 && ++trace_calls == 5) {
+      cudaMemsetAsync(trace_buf, 0, 32 * 32 * sizeof(long long), c->stream);
+      a.trace = trace_buf;
+    }
     if (g_attn_v1)
       PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
     else
-      PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
+      PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream, g_attn_colsplit), "attention");
     if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
+    if (a.trace) {
+      long long h[32 * 32];
+      cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
+      cudaStreamSynchronize(c->stream);
+      const long long t0 = h[0];
+      fprintf(stderr, "[trace] j | t0: S_rdy[4] Ph0[4] Ph1[4] | t1: S_rdy[4] Ph0[4] Ph1[4] | mma t0: wait h0 h1 qk | t1: wait h0 h1 qk\n");
+      for (int j = 0; j < std::min(a.tiles_per_split, 32); ++j) {
+        fprintf(stderr, "[trace] %2d", j);
+        for (int e = 0; e < 32; ++e) fprintf(stderr, "%s%6lld", (e % 4 == 0) ? " |" : " ", h[j * 32 + e] ? h[j * 32 + e] - t0 : -1);
+        fprintf(stderr, "\n");
+      }
+    }
   } else {
     AttnArgs a;
     a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->S; a.vt_ld = c->vt_ld; a.valid = valid;
@@ -757,6 +809,15 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
   return VI_OK;
 }
 
+// The device part of one step (split+embed, L blocks, back-projection+composite).
+static vi_status step_body(vi_ctx* c, const void* fin, int n, void* fout) {
+  vi_status st;
+  if ((st = vi_soft_split(c, fin, n, c->x_ws, 1)) != VI_OK) return st;
+  for (int l = 0; l < c->L; ++l)
+    if ((st = vi_memory_step(c, l, c->x_ws, c->x_ws)) != VI_OK) return st;
+  return vi_soft_composite(c, c->x_ws, n, fout, 1);
+}
+
 extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, int64_t* first_id) {
   LIVE(c);
   if (!feat || !out || n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_run_step: bad argument");
@@ -768,13 +829,55 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
     CK(cudaMemcpyAsync(c->feat_in, feat, fbytes, cudaMemcpyHostToDevice, c->stream), "run_step h2d");
     fin = c->feat_in;
   }
-  vi_status st = vi_memory_push(c, n, first_id, nullptr, nullptr);
+  vi_status st = vi_memory_push(c, n, first_id, nullptr, nullptr);   // host bookkeeping + queued commits
   if (st != VI_OK) return st;
-  if ((st = vi_soft_split(c, fin, n, c->x_ws, 1)) != VI_OK) return st;
-  for (int l = 0; l < c->L; ++l)
-    if ((st = vi_memory_step(c, l, c->x_ws, c->x_ws)) != VI_OK) return st;
   void* fout = hout ? c->feat_out : out;
-  if ((st = vi_soft_composite(c, c->x_ws, n, fout, 1)) != VI_OK) return st;
+  const bool graphs = c->use_graphs && !g_debug_sync && c->prof_mode != 2 && !getenv("VI_ATTN_TRACE");
+  if (!graphs) {
+    if ((st = step_body(c, fin, n, fout)) != VI_OK) return st;
+  } else {
+    // everything a replay bakes in: shapes, ring state, buffers, weights, profiling mode
+    std::vector<uint64_t> key = {uint64_t(n), uint64_t(c->ring.cur_first % c->S), c->ring.valid_mask(),
+                                 uint64_t(reinterpret_cast<uintptr_t>(fin)), uint64_t(reinterpret_cast<uintptr_t>(fout)),
+                                 uint64_t(c->prof_mode), uint64_t(c->weights_gen)};
+    vi_ctx::GraphEntry* hit = nullptr;
+    for (auto& g : c->graphs)
+      if (g.key == key) hit = &g;
+    if (!hit) {
+      const int64_t l0 = c->launches;
+      cudaGraph_t graph = nullptr;
+      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+      st = step_body(c, fin, n, fout);
+      cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+      if (st != VI_OK) {
+        if (graph) cudaGraphDestroy(graph);
+        return st;
+      }
+      if (ce != cudaSuccess) return c->cuda_fail(ce, "graph capture end");
+      cudaGraphExec_t exec = nullptr;
+      ce = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      if (ce != cudaSuccess) return c->cuda_fail(ce, "graph instantiate");
+      if (c->graphs.size() >= 32) {   // evict the least recently used
+        auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                    [](const vi_ctx::GraphEntry& a, const vi_ctx::GraphEntry& b) {
+                                      return a.last_use < b.last_use;
+                                    });
+        cudaGraphExecDestroy(lru->exec);
+        c->graphs.erase(lru);
+      }
+      c->graphs.push_back({key, exec, c->launches - l0, 0});
+      c->launches = l0;
+      hit = &c->graphs.back();
+    } else {
+      c->next_layer = c->L;               // the host-side protocol state a replay skips
+      std::lock_guard<std::mutex> lk(c->mu);
+      c->ring.mark_stepped();
+    }
+    hit->last_use = ++c->graph_clock;
+    c->launches += hit->launches;
+    CK(cudaGraphLaunch(hit->exec, c->stream), "graph launch");
+  }
   if (hout) {
     CK(cudaMemcpyAsync(out, c->feat_out, fbytes, cudaMemcpyDeviceToHost, c->stream), "run_step d2h");
     CK(cudaStreamSynchronize(c->stream), "run_step sync");
@@ -800,6 +903,15 @@ extern "C" vi_status vi_profile_read(vi_ctx* c, double* ms, int64_t* launches) {
   CK(cudaStreamSynchronize(c->stream), "profile sync");
   double acc[VI_PROF_N] = {0, 0, 0, 0};
   int64_t cnt[VI_PROF_N] = {0, 0, 0, 0};
+  {  // attention kernels' self-timing (mode 1; graph-safe)
+    KernelTiming kt;
+    CK(cudaMemcpy(&kt, c->attn_timing, sizeof(kt), cudaMemcpyDeviceToHost), "profile read");
+    acc[VI_PROF_ATTN] += double(kt.total_ns) * 1e-6;
+    cnt[VI_PROF_ATTN] += int64_t(kt.launches);
+    std::memset(&kt, 0, sizeof(kt));
+    kt.tmin = ~0ull;
+    CK(cudaMemcpy(c->attn_timing, &kt, sizeof(kt), cudaMemcpyHostToDevice), "profile reset");
+  }
   for (auto& r : c->prof_recs) {
     float t = 0.f;
     if (cudaEventElapsedTime(&t, r.a, r.b) == cudaSuccess) {

@@ -374,11 +374,21 @@ struct Attn2Smem {
   static constexpr int K_OFF = 2 * QB;
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
-  static constexpr int NBAR = 1 + 4 * ST + 2 + 2 + 2;
-  static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
+  static constexpr int NBAR = 1 + 4 * ST + 2 + 4 + 2;
+  static constexpr int XCH_OFF = BAR_OFF + NBAR * 8 + 16;      // [2 phases][2 halves][128 rows] fp32
+  static constexpr int TOTAL = XCH_OFF + 2 * 2 * 128 * 4 + 1024;
 };
 
-template <int HD>
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+
+// CS = false: one softmax warpgroup per Q tile (thread = row, all 128 keys);
+// CS = true : column split -- all 8 softmax warps work on each Q tile in turn, warp w and
+//             w+4 own the same 32 rows and keys [0,64) / [64,128) of the tile; the row max
+//             is exchanged through shared memory (named barrier per warp pair).  Halves
+//             the per-tile softmax latency that sits on the tensor core's critical path.
+template <int HD, bool CS>
 __global__ void __launch_bounds__(384, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
@@ -393,8 +403,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint64_t* v_full = k_empty + ST;
   uint64_t* v_empty = v_full + ST;
   uint64_t* s_full = v_empty + ST;    // [2] per Q tile
-  uint64_t* p_full = s_full + 2;      // [2]
-  uint64_t* o_final = p_full + 2;     // [2]
+  uint64_t* p_full = s_full + 2;      // [2 tiles][2 key halves]
+  uint64_t* o_final = p_full + 4;     // [2]
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -418,7 +428,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[t], 128);
+      mbar_init(&p_full[2 * t], 128);
+      mbar_init(&p_full[2 * t + 1], 128);
       mbar_init(&o_final[t], 1);
     }
     fence_barrier_init();
@@ -428,6 +439,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) time_begin(a.timing);
 
   if (warp == 8) {
     if (lane == 0 && n > 0) {
@@ -462,17 +474,24 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD);
       const uint32_t sq = smem_u32(smem + L::Q_OFF);
       mbar_wait(q_full, 0);
-      auto issue_pv = [&](int t, int j) {            // O_t (+)= P_t(j) V(j)
+      const bool trm = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0;
+      auto issue_pv = [&](int t, int j) {            // O_t (+)= P_t(j) V(j), one key half at a time
         const int st = j % ST;
-        mbar_wait(&p_full[t], j & 1);
+        if (trm && j < 32) a.trace[j * 32 + 24 + t * 4] = clock64();
         if (t == 0) mbar_wait(&v_full[st], (j / ST) & 1);
-        tc_fence_after();
         const uint32_t sv = smem_u32(smem + L::V_OFF + st * L::VB);
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t offv = (kk >> 2) * (HD * 128) + (kk & 3) * 32;
-          umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_k_sw128(sv + offv), idesc_o,
-                       (j | kk) != 0);
+        for (int hh = 0; hh < 2; ++hh) {
+          mbar_wait(&p_full[2 * t + hh], j & 1);
+          if (trm && j < 32) a.trace[j * 32 + 25 + t * 4 + hh] = clock64();
+          tc_fence_after();
+#pragma unroll
+          for (int k4 = 0; k4 < 4; ++k4) {
+            const int kk = hh * 4 + k4;
+            const uint32_t offv = hh * (HD * 128) + k4 * 32;
+            umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8, sdesc_k_sw128(sv + offv), idesc_o,
+                         (j | kk) != 0);
+          }
         }
         if (t == 1) umma_commit(&v_empty[st]);
       };
@@ -491,6 +510,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         umma_commit(&s_full[t]);
         if (t == 1) umma_commit(&k_empty[st]);
+        if (trm && j > 0 && j <= 32) a.trace[(j - 1) * 32 + 27 + t * 4] = clock64();
       };
       for (int j = 0; j < n; ++j) {
         for (int t = 0; t < 2; ++t) {
@@ -503,6 +523,138 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         umma_commit(&o_final[t]);
       }
     }
+  } else if (warp < 8 && CS) {
+    const int qd = warp & 3, hf = warp >> 2;          // lane quadrant, key half
+    const int row = qd * 32 + lane;
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    float* xch = reinterpret_cast<float*>(smem + L::XCH_OFF);
+    constexpr int OH = HD / 2;                        // O columns owned by this half
+    float m_use[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
+    int phase = 0;
+    const float2 cc = make_float2(a.scale_log2, a.scale_log2);
+    for (int jj = 0; jj < n; ++jj) {
+      int row0, nv, nskip;
+      key_tile(a.segs, t_begin + jj, row0, nv, nskip);
+      const int lo = nskip - hf * 64, hi = nv - hf * 64;   // valid local keys [lo, hi)
+#pragma unroll 1
+      for (int t = 0; t < 2; ++t, ++phase) {
+        const uint32_t TS = tmem + t * 128 + lane_off, TO = tmem + 256 + t * 128 + lane_off;
+        mbar_wait(&s_full[t], jj & 1);
+        tc_fence_after();
+        float s[64];
+        tmem_ld32(TS + hf * 64, reinterpret_cast<uint32_t*>(s));
+        tmem_ld32(TS + hf * 64 + 32, reinterpret_cast<uint32_t*>(s + 32));
+        tmem_wait_ld();
+        if (lo > 0 || hi < 64) {
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i < lo || i >= hi) s[i] = -INFINITY;
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 64; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
+        const float lm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
+        float* xb = xch + (phase & 1) * 256;
+        xb[hf * 128 + row] = lm;
+        named_bar_sync(1 + qd, 64);                   // both halves loaded S and posted a max
+        const float rmax = fmaxf(lm, xb[(hf ^ 1) * 128 + row]) * a.scale_log2;
+        const bool grow = rmax > m_use[t] + 8.f;      // lazy rescale (identical in both halves)
+        float alpha = 1.f;
+        if (grow) {
+          alpha = ex2(m_use[t] - rmax);
+          m_use[t] = rmax;
+        }
+        if (__any_sync(0xffffffffu, grow) && jj > 0) {
+#pragma unroll 1
+          for (int c = 0; c < OH; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(TO + hf * OH + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(TO + hf * OH + c, r);
+          }
+        }
+        const float2 mm = make_float2(-m_use[t], -m_use[t]);
+        float2 sum[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sum[i] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 2; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int i = c * 16 + k;
+            const float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
+            float2 p;
+            if ((k & 3) == 3) {
+              p = exp2_poly2(x);
+            } else {
+              p.x = ex2(x.x);
+              p.y = ex2(x.y);
+            }
+            __nv_bfloat162 b = __floats2bfloat162_rn(p.x, p.y);
+            pk[k] = *reinterpret_cast<uint32_t*>(&b);
+            sum[k & 3] = fadd2(sum[k & 3], p);
+          }
+          tmem_st16(TS + hf * 32 + c * 16, pk);     // P keys [hf*64, +64) -> packed cols [hf*32, +32)
+        }
+        const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
+        l[t] = l[t] * alpha + (s01.x + s01.y);
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * t + hf]);
+      }
+    }
+    // epilogue: combine the two halves' row sums, each warp writes its O column half
+#pragma unroll 1
+    for (int t = 0; t < 2; ++t, ++phase) {
+      float* xb = xch + (phase & 1) * 256;
+      xb[hf * 128 + row] = l[t];
+      named_bar_sync(1 + qd, 64);
+      const float lt = l[t] + xb[(hf ^ 1) * 128 + row];
+      const uint32_t TO = tmem + 256 + t * 128 + lane_off + hf * OH;
+      const int q = q0 + t * 128 + row;
+      if (n > 0) {
+        mbar_wait(&o_final[t], 0);
+        tc_fence_after();
+      }
+      const float inv = n > 0 ? 1.f / lt : 0.f;
+#pragma unroll 1
+      for (int c = 0; c < OH; c += 32) {
+        uint32_t r[32];
+        if (n > 0) {
+          tmem_ld32(TO + c, r);
+          tmem_wait_ld();
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
+        }
+        if (q < a.Nq) {
+          const float* f = reinterpret_cast<const float*>(r);
+          const int col = h * HD + hf * OH + c;
+          if (a.nsplit == 1) {
+            uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.D + col);
+#pragma unroll
+            for (int i = 0; i < 4; ++i)
+              dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv),
+                                  pack_bf16(f[8 * i + 2] * inv, f[8 * i + 3] * inv),
+                                  pack_bf16(f[8 * i + 4] * inv, f[8 * i + 5] * inv),
+                                  pack_bf16(f[8 * i + 6] * inv, f[8 * i + 7] * inv));
+          } else {
+            float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)z * a.Nq + q) * a.D + col);
+#pragma unroll
+            for (int i = 0; i < 8; ++i)
+              dst[i] = make_float4(f[4 * i] * inv, f[4 * i + 1] * inv, f[4 * i + 2] * inv, f[4 * i + 3] * inv);
+          }
+        }
+      }
+      if (a.nsplit > 1 && hf == 0 && q < a.Nq)
+        a.lse[((size_t)z * a.H + h) * a.Nq + q] = n > 0 ? m_use[t] + __log2f(lt) : -INFINITY;
+    }
   } else if (warp < 8) {
     const int t = warp >> 2;                          // Q tile of this warpgroup
     const int qd = warp & 3;                          // TMEM lane quadrant
@@ -512,7 +664,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     for (int jj = 0; jj < n; ++jj) {
       int row0, nv, nskip;
       key_tile(a.segs, t_begin + jj, row0, nv, nskip);
+      const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && jj < 32;
       mbar_wait(&s_full[t], jj & 1);
+      if (tr) a.trace[jj * 32 + t * 12 + qd] = clock64();
       tc_fence_after();
       float s[128];
 #pragma unroll
@@ -548,25 +702,42 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           tmem_st32(TO + c, r);
         }
       }
-      float sum[8];
+      // p = 2^(s c - m): 10 of every 16 pairs on the MUFU (ex2), 6 by polynomial on the FMA
+      // pipe (balances MUFU time and issue slots); packed FFMA2 / FADD2.  P goes back to
+      // TMEM 32 keys (16 packed columns) at a time and each key half is handed to the MMA
+      // warp as soon as it is written, so PV on keys 0-63 overlaps the exps of 64-127.
+      const float2 cc = make_float2(a.scale_log2, a.scale_log2), mm = make_float2(-m_use, -m_use);
+      float2 sum[4];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) sum[i] = 0.f;
-      uint32_t pk[64];
+      for (int i = 0; i < 4; ++i) sum[i] = make_float2(0.f, 0.f);
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float p0 = ex2(fmaf(s[2 * i], a.scale_log2, -m_use));
-        const float p1 = ex2(fmaf(s[2 * i + 1], a.scale_log2, -m_use));
-        __nv_bfloat162 b = __floats2bfloat162_rn(p0, p1);
-        pk[i] = *reinterpret_cast<uint32_t*>(&b);
-        const float2 r = __bfloat1622float2(b);       // the row sum uses the rounded P
-        sum[i & 7] += r.x + r.y;
+      for (int c = 0; c < 4; ++c) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int k = 0; k < 16; ++k) {
+          const int i = c * 16 + k;
+          const float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
+          float2 p;
+          if (k % 5 >= 3) {
+            p = exp2_poly2(x);
+          } else {
+            p.x = ex2(x.x);
+            p.y = ex2(x.y);
+          }
+          __nv_bfloat162 b = __floats2bfloat162_rn(p.x, p.y);
+          pk[k] = *reinterpret_cast<uint32_t*>(&b);
+          sum[k & 3] = fadd2(sum[k & 3], p);
+        }
+        tmem_st16(TS + c * 16, pk);
+        if (c & 1) {
+          tmem_wait_st();
+          tc_fence_before();
+          if (tr) a.trace[jj * 32 + t * 12 + 4 + (c >> 1) * 4 + qd] = clock64();
+          mbar_arrive(&p_full[2 * t + (c >> 1)]);
+        }
       }
-      l = l * alpha + (((sum[0] + sum[1]) + (sum[2] + sum[3])) + ((sum[4] + sum[5]) + (sum[6] + sum[7])));
-#pragma unroll
-      for (int c = 0; c < 2; ++c) tmem_st32(TS + c * 32, pk + c * 32);
-      tmem_wait_st();
-      tc_fence_before();
-      mbar_arrive(&p_full[t]);
+      const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
+      l = l * alpha + (s01.x + s01.y);
     }
     // epilogue
     const int q = q0 + t * 128 + qd * 32 + lane;
@@ -613,36 +784,39 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
+  if (threadIdx.x == 0) time_end(a.timing, gridDim.x * gridDim.y * gridDim.z);
   if (warp == 10) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
 
-template <int HD>
+template <int HD, bool CS>
 static cudaError_t launch2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                               cudaStream_t st) {
   using L = Attn2Smem<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_tc2_kernel<HD, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   dim3 grid((a.Nq + 255) / 256, a.H, a.nsplit);
-  attn_tc2_kernel<HD><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
+  attn_tc2_kernel<HD, CS><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                            cudaStream_t st) {
-  if (a.hd == 128) return launch2_hd<128>(tq, tk, tvt, a, st);
-  if (a.hd == 64) return launch2_hd<64>(tq, tk, tvt, a, st);
+                            cudaStream_t st, bool colsplit) {
+  if (a.hd == 128) return colsplit ? launch2_hd<128, true>(tq, tk, tvt, a, st) : launch2_hd<128, false>(tq, tk, tvt, a, st);
+  if (a.hd == 64) return colsplit ? launch2_hd<64, true>(tq, tk, tvt, a, st) : launch2_hd<64, false>(tq, tk, tvt, a, st);
   return cudaErrorInvalidValue;
 }
 
 // Merge KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), fixed order.
 __global__ void attn_combine_kernel(const AttnTC a) {
+  if (threadIdx.x == 0) time_begin(a.timing);
   const int hd4 = a.hd / 4;
   const size_t total = (size_t)a.Nq * a.H * hd4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -665,6 +839,8 @@ __global__ void attn_combine_kernel(const AttnTC a) {
     uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)q * a.D + h * a.hd + c4 * 4);
     *dst = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   }
+  __syncthreads();
+  if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
 }
 
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st) {

@@ -179,6 +179,68 @@ __device__ __forceinline__ void tmem_st32(uint32_t taddr, const uint32_t* r) {
 __device__ __forceinline__ void tmem_wait_ld(){ asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
 __device__ __forceinline__ void tmem_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
 
+// packed fp32x2 arithmetic (Blackwell FFMA2 / FADD2: two lanes of work per instruction)
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rc, rd;\n\t"
+      "mov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\tmov.b64 rc, {%6,%7};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rc;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y), "f"(c.x), "f"(c.y));
+  return d;
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  float2 d;
+  asm("{.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2,%3};\n\tmov.b64 rb, {%4,%5};\n\t"
+      "add.rn.f32x2 rd, ra, rb;\n\tmov.b64 {%0,%1}, rd;}"
+      : "=f"(d.x), "=f"(d.y)
+      : "f"(a.x), "f"(a.y), "f"(b.x), "f"(b.y));
+  return d;
+}
+// 2^x for two lanes on the FMA/ALU pipes (offloads the MUFU unit): x = j + f with
+// j = rint(x) (magic-number rounding), f in [-1/2, 1/2], 2^f by a degree-3 minimax
+// polynomial (max rel. error 7.5e-5, far below the bf16 rounding P then gets), and j
+// added to the exponent field.  x is clamped to >= -125 (2^-125 ~ 0 for softmax).
+__device__ __forceinline__ float2 exp2_poly2(float2 x) {
+  const float2 magic = make_float2(12582912.f, 12582912.f);   // 1.5 * 2^23
+  x.x = fmaxf(x.x, -125.f);
+  x.y = fmaxf(x.y, -125.f);
+  const float2 t = fadd2(x, magic);
+  const float2 r = fadd2(t, make_float2(-12582912.f, -12582912.f));
+  const float2 f = ffma2(r, make_float2(-1.f, -1.f), x);
+  float2 p = ffma2(make_float2(0.0551716685f, 0.0551716685f), f, make_float2(0.2426111549f, 0.2426111549f));
+  p = ffma2(p, f, make_float2(0.6932609677f, 0.6932609677f));
+  p = ffma2(p, f, make_float2(0.9999280572f, 0.9999280572f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(t.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
+}
+
+__device__ __forceinline__ unsigned long long globaltimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+// kernel self-timing (see KernelTiming in kernels.h): call time_begin at CTA start and
+// time_end when the CTA is done (thread 0 only).
+__device__ __forceinline__ void time_begin(unsigned long long* tm) {
+  if (tm) atomicMin(&tm[0], globaltimer());
+}
+__device__ __forceinline__ void time_end(unsigned long long* tm, unsigned int nctas) {
+  if (!tm) return;
+  atomicMax(&tm[1], globaltimer());
+  __threadfence();
+  if (atomicAdd(&tm[2], 1ull) == nctas - 1) {
+    __threadfence();
+    const unsigned long long t0 = atomicAdd(&tm[0], 0ull), t1 = atomicAdd(&tm[1], 0ull);
+    atomicAdd(&tm[3], t1 - t0);
+    atomicAdd(&tm[4], 1ull);
+    atomicExch(&tm[0], ~0ull);
+    atomicExch(&tm[1], 0ull);
+    atomicExch(&tm[2], 0ull);
+  }
+}
+
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));

@@ -48,6 +48,13 @@ struct KeySegs {            // contiguous runs of valid ring slots, as slab row 
   int tile0[33];            // prefix count of 128-key tiles per segment
 };
 
+// Device-side self-timing of a sequence of stream-ordered launches (graph-safe): every CTA
+// folds its start / end globaltimer into [tmin, tmax]; the last CTA to finish adds
+// tmax - tmin to total_ns, counts the launch and resets the window.
+struct KernelTiming {
+  unsigned long long tmin, tmax, done, total_ns, launches, pad[3];
+};
+
 struct AttnArgs {
   int Nq, D, H, hd, P, S, vt_ld;
   uint64_t valid;           // slot validity mask
@@ -67,13 +74,15 @@ struct AttnTC {
   bf16* o;                  // [Nq][D] final (nsplit == 1)
   float* opart;             // [nsplit][Nq][D] normalised partial outputs (nsplit > 1)
   float* lse;               // [nsplit][H][Nq] log2-sum-exp of the partials
+  long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
+  unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves
   int H;
 };
 cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            cudaStream_t st);
 // two 128-query tiles per CTA, P kept in TMEM (see attn.cu)
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                            cudaStream_t st);
+                            cudaStream_t st, bool colsplit);
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st);
 
 }  // namespace vi

@@ -1,0 +1,57 @@
+// Standalone timing of the tcgen05 GEMM kernel (gemm_tc.cu) on the memory-step shapes.
+#include <cstdio>
+#include <vector>
+#include "../../paper_2403_16161_b200/csrc/kernels/gemm_tc.cu"
+using namespace vi;
+
+typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN enc() {
+  void* p; cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  return (PFN)p;
+}
+static CUtensorMap tmap(void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
+  CUtensorMap m; cuuint64_t d[2] = {inner, outer}; cuuint64_t s[1] = {inner * 2}; cuuint32_t b[2] = {bi, bo}, e[2] = {1, 1};
+  enc()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+        CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return m;
+}
+
+static void run(const char* name, int M, int N, int K, int bn, int kind) {
+  void *A, *W, *O; float *bias, *x;
+  cudaMalloc(&A, (size_t)M * K * 2); cudaMalloc(&W, (size_t)N * K * 2); cudaMalloc(&O, (size_t)M * N * 4);
+  cudaMalloc(&bias, N * 4); cudaMalloc(&x, (size_t)M * N * 4);
+  cudaMemset(A, 0, (size_t)M * K * 2); cudaMemset(W, 0, (size_t)N * K * 2); cudaMemset(bias, 0, N * 4); cudaMemset(x, 0, (size_t)M * N * 4);
+  CUtensorMap ta = tmap(A, K, M, 64, 128), tb = tmap(W, K, N, 64, bn);
+  Epi e; memset(&e, 0, sizeof(e));
+  e.kind = kind; e.M = M; e.N = N; e.bias = bias; e.out = O; e.ldo = N; e.P = 1; e.S = 1; e.x_in = x; e.x_out = x;
+  cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
+  for (int i = 0; i < 3; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0);
+  const int it = 50;
+  cudaEventRecord(a);
+  for (int i = 0; i < it; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0);
+  cudaEventRecord(b);
+  cudaError_t err = cudaEventSynchronize(b);
+  float ms; cudaEventElapsedTime(&ms, a, b);
+  const double us = ms * 1000 / it, tf = 2.0 * M * N * K / (us * 1e-6) / 1e12;
+  printf("%-8s M=%d N=%d K=%d BN=%d epi=%d: %s %.2f us  %.0f TFLOP/s\n", name, M, N, K, bn, kind, cudaGetErrorString(err), us, tf);
+  cudaFree(A); cudaFree(W); cudaFree(O); cudaFree(bias); cudaFree(x);
+}
+
+int main() {
+  run("qkv", 3600, 1536, 512, 128, EPI_STORE);
+  run("oproj", 3600, 512, 512, 128, EPI_RESID);
+  run("ffn1", 3600, 1960, 512, 128, EPI_STORE);
+  run("ffn2", 3600, 512, 1960, 128, EPI_RESID);
+  run("embed", 3600, 512, 6272, 128, EPI_STORE);
+  run("back", 3600, 6272, 1024, 256, EPI_STORE);
+  run("big", 8192, 8192, 8192, 256, EPI_STORE);
+  run("o_k64", 3600, 512, 64, 128, EPI_RESID);
+  run("o_k64s", 3600, 512, 64, 128, EPI_STORE);
+  run("one", 128, 128, 64, 128, EPI_STORE);
+  run("one_k512", 128, 128, 512, 128, EPI_STORE);
+  run("m3600n128", 3600, 128, 512, 128, EPI_STORE);
+  return 0;
+}
