@@ -12,7 +12,7 @@
 
 namespace vi {
 
-enum EpiKind : int { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_QKV = 3 };
+enum EpiKind : int { EPI_STORE = 0, EPI_GELU = 1, EPI_RESID = 2, EPI_QKV = 3, EPI_NONE = 4 };
 
 struct Epi {
   int kind;
@@ -65,20 +65,20 @@ __device__ __forceinline__ void epi_one(const Epi& e, int m, int n, float acc) {
 }
 
 // 32 consecutive columns n0..n0+31 of row m (tensor-core epilogue; one thread per row).
-__device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, float* v) {
-  if (m >= e.M) return;
-  const bool full = (n0 + 32 <= e.N);
-  if (!full) {
-    for (int i = 0; i < 32 && n0 + i < e.N; ++i) epi_one<bf16>(e, m, n0 + i, v[i]);
+// bias_s: the bias of these columns staged in shared memory (broadcast reads) or NULL;
+// xin: x_in[m][n0..n0+31] already loaded (EPI_RESID; issued before the TMEM load wait).
+__device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, float* v, const float* bias_s,
+                                               const float4* xin) {
+  if (m >= e.M || e.kind == EPI_NONE) return;
+  if (n0 + 32 > e.N) {                        // ragged N tail: element-wise, still in registers
+#pragma unroll
+    for (int i = 0; i < 32; ++i)
+      if (n0 + i < e.N) epi_one<bf16>(e, m, n0 + i, v[i]);
     return;
   }
-  if (e.bias) {
-    const float4* b4 = reinterpret_cast<const float4*>(e.bias + n0);
+  if (bias_s) {
 #pragma unroll
-    for (int i = 0; i < 8; ++i) {
-      float4 b = __ldg(b4 + i);
-      v[4 * i] += b.x; v[4 * i + 1] += b.y; v[4 * i + 2] += b.z; v[4 * i + 3] += b.w;
-    }
+    for (int i = 0; i < 32; ++i) v[i] += bias_s[i];
   }
   switch (e.kind) {
     case EPI_STORE:
@@ -87,9 +87,12 @@ __device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, floa
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
       } else if (e.pos) {
-        const float* pr = e.pos + (size_t)(m % e.P) * e.N + n0;
+        const float4* pr = reinterpret_cast<const float4*>(e.pos + (size_t)(m % e.P) * e.N + n0);
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] += pr[i];
+        for (int i = 0; i < 8; ++i) {
+          const float4 p = __ldg(pr + i);
+          v[4 * i] += p.x; v[4 * i + 1] += p.y; v[4 * i + 2] += p.z; v[4 * i + 3] += p.w;
+        }
       }
       if (e.out_f32) {
         float4* d4 = reinterpret_cast<float4*>(reinterpret_cast<float*>(e.out) + (size_t)m * e.ldo + n0);
@@ -105,11 +108,10 @@ __device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, floa
       break;
     }
     case EPI_RESID: {
-      const float4* xi = reinterpret_cast<const float4*>(e.x_in + (size_t)m * e.N + n0);
       float4* xo = reinterpret_cast<float4*>(e.x_out + (size_t)m * e.N + n0);
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        float4 a = xi[i];
+        const float4 a = xin[i];
         xo[i] = make_float4(a.x + v[4 * i], a.y + v[4 * i + 1], a.z + v[4 * i + 2], a.w + v[4 * i + 3]);
       }
       break;

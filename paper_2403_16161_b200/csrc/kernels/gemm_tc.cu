@@ -2,17 +2,24 @@
 //
 // Persistent, warp-specialised: grid = min(#tiles, #SMs) CTAs, each walks the 128 x BN
 // output tiles blockIdx.x, blockIdx.x + gridDim.x, ... (m fastest, so CTAs running at
-// the same time share the weight block in L2).  Warp roles (256 threads):
+// the same time share the weight block in L2).  Warp roles (384 threads):
 //   warp 0, lane 0 : TMA producer  (A box 64x128, W box 64xBN, 128-byte swizzle), an
 //                    STAGES-deep smem ring that keeps streaming across tile boundaries
 //   warp 1, lane 0 : MMA issuer    (tcgen05.mma kind::f16, M=128, N=BN, K=16 per instr)
 //   warp 2         : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
-//   warps 4..7     : epilogue      (tcgen05.ld 32x32b, thread = accumulator row)
-// With two accumulators the epilogue of tile i overlaps the mainloop of tile i+1.
+//   warps 4..11    : epilogue      (tcgen05.ld 32x32b, thread = accumulator row; warps w and
+//                    w+4 share a TMEM lane quadrant and split the tile's columns in half)
+// With two accumulators the epilogue of tile i overlaps the mainloop of tile i+1.  The
+// bias of a tile is staged in shared memory (broadcast reads) and residual rows are
+// loaded before the TMEM load is waited on, so the epilogue keeps pace with the MMAs.
 #include "epilogue.cuh"
 #include "kernels.h"
 
 namespace vi {
+
+__device__ __forceinline__ void gemm_named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
 
 template <int BN, int STAGES>
 struct GemmSmem {
@@ -20,11 +27,12 @@ struct GemmSmem {
   static constexpr int B_BYTES = BN * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int TOTAL = BAR_OFF + (2 * STAGES + 4) * 8 + 16 + 1024;  // +1024 alignment slack
+  static constexpr int BIAS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;   // [2][BN] fp32
+  static constexpr int TOTAL = BIAS_OFF + 2 * BN * 4 + 1024;              // +1024 alignment slack
 };
 
 template <int BN, int STAGES>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int brow0,
                Epi epi) {
   using L = GemmSmem<BN, STAGES>;
@@ -51,7 +59,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 128);
+      mbar_init(&tempty[b], 256);
     }
     fence_barrier_init();
   }
@@ -100,21 +108,35 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
     }
   } else if (warp >= 4) {
-    const int q = warp - 4;                      // TMEM lane quadrant of this warp
+    const int ew = warp - 4;                     // 0..7
+    const int q = ew & 3, hc = ew >> 2;          // TMEM lane quadrant, column half
+    const int etid = ew * 32 + lane;             // 0..255
+    float* bias_s = reinterpret_cast<float*>(smem + L::BIAS_OFF);
     int lt = 0;
     for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
       const int acc = lt & 1;
       const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+      float* bs = bias_s + acc * BN;
+      if (epi.bias) {
+        for (int i = etid; i < BN; i += 256) bs[i] = n0 + i < epi.N ? __ldg(epi.bias + n0 + i) : 0.f;
+      }
+      gemm_named_bar_sync(1, 256);
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
 #pragma unroll 1
-      for (int c = 0; c < BN; c += 32) {
+      for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += 32) {
         if (n0 + c >= epi.N) break;
         uint32_t r[32];
         tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c, r);
+        float4 xin[8];
+        if (epi.kind == EPI_RESID && m < epi.M && n0 + c + 32 <= epi.N) {
+          const float4* xi = reinterpret_cast<const float4*>(epi.x_in + (size_t)m * epi.N + n0 + c);
+#pragma unroll
+          for (int i = 0; i < 8; ++i) xin[i] = xi[i];
+        }
         tmem_wait_ld();
-        epi_row32_bf16(epi, m, n0 + c, reinterpret_cast<float*>(r));
+        epi_row32_bf16(epi, m, n0 + c, reinterpret_cast<float*>(r), epi.bias ? bs + c : nullptr, xin);
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
@@ -148,7 +170,7 @@ static cudaError_t launch_bn(const CUtensorMap& a, const CUtensorMap& b, int bro
   }
   const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN);
   const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  kfn<<<grid, 256, L::TOTAL, st>>>(a, b, K, brow0, e);
+  kfn<<<grid, 384, L::TOTAL, st>>>(a, b, K, brow0, e);
   return cudaGetLastError();
 }
 

@@ -40,18 +40,16 @@ static void run(const char* name, int M, int N, int K, int bn, int kind) {
   cudaFree(A); cudaFree(W); cudaFree(O); cudaFree(bias); cudaFree(x);
 }
 
-int main() {
-  run("qkv", 3600, 1536, 512, 128, EPI_STORE);
+int main(int argc, char** argv) {
+  if (argc > 1) { run("qkvS", 3600, 1536, 512, 128, EPI_STORE); return 0; }
   run("oproj", 3600, 512, 512, 128, EPI_RESID);
+  run("oprojS", 3600, 512, 512, 128, EPI_STORE);
+  run("oprojN", 3600, 512, 512, 128, EPI_NONE);
+  run("qkvN", 3600, 1536, 512, 128, EPI_NONE);
+  run("qkvS", 3600, 1536, 512, 128, EPI_STORE);
   run("ffn1", 3600, 1960, 512, 128, EPI_STORE);
   run("ffn2", 3600, 512, 1960, 128, EPI_RESID);
   run("embed", 3600, 512, 6272, 128, EPI_STORE);
   run("back", 3600, 6272, 1024, 256, EPI_STORE);
-  run("big", 8192, 8192, 8192, 256, EPI_STORE);
-  run("o_k64", 3600, 512, 64, 128, EPI_RESID);
-  run("o_k64s", 3600, 512, 64, 128, EPI_STORE);
-  run("one", 128, 128, 64, 128, EPI_STORE);
-  run("one_k512", 128, 128, 512, 128, EPI_STORE);
-  run("m3600n128", 3600, 128, 512, 128, EPI_STORE);
   return 0;
 }
