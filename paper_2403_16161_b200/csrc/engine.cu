@@ -278,6 +278,8 @@ static vi_status validate(const vi_config* k, std::string* why) {
   if (k->kh < k->sh || k->kw < k->sw || (oh - 1) * k->sh - k->ph + k->kh < k->feat_h ||
       (ow - 1) * k->sw - k->pw + k->kw < k->feat_w || k->ph >= k->kh || k->pw >= k->kw)
     return bad("split geometry leaves feature cells uncovered");
+  if ((k->kh + k->sh - 1) / k->sh > 3 || (k->kw + k->sw - 1) / k->sw > 3)
+    return bad("soft split/composite kernels support at most 3 overlapping windows per dimension");
   const int vec = k->dtype == VI_DTYPE_BF16 ? 8 : 4;
   if (k->feat_c % vec) return bad("feat_c must be a multiple of 8 (bf16) / 4 (fp32)");
   if (k->ffn_hidden < 1 || (k->ffn_kind != VI_FFN_MLP && k->ffn_kind != VI_FFN_F3N)) return bad("bad ffn");
@@ -761,8 +763,9 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_1 + (size_t)l * F * D, M, F, D, e1, c->stream),
            "ffn1 gemm");
   if (f3n) {
-    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, 1, n, c->gf, c->stream), "f3n fold");
-    PLAUNCH(VI_PROF_PATCH, launch_unfold_gelu(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream), "f3n unfold");
+    // g = GELU(unfold(fold(u))) = unfold(GELU(fold(u))): GELU once per folded cell
+    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, dt, n, c->gf, true, c->stream), "f3n fold");
+    PLAUNCH(VI_PROF_PATCH, launch_unfold(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream), "f3n unfold");
   }
   // a11: FFN2 + residual
   Epi e2 = epi_base(EPI_RESID, M, D, c->b_2 + (size_t)l * D);
@@ -805,7 +808,7 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
     }
     tok = c->bf16 ? c->yp32 : c->tokens;
   }
-  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, (project && c->bf16) ? 1 : dt, feat, dt, n, c->g, c->stream), "fold");
+  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, (project && c->bf16) ? 1 : dt, feat, dt, n, c->g, false, c->stream), "fold");
   return VI_OK;
 }
 

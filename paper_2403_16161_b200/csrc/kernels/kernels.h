@@ -15,10 +15,9 @@ struct Geom {
 // ---- patch gather kernels (HBM-bound) -------------------
 // soft split: in [n][H][W][C] -> out [n][P][kh*kw*C]; dtype 0 = bf16, 1 = fp32.
 cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st);
-// F3N second half: folded fp32 [n][H][W][Cf] -> GELU(unfold) bf16/fp32 [n][P][kh*kw*Cf]
-cudaError_t launch_unfold_gelu(const float* in, void* out, int n, const Geom& g, int out_dtype, cudaStream_t st);
-// fold with cover-count division: in [n][P][kh*kw*C] (in_dtype) -> out [n][H][W][C] (out_dtype)
-cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g,
+// fold with cover-count division: in [n][P][kh*kw*C] (in_dtype) -> out [n][H][W][C] (out_dtype),
+// optionally GELU of the folded value (Fusion-FFN).  Requires ceil(k/s) <= 3 per dimension.
+cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g, bool gelu,
                         cudaStream_t st);
 
 // ---- row kernels -------------------------------------------------------------------

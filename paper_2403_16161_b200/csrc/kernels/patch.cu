@@ -54,141 +54,110 @@ template <> struct Vec<float, 8> {
   }
 };
 
-// Pure copy (bit-exact) unfold: one thread per output vector.
+// Pure copy (bit-exact) unfold.  One CTA per token (t, oy, ox): its kh*kw*C outputs are
+// contiguous, so the CTA writes one contiguous run with 16-byte vectors; 32-bit index math.
 template <typename T, int VEC>
-__global__ void unfold_kernel(const T* __restrict__ in, T* __restrict__ out, int n, Geom g) {
+__global__ void __launch_bounds__(128) unfold_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g) {
   const int CV = g.C / VEC, KK = g.kh * g.kw, P = g.oh * g.ow;
-  const size_t total = (size_t)n * P * KK * CV;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int cv = int(i % CV);
-    size_t r = i / CV;
-    const int j = int(r % KK); r /= KK;
-    const int tok = int(r % P);
-    const int t = int(r / P);
-    const int oy = tok / g.ow, ox = tok - oy * g.ow;
+  const int tok = blockIdx.x % P, t = blockIdx.x / P;
+  const int oy = tok / g.ow, ox = tok - oy * g.ow;
+  const int y0 = oy * g.sh - g.ph, x0 = ox * g.sw - g.pw;
+  const T* src_t = in + (size_t)t * g.H * g.W * g.C;
+  T* dst = out + (size_t)blockIdx.x * KK * g.C;
+  for (int v = threadIdx.x; v < KK * CV; v += blockDim.x) {
+    const int j = v / CV, cv = v - j * CV;
     const int ky = j / g.kw, kx = j - ky * g.kw;
-    const int y = oy * g.sh - g.ph + ky, x = ox * g.sw - g.pw + kx;
-    T* dst = out + i * VEC;
+    const int y = y0 + ky, x = x0 + kx;
+    T* d = dst + v * VEC;
     if (y < 0 || y >= g.H || x < 0 || x >= g.W) {
-      Vec<T, VEC>::zero(dst);
+      Vec<T, VEC>::zero(d);
     } else {
-      const T* src = in + (((size_t)t * g.H + y) * g.W + x) * g.C + cv * VEC;
+      const T* src = src_t + (y * g.W + x) * g.C + cv * VEC;
       if constexpr (sizeof(T) == 2)
-        *reinterpret_cast<uint4*>(dst) = __ldg(reinterpret_cast<const uint4*>(src));
+        *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(src));
       else
-        *reinterpret_cast<float4*>(dst) = __ldg(reinterpret_cast<const float4*>(src));
+        *reinterpret_cast<float4*>(d) = __ldg(reinterpret_cast<const float4*>(src));
     }
   }
 }
 
-// F3N: GELU(unfold(folded fp32 map)) -> Tout.
-template <typename Tout, int VEC>
-__global__ void unfold_gelu_kernel(const float* __restrict__ in, Tout* __restrict__ out, int n, Geom g) {
+// Fold with cover-count normalisation (gather form), optional GELU of the folded value.
+// One CTA per output row (t, y): the covering window rows are CTA-uniform; each thread
+// owns 16-byte vectors of cells (x, c).  Up to MAXC x MAXC covering windows are loaded
+// first (predicated, all in flight) and then summed in token order (oy, then ox).
+// GELU(unfold(z)) = unfold(GELU(z)) (unfold copies, GELU(0) = 0), so the Fusion-FFN
+// applies its GELU here, once per folded cell.
+template <typename Tin, typename Tout, int VEC, bool GELU>
+__global__ void __launch_bounds__(256) fold_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g) {
+  constexpr int MAXC = 3;
   const int CV = g.C / VEC, KK = g.kh * g.kw, P = g.oh * g.ow;
-  const size_t total = (size_t)n * P * KK * CV;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int cv = int(i % CV);
-    size_t r = i / CV;
-    const int j = int(r % KK); r /= KK;
-    const int tok = int(r % P);
-    const int t = int(r / P);
-    const int oy = tok / g.ow, ox = tok - oy * g.ow;
-    const int ky = j / g.kw, kx = j - ky * g.kw;
-    const int y = oy * g.sh - g.ph + ky, x = ox * g.sw - g.pw + kx;
-    float f[VEC];
-    if (y < 0 || y >= g.H || x < 0 || x >= g.W) {
+  const int y = blockIdx.x % g.H, t = blockIdx.x / g.H;
+  const int yy = y + g.ph;
+  int oy0 = yy - g.kh + 1;
+  oy0 = oy0 <= 0 ? 0 : (oy0 + g.sh - 1) / g.sh;
+  int oy1 = yy / g.sh;
+  if (oy1 > g.oh - 1) oy1 = g.oh - 1;
+  const Tin* in_t = in + (size_t)t * P * KK * g.C;
+  Tout* out_row = out + ((size_t)t * g.H + y) * g.W * g.C;
+  for (int v = threadIdx.x; v < g.W * CV; v += blockDim.x) {
+    const int x = v / CV, cv = v - x * CV;
+    const int xx = x + g.pw;
+    int ox0 = xx - g.kw + 1;
+    ox0 = ox0 <= 0 ? 0 : (ox0 + g.sw - 1) / g.sw;
+    int ox1 = xx / g.sw;
+    if (ox1 > g.ow - 1) ox1 = g.ow - 1;
+    float f[MAXC][MAXC][VEC];
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) f[v] = 0.f;      // GELU(0) = 0
-    } else {
-      Vec<float, VEC>::ld(in + (((size_t)t * g.H + y) * g.W + x) * g.C + cv * VEC, f);
+    for (int a = 0; a < MAXC; ++a)
 #pragma unroll
-      for (int v = 0; v < VEC; ++v) f[v] = gelu_erf(f[v]);
-    }
-    Vec<Tout, VEC>::st(out + i * VEC, f);
-  }
-}
-
-// Fold with cover-count normalisation, gather formulation.
-template <typename Tin, typename Tout, int VEC>
-__global__ void fold_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, int n, Geom g) {
-  const int CV = g.C / VEC, KK = g.kh * g.kw, P = g.oh * g.ow;
-  const size_t total = (size_t)n * g.H * g.W * CV;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int cv = int(i % CV);
-    size_t r = i / CV;
-    const int x = int(r % g.W); r /= g.W;
-    const int y = int(r % g.H);
-    const int t = int(r / g.H);
-    // windows oy with oy*sh - ph <= y <= oy*sh - ph + kh - 1
-    const int yy = y + g.ph, xx = x + g.pw;
-    int oy0 = yy - g.kh + 1; oy0 = oy0 <= 0 ? 0 : (oy0 + g.sh - 1) / g.sh;
-    int oy1 = yy / g.sh; if (oy1 > g.oh - 1) oy1 = g.oh - 1;
-    int ox0 = xx - g.kw + 1; ox0 = ox0 <= 0 ? 0 : (ox0 + g.sw - 1) / g.sw;
-    int ox1 = xx / g.sw; if (ox1 > g.ow - 1) ox1 = g.ow - 1;
+      for (int b = 0; b < MAXC; ++b) {
+        const int oy = oy0 + a, ox = ox0 + b;
+        if (oy <= oy1 && ox <= ox1) {
+          const int ky = yy - oy * g.sh, kx = xx - ox * g.sw;
+          Vec<Tin, VEC>::ld(in_t + ((size_t)(oy * g.ow + ox) * KK + ky * g.kw + kx) * g.C + cv * VEC, f[a][b]);
+        }
+      }
     float acc[VEC];
 #pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[v] = 0.f;
-    int cnt = 0;
-    for (int oy = oy0; oy <= oy1; ++oy) {
-      const int ky = yy - oy * g.sh;
-      for (int ox = ox0; ox <= ox1; ++ox) {
-        const int kx = xx - ox * g.sw;
-        const Tin* src = in + (((size_t)t * P + oy * g.ow + ox) * KK + ky * g.kw + kx) * g.C + cv * VEC;
-        float f[VEC];
-        Vec<Tin, VEC>::ld(src, f);
+    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
 #pragma unroll
-        for (int v = 0; v < VEC; ++v) acc[v] += f[v];
-        ++cnt;
-      }
+    for (int a = 0; a < MAXC; ++a)
+#pragma unroll
+      for (int b = 0; b < MAXC; ++b)
+        if (oy0 + a <= oy1 && ox0 + b <= ox1) {
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) acc[k] += f[a][b][k];
+        }
+    const float c = (float)((oy1 - oy0 + 1) * (ox1 - ox0 + 1));
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      acc[k] = __fdiv_rn(acc[k], c);
+      if (GELU) acc[k] = gelu_erf(acc[k]);
     }
-    const float c = (float)cnt;
-#pragma unroll
-    for (int v = 0; v < VEC; ++v) acc[v] = __fdiv_rn(acc[v], c);
-    Vec<Tout, VEC>::st(out + i * VEC, acc);
+    Vec<Tout, VEC>::st(out_row + x * g.C + cv * VEC, acc);
   }
-}
-
-static int grid_for(size_t total) {
-  size_t b = (total + 255) / 256;
-  const size_t cap = 148 * 16;
-  return int(b < cap ? (b ? b : 1) : cap);
 }
 
 cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st) {
-  const int VEC = dtype == 0 ? 8 : 4;
-  const size_t total = (size_t)n * g.oh * g.ow * g.kh * g.kw * (g.C / VEC);
+  const int blocks = n * g.oh * g.ow;
   if (dtype == 0)
-    unfold_kernel<bf16, 8><<<grid_for(total), 256, 0, st>>>((const bf16*)in, (bf16*)out, n, g);
+    unfold_kernel<bf16, 8><<<blocks, 128, 0, st>>>((const bf16*)in, (bf16*)out, g);
   else
-    unfold_kernel<float, 4><<<grid_for(total), 256, 0, st>>>((const float*)in, (float*)out, n, g);
+    unfold_kernel<float, 4><<<blocks, 128, 0, st>>>((const float*)in, (float*)out, g);
   return cudaGetLastError();
 }
 
-cudaError_t launch_unfold_gelu(const float* in, void* out, int n, const Geom& g, int out_dtype, cudaStream_t st) {
-  const int VEC = out_dtype == 0 ? 8 : 4;
-  const size_t total = (size_t)n * g.oh * g.ow * g.kh * g.kw * (g.C / VEC);
-  if (out_dtype == 0)
-    unfold_gelu_kernel<bf16, 8><<<grid_for(total), 256, 0, st>>>(in, (bf16*)out, n, g);
-  else
-    unfold_gelu_kernel<float, 4><<<grid_for(total), 256, 0, st>>>(in, (float*)out, n, g);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g,
+cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g, bool gelu,
                         cudaStream_t st) {
-  if (in_dtype == 0) {
-    const size_t total = (size_t)n * g.H * g.W * (g.C / 8);
-    if (out_dtype == 0)
-      fold_kernel<bf16, bf16, 8><<<grid_for(total), 256, 0, st>>>((const bf16*)in, (bf16*)out, n, g);
-    else
-      fold_kernel<bf16, float, 8><<<grid_for(total), 256, 0, st>>>((const bf16*)in, (float*)out, n, g);
-  } else if (out_dtype == 1) {
-    const size_t total = (size_t)n * g.H * g.W * (g.C / 4);
-    fold_kernel<float, float, 4><<<grid_for(total), 256, 0, st>>>((const float*)in, (float*)out, n, g);
-  } else {
-    const size_t total = (size_t)n * g.H * g.W * (g.C / 8);
-    fold_kernel<float, bf16, 8><<<grid_for(total), 256, 0, st>>>((const float*)in, (bf16*)out, n, g);
-  }
+  const int blocks = n * g.H;
+#define FOLD(TI, TO, V)                                                                              \
+  (gelu ? (fold_kernel<TI, TO, V, true><<<blocks, 256, 0, st>>>((const TI*)in, (TO*)out, g), 0)        \
+        : (fold_kernel<TI, TO, V, false><<<blocks, 256, 0, st>>>((const TI*)in, (TO*)out, g), 0))
+  if (in_dtype == 0 && out_dtype == 0) FOLD(bf16, bf16, 8);
+  else if (in_dtype == 0) FOLD(bf16, float, 8);
+  else if (out_dtype == 1) FOLD(float, float, 4);
+  else FOLD(float, bf16, 8);
+#undef FOLD
   return cudaGetLastError();
 }
 
