@@ -23,6 +23,7 @@ SOURCES = [
     "kernels/gemm_simt.cu",
     "kernels/gemm_tc.cu",
     "kernels/attn.cu",
+    "kernels/attn_sk.cu",
 ]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

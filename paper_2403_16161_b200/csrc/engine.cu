@@ -123,6 +123,9 @@ struct vi_ctx {
   // profiling (vi_profile)
   int prof_mode = 0;
   unsigned long long* attn_timing = nullptr;   // KernelTiming (device), used in profile mode 1
+  int num_sms = 148;
+  float *sk_part = nullptr, *sk_lse = nullptr;  // stream-K partial slots [num_sms][256][hd], [num_sms][256]
+  int* sk_flag = nullptr;                       // [num_sms], zero between launches
   // CUDA graphs of whole steps (vi_run_step), keyed by everything baked into the launches
   struct GraphEntry {
     std::vector<uint64_t> key;
@@ -195,6 +198,11 @@ static const bool g_debug_sync = [] {
 // VI_ATTN_V1=1 selects the one-Q-tile attention kernel (A/B comparisons).
 static const bool g_attn_v1 = [] {
   const char* e = getenv("VI_ATTN_V1");
+  return e && e[0] == '1';
+}();
+// VI_ATTN_SPLIT=1: attention v2 with a fixed KV split + combine kernel instead of stream-K.
+static const bool g_attn_split = [] {
+  const char* e = getenv("VI_ATTN_SPLIT");
   return e && e[0] == '1';
 }();
 // VI_ATTN_COLSPLIT=1: attention v2 with the column-split softmax (A/B experiments).
@@ -404,6 +412,12 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   }
   c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);
   c->attn_timing = (unsigned long long*)A(sizeof(KernelTiming));
+  c->num_sms = prop.multiProcessorCount;
+  if (c->bf16) {
+    c->sk_part = (float*)A((size_t)c->num_sms * 256 * c->hd * 4);
+    c->sk_lse = (float*)A((size_t)c->num_sms * 256 * 4);
+    c->sk_flag = (int*)A((size_t)c->num_sms * 4);
+  }
   if (!ok) {
     delete c;
     return VI_E_OOM;
@@ -720,11 +734,47 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
       cudaMemsetAsync(trace_buf, 0, 32 * 32 * sizeof(long long), c->stream);
       a.trace = trace_buf;
     }
-    if (g_attn_v1)
-      PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
-    else
-      PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream, g_attn_colsplit), "attention");
-    if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
+    static long long* sk_trace = nullptr;
+    static int sk_calls = 0;
+    const bool sk_tr = getenv("VI_SK_TRACE") && l == 0 && ++sk_calls == 5;
+    if (sk_tr) {
+      if (!sk_trace) cudaMalloc(&sk_trace, 148 * 32 * sizeof(long long));
+      cudaMemsetAsync(sk_trace, 0, 148 * 32 * sizeof(long long), c->stream);
+    }
+    if (!g_attn_v1 && !g_attn_split && !a.trace) {
+      if (sk_tr) a.trace = sk_trace;
+      // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
+      a.npairs = (M + 255) / 256;
+      a.units = a.npairs * c->H;
+      a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
+      const long long work = (long long)a.units * ntiles;
+      int grid = int(work < c->num_sms ? work : c->num_sms);
+      if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
+      PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+      if (sk_tr) {
+        std::vector<long long> h(148 * 32);
+        cudaMemcpyAsync(h.data(), sk_trace, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
+        cudaStreamSynchronize(c->stream);
+        long long t0 = h[31];
+        for (int i = 0; i < grid; ++i) t0 = std::min(t0, h[i * 32 + 31]);
+        auto T = [&](long long v) { return v ? (v - t0) / 1000.0 : -1.0; };
+        for (int i = 0; i < grid; ++i) {
+          fprintf(stderr, "[sk] cta %3d |", i);
+          for (int k = 0; k < 3 && h[i * 32 + k * 8]; ++k) {
+            const long long* e = &h[i * 32 + k * 8];
+            fprintf(stderr, " u%lld[%lld,%lld) loop %5.1f-%5.1f ld %5.1f wait %5.1f merge %5.1f end %5.1f |", e[3] >> 32,
+                    (e[3] >> 16) & 0xffff, e[3] & 0xffff, T(e[0]), T(e[1]), T(e[4]), T(e[5]), T(e[6]), T(e[2]));
+          }
+          fprintf(stderr, "\n");
+        }
+      }
+    } else {
+      if (g_attn_v1)
+        PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
+      else
+        PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream, g_attn_colsplit), "attention");
+      if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
+    }
     if (a.trace) {
       long long h[32 * 32];
       cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, c->stream);

@@ -1,0 +1,477 @@
+// Memory attention, persistent stream-K variant (the default bf16 path).
+//
+// Same math and per-tile pipeline as attn_tc2_kernel (attn.cu): two 128-query tiles per
+// CTA, S/P and O in TMEM, P as the TMEM A operand of O += P V, ping-pong softmax
+// warpgroups, lazy rescale, 3/8 of the exponentials by polynomial.  What changes is the
+// work split: work = units x key tiles, unit = (query-tile pair, head); a grid of one CTA
+// per SM takes contiguous, equal slices of that work (no idle SMs, no separate combine
+// kernel).  A unit cut by a slice boundary is finished by the CTA holding its first tile
+// (the "owner"): every other CTA holding a piece of it writes a normalised partial (O/l,
+// log2-sum-exp) into its own slot and raises a flag; the owner merges the slots in CTA
+// order (deterministic) with its own TMEM accumulator and writes the output.  A CTA's
+// continuation piece is always at the start of its slice, so it is ready long before the
+// owner reaches the end of its slice.  The launch is cooperative (all CTAs co-resident).
+#include "kernels.h"
+
+namespace vi {
+
+template <int HD>
+struct AttnSkSmem {
+  static constexpr int ST = 2;
+  static constexpr int QB = 128 * HD * 2;
+  static constexpr int KB = 128 * HD * 2;
+  static constexpr int VB = HD * 128 * 2;
+  static constexpr int Q_OFF = 0;
+  static constexpr int K_OFF = 2 * QB;
+  static constexpr int V_OFF = K_OFF + ST * KB;
+  static constexpr int BAR_OFF = V_OFF + ST * VB;
+  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2;
+  static constexpr int STG_OFF = BAR_OFF + NBAR * 8 + 16;      // [8 warps][32 rows][80 B] output staging
+  static constexpr int TOTAL = STG_OFF + 8 * 32 * 80 + 1024;
+};
+
+__device__ __forceinline__ void sk_key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
+  int i = 0;
+  while (i + 1 < s.n && g >= s.tile0[i + 1]) ++i;
+  const int off = (g - s.tile0[i]) * 128;
+  row0 = s.row0[i] + off;
+  const int rem = s.len[i] - off;
+  nvalid = rem < 128 ? rem : 128;
+  nskip = off == 0 ? s.lead[i] : 0;
+}
+
+__device__ __forceinline__ void sk_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+// slice of the flattened work [0, W) owned by CTA c of G
+__device__ __forceinline__ long long sk_begin(long long W, int G, int c) { return W * c / G; }
+
+template <int HD>
+__global__ void __launch_bounds__(384, 1)
+attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+               const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
+  using L = AttnSkSmem<HD>;
+  constexpr int ST = L::ST;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
+  uint64_t* q_full = bars;
+  uint64_t* q_empty = bars + 1;
+  uint64_t* k_full = bars + 2;
+  uint64_t* k_empty = k_full + ST;
+  uint64_t* v_full = k_empty + ST;
+  uint64_t* v_empty = v_full + ST;
+  uint64_t* s_full = v_empty + ST;    // [2] per Q tile
+  uint64_t* p_full = s_full + 2;      // [2 tiles][2 key halves]
+  uint64_t* o_final = p_full + 4;     // [2] all PV of a segment done
+  uint64_t* o_free = o_final + 2;     // [2] O read out by the epilogue
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int NT = a.segs.tile0[a.segs.n];
+  const long long W = (long long)a.units * NT;
+  const int G = gridDim.x, cta = blockIdx.x;
+  const long long w_begin = sk_begin(W, G, cta), w_end = sk_begin(W, G, cta + 1);
+
+  if (warp == 8 && lane == 0) {
+    tma_prefetch(&tq);
+    tma_prefetch(&tk);
+    tma_prefetch(&tvt);
+    mbar_init(q_full, 1);
+    mbar_init(q_empty, 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(&k_full[s], 1);
+      mbar_init(&k_empty[s], 1);
+      mbar_init(&v_full[s], 1);
+      mbar_init(&v_empty[s], 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(&s_full[t], 1);
+      mbar_init(&p_full[2 * t], 128);
+      mbar_init(&p_full[2 * t + 1], 128);
+      mbar_init(&o_final[t], 1);
+      mbar_init(&o_free[t], 128);
+    }
+    fence_barrier_init();
+  }
+  if (warp == 10) tmem_alloc(tmem_slot, 512);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) time_begin(a.timing);
+  if (a.trace && threadIdx.x == 0) a.trace[(size_t)cta * 32 + 31] = (long long)globaltimer();
+
+  if (warp == 8) {
+    if (lane == 0) {
+      int jg = 0, sg = 0;
+      for (long long w = w_begin; w < w_end; ++sg) {
+        const int u = int(w / NT), ta = int(w - (long long)u * NT);
+        const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
+        const int h = u / a.npairs, q0 = (u - h * a.npairs) * 256;
+        if (sg > 0) mbar_wait(q_empty, (sg - 1) & 1);
+        mbar_arrive_expect_tx(q_full, 2 * L::QB);
+#pragma unroll
+        for (int t = 0; t < 2; ++t)
+#pragma unroll
+          for (int at = 0; at < HD / 64; ++at)
+            tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, q0 + t * 128);
+        for (int j = ta; j < tb; ++j, ++jg) {
+          int row0, nv, nskip;
+          sk_key_tile(a.segs, j, row0, nv, nskip);
+          const int st = jg % ST;
+          const uint32_t par = ((jg / ST) & 1) ^ 1;
+          if (jg >= ST) mbar_wait(&k_empty[st], par);
+          uint8_t* sk = smem + L::K_OFF + st * L::KB;
+          mbar_arrive_expect_tx(&k_full[st], L::KB);
+#pragma unroll
+          for (int at = 0; at < HD / 64; ++at)
+            tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + row0);
+          if (jg >= ST) mbar_wait(&v_empty[st], par);
+          uint8_t* sv = smem + L::V_OFF + st * L::VB;
+          mbar_arrive_expect_tx(&v_full[st], L::VB);
+#pragma unroll
+          for (int at = 0; at < 2; ++at)
+            tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], row0 + at * 64, a.vrow_base + h * HD);
+        }
+        w += tb - ta;
+      }
+    }
+  } else if (warp == 9) {
+    if (lane == 0) {
+      constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
+      constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD);
+      const uint32_t sq = smem_u32(smem + L::Q_OFF);
+      int jg = 0, sg = 0;
+      for (long long w = w_begin; w < w_end; ++sg) {
+        const int u = int(w / NT), ta = int(w - (long long)u * NT);
+        const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
+        const int n = tb - ta;
+        mbar_wait(q_full, sg & 1);
+        auto issue_pv = [&](int t, int j) {          // O_t (+)= P_t(j) V(j), j local to the segment
+          const int g = jg + j, st = g % ST;
+          if (t == 0) mbar_wait(&v_full[st], (g / ST) & 1);
+          if (j == 0 && sg > 0) mbar_wait(&o_free[t], (sg - 1) & 1);   // previous segment's O read out
+          const uint32_t sv = smem_u32(smem + L::V_OFF + st * L::VB);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&p_full[2 * t + hh], g & 1);
+            tc_fence_after();
+#pragma unroll
+            for (int k4 = 0; k4 < 4; ++k4) {
+              const int kk = hh * 4 + k4;
+              umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + kk * 8,
+                           sdesc_k_sw128(sv + hh * (HD * 128) + k4 * 32), idesc_o, (j | kk) != 0);
+            }
+          }
+          if (t == 1) umma_commit(&v_empty[st]);
+        };
+        auto issue_qk = [&](int t, int j) {          // S_t = Q_t K(j)^T
+          const int g = jg + j, st = g % ST;
+          if (t == 0) {
+            mbar_wait(&k_full[st], (g / ST) & 1);
+            tc_fence_after();
+          }
+          const uint32_t sk = smem_u32(smem + L::K_OFF + st * L::KB);
+          const uint32_t sqt = sq + t * L::QB;
+#pragma unroll
+          for (int kk = 0; kk < HD / 16; ++kk) {
+            const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
+            umma_bf16_ss(tmem + t * 128, sdesc_k_sw128(sqt + off), sdesc_k_sw128(sk + off), idesc_s, kk > 0);
+          }
+          umma_commit(&s_full[t]);
+          if (t == 1) umma_commit(&k_empty[st]);
+        };
+        for (int j = 0; j < n; ++j)
+          for (int t = 0; t < 2; ++t) {
+            if (j > 0) issue_pv(t, j - 1);
+            issue_qk(t, j);
+          }
+        umma_commit(q_empty);                       // all QK of the segment issued: Q smem free when done
+        for (int t = 0; t < 2; ++t) {
+          issue_pv(t, n - 1);
+          umma_commit(&o_final[t]);
+        }
+        jg += n;
+        w += n;
+      }
+    }
+  } else if (warp < 8) {
+    const int t = warp >> 2;                        // Q tile of this warpgroup
+    const int qd = warp & 3;                        // TMEM lane quadrant
+    const int row = qd * 32 + lane;                 // row within the Q tile
+    const uint32_t lane_off = uint32_t(qd * 32) << 16;
+    const uint32_t TS = tmem + t * 128 + lane_off, TO = tmem + 256 + t * 128 + lane_off;
+    const float2 cc = make_float2(a.scale_log2, a.scale_log2);
+    int jg = 0, sg = 0;
+    for (long long w = w_begin; w < w_end; ++sg) {
+      const int u = int(w / NT), ta = int(w - (long long)u * NT);
+      const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
+      const int n = tb - ta;
+      const int h = u / a.npairs, q0 = (u - h * a.npairs) * 256;
+      float m_use = -INFINITY, l = 0.f;
+      long long* trc = (a.trace && threadIdx.x == 0 && sg < 3) ? a.trace + (size_t)cta * 32 + sg * 8 : nullptr;
+      if (trc) trc[0] = (long long)globaltimer();
+      for (int j = 0; j < n; ++j) {
+        const int g = jg + j;
+        int row0, nv, nskip;
+        sk_key_tile(a.segs, ta + j, row0, nv, nskip);
+        mbar_wait(&s_full[t], g & 1);
+        tc_fence_after();
+        float s[128];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) tmem_ld32(TS + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
+        tmem_wait_ld();
+        if (nv < 128 || nskip > 0) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i >= nv || i < nskip) s[i] = -INFINITY;
+        }
+        float mx[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
+#pragma unroll
+        for (int i = 0; i < 128; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
+        const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
+                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * a.scale_log2;
+        const bool grow = rmax > m_use + 8.f;       // lazy rescale (exact either way)
+        float alpha = 1.f;
+        if (grow) {
+          alpha = ex2(m_use - rmax);
+          m_use = rmax;
+        }
+        if (__any_sync(0xffffffffu, grow) && j > 0) {   // PV(j-1) done: O idle (s_full implies it)
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(TO + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(TO + c, r);
+          }
+        }
+        const float2 mm = make_float2(-m_use, -m_use);
+        float2 sum[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) sum[i] = make_float2(0.f, 0.f);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int k = 0; k < 16; ++k) {
+            const int i = c * 16 + k;
+            const float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
+            float2 p;
+            if (k % 5 >= 3) {
+              p = exp2_poly2(x);
+            } else {
+              p.x = ex2(x.x);
+              p.y = ex2(x.y);
+            }
+            __nv_bfloat162 b = __floats2bfloat162_rn(p.x, p.y);
+            pk[k] = *reinterpret_cast<uint32_t*>(&b);
+            sum[k & 3] = fadd2(sum[k & 3], p);
+          }
+          tmem_st16(TS + c * 16, pk);
+          if (c & 1) {
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(&p_full[2 * t + (c >> 1)]);
+          }
+        }
+        const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
+        l = l * alpha + (s01.x + s01.y);
+      }
+      // ---- segment epilogue, 32 O columns at a time straight from TMEM (no 128-float
+      // register array: keeps the global loads of a merge all in flight)
+      if (trc) trc[1] = (long long)globaltimer();
+      mbar_wait(&o_final[t], sg & 1);
+      tc_fence_after();
+      const int r256 = t * 128 + row;               // row in the CTA's 256-row slot
+      const float lse_own = m_use + __log2f(l);
+      uint8_t* stg = smem + L::STG_OFF + warp * (32 * 80);
+      const int rbase = q0 + t * 128 + qd * 32;
+      // write one 32-column chunk of bf16 output rows through the per-warp stage (8 rows x 64 B
+      // per store instruction; output rows are D*2 bytes apart)
+      auto write_out = [&](int c, const float* f, float scale) {
+        uint4* my = reinterpret_cast<uint4*>(stg + lane * 80);
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          my[k] = make_uint4(pack_bf16(f[8 * k] * scale, f[8 * k + 1] * scale),
+                             pack_bf16(f[8 * k + 2] * scale, f[8 * k + 3] * scale),
+                             pack_bf16(f[8 * k + 4] * scale, f[8 * k + 5] * scale),
+                             pack_bf16(f[8 * k + 6] * scale, f[8 * k + 7] * scale));
+        __syncwarp();
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int rr = i * 8 + (lane >> 2), part = lane & 3;
+          const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
+          if (rbase + rr < a.Nq)
+            *reinterpret_cast<uint4*>(a.o + (size_t)(rbase + rr) * a.D + h * HD + c + part * 8) = v;
+        }
+        __syncwarp();
+      };
+      if (ta > 0) {
+        // continuation piece: normalised partial -> this CTA's slot (float4-interleaved over
+        // the 256 rows, coalesced), then raise the flag
+        float4* dst = reinterpret_cast<float4*>(a.spart) + (size_t)cta * (HD / 4) * 256 + r256;
+        const float inv = 1.f / l;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          float f[32];
+          tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+          tmem_wait_ld();
+#pragma unroll
+          for (int k = 0; k < 32; k += 4)
+            dst[((c + k) / 4) * 256] = make_float4(f[k] * inv, f[k + 1] * inv, f[k + 2] * inv, f[k + 3] * inv);
+        }
+        tc_fence_before();
+        mbar_arrive(&o_free[t]);
+        if (trc) trc[4] = (long long)globaltimer();
+        a.slse[(size_t)cta * 256 + r256] = lse_own;
+        sk_bar_sync(1, 256);                         // every row of the slot written (CTA scope) ...
+        if (threadIdx.x == 0) {                      // ... then one cumulative gpu-scope release
+          __threadfence();
+          atomicExch(&a.sflag[cta], 1);
+        }
+      } else if (tb < NT) {
+        // owner of a split unit (always the last segment of this CTA): merge the pieces of
+        // CTAs cta+1 .. (the unit's last tile) in CTA order
+        const long long unit_end = (long long)(u + 1) * NT;
+        int last = cta + 1;
+        while (last + 1 < G && sk_begin(W, G, last + 1) < unit_end) ++last;
+        const int np = last - cta;                  // <= 3 for the shapes used (checked on the host)
+        if (lane < np) {                            // lane i polls the flag of CTA cta+1+i
+          const int* fl = a.sflag + cta + 1 + lane;
+          while (*reinterpret_cast<const volatile int*>(fl) == 0) __nanosleep(32);
+        }
+        __syncwarp();
+        __threadfence();
+        if (trc) trc[4] = (long long)globaltimer();
+        float lk[4], mx = lse_own;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          lk[k] = k < np ? __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) : -INFINITY;
+          mx = fmaxf(mx, lk[k]);
+        }
+        const float wown = ex2(lse_own - mx);
+        float wk[4], wsum = wown;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          wk[k] = k < np ? ex2(lk[k] - mx) : 0.f;
+          wsum += wk[k];
+        }
+        const float inv_w = 1.f / wsum;
+        if (trc) trc[5] = (long long)globaltimer();
+        // fold each 128 KB slot in turn: copied (coalesced, all loads in flight) into the
+        // now idle K/V stage buffers, then accumulated into this CTA's O in TMEM
+        float4* stage = reinterpret_cast<float4*>(smem + L::K_OFF);
+        float scale = wown / l;
+#pragma unroll 1
+        for (int k = 0; k < np; ++k) {
+          const float4* src = reinterpret_cast<const float4*>(a.spart) + (size_t)(cta + 1 + k) * (HD / 4) * 256;
+          // thread i moves float4s i, i+256, ... (HD/4 of them), 16 loads in flight
+#pragma unroll 1
+          for (int i0 = 0; i0 < HD / 4; i0 += 16) {
+            float4 r[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) r[e] = __ldcg(src + (i0 + e) * 256 + threadIdx.x);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) stage[(i0 + e) * 256 + threadIdx.x] = r[e];
+          }
+          sk_bar_sync(3, 256);
+          const float w = wk[k];
+#pragma unroll 1
+          for (int c = 0; c < HD; c += 32) {
+            float f[32];
+            tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+            tmem_wait_ld();
+#pragma unroll
+            for (int q4 = 0; q4 < 8; ++q4) {
+              const float4 v = stage[((c / 4) + q4) * 256 + r256];
+              f[4 * q4] = f[4 * q4] * scale + w * v.x;
+              f[4 * q4 + 1] = f[4 * q4 + 1] * scale + w * v.y;
+              f[4 * q4 + 2] = f[4 * q4 + 2] * scale + w * v.z;
+              f[4 * q4 + 3] = f[4 * q4 + 3] * scale + w * v.w;
+            }
+            tmem_st32(TO + c, reinterpret_cast<uint32_t*>(f));
+            tmem_wait_st();
+          }
+          scale = 1.f;
+          sk_bar_sync(3, 256);                      // stage free for the next slot
+        }
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          float f[32];
+          tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+          tmem_wait_ld();
+          write_out(c, f, scale * inv_w);
+        }
+        tc_fence_before();
+        mbar_arrive(&o_free[t]);
+        if (trc) trc[6] = (long long)globaltimer();
+        sk_bar_sync(2, 256);                        // both tiles' rows have read the slots
+        if (threadIdx.x < np) a.sflag[cta + 1 + threadIdx.x] = 0;
+      } else {
+        // whole unit in this CTA
+        const float inv = 1.f / l;
+#pragma unroll 1
+        for (int c = 0; c < HD; c += 32) {
+          float f[32];
+          tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+          tmem_wait_ld();
+          write_out(c, f, inv);
+        }
+        tc_fence_before();
+        mbar_arrive(&o_free[t]);
+      }
+      if (trc) {
+        trc[2] = (long long)globaltimer();
+        trc[3] = ((long long)u << 32) | ((long long)ta << 16) | tb;
+      }
+      jg += n;
+      w += n;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
+  if (warp == 10) {
+    tc_fence_after();
+    tmem_dealloc(tmem, 512);
+  }
+}
+
+template <int HD>
+static cudaError_t launch_sk_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
+                                const AttnTC& a, int grid, cudaStream_t st) {
+  using L = AttnSkSmem<HD>;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(attn_sk_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;     // owners wait on other CTAs: all must be resident
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, attn_sk_kernel<HD>, tq, tk, tvt, a);
+}
+
+cudaError_t launch_attn_sk(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                           int grid, cudaStream_t st) {
+  if (a.hd == 128) return launch_sk_hd<128>(tq, tk, tvt, a, grid, st);
+  if (a.hd == 64) return launch_sk_hd<64>(tq, tk, tvt, a, grid, st);
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace vi

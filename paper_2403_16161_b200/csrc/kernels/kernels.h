@@ -73,6 +73,13 @@ struct AttnTC {
   bf16* o;                  // [Nq][D] final (nsplit == 1)
   float* opart;             // [nsplit][Nq][D] normalised partial outputs (nsplit > 1)
   float* lse;               // [nsplit][H][Nq] log2-sum-exp of the partials
+  // stream-K (attn_sk_kernel): units = (query-tile pair, head), work = units x key tiles,
+  // split evenly over the persistent grid; partial results of split units go through
+  // spart/slse/sflag (one slot per CTA) and are merged by the unit's first CTA.
+  int npairs, units;
+  float* spart;             // [grid][256][hd]
+  float* slse;              // [grid][256]
+  int* sflag;               // [grid], 0 between launches
   long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
   unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves
   int H;
@@ -83,5 +90,8 @@ cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const C
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                             cudaStream_t st, bool colsplit);
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st);
+// persistent stream-K variant (one CTA per SM, no combine kernel)
+cudaError_t launch_attn_sk(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                           int grid, cudaStream_t st);
 
 }  // namespace vi
