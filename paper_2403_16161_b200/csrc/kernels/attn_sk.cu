@@ -342,27 +342,19 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
         const long long unit_end = (long long)(u + 1) * NT;
         int last = cta + 1;
         while (last + 1 < G && sk_begin(W, G, last + 1) < unit_end) ++last;
-        const int np = last - cta;                  // <= 3 for the shapes used (checked on the host)
-        if (lane < np) {                            // lane i polls the flag of CTA cta+1+i
-          const int* fl = a.sflag + cta + 1 + lane;
+        const int np = last - cta;                  // pieces to merge (any number)
+        for (int k = lane; k < np; k += 32) {       // lane i polls the flags of CTAs cta+1+i, +33, ...
+          const int* fl = a.sflag + cta + 1 + k;
           while (*reinterpret_cast<const volatile int*>(fl) == 0) __nanosleep(32);
         }
         __syncwarp();
         __threadfence();
         if (trc) trc[4] = (long long)globaltimer();
-        float lk[4], mx = lse_own;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          lk[k] = k < np ? __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) : -INFINITY;
-          mx = fmaxf(mx, lk[k]);
-        }
+        float mx = lse_own;
+        for (int k = 0; k < np; ++k) mx = fmaxf(mx, __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256));
         const float wown = ex2(lse_own - mx);
-        float wk[4], wsum = wown;
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          wk[k] = k < np ? ex2(lk[k] - mx) : 0.f;
-          wsum += wk[k];
-        }
+        float wsum = wown;
+        for (int k = 0; k < np; ++k) wsum += ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
         const float inv_w = 1.f / wsum;
         if (trc) trc[5] = (long long)globaltimer();
         // fold each 128 KB slot in turn: copied (coalesced, all loads in flight) into the
@@ -382,7 +374,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
             for (int e = 0; e < 16; ++e) stage[(i0 + e) * 256 + threadIdx.x] = r[e];
           }
           sk_bar_sync(3, 256);
-          const float w = wk[k];
+          const float w = ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
 #pragma unroll 1
           for (int c = 0; c < HD; c += 32) {
             float f[32];
@@ -413,7 +405,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
         mbar_arrive(&o_free[t]);
         if (trc) trc[6] = (long long)globaltimer();
         sk_bar_sync(2, 256);                        // both tiles' rows have read the slots
-        if (threadIdx.x < np) a.sflag[cta + 1 + threadIdx.x] = 0;
+        for (int k = threadIdx.x; k < np; k += 256) a.sflag[cta + 1 + k] = 0;
       } else {
         // whole unit in this CTA
         const float inv = 1.f / l;

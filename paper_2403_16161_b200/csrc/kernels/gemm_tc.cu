@@ -1,8 +1,13 @@
 // tcgen05 GEMM with fused epilogues: C[M][N] = A[M][K] * W[N][K]^T (bf16 in, fp32 acc).
 //
-// Persistent, warp-specialised: grid = min(#tiles, #SMs) CTAs, each walks the 128 x BN
-// output tiles blockIdx.x, blockIdx.x + gridDim.x, ... (m fastest, so CTAs running at
-// the same time share the weight block in L2).  Warp roles (384 threads):
+// Persistent, warp-specialised, in clusters of CM x CN CTAs: a cluster owns CM x CN
+// adjacent 128 x BN output tiles (a "super-tile") and walks super-tiles cid, cid + #clusters,
+// ...  The A tile (128 rows x 64 k) of a cluster row is loaded in CN slices, each CTA of the
+// row loading one slice and TMA-multicasting it to the row; the W tile of a cluster column
+// likewise in CM slices.  At M = 3600 the operands are re-read once per tile from L2, so
+// multicast is what keeps these GEMMs off the L2 bandwidth ceiling.  A stage is refilled
+// only after every CTA of the cluster has consumed it (tcgen05.commit multicast to all).
+// Warp roles (384 threads):
 //   warp 0, lane 0 : TMA producer  (A box 64x128, W box 64xBN, 128-byte swizzle), an
 //                    STAGES-deep smem ring that keeps streaming across tile boundaries
 //   warp 1, lane 0 : MMA issuer    (tcgen05.mma kind::f16, M=128, N=BN, K=16 per instr)
@@ -22,7 +27,7 @@ __device__ __forceinline__ void gemm_named_bar_sync(int id, int n) {
 }
 
 template <int BN, int STAGES>
-struct GemmSmem {
+struct GemmSmem {  // (cluster shape does not change the layout)
   static constexpr int A_BYTES = 128 * 64 * 2;
   static constexpr int B_BYTES = BN * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
@@ -31,11 +36,19 @@ struct GemmSmem {
   static constexpr int TOTAL = BIAS_OFF + 2 * BN * 4 + 1024;              // +1024 alignment slack
 };
 
-template <int BN, int STAGES>
+#ifdef VI_GEMM_TRACE
+__device__ long long g_gemm_trace[16];
+#define GTR(i) do { if (blockIdx.x == 0) g_gemm_trace[i] = (long long)globaltimer(); } while (0)
+#else
+#define GTR(i) do { } while (0)
+#endif
+
+template <int BN, int STAGES, int CM, int CN>
 __global__ void __launch_bounds__(384, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int brow0,
                Epi epi) {
   using L = GemmSmem<BN, STAGES>;
+  constexpr int CS = CM * CN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
@@ -45,17 +58,28 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (threadIdx.x == 0) GTR(0);
+  const int rank = CS > 1 ? int(cluster_ctarank()) : 0;
+  const int cx = rank % CN, cy = rank / CN;           // position inside the cluster
+  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
   const int tiles_m = (epi.M + 127) / 128, tiles_n = (epi.N + BN - 1) / BN;
-  const int ntiles = tiles_m * tiles_n;
+  const int super_m = (tiles_m + CM - 1) / CM, super_n = (tiles_n + CN - 1) / CN;
+  const int nsuper = super_m * super_n;
   const int nk = (K + 63) / 64;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
+  constexpr int A_SLICE = L::A_BYTES / CN, B_SLICE = L::B_BYTES / CM;
+  const uint16_t row_mask = uint16_t(((1u << CN) - 1) << (cy * CN));
+  uint16_t col_mask = 0;
+#pragma unroll
+  for (int y = 0; y < CM; ++y) col_mask |= uint16_t(1u << (y * CN + cx));
+  const uint16_t all_mask = uint16_t((1u << CS) - 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+      mbar_init(&empty[s], CS);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
@@ -65,22 +89,31 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   }
   if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
   tc_fence_before();
-  __syncthreads();
+  if (CS > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) GTR(1);
 
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;                               // global k-block counter (ring position)
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+      for (int st = cid; st < nsuper; st += ncl) {
+        const int m0 = ((st % super_m) * CM + cy) * 128, n0 = ((st / super_m) * CN + cx) * BN;
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
-          tma_load_2d(sa, &tmA, &full[s], kb * 64, m0);
-          tma_load_2d(sa + L::A_BYTES, &tmB, &full[s], kb * 64, brow0 + n0);
+          if (CN > 1)
+            tma_load_2d_mc(sa + cx * A_SLICE, &tmA, &full[s], kb * 64, m0 + cx * (128 / CN), row_mask);
+          else
+            tma_load_2d(sa, &tmA, &full[s], kb * 64, m0);
+          if (CM > 1)
+            tma_load_2d_mc(sa + L::A_BYTES + cy * B_SLICE, &tmB, &full[s], kb * 64, brow0 + n0 + cy * (BN / CM),
+                           col_mask);
+          else
+            tma_load_2d(sa + L::A_BYTES, &tmB, &full[s], kb * 64, brow0 + n0);
         }
       }
     }
@@ -88,7 +121,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {
       constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
       int it = 0, lt = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      for (int st = cid; st < nsuper; st += ncl, ++lt) {
         const int acc = lt & 1;
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -96,15 +129,20 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
+          if (it == 0) GTR(2);
           tc_fence_after();
           const uint32_t a = smem_u32(smem + s * L::STAGE_BYTES);
           const uint32_t b = a + L::A_BYTES;
 #pragma unroll
           for (int k = 0; k < 4; ++k)
             umma_bf16_ss(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
-          umma_commit(&empty[s]);
+          if (CS > 1)
+            umma_commit_mc(&empty[s], all_mask);    // stage free in every CTA that shares it
+          else
+            umma_commit(&empty[s]);
         }
         umma_commit(&tfull[acc]);
+        if (lt == 0) GTR(3);
       }
     }
   } else if (warp >= 4) {
@@ -113,15 +151,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int etid = ew * 32 + lane;             // 0..255
     float* bias_s = reinterpret_cast<float*>(smem + L::BIAS_OFF);
     int lt = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+    for (int st = cid; st < nsuper; st += ncl, ++lt) {
       const int acc = lt & 1;
-      const int m0 = (tile % tiles_m) * 128, n0 = (tile / tiles_m) * BN;
+      const int m0 = ((st % super_m) * CM + cy) * 128, n0 = ((st / super_m) * CN + cx) * BN;
       float* bs = bias_s + acc * BN;
       if (epi.bias) {
         for (int i = etid; i < BN; i += 256) bs[i] = n0 + i < epi.N ? __ldg(epi.bias + n0 + i) : 0.f;
       }
       gemm_named_bar_sync(1, 256);
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      if (lt == 0 && ew == 0 && lane == 0) GTR(4);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
 #pragma unroll 1
@@ -140,48 +179,86 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
+      if (lt == 0 && ew == 0 && lane == 0) GTR(5);
     }
   }
   tc_fence_before();
-  __syncthreads();
+  if (CS > 1) cluster_sync_all();   // no CTA leaves while peers may still multicast into it
+  else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
+  if (threadIdx.x == 0) GTR(6);
 }
 
 static int g_num_sms = 0;
 
-template <int BN, int STAGES>
-static cudaError_t launch_bn(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
-                             const Epi& e, cudaStream_t st) {
+template <int BN, int STAGES, int CM, int CN>
+static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
+                              const Epi& e, cudaStream_t st) {
   using L = GemmSmem<BN, STAGES>;
-  auto kfn = gemm_tc_kernel<BN, STAGES>;
-  static bool configured = false;
-  if (!configured) {
+  constexpr int CS = CM * CN;
+  auto kfn = gemm_tc_kernel<BN, STAGES, CM, CN>;
+  static int max_clusters = 0;
+  if (!max_clusters) {
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (err != cudaSuccess) return err;
-    configured = true;
-  }
-  if (!g_num_sms) {
+    if (CS > 1) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
+    max_clusters = g_num_sms / CS;
+    if (CS > 1) {
+      cudaLaunchConfig_t q = {};
+      q.gridDim = dim3(CS * max_clusters);
+      q.blockDim = dim3(384);
+      q.dynamicSmemBytes = L::TOTAL;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      q.attrs = at;
+      q.numAttrs = 1;
+      int n = 0;
+      if (cudaOccupancyMaxActiveClusters(&n, kfn, &q) == cudaSuccess && n > 0) max_clusters = n;
+      cudaGetLastError();
+    }
   }
-  const int tiles = ((M + 127) / 128) * ((N + BN - 1) / BN);
-  const int grid = tiles < g_num_sms ? tiles : g_num_sms;
-  kfn<<<grid, 384, L::TOTAL, st>>>(a, b, K, brow0, e);
-  return cudaGetLastError();
+  const int tiles_m = (M + 127) / 128, tiles_n = (N + BN - 1) / BN;
+  const int nsuper = ((tiles_m + CM - 1) / CM) * ((tiles_n + CN - 1) / CN);
+  const int ncl = nsuper < max_clusters ? nsuper : max_clusters;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(ncl * CS);
+  cfg.blockDim = dim3(384);
+  cfg.dynamicSmemBytes = L::TOTAL;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kfn, a, b, K, brow0, e);
 }
 
+// cluster: 0 = none, 1 = 2 CTAs along m (W tile multicast), 2 = 2 along n (A multicast),
+// 3 = 2 x 2.  The A map's box must be 64 x (128 / CN), the W map's 64 x (BN / CM).
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K, int bn,
-                           const Epi& e, cudaStream_t st) {
+                           const Epi& e, cudaStream_t st, int cluster) {
+#define CASES(BN, ST)                                                              \
+  switch (cluster) {                                                               \
+    case 0: return launch_cfg<BN, ST, 1, 1>(a, b, brow0, M, N, K, e, st);          \
+    case 1: return launch_cfg<BN, ST, 2, 1>(a, b, brow0, M, N, K, e, st);          \
+    case 2: return launch_cfg<BN, ST, 1, 2>(a, b, brow0, M, N, K, e, st);          \
+    case 3: return launch_cfg<BN, ST, 2, 2>(a, b, brow0, M, N, K, e, st);          \
+    default: return cudaErrorInvalidValue;                                         \
+  }
   switch (bn) {
-    case 64: return launch_bn<64, 8>(a, b, brow0, M, N, K, e, st);
-    case 128: return launch_bn<128, 6>(a, b, brow0, M, N, K, e, st);
-    case 256: return launch_bn<256, 4>(a, b, brow0, M, N, K, e, st);
+    case 64: CASES(64, 8)
+    case 128: CASES(128, 6)
+    case 256: CASES(256, 4)
     default: return cudaErrorInvalidValue;
   }
+#undef CASES
 }
 
 }  // namespace vi

@@ -33,8 +33,10 @@ cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D,
 // tensor cores (bf16): A [M][K] and W [N][K] described by 2-D TMA maps with 64 x 128 /
 // 64 x BN boxes and 128-byte swizzle.
 // brow0: row offset of this layer's weight block inside the stacked W map.
+// cluster: 0 none, 1 = 2 CTAs along m (W multicast; W box 64 x BN/2), 2 = 2 along n (A
+// multicast; A box 64 x 64), 3 = 2 x 2.
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& w, int brow0, int M, int N, int K, int bn,
-                           const Epi& e, cudaStream_t st);
+                           const Epi& e, cudaStream_t st, int cluster = 0);
 // SIMT (fp32 path): A [M][K], W [N][K] row-major fp32, FFMA accumulate.
 cudaError_t launch_gemm_simt_f32(const float* A, const float* W, int M, int N, int K, const Epi& e, cudaStream_t st);
 

@@ -57,22 +57,26 @@ template <> struct Vec<float, 8> {
 // Pure copy (bit-exact) unfold.  One CTA per token (t, oy, ox): its kh*kw*C outputs are
 // contiguous, so the CTA writes one contiguous run with 16-byte vectors; 32-bit index math.
 template <typename T, int VEC>
-__global__ void __launch_bounds__(128) unfold_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g) {
+__global__ void __launch_bounds__(256) unfold_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g, int ntok) {
   const int CV = g.C / VEC, KK = g.kh * g.kw, P = g.oh * g.ow;
-  const int tok = blockIdx.x % P, t = blockIdx.x / P;
-  const int oy = tok / g.ow, ox = tok - oy * g.ow;
-  const int y0 = oy * g.sh - g.ph, x0 = ox * g.sw - g.pw;
-  const T* src_t = in + (size_t)t * g.H * g.W * g.C;
-  T* dst = out + (size_t)blockIdx.x * KK * g.C;
-  for (int v = threadIdx.x; v < KK * CV; v += blockDim.x) {
+  // a CTA covers tpb consecutive tokens (one contiguous output run); v = (j, cv) per token
+  const int per = KK * CV;
+  const int tpb = (per >= 512) ? 1 : (512 + per - 1) / per;
+  const int tok0 = blockIdx.x * tpb;
+  for (int vv = threadIdx.x; vv < tpb * per; vv += blockDim.x) {
+    const int ti = vv / per, v = vv - ti * per;
+    const int gt = tok0 + ti;
+    if (gt >= ntok) break;
+    const int tok = gt % P, t = gt / P;
+    const int oy = tok / g.ow, ox = tok - oy * g.ow;
     const int j = v / CV, cv = v - j * CV;
     const int ky = j / g.kw, kx = j - ky * g.kw;
-    const int y = y0 + ky, x = x0 + kx;
-    T* d = dst + v * VEC;
+    const int y = oy * g.sh - g.ph + ky, x = ox * g.sw - g.pw + kx;
+    T* d = out + (size_t)gt * KK * g.C + v * VEC;
     if (y < 0 || y >= g.H || x < 0 || x >= g.W) {
       Vec<T, VEC>::zero(d);
     } else {
-      const T* src = src_t + (y * g.W + x) * g.C + cv * VEC;
+      const T* src = in + (((size_t)t * g.H + y) * g.W + x) * g.C + cv * VEC;
       if constexpr (sizeof(T) == 2)
         *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(src));
       else
@@ -138,18 +142,146 @@ __global__ void __launch_bounds__(256) fold_kernel(const Tin* __restrict__ in, T
   }
 }
 
+// ---- compile-time-geometry variants (the hot shapes: 7x7 kernel, stride 3) ----------------
+// Same results as the generic kernels above; all index divisions are by constants.
+template <typename T, int VEC, int CV, int KH, int KW>
+__global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g,
+                                                           int ntok) {
+  constexpr int KK = KH * KW, PER = KK * CV;
+  const int P = g.oh * g.ow;
+  const int total = ntok * PER;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int gt = i / PER, v = i - gt * PER;        // token, vector within the token
+    const int j = v / CV, cv = v - j * CV;
+    const int ky = j / KW, kx = j - ky * KW;
+    const int t = gt / P, tok = gt - t * P;
+    const int oy = tok / g.ow, ox = tok - oy * g.ow;
+    const int y = oy * g.sh - g.ph + ky, x = ox * g.sw - g.pw + kx;
+    T* d = out + (size_t)i * VEC;
+    if (y < 0 || y >= g.H || x < 0 || x >= g.W) {
+      Vec<T, VEC>::zero(d);
+    } else {
+      const T* src = in + (((size_t)t * g.H + y) * g.W + x) * (CV * VEC) + cv * VEC;
+      if constexpr (sizeof(T) == 2)
+        *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(src));
+      else
+        *reinterpret_cast<float4*>(d) = __ldg(reinterpret_cast<const float4*>(src));
+    }
+  }
+}
+
+template <typename Tin, typename Tout, int VEC, int CV, int KH, int KW, int SH, int SW, bool GELU>
+__global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g,
+                                                         int ncell) {
+  constexpr int KK = KH * KW, C = CV * VEC;
+  constexpr int MAXC = (KH + SH - 1) / SH > (KW + SW - 1) / SW ? (KH + SH - 1) / SH : (KW + SW - 1) / SW;
+  const int P = g.oh * g.ow;
+  const int total = ncell * CV;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int cell = i / CV, cv = i - cell * CV;
+    const int tw = cell / g.W, x = cell - tw * g.W;
+    const int t = tw / g.H, y = tw - t * g.H;
+    const int yy = y + g.ph, xx = x + g.pw;
+    int oy0 = yy - KH + 1;
+    oy0 = oy0 <= 0 ? 0 : (oy0 + SH - 1) / SH;
+    int oy1 = yy / SH;
+    oy1 = oy1 < g.oh - 1 ? oy1 : g.oh - 1;
+    int ox0 = xx - KW + 1;
+    ox0 = ox0 <= 0 ? 0 : (ox0 + SW - 1) / SW;
+    int ox1 = xx / SW;
+    ox1 = ox1 < g.ow - 1 ? ox1 : g.ow - 1;
+    const Tin* in_t = in + (size_t)t * P * KK * C + cv * VEC;
+    float acc[VEC];
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
+    float f[MAXC][MAXC][VEC];
+#pragma unroll
+    for (int a = 0; a < MAXC; ++a)
+#pragma unroll
+      for (int b = 0; b < MAXC; ++b)
+        if (oy0 + a <= oy1 && ox0 + b <= ox1) {
+          const int oy = oy0 + a, ox = ox0 + b;
+          const int ky = yy - oy * SH, kx = xx - ox * SW;
+          Vec<Tin, VEC>::ld(in_t + ((size_t)(oy * g.ow + ox) * KK + ky * KW + kx) * C, f[a][b]);
+        }
+#pragma unroll
+    for (int a = 0; a < MAXC; ++a)
+#pragma unroll
+      for (int b = 0; b < MAXC; ++b)
+        if (oy0 + a <= oy1 && ox0 + b <= ox1) {
+#pragma unroll
+          for (int k = 0; k < VEC; ++k) acc[k] += f[a][b][k];
+        }
+    const float c = (float)((oy1 - oy0 + 1) * (ox1 - ox0 + 1));
+#pragma unroll
+    for (int k = 0; k < VEC; ++k) {
+      acc[k] = __fdiv_rn(acc[k], c);
+      if (GELU) acc[k] = gelu_erf(acc[k]);
+    }
+    Vec<Tout, VEC>::st(out + (size_t)cell * C + cv * VEC, acc);
+  }
+}
+
+template <> struct Vec<bf16, 4> {
+  static __device__ __forceinline__ void ld(const bf16* p, float* f) {
+    uint2 u = *reinterpret_cast<const uint2*>(p);
+    f[0] = __uint_as_float(u.x << 16); f[1] = __uint_as_float(u.x & 0xFFFF0000u);
+    f[2] = __uint_as_float(u.y << 16); f[3] = __uint_as_float(u.y & 0xFFFF0000u);
+  }
+  static __device__ __forceinline__ void st(bf16* p, const float* f) {
+    *reinterpret_cast<uint2*>(p) = make_uint2(pack_bf16(f[0], f[1]), pack_bf16(f[2], f[3]));
+  }
+  static __device__ __forceinline__ void zero(bf16* p) { *reinterpret_cast<uint2*>(p) = make_uint2(0, 0); }
+};
+
+static int grid_cap(long long total, int per_block = 256) {
+  long long b = (total + per_block - 1) / per_block;
+  return int(b < 148 * 32 ? (b ? b : 1) : 148 * 32);
+}
+
 cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st) {
-  const int blocks = n * g.oh * g.ow;
+  const int ntok = n * g.oh * g.ow;
+  if (g.kh == 7 && g.kw == 7) {
+    const int CV = g.C / (dtype == 0 ? 8 : 4);
+    const long long total = (long long)ntok * 49 * CV;
+#define UF(T, V, CVV)                                                                                     \
+    if (CV == CVV) {                                                                                      \
+      unfold_fixed_kernel<T, V, CVV, 7, 7><<<grid_cap(total), 256, 0, st>>>((const T*)in, (T*)out, g, ntok); \
+      return cudaGetLastError();                                                                          \
+    }
+    if (dtype == 0) { UF(bf16, 8, 16) UF(bf16, 8, 5) UF(bf16, 8, 32) }
+    else { UF(float, 4, 4) UF(float, 4, 10) UF(float, 4, 32) }
+#undef UF
+  }
+  const int per = g.kh * g.kw * (g.C / (dtype == 0 ? 8 : 4));
+  const int tpb = (per >= 512) ? 1 : (512 + per - 1) / per;
+  const int blocks = (ntok + tpb - 1) / tpb;
   if (dtype == 0)
-    unfold_kernel<bf16, 8><<<blocks, 128, 0, st>>>((const bf16*)in, (bf16*)out, g);
+    unfold_kernel<bf16, 8><<<blocks, 256, 0, st>>>((const bf16*)in, (bf16*)out, g, ntok);
   else
-    unfold_kernel<float, 4><<<blocks, 128, 0, st>>>((const float*)in, (float*)out, g);
+    unfold_kernel<float, 4><<<blocks, 256, 0, st>>>((const float*)in, (float*)out, g, ntok);
   return cudaGetLastError();
 }
 
 cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g, bool gelu,
                         cudaStream_t st) {
   const int blocks = n * g.H;
+  if (g.kh == 7 && g.kw == 7 && g.sh == 3 && g.sw == 3) {
+    const int ncell = n * g.H * g.W;
+#define FF(TI, TO, V, CVV)                                                                                    \
+    if (g.C == CVV * V) {                                                                                     \
+      const long long total = (long long)ncell * CVV;                                                        \
+      if (gelu)                                                                                               \
+        fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true><<<grid_cap(total), 256, 0, st>>>((const TI*)in, (TO*)out, g, ncell); \
+      else                                                                                                    \
+        fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false><<<grid_cap(total), 256, 0, st>>>((const TI*)in, (TO*)out, g, ncell); \
+      return cudaGetLastError();                                                                              \
+    }
+    if (in_dtype == 1 && out_dtype == 0) { FF(float, bf16, 4, 10) FF(float, bf16, 4, 32) }
+    if (in_dtype == 1 && out_dtype == 1) { FF(float, float, 4, 10) FF(float, float, 4, 4) FF(float, float, 4, 32) }
+    if (in_dtype == 0 && out_dtype == 0) { FF(bf16, bf16, 8, 16) FF(bf16, bf16, 8, 5) }
+#undef FF
+  }
 #define FOLD(TI, TO, V)                                                                              \
   (gelu ? (fold_kernel<TI, TO, V, true><<<blocks, 256, 0, st>>>((const TI*)in, (TO*)out, g), 0)        \
         : (fold_kernel<TI, TO, V, false><<<blocks, 256, 0, st>>>((const TI*)in, (TO*)out, g), 0))

@@ -40,9 +40,56 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
   }
 }
 
+// Vectorised variant for D % 128 == 0 (D <= 1024): lane l owns float4 columns l, l+32, ...
+// so every load / store instruction of a warp covers one contiguous 512 B (256 B) span.
+template <typename Tout, int NV>
+__global__ void __launch_bounds__(256) layernorm_v4_kernel(const float4* __restrict__ x, const float4* __restrict__ g,
+                                                           const float4* __restrict__ b, Tout* __restrict__ out,
+                                                           int rows, int D) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const int D4 = D / 4;
+  const float4* xr = x + (size_t)warp * D4;
+  float4 v[NV];
+  float sm = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    v[i] = xr[i * 32 + lane];
+    sm += (v[i].x + v[i].y) + (v[i].z + v[i].w);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
+  const float mu = sm / D;
+  float q = 0.f;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float a0 = v[i].x - mu, a1 = v[i].y - mu, a2 = v[i].z - mu, a3 = v[i].w - mu;
+    q += (a0 * a0 + a1 * a1) + (a2 * a2 + a3 * a3);
+  }
+#pragma unroll
+  for (int o = 16; o; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+  const float rstd = rsqrtf(q / D + 1e-5f);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    const float4 gg = __ldg(g + i * 32 + lane), bb = __ldg(b + i * 32 + lane);
+    const float o0 = (v[i].x - mu) * rstd * gg.x + bb.x, o1 = (v[i].y - mu) * rstd * gg.y + bb.y;
+    const float o2 = (v[i].z - mu) * rstd * gg.z + bb.z, o3 = (v[i].w - mu) * rstd * gg.w + bb.w;
+    if constexpr (sizeof(Tout) == 2) {
+      reinterpret_cast<uint2*>(out)[(size_t)warp * D4 + i * 32 + lane] = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+    } else {
+      reinterpret_cast<float4*>(out)[(size_t)warp * D4 + i * 32 + lane] = make_float4(o0, o1, o2, o3);
+    }
+  }
+}
+
 cudaError_t launch_layernorm(const float* x, const float* g, const float* b, void* out, int out_dtype, int rows,
                              int D, cudaStream_t st) {
   const int blocks = (rows * 32 + 255) / 256;
+  if (D % 128 == 0 && D <= 1024) {
+#define LNV(NV)                                                                                                    if (D == NV * 128) {                                                                                               if (out_dtype == 0)                                                                                                layernorm_v4_kernel<bf16, NV><<<blocks, 256, 0, st>>>((const float4*)x, (const float4*)g, (const float4*)b,                                                             (bf16*)out, rows, D);                                   else                                                                                                               layernorm_v4_kernel<float, NV><<<blocks, 256, 0, st>>>((const float4*)x, (const float4*)g,                                                                              (const float4*)b, (float*)out, rows, D);                return cudaGetLastError();                                                                                     }
+    LNV(1) LNV(2) LNV(3) LNV(4) LNV(5) LNV(6) LNV(7) LNV(8)
+#undef LNV
+  }
 #define LN_CASE(PER)                                                                                   \
   if (D <= PER * 32) {                                                                                 \
     if (out_dtype == 0)                                                                                \

@@ -1,6 +1,7 @@
 // Standalone timing of the tcgen05 GEMM kernel (gemm_tc.cu) on the memory-step shapes.
 #include <cstdio>
 #include <vector>
+#define VI_GEMM_TRACE 1
 #include "../../paper_2403_16161_b200/csrc/kernels/gemm_tc.cu"
 using namespace vi;
 
@@ -19,37 +20,35 @@ static CUtensorMap tmap(void* base, uint64_t inner, uint64_t outer, uint32_t bi,
   return m;
 }
 
-static void run(const char* name, int M, int N, int K, int bn, int kind) {
+static void run(const char* name, int M, int N, int K, int bn, int kind, int cl = 0) {
   void *A, *W, *O; float *bias, *x;
   cudaMalloc(&A, (size_t)M * K * 2); cudaMalloc(&W, (size_t)N * K * 2); cudaMalloc(&O, (size_t)M * N * 4);
   cudaMalloc(&bias, N * 4); cudaMalloc(&x, (size_t)M * N * 4);
   cudaMemset(A, 0, (size_t)M * K * 2); cudaMemset(W, 0, (size_t)N * K * 2); cudaMemset(bias, 0, N * 4); cudaMemset(x, 0, (size_t)M * N * 4);
-  CUtensorMap ta = tmap(A, K, M, 64, 128), tb = tmap(W, K, N, 64, bn);
+  const int CM = (cl & 1) ? 2 : 1, CN = (cl & 2) ? 2 : 1;
+  CUtensorMap ta = tmap(A, K, M, 64, 128 / CN), tb = tmap(W, K, N, 64, bn / CM);
   Epi e; memset(&e, 0, sizeof(e));
   e.kind = kind; e.M = M; e.N = N; e.bias = bias; e.out = O; e.ldo = N; e.P = 1; e.S = 1; e.x_in = x; e.x_out = x;
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
-  for (int i = 0; i < 3; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0);
+  for (int i = 0; i < 3; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0, cl);
   const int it = 50;
   cudaEventRecord(a);
-  for (int i = 0; i < it; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0);
+  for (int i = 0; i < it; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0, cl);
   cudaEventRecord(b);
   cudaError_t err = cudaEventSynchronize(b);
+  long long tr[16]; cudaMemcpyFromSymbol(tr, g_gemm_trace, sizeof(tr));
+  printf("   trace(us): setup %.2f firstfull %.2f mma_done %.2f epi_start %.2f epi_end %.2f exit %.2f\n",
+         (tr[1]-tr[0])/1e3, (tr[2]-tr[0])/1e3, (tr[3]-tr[0])/1e3, (tr[4]-tr[0])/1e3, (tr[5]-tr[0])/1e3, (tr[6]-tr[0])/1e3);
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double us = ms * 1000 / it, tf = 2.0 * M * N * K / (us * 1e-6) / 1e12;
-  printf("%-8s M=%d N=%d K=%d BN=%d epi=%d: %s %.2f us  %.0f TFLOP/s\n", name, M, N, K, bn, kind, cudaGetErrorString(err), us, tf);
+  printf("%-8s M=%d N=%d K=%d BN=%d epi=%d cl=%d: %s %.2f us  %.0f TFLOP/s\n", name, M, N, K, bn, kind, cl, cudaGetErrorString(err), us, tf);
   cudaFree(A); cudaFree(W); cudaFree(O); cudaFree(bias); cudaFree(x);
 }
 
 int main(int argc, char** argv) {
-  if (argc > 1) { run("qkvS", 3600, 1536, 512, 128, EPI_STORE); return 0; }
   run("oproj", 3600, 512, 512, 128, EPI_RESID);
-  run("oprojS", 3600, 512, 512, 128, EPI_STORE);
   run("oprojN", 3600, 512, 512, 128, EPI_NONE);
-  run("qkvN", 3600, 1536, 512, 128, EPI_NONE);
-  run("qkvS", 3600, 1536, 512, 128, EPI_STORE);
-  run("ffn1", 3600, 1960, 512, 128, EPI_STORE);
-  run("ffn2", 3600, 512, 1960, 128, EPI_RESID);
-  run("embed", 3600, 512, 6272, 128, EPI_STORE);
-  run("back", 3600, 6272, 1024, 256, EPI_STORE);
+  run("qkv", 3600, 1536, 512, 128, EPI_STORE);
+  run("one", 128, 128, 512, 128, EPI_STORE);
   return 0;
 }
