@@ -214,10 +214,10 @@ def run_ours(args, cfg):
     e2e_value = streams.aggregate_fps(T * e2e_steps, world, e2e_s)
     bf16_peak, hbm_peak, peak_src = peaks()
     attn_ms, attn_recs = prof["attention"]
-    per_block_ms = attn_ms / (args.steps * cfg.layers)
+    per_block_ms = attn_ms / (args.steps * cfg.layers) if attn_ms > 0 else float("nan")
     nq, nk = T * P, cfg.slots * P
     attn_flop = 4.0 * nq * nk * D
-    achieved = attn_flop / (per_block_ms * 1e-3) / 1e12
+    achieved = attn_flop / (per_block_ms * 1e-3) / 1e12 if attn_ms > 0 else float("nan")
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "attention_traffic.json")) as f:
@@ -243,6 +243,8 @@ def run_ours(args, cfg):
         "gpu_launches": launches,
         "clocks": clk,
     }
+    line["device_time_ms_per_step"] = {"attention": attn_ms / args.steps, "gemm": prof["gemm"][0] / args.steps,
+                                       "other": (total_ms - attn_ms - prof["gemm"][0]) / args.steps}
     if os.environ.get("VI_PROFILE_MODE") == "2":
         line["profile_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}
         line["profile_launches_per_step"] = {k: v[1] / args.steps for k, v in prof.items()}

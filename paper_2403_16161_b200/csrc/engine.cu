@@ -411,7 +411,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     c->lse = (float*)A((size_t)kMaxSplit * c->H * rows * 4);
   }
   c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);
-  c->attn_timing = (unsigned long long*)A(sizeof(KernelTiming));
+  c->attn_timing = (unsigned long long*)A(2 * sizeof(KernelTiming));   // [0] attention, [1] GEMMs
   c->num_sms = prop.multiProcessorCount;
   if (c->bf16) {
     c->sk_part = (float*)A((size_t)c->num_sms * 256 * c->hd * 4);
@@ -427,10 +427,10 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     return VI_E_CUDA;
   }
   {
-    KernelTiming kt;
-    std::memset(&kt, 0, sizeof(kt));
-    kt.tmin = ~0ull;
-    if (cudaMemcpy(c->attn_timing, &kt, sizeof(kt), cudaMemcpyHostToDevice) != cudaSuccess) {
+    KernelTiming kt[2];
+    std::memset(kt, 0, sizeof(kt));
+    kt[0].tmin = kt[1].tmin = ~0ull;
+    if (cudaMemcpy(c->attn_timing, kt, sizeof(kt), cudaMemcpyHostToDevice) != cudaSuccess) {
       delete c;
       return VI_E_CUDA;
     }
@@ -622,15 +622,19 @@ extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refin
 
 // ------------------------------------------------------------------------------ compute
 
+static vi_ctx* g_epi_ctx = nullptr;   // set by the launching entry point (single-threaded per ctx)
 static Epi epi_base(int kind, int M, int N, const float* bias) {
   Epi e;
   std::memset(&e, 0, sizeof(e));
   e.kind = kind; e.M = M; e.N = N; e.bias = bias; e.P = 1; e.S = 1;
+  if (g_epi_ctx && g_epi_ctx->prof_mode == 3)
+    e.timing = g_epi_ctx->attn_timing + sizeof(KernelTiming) / sizeof(unsigned long long);
   return e;
 }
 
 extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out, int project) {
   LIVE(c);
+  g_epi_ctx = c;
   if (!feat || !out || n < 1 || n > c->Tmax || (project != 0 && project != 1))
     return c->fail(VI_E_ARG, "vi_soft_split: bad argument");
   if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_split: weights not set");
@@ -691,6 +695,7 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
 
 extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, float* x_out) {
   LIVE(c);
+  g_epi_ctx = c;
   if (!x_in || !x_out) return c->fail(VI_E_ARG, "vi_memory_step: NULL x");
   if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_memory_step: weights not set");
   if (c->next_layer < 0 || layer != c->next_layer || layer >= c->L)
@@ -726,7 +731,7 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
     a.o = static_cast<bf16*>(c->o); a.opart = c->opart; a.lse = c->lse;
-    a.timing = c->prof_mode == 1 ? c->attn_timing : nullptr;
+    a.timing = (c->prof_mode == 1 || c->prof_mode == 3) ? c->attn_timing : nullptr;
     static long long* trace_buf = nullptr;
     static int trace_calls = 0;
     if (getenv("VI_ATTN_TRACE") && !trace_buf) cudaMalloc(&trace_buf, 32 * 32 * sizeof(long long));
@@ -836,6 +841,7 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
 
 extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* feat, int project) {
   LIVE(c);
+  g_epi_ctx = c;
   if (!in || !feat || n < 1 || n > c->Tmax || (project != 0 && project != 1))
     return c->fail(VI_E_ARG, "vi_soft_composite: bad argument");
   if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_composite: weights not set");
@@ -946,7 +952,7 @@ extern "C" vi_status vi_sync(vi_ctx* c) {
 
 extern "C" vi_status vi_profile(vi_ctx* c, int mode) {
   LIVE(c);
-  if (mode < 0 || mode > 2) return VI_E_ARG;
+  if (mode < 0 || mode > 3) return VI_E_ARG;
   c->prof_mode = mode;
   return VI_OK;
 }
@@ -956,14 +962,16 @@ extern "C" vi_status vi_profile_read(vi_ctx* c, double* ms, int64_t* launches) {
   CK(cudaStreamSynchronize(c->stream), "profile sync");
   double acc[VI_PROF_N] = {0, 0, 0, 0};
   int64_t cnt[VI_PROF_N] = {0, 0, 0, 0};
-  {  // attention kernels' self-timing (mode 1; graph-safe)
-    KernelTiming kt;
-    CK(cudaMemcpy(&kt, c->attn_timing, sizeof(kt), cudaMemcpyDeviceToHost), "profile read");
-    acc[VI_PROF_ATTN] += double(kt.total_ns) * 1e-6;
-    cnt[VI_PROF_ATTN] += int64_t(kt.launches);
-    std::memset(&kt, 0, sizeof(kt));
-    kt.tmin = ~0ull;
-    CK(cudaMemcpy(c->attn_timing, &kt, sizeof(kt), cudaMemcpyHostToDevice), "profile reset");
+  {  // kernels' self-timing (mode 1; graph-safe): [0] attention, [1] GEMMs
+    KernelTiming kt[2];
+    CK(cudaMemcpy(kt, c->attn_timing, sizeof(kt), cudaMemcpyDeviceToHost), "profile read");
+    acc[VI_PROF_ATTN] += double(kt[0].total_ns) * 1e-6;
+    cnt[VI_PROF_ATTN] += int64_t(kt[0].launches);
+    acc[VI_PROF_GEMM] += double(kt[1].total_ns) * 1e-6;
+    cnt[VI_PROF_GEMM] += int64_t(kt[1].launches);
+    std::memset(kt, 0, sizeof(kt));
+    kt[0].tmin = kt[1].tmin = ~0ull;
+    CK(cudaMemcpy(c->attn_timing, kt, sizeof(kt), cudaMemcpyHostToDevice), "profile reset");
   }
   for (auto& r : c->prof_recs) {
     float t = 0.f;

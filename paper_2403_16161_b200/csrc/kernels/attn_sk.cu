@@ -8,7 +8,8 @@
 // kernel).  A unit cut by a slice boundary is finished by the CTA holding its first tile
 // (the "owner"): every other CTA holding a piece of it writes a normalised partial (O/l,
 // log2-sum-exp) into its own slot and raises a flag; the owner merges the slots in CTA
-// order (deterministic) with its own TMEM accumulator and writes the output.  A CTA's
+// order (deterministic) with its own TMEM accumulator and writes the output.  320 threads:
+// warps 0-7 softmax (two warpgroups), warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.  A CTA's
 // continuation piece is always at the start of its slice, so it is ready long before the
 // owner reaches the end of its slice.  The launch is cooperative (all CTAs co-resident).
 #include "kernels.h"
@@ -48,13 +49,13 @@ __device__ __forceinline__ void sk_bar_sync(int id, int n) {
 __device__ __forceinline__ long long sk_begin(long long W, int G, int c) { return W * c / G; }
 
 template <int HD>
-__global__ void __launch_bounds__(384, 1)
+__global__ void __launch_bounds__(320, 1)
 attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
   using L = AttnSkSmem<HD>;
   constexpr int ST = L::ST;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays in .shared
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* q_full = bars;
   uint64_t* q_empty = bars + 1;
@@ -95,7 +96,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
     }
     fence_barrier_init();
   }
-  if (warp == 10) tmem_alloc(tmem_slot, 512);
+  if (warp == 9) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
@@ -430,7 +431,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
-  if (warp == 10) {
+  if (warp == 9) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
@@ -448,7 +449,7 @@ static cudaError_t launch_sk_hd(const CUtensorMap& tq, const CUtensorMap& tk, co
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(384);
+  cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = L::TOTAL;
   cfg.stream = st;
   cudaLaunchAttribute at[1];

@@ -31,6 +31,7 @@ struct Epi {
   void* vtslab;           // [D][S*P] (this layer)
   int first_slot, S;
   int vt_ld;              // row pitch (elements) of the Vt slab, >= S*P, multiple of 64
+  unsigned long long* timing;  // KernelTiming of the GEMM category (profile mode 1) or NULL
 };
 
 template <typename T>

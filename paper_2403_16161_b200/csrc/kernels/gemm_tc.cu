@@ -50,7 +50,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   using L = GemmSmem<BN, STAGES>;
   constexpr int CS = CM * CN;
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays in .shared
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;     // [2] accumulator ready for the epilogue
@@ -94,6 +94,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) GTR(1);
+  if (threadIdx.x == 0) time_begin(epi.timing);
 
   if (warp == 0) {
     if (lane == 0) {
@@ -190,6 +191,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tmem_dealloc(tmem, TMEM_COLS);
   }
   if (threadIdx.x == 0) GTR(6);
+  if (threadIdx.x == 0) time_end(epi.timing, gridDim.x);
 }
 
 static int g_num_sms = 0;
@@ -240,8 +242,9 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   return cudaLaunchKernelEx(&cfg, kfn, a, b, K, brow0, e);
 }
 
-// cluster: 0 = none, 1 = 2 CTAs along m (W tile multicast), 2 = 2 along n (A multicast),
-// 3 = 2 x 2.  The A map's box must be 64 x (128 / CN), the W map's 64 x (BN / CM).
+// cluster (CM x CN): 0 = 1x1, 1 = 2x1 (W tile multicast), 2 = 1x2 (A multicast), 3 = 2x2,
+// 4 = 1x4, 5 = 2x4, 6 = 1x8, 7 = 4x2.  The A map's box must be 64 x (128 / CN), the W map's
+// 64 x (BN / CM).
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K, int bn,
                            const Epi& e, cudaStream_t st, int cluster) {
 #define CASES(BN, ST)                                                              \
@@ -250,6 +253,10 @@ cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0
     case 1: return launch_cfg<BN, ST, 2, 1>(a, b, brow0, M, N, K, e, st);          \
     case 2: return launch_cfg<BN, ST, 1, 2>(a, b, brow0, M, N, K, e, st);          \
     case 3: return launch_cfg<BN, ST, 2, 2>(a, b, brow0, M, N, K, e, st);          \
+    case 4: return launch_cfg<BN, ST, 1, 4>(a, b, brow0, M, N, K, e, st);          \
+    case 5: return launch_cfg<BN, ST, 2, 4>(a, b, brow0, M, N, K, e, st);          \
+    case 6: return launch_cfg<BN, ST, 1, 8>(a, b, brow0, M, N, K, e, st);          \
+    case 7: return launch_cfg<BN, ST, 4, 2>(a, b, brow0, M, N, K, e, st);          \
     default: return cudaErrorInvalidValue;                                         \
   }
   switch (bn) {

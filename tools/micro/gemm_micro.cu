@@ -1,7 +1,7 @@
 // Standalone timing of the tcgen05 GEMM kernel (gemm_tc.cu) on the memory-step shapes.
 #include <cstdio>
 #include <vector>
-#define VI_GEMM_TRACE 1
+
 #include "../../paper_2403_16161_b200/csrc/kernels/gemm_tc.cu"
 using namespace vi;
 
@@ -25,7 +25,8 @@ static void run(const char* name, int M, int N, int K, int bn, int kind, int cl 
   cudaMalloc(&A, (size_t)M * K * 2); cudaMalloc(&W, (size_t)N * K * 2); cudaMalloc(&O, (size_t)M * N * 4);
   cudaMalloc(&bias, N * 4); cudaMalloc(&x, (size_t)M * N * 4);
   cudaMemset(A, 0, (size_t)M * K * 2); cudaMemset(W, 0, (size_t)N * K * 2); cudaMemset(bias, 0, N * 4); cudaMemset(x, 0, (size_t)M * N * 4);
-  const int CM = (cl & 1) ? 2 : 1, CN = (cl & 2) ? 2 : 1;
+  const int CMs[8] = {1, 2, 1, 2, 1, 2, 1, 4}, CNs[8] = {1, 1, 2, 2, 4, 4, 8, 2};
+  const int CM = CMs[cl], CN = CNs[cl];
   CUtensorMap ta = tmap(A, K, M, 64, 128 / CN), tb = tmap(W, K, N, 64, bn / CM);
   Epi e; memset(&e, 0, sizeof(e));
   e.kind = kind; e.M = M; e.N = N; e.bias = bias; e.out = O; e.ldo = N; e.P = 1; e.S = 1; e.x_in = x; e.x_out = x;
@@ -36,9 +37,7 @@ static void run(const char* name, int M, int N, int K, int bn, int kind, int cl 
   for (int i = 0; i < it; ++i) launch_gemm_tc(ta, tb, 0, M, N, K, bn, e, 0, cl);
   cudaEventRecord(b);
   cudaError_t err = cudaEventSynchronize(b);
-  long long tr[16]; cudaMemcpyFromSymbol(tr, g_gemm_trace, sizeof(tr));
-  printf("   trace(us): setup %.2f firstfull %.2f mma_done %.2f epi_start %.2f epi_end %.2f exit %.2f\n",
-         (tr[1]-tr[0])/1e3, (tr[2]-tr[0])/1e3, (tr[3]-tr[0])/1e3, (tr[4]-tr[0])/1e3, (tr[5]-tr[0])/1e3, (tr[6]-tr[0])/1e3);
+
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double us = ms * 1000 / it, tf = 2.0 * M * N * K / (us * 1e-6) / 1e12;
   printf("%-8s M=%d N=%d K=%d BN=%d epi=%d cl=%d: %s %.2f us  %.0f TFLOP/s\n", name, M, N, K, bn, kind, cl, cudaGetErrorString(err), us, tf);
@@ -46,9 +45,7 @@ static void run(const char* name, int M, int N, int K, int bn, int kind, int cl 
 }
 
 int main(int argc, char** argv) {
-  run("oproj", 3600, 512, 512, 128, EPI_RESID);
-  run("oprojN", 3600, 512, 512, 128, EPI_NONE);
-  run("qkv", 3600, 1536, 512, 128, EPI_STORE);
-  run("one", 128, 128, 512, 128, EPI_STORE);
+  run("qkvS", 3600, 1536, 512, 128, EPI_STORE, 0);
+  run("qkvN", 3600, 1536, 512, 128, EPI_NONE, 0);
   return 0;
 }
