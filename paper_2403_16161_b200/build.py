@@ -24,6 +24,7 @@ SOURCES = [
     "kernels/gemm_tc.cu",
     "kernels/attn.cu",
     "kernels/attn_sk.cu",
+    "kernels/attn_sk2.cu",
 ]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -1,3 +1,4 @@
+#include <climits>
 // libvi.so engine: the vi_* C-ABI (include/vi.h) over the sm_100a kernels.
 //
 // Per context (one live stream on one GPU) the engine owns, in HBM:
@@ -209,6 +210,11 @@ static const bool g_attn_split = [] {
 static const bool g_attn_colsplit = [] {
   const char* e = getenv("VI_ATTN_COLSPLIT");
   return e && e[0] == '1';
+}();
+// VI_ATTN_SK=1|2: stream-K attention with 8 (row-per-thread) or 16 (column-split) softmax warps.
+static const int g_attn_sk = [] {
+  const char* e = getenv("VI_ATTN_SK");
+  return e ? atoi(e) : 2;
 }();
 static void debug_wait(vi_ctx* c, const char* where) {
   for (int i = 0; i < 20000; ++i) {
@@ -755,8 +761,35 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
       const long long work = (long long)a.units * ntiles;
       int grid = int(work < c->num_sms ? work : c->num_sms);
       if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
-      PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-      if (sk_tr) {
+      if (g_attn_sk == 1)
+        PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+      else
+        PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+      if (sk_tr && g_attn_sk == 2) {
+        std::vector<long long> h(32 * 32);
+        cudaMemcpyAsync(h.data(), sk_trace, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
+        cudaStreamSynchronize(c->stream);
+        const long long t0 = h[24];
+        fprintf(stderr, "[sk2] j | per tile: S_rdy max P_arr(hf0 min..max) P_arr(hf1 min..max) mma_p0 mma_p1 qk_issued\n");
+        for (int j = 0; j < 32 && h[j * 32 + 24]; ++j) {
+          fprintf(stderr, "[sk2] %2d", j);
+          for (int t = 0; t < 2; ++t) {
+            const long long* e = &h[j * 32];
+            long long pm[2][2];
+            for (int hf = 0; hf < 2; ++hf) {
+              pm[hf][0] = LLONG_MAX; pm[hf][1] = 0;
+              for (int q = 0; q < 4; ++q) {
+                pm[hf][0] = std::min(pm[hf][0], e[4 + t * 8 + hf * 4 + q]);
+                pm[hf][1] = std::max(pm[hf][1], e[4 + t * 8 + hf * 4 + q]);
+              }
+            }
+            fprintf(stderr, " | %6lld %6lld %6lld..%-6lld %6lld..%-6lld pv_in %6lld v %6lld p0 %6lld p1 %6lld qk %6lld", e[t] - t0,
+                    e[2 + t] - t0, pm[0][0] - t0, pm[0][1] - t0, pm[1][0] - t0, pm[1][1] - t0, e[28 + t] - t0,
+                    t == 0 ? e[30] - t0 : 0, e[20 + t] - t0, e[26 + t] - t0, e[24 + t] - t0);
+          }
+          fprintf(stderr, "\n");
+        }
+      } else if (sk_tr) {
         std::vector<long long> h(148 * 32);
         cudaMemcpyAsync(h.data(), sk_trace, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
         cudaStreamSynchronize(c->stream);

@@ -1,23 +1,20 @@
-// Memory attention, persistent stream-K variant (the default bf16 path).
+// Memory attention, persistent stream-K, COLUMN-SPLIT softmax (the default bf16 kernel).
 //
-// Same math and per-tile pipeline as attn_tc2_kernel (attn.cu): two 128-query tiles per
-// CTA, S/P and O in TMEM, P as the TMEM A operand of O += P V, ping-pong softmax
-// warpgroups, lazy rescale, 3/8 of the exponentials by polynomial.  What changes is the
-// work split: work = units x key tiles, unit = (query-tile pair, head); a grid of one CTA
-// per SM takes contiguous, equal slices of that work (no idle SMs, no separate combine
-// kernel).  A unit cut by a slice boundary is finished by the CTA holding its first tile
-// (the "owner"): every other CTA holding a piece of it writes a normalised partial (O/l,
-// log2-sum-exp) into its own slot and raises a flag; the owner merges the slots in CTA
-// order (deterministic) with its own TMEM accumulator and writes the output.  320 threads:
-// warps 0-7 softmax (two warpgroups), warp 8 TMA producer, warp 9 TMEM allocator + MMA issuer.  A CTA's
-// continuation piece is always at the start of its slice, so it is ready long before the
-// owner reaches the end of its slice.  The launch is cooperative (all CTAs co-resident).
+// attn_sk.cu's design (two 128-query tiles per CTA, S/P and O in TMEM, P as the TMEM A
+// operand, stream-K work split with owner merge) with 16 softmax warps instead of 8: for
+// each Q tile, warps w and w+4 own the same 32 rows and keys [0,64) / [64,128) of every
+// key tile (and O columns [0,64) / [64,128)).  The row max of a tile is exchanged through
+// shared memory between the two warps (one named barrier per warp pair); everything else
+// (exponentials, P halves, row sums, O rescale, epilogue columns) is per half.  This halves
+// the softmax latency that sits on the per-Q-tile chain softmax -> PV -> QK -> softmax.
+// 576 threads: warps 0-15 softmax (tile t = w / 8, key half = (w / 4) % 2, lane quadrant
+// = w % 4), warp 16 TMA producer, warp 17 TMEM allocator + MMA issuer.
 #include "kernels.h"
 
 namespace vi {
 
 template <int HD>
-struct AttnSkSmem {
+struct AttnSk2Smem {
   static constexpr int ST = 2;
   static constexpr int QB = 128 * HD * 2;
   static constexpr int KB = 128 * HD * 2;
@@ -27,11 +24,12 @@ struct AttnSkSmem {
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
   static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2;
-  static constexpr int STG_OFF = BAR_OFF + NBAR * 8 + 16;      // [8 warps][32 rows][80 B] output staging
-  static constexpr int TOTAL = STG_OFF + 8 * 32 * 80 + 1024;
+  static constexpr int STG_OFF = BAR_OFF + NBAR * 8 + 16;      // [16 warps][32 rows][48 B] output staging
+  static constexpr int XCH_OFF = STG_OFF + 16 * 32 * 48;        // [2 phases][2 tiles][2 halves][128] fp32
+  static constexpr int TOTAL = XCH_OFF + 2 * 2 * 2 * 128 * 4 + 1024;
 };
 
-__device__ __forceinline__ void sk_key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
+__device__ __forceinline__ void sk2_key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
   int i = 0;
   while (i + 1 < s.n && g >= s.tile0[i + 1]) ++i;
   const int off = (g - s.tile0[i]) * 128;
@@ -41,18 +39,21 @@ __device__ __forceinline__ void sk_key_tile(const KeySegs& s, int g, int& row0, 
   nskip = off == 0 ? s.lead[i] : 0;
 }
 
-__device__ __forceinline__ void sk_bar_sync(int id, int n) {
+__device__ __forceinline__ void sk2_named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ void sk2_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
 // slice of the flattened work [0, W) owned by CTA c of G
-__device__ __forceinline__ long long sk_begin(long long W, int G, int c) { return W * c / G; }
+__device__ __forceinline__ long long sk2_begin(long long W, int G, int c) { return W * c / G; }
 
 template <int HD>
-__global__ void __launch_bounds__(320, 1)
-attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
+__global__ void __launch_bounds__(576, 1)
+attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
-  using L = AttnSkSmem<HD>;
+  using L = AttnSk2Smem<HD>;
   constexpr int ST = L::ST;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays in .shared
@@ -73,9 +74,9 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
   const int NT = a.segs.tile0[a.segs.n];
   const long long W = (long long)a.units * NT;
   const int G = gridDim.x, cta = blockIdx.x;
-  const long long w_begin = sk_begin(W, G, cta), w_end = sk_begin(W, G, cta + 1);
+  const long long w_begin = sk2_begin(W, G, cta), w_end = sk2_begin(W, G, cta + 1);
 
-  if (warp == 8 && lane == 0) {
+  if (warp == 16 && lane == 0) {
     tma_prefetch(&tq);
     tma_prefetch(&tk);
     tma_prefetch(&tvt);
@@ -92,19 +93,20 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
       mbar_init(&p_full[2 * t], 128);
       mbar_init(&p_full[2 * t + 1], 128);
       mbar_init(&o_final[t], 1);
-      mbar_init(&o_free[t], 128);
+      mbar_init(&o_free[t], 256);
     }
     fence_barrier_init();
   }
-  if (warp == 9) tmem_alloc(tmem_slot, 512);
+  if (warp == 17) tmem_alloc(tmem_slot, 512);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) time_begin(a.timing);
-  if (a.trace && threadIdx.x == 0) a.trace[(size_t)cta * 32 + 31] = (long long)globaltimer();
+  // debug timeline (VI_SK_TRACE): CTA 0, first segment's first 32 key tiles, 32 clock64 stamps per tile
+  long long* const trc = (a.trace && cta == 0) ? a.trace : nullptr;
 
-  if (warp == 8) {
+  if (warp == 16) {
     // TMA producer: the whole warp walks the schedule, one elected lane issues
     int jg = 0, sg = 0;
     for (long long w = w_begin; w < w_end; ++sg) {
@@ -123,7 +125,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
       __syncwarp();
       for (int j = ta; j < tb; ++j, ++jg) {
         int row0, nv, nskip;
-        sk_key_tile(a.segs, j, row0, nv, nskip);
+        sk2_key_tile(a.segs, j, row0, nv, nskip);
         const int st = jg % ST;
         const uint32_t par = ((jg / ST) & 1) ^ 1;
         if (jg >= ST) mbar_wait(&k_empty[st], par);
@@ -147,7 +149,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
       }
       w += tb - ta;
     }
-  } else if (warp == 9) {
+  } else if (warp == 17) {
     // The whole warp walks the schedule (warp-uniform control flow keeps the descriptors in
     // uniform registers); one elected lane issues each group of MMAs and commits.
     constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
@@ -171,9 +173,10 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
           mbar_wait(&p_full[2 * t + hh], g & 1);
           tc_fence_after();
           if (elect_one()) {
+            if (trc && g < 32) trc[g * 32 + 20 + hh * 6 + t] = clock64();
 #pragma unroll
             for (int k4 = 0; k4 < 4; ++k4)
-              umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + hh * 32 + k4 * 8,
+              umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + hh * 64 + k4 * 8,
                            dv + uint64_t((hh * (HD * 128) + k4 * 32) >> 4), idesc_o, (j | hh | k4) != 0);
             if (hh == 1 && t == 1) umma_commit(&v_empty[st]);
           }
@@ -194,6 +197,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
             umma_bf16_ss(tmem + t * 128, dq + off, dk + off, idesc_s, kk > 0);
           }
           umma_commit(&s_full[t]);
+          if (trc && g < 32) trc[g * 32 + 24 + t] = clock64();
           if (t == 1) umma_commit(&k_empty[st]);
         }
         __syncwarp();
@@ -213,67 +217,70 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
       jg += n;
       w += n;
     }
-  } else if (warp < 8) {
-    const int t = warp >> 2;                        // Q tile of this warpgroup
+  } else if (warp < 16) {
+    const int t = warp >> 3;                        // Q tile
+    const int hf = (warp >> 2) & 1;                 // key half / O column half
     const int qd = warp & 3;                        // TMEM lane quadrant
     const int row = qd * 32 + lane;                 // row within the Q tile
+    const int pair_bar = 1 + t * 4 + qd;            // named barrier of warps (w, w ^ 4)
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
     const uint32_t TS = tmem + t * 128 + lane_off, TO = tmem + 256 + t * 128 + lane_off;
+    constexpr int OH = HD / 2;                      // O columns of this half
+    float* xch = reinterpret_cast<float*>(smem + L::XCH_OFF);
     const float2 cc = make_float2(a.scale_log2, a.scale_log2);
-    int jg = 0, sg = 0;
+    int jg = 0, sg = 0, ph = 0;
+    // partner exchange of one float per row (double-buffered by phase parity)
+    auto exchange = [&](float v) {
+      float* xb = xch + ((ph & 1) * 4 + t * 2) * 128;
+      xb[hf * 128 + row] = v;
+      sk2_named_bar_sync(pair_bar, 64);
+      const float o = xb[(hf ^ 1) * 128 + row];
+      ++ph;
+      return o;
+    };
     for (long long w = w_begin; w < w_end; ++sg) {
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
       const int h = u / a.npairs, q0 = (u - h * a.npairs) * 256;
       float m_use = -INFINITY, l = 0.f;
-      long long* trc = (a.trace && threadIdx.x == 0 && sg < 3) ? a.trace + (size_t)cta * 32 + sg * 8 : nullptr;
-      if (trc) trc[0] = (long long)globaltimer();
       for (int j = 0; j < n; ++j) {
         const int g = jg + j;
         int row0, nv, nskip;
-        sk_key_tile(a.segs, ta + j, row0, nv, nskip);
+        sk2_key_tile(a.segs, ta + j, row0, nv, nskip);
         mbar_wait(&s_full[t], g & 1);
         tc_fence_after();
-        float s[128];
-#pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld32(TS + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
+        const bool tr = trc && lane == 0 && g < 32;
+        if (tr && hf == 0 && qd == 0) trc[g * 32 + 0 + t] = clock64();
+        float s[64];
+        tmem_ld32(TS + hf * 64, reinterpret_cast<uint32_t*>(s));
+        tmem_ld32(TS + hf * 64 + 32, reinterpret_cast<uint32_t*>(s + 32));
         tmem_wait_ld();
-        if (nv < 128 || nskip > 0) {
+        const int lo = nskip - hf * 64, hi = nv - hf * 64;   // valid local keys [lo, hi)
+        if (lo > 0 || hi < 64) {
 #pragma unroll
-          for (int i = 0; i < 128; ++i)
-            if (i >= nv || i < nskip) s[i] = -INFINITY;
+          for (int i = 0; i < 64; ++i)
+            if (i < lo || i >= hi) s[i] = -INFINITY;
         }
-        float mx[8];
+        float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 128; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
-        const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                                 fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7]))) * a.scale_log2;
-        const bool grow = rmax > m_use + 8.f;       // lazy rescale (exact either way)
+        for (int i = 0; i < 64; ++i) mx[i & 3] = fmaxf(mx[i & 3], s[i]);
+        const float lm = fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3]));
+        // both halves see the same row max, hence the same lazy-rescale decision
+        const float rmax = fmaxf(lm, exchange(lm)) * a.scale_log2;
+        if (tr && hf == 0 && qd == 0) trc[g * 32 + 2 + t] = clock64();
+        const bool grow = rmax > m_use + 8.f;
         float alpha = 1.f;
         if (grow) {
           alpha = ex2(m_use - rmax);
           m_use = rmax;
-        }
-        if (__any_sync(0xffffffffu, grow) && j > 0) {   // PV(j-1) done: O idle (s_full implies it)
-#pragma unroll 1
-          for (int c = 0; c < HD; c += 32) {
-            uint32_t r[32];
-            tmem_ld32(TO + c, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(TO + c, r);
-          }
         }
         const float2 mm = make_float2(-m_use, -m_use);
         float2 sum[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) sum[i] = make_float2(0.f, 0.f);
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t pk[16];
 #pragma unroll
           for (int k = 0; k < 16; ++k) {
@@ -290,64 +297,72 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
             pk[k] = *reinterpret_cast<uint32_t*>(&b);
             sum[k & 3] = fadd2(sum[k & 3], p);
           }
-          tmem_st16(TS + c * 16, pk);
-          if (c & 1) {
-            tmem_wait_st();
-            tc_fence_before();
-            mbar_arrive(&p_full[2 * t + (c >> 1)]);
+          tmem_st16(TS + hf * 64 + c * 16, pk);   // P keys [hf*64, +64) -> packed cols [hf*64, +32)
+        }
+        // O rescale after P (S registers dead by now); PV(j-1) is complete (s_full implies it)
+        if (__any_sync(0xffffffffu, grow) && j > 0) {   // PV(j-1) done (s_full implies it)
+#pragma unroll 1
+          for (int c = 0; c < OH; c += 32) {
+            uint32_t r[32];
+            tmem_ld32(TO + hf * OH + c, r);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
+            tmem_st32(TO + hf * OH + c, r);
           }
         }
+        tmem_wait_st();
+        tc_fence_before();
+        mbar_arrive(&p_full[2 * t + hf]);
+        if (tr) trc[g * 32 + 4 + t * 8 + hf * 4 + qd] = clock64();
         const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
         l = l * alpha + (s01.x + s01.y);
       }
-      // ---- segment epilogue, 32 O columns at a time straight from TMEM (no 128-float
-      // register array: keeps the global loads of a merge all in flight)
-      if (trc) trc[1] = (long long)globaltimer();
+      // ---- segment epilogue: each warp owns O columns [hf*64, +64) of its 32 rows
       mbar_wait(&o_final[t], sg & 1);
       tc_fence_after();
+      l += exchange(l);                             // row sum over both key halves
       const int r256 = t * 128 + row;               // row in the CTA's 256-row slot
       const float lse_own = m_use + __log2f(l);
-      uint8_t* stg = smem + L::STG_OFF + warp * (32 * 80);
+      uint8_t* stg = smem + L::STG_OFF + warp * (32 * 48);
       const int rbase = q0 + t * 128 + qd * 32;
-      // write one 32-column chunk of bf16 output rows through the per-warp stage (8 rows x 64 B
-      // per store instruction; output rows are D*2 bytes apart)
-      auto write_out = [&](int c, const float* f, float scale) {
-        uint4* my = reinterpret_cast<uint4*>(stg + lane * 80);
+      const uint32_t TOh = TO + hf * OH;
+      // 16 O columns -> bf16 output rows via the per-warp stage (16 rows x 32 B per store)
+      auto write_out16 = [&](int c, const float* f, float scale) {   // c: column within the half
+        uint4* my = reinterpret_cast<uint4*>(stg + lane * 48);
 #pragma unroll
-        for (int k = 0; k < 4; ++k)
+        for (int k = 0; k < 2; ++k)
           my[k] = make_uint4(pack_bf16(f[8 * k] * scale, f[8 * k + 1] * scale),
                              pack_bf16(f[8 * k + 2] * scale, f[8 * k + 3] * scale),
                              pack_bf16(f[8 * k + 4] * scale, f[8 * k + 5] * scale),
                              pack_bf16(f[8 * k + 6] * scale, f[8 * k + 7] * scale));
         __syncwarp();
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int rr = i * 8 + (lane >> 2), part = lane & 3;
-          const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
+        for (int i = 0; i < 2; ++i) {
+          const int rr = i * 16 + (lane >> 1), part = lane & 1;
+          const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 48 + part * 16);
           if (rbase + rr < a.Nq)
-            *reinterpret_cast<uint4*>(a.o + (size_t)(rbase + rr) * a.D + h * HD + c + part * 8) = v;
+            *reinterpret_cast<uint4*>(a.o + (size_t)(rbase + rr) * a.D + h * HD + hf * OH + c + part * 8) = v;
         }
         __syncwarp();
       };
       if (ta > 0) {
-        // continuation piece: normalised partial -> this CTA's slot (float4-interleaved over
-        // the 256 rows, coalesced), then raise the flag
+        // continuation piece: normalised partial -> this CTA's slot, then raise the flag
         float4* dst = reinterpret_cast<float4*>(a.spart) + (size_t)cta * (HD / 4) * 256 + r256;
         const float inv = 1.f / l;
 #pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
+        for (int c = 0; c < OH; c += 32) {
           float f[32];
-          tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+          tmem_ld32(TOh + c, reinterpret_cast<uint32_t*>(f));
           tmem_wait_ld();
 #pragma unroll
           for (int k = 0; k < 32; k += 4)
-            dst[((c + k) / 4) * 256] = make_float4(f[k] * inv, f[k + 1] * inv, f[k + 2] * inv, f[k + 3] * inv);
+            dst[((hf * OH + c + k) / 4) * 256] = make_float4(f[k] * inv, f[k + 1] * inv, f[k + 2] * inv, f[k + 3] * inv);
         }
         tc_fence_before();
         mbar_arrive(&o_free[t]);
-        if (trc) trc[4] = (long long)globaltimer();
-        a.slse[(size_t)cta * 256 + r256] = lse_own;
-        sk_bar_sync(1, 256);                         // every row of the slot written (CTA scope) ...
+        if (hf == 0) a.slse[(size_t)cta * 256 + r256] = lse_own;
+        sk2_bar_sync(9, 512);                         // every row of the slot written (CTA scope) ...
         if (threadIdx.x == 0) {                      // ... then one cumulative gpu-scope release
           __threadfence();
           atomicExch(&a.sflag[cta], 1);
@@ -357,87 +372,77 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
         // CTAs cta+1 .. (the unit's last tile) in CTA order
         const long long unit_end = (long long)(u + 1) * NT;
         int last = cta + 1;
-        while (last + 1 < G && sk_begin(W, G, last + 1) < unit_end) ++last;
-        const int np = last - cta;                  // pieces to merge (any number)
-        for (int k = lane; k < np; k += 32) {       // lane i polls the flags of CTAs cta+1+i, +33, ...
+        while (last + 1 < G && sk2_begin(W, G, last + 1) < unit_end) ++last;
+        const int np = last - cta;
+        for (int k = lane; k < np; k += 32) {
           const int* fl = a.sflag + cta + 1 + k;
           while (*reinterpret_cast<const volatile int*>(fl) == 0) __nanosleep(32);
         }
         __syncwarp();
         __threadfence();
-        if (trc) trc[4] = (long long)globaltimer();
         float mx = lse_own;
         for (int k = 0; k < np; ++k) mx = fmaxf(mx, __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256));
         const float wown = ex2(lse_own - mx);
         float wsum = wown;
         for (int k = 0; k < np; ++k) wsum += ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
         const float inv_w = 1.f / wsum;
-        if (trc) trc[5] = (long long)globaltimer();
-        // fold each 128 KB slot in turn: copied (coalesced, all loads in flight) into the
-        // now idle K/V stage buffers, then accumulated into this CTA's O in TMEM
-        float4* stage = reinterpret_cast<float4*>(smem + L::K_OFF);
+        float4* stage = reinterpret_cast<float4*>(smem + L::K_OFF);   // idle K/V stages (128 KB)
         float scale = wown / l;
+        const int etid = threadIdx.x;               // 0..511 (softmax warps)
 #pragma unroll 1
         for (int k = 0; k < np; ++k) {
           const float4* src = reinterpret_cast<const float4*>(a.spart) + (size_t)(cta + 1 + k) * (HD / 4) * 256;
-          // thread i moves float4s i, i+256, ... (HD/4 of them), 16 loads in flight
 #pragma unroll 1
-          for (int i0 = 0; i0 < HD / 4; i0 += 16) {
-            float4 r[16];
+          for (int i0 = 0; i0 < (HD / 4) * 256; i0 += 512 * 8) {
+            float4 r[8];
 #pragma unroll
-            for (int e = 0; e < 16; ++e) r[e] = __ldcg(src + (i0 + e) * 256 + threadIdx.x);
+            for (int e = 0; e < 8; ++e) r[e] = __ldcg(src + i0 + e * 512 + etid);
 #pragma unroll
-            for (int e = 0; e < 16; ++e) stage[(i0 + e) * 256 + threadIdx.x] = r[e];
+            for (int e = 0; e < 8; ++e) stage[i0 + e * 512 + etid] = r[e];
           }
-          sk_bar_sync(3, 256);
-          const float w = ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
+          sk2_bar_sync(10, 512);
+          const float wk = ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
 #pragma unroll 1
-          for (int c = 0; c < HD; c += 32) {
+          for (int c = 0; c < OH; c += 32) {
             float f[32];
-            tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+            tmem_ld32(TOh + c, reinterpret_cast<uint32_t*>(f));
             tmem_wait_ld();
 #pragma unroll
             for (int q4 = 0; q4 < 8; ++q4) {
-              const float4 v = stage[((c / 4) + q4) * 256 + r256];
-              f[4 * q4] = f[4 * q4] * scale + w * v.x;
-              f[4 * q4 + 1] = f[4 * q4 + 1] * scale + w * v.y;
-              f[4 * q4 + 2] = f[4 * q4 + 2] * scale + w * v.z;
-              f[4 * q4 + 3] = f[4 * q4 + 3] * scale + w * v.w;
+              const float4 v = stage[((hf * OH + c) / 4 + q4) * 256 + r256];
+              f[4 * q4] = f[4 * q4] * scale + wk * v.x;
+              f[4 * q4 + 1] = f[4 * q4 + 1] * scale + wk * v.y;
+              f[4 * q4 + 2] = f[4 * q4 + 2] * scale + wk * v.z;
+              f[4 * q4 + 3] = f[4 * q4 + 3] * scale + wk * v.w;
             }
-            tmem_st32(TO + c, reinterpret_cast<uint32_t*>(f));
+            tmem_st32(TOh + c, reinterpret_cast<uint32_t*>(f));
             tmem_wait_st();
           }
           scale = 1.f;
-          sk_bar_sync(3, 256);                      // stage free for the next slot
+          sk2_bar_sync(10, 512);                     // stage free for the next slot
         }
 #pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
-          float f[32];
-          tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+        for (int c = 0; c < OH; c += 16) {
+          float f[16];
+          tmem_ld16(TOh + c, reinterpret_cast<uint32_t*>(f));
           tmem_wait_ld();
-          write_out(c, f, scale * inv_w);
+          write_out16(c, f, scale * inv_w);
         }
         tc_fence_before();
         mbar_arrive(&o_free[t]);
-        if (trc) trc[6] = (long long)globaltimer();
-        sk_bar_sync(2, 256);                        // both tiles' rows have read the slots
-        for (int k = threadIdx.x; k < np; k += 256) a.sflag[cta + 1 + k] = 0;
+        sk2_bar_sync(11, 512);                       // every row has read the slots
+        for (int k = threadIdx.x; k < np; k += 512) a.sflag[cta + 1 + k] = 0;
       } else {
-        // whole unit in this CTA
         const float inv = 1.f / l;
 #pragma unroll 1
-        for (int c = 0; c < HD; c += 32) {
-          float f[32];
-          tmem_ld32(TO + c, reinterpret_cast<uint32_t*>(f));
+        for (int c = 0; c < OH; c += 16) {
+          float f[16];
+          tmem_ld16(TOh + c, reinterpret_cast<uint32_t*>(f));
           tmem_wait_ld();
-          write_out(c, f, inv);
+          write_out16(c, f, inv);
         }
         tc_fence_before();
         mbar_arrive(&o_free[t]);
-      }
-      if (trc) {
-        trc[2] = (long long)globaltimer();
-        trc[3] = ((long long)u << 32) | ((long long)ta << 16) | tb;
       }
       jg += n;
       w += n;
@@ -446,25 +451,25 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
-  if (warp == 9) {
+  if (warp == 17) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
 }
 
 template <int HD>
-static cudaError_t launch_sk_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
+static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
                                 const AttnTC& a, int grid, cudaStream_t st) {
-  using L = AttnSkSmem<HD>;
+  using L = AttnSk2Smem<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sk_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    cudaError_t e = cudaFuncSetAttribute(attn_sk2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (e != cudaSuccess) return e;
     configured = true;
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(320);
+  cfg.blockDim = dim3(576);
   cfg.dynamicSmemBytes = L::TOTAL;
   cfg.stream = st;
   cudaLaunchAttribute at[1];
@@ -472,13 +477,13 @@ static cudaError_t launch_sk_hd(const CUtensorMap& tq, const CUtensorMap& tk, co
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_sk_kernel<HD>, tq, tk, tvt, a);
+  return cudaLaunchKernelEx(&cfg, attn_sk2_kernel<HD>, tq, tk, tvt, a);
 }
 
-cudaError_t launch_attn_sk(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            int grid, cudaStream_t st) {
-  if (a.hd == 128) return launch_sk_hd<128>(tq, tk, tvt, a, grid, st);
-  if (a.hd == 64) return launch_sk_hd<64>(tq, tk, tvt, a, grid, st);
+  if (a.hd == 128) return launch_sk2_hd<128>(tq, tk, tvt, a, grid, st);
+  if (a.hd == 64) return launch_sk2_hd<64>(tq, tk, tvt, a, grid, st);
   return cudaErrorInvalidValue;
 }
 

@@ -115,6 +115,17 @@ __device__ __forceinline__ uint64_t sdesc_k_sw128(uint32_t saddr) {
   d |= uint64_t(2) << 61;                          // layout: SWIZZLE_128B
   return d;
 }
+// one lane of a converged warp (the others get false): keeps the caller's control flow
+// warp-uniform so tcgen05 operands stay in uniform registers
+__device__ __forceinline__ bool elect_one() {
+  uint32_t pred = 0;
+  asm volatile(
+      "{\n\t.reg .pred P;\n\t"
+      "elect.sync _|P, 0xffffffff;\n\t"
+      "selp.b32 %0, 1, 0, P;\n}"
+      : "=r"(pred));
+  return pred != 0;
+}
 // Instruction descriptor: kind::f16, A=B=bf16, D=f32, both K-major, shape M x N.
 __host__ __device__ constexpr uint32_t idesc_bf16_f32(int M, int N) {
   return (1u << 4) | (1u << 7) | (1u << 10) | (uint32_t(N >> 3) << 17) | (uint32_t(M >> 4) << 24);

@@ -95,5 +95,8 @@ cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st);
 // persistent stream-K variant (one CTA per SM, no combine kernel)
 cudaError_t launch_attn_sk(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            int grid, cudaStream_t st);
+// same with column-split softmax, 16 softmax warps (attn_sk2.cu; the default)
+cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                            int grid, cudaStream_t st);
 
 }  // namespace vi
