@@ -232,7 +232,7 @@ def run_ours(args, cfg):
         "fps_per_stream": value / world,
         "step_latency_ms": {"p50": statistics.median(step_ms), "p5": sorted(step_ms)[int(0.05 * len(step_ms))],
                             "p95": sorted(step_ms)[min(len(step_ms) - 1, int(0.95 * len(step_ms)))]},
-        "roofline": {"kernel": "memory attention (attn_sk_kernel, persistent stream-K), per block",
+        "roofline": {"kernel": "memory attention (attn_sk2_kernel, persistent stream-K, column-split softmax), per block",
                      "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
                      "frac": achieved / bf16_peak, "traffic": traffic,
                      "flop_per_launch": attn_flop, "avg_launch_ms": per_block_ms,
