@@ -38,13 +38,15 @@ def peaks():
         return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
-def workload_config(cfg):
+def workload_config(cfg, args=None, world=1):
     return {"workload": f"{cfg.name}: FuseFormer-shaped memory step (BASELINE.json configs[2])",
             "layers": cfg.layers, "heads": cfg.heads, "d_model": cfg.d_model, "tokens_per_frame": cfg.tokens,
             "new_frames_per_step": cfg.t_new, "mem_frames": cfg.mem_frames,
             "keys_per_block": cfg.slots * cfg.tokens, "queries_per_block": cfg.t_new * cfg.tokens,
             "feature_map": [cfg.feat_h, cfg.feat_w, cfg.feat_c], "ffn": "F3N 1960",
-            "l2": "flushed between timed steps (256 MiB write)", "streams_per_gpu": 1}
+            "l2": "flushed between timed steps (256 MiB write)",
+            "parallelism": (f"heads sharded over {world} GPUs (NCCL all-gather per block), 1 stream"
+                            if args is not None and args.tp else f"{world} independent live streams, 1 per GPU")}
 
 
 class ClockSampler:
@@ -140,7 +142,7 @@ def run_reference(args, cfg):
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-            "config": workload_config(cfg), "impl": "reference",
+            "config": workload_config(cfg, args, args.gpus), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -155,15 +157,23 @@ def run_ours(args, cfg):
     info = streams.DistInfo.from_env()
     world, rank, local = info.world, info.rank, info.local_rank
     torch.cuda.set_device(local)
-    streams.init("nccl", info, torch.device("cuda", local))   # one live stream per GPU
+    streams.init("nccl", info, torch.device("cuda", local))
 
     T, P, D = cfg.t_new, cfg.tokens, cfg.d_model
-    ctx = vi.Context.from_synth(cfg, device=local)
+    if args.tp:
+        # one live stream, heads sharded over the N ranks (NCCL all-gather of the head
+        # outputs inside every block): strong scaling of one stream's step latency
+        nccl_id = streams.broadcast_bytes(vi.tp_unique_id() if rank == 0 else None, torch.device("cuda", local))
+        ctx = vi.Context.from_synth(cfg, device=local, tp_size=world, tp_rank=rank, nccl_id=nccl_id)
+        n_streams = 1
+    else:
+        ctx = vi.Context.from_synth(cfg, device=local)   # one independent live stream per GPU
+        n_streams = world
     ctx.set_weights(make_weights(cfg, seed=0))
     stream = torch.cuda.ExternalStream(ctx.stream())
     dt = torch.bfloat16
     nchunks = 4
-    seed = streams.stream_seed(streams.stream_ids(rank, world, world)[0])
+    seed = streams.stream_seed(0 if args.tp else streams.stream_ids(rank, world, world)[0])
     feats = [torch.from_numpy(make_features(cfg, T, first_frame=i * T, seed=seed)).to(dt).cuda()
              for i in range(nchunks)]
     out = torch.empty_like(feats[0])
@@ -210,13 +220,13 @@ def run_ours(args, cfg):
     clk = clocks.stop()
 
     total_ms, e2e_s = streams.max_over_ranks([total_ms, e2e_s], torch.device("cuda", local))
-    value = streams.aggregate_fps(T * args.steps, world, total_ms / 1e3)
-    e2e_value = streams.aggregate_fps(T * e2e_steps, world, e2e_s)
+    value = streams.aggregate_fps(T * args.steps, n_streams, total_ms / 1e3)
+    e2e_value = streams.aggregate_fps(T * e2e_steps, n_streams, e2e_s)
     bf16_peak, hbm_peak, peak_src = peaks()
     attn_ms, attn_recs = prof["attention"]
     per_block_ms = attn_ms / (args.steps * cfg.layers) if attn_ms > 0 else float("nan")
     nq, nk = T * P, cfg.slots * P
-    attn_flop = 4.0 * nq * nk * D
+    attn_flop = 4.0 * nq * nk * D / (world if args.tp else 1)   # this rank's share when head-sharded
     achieved = attn_flop / (per_block_ms * 1e-3) / 1e12 if attn_ms > 0 else float("nan")
     traffic = None
     try:
@@ -226,10 +236,11 @@ def run_ours(args, cfg):
         pass
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-        "warmup": warm, "ms_per_step": total_ms / args.steps, "higher_is_better": True, "scaling": "weak",
+        "warmup": warm, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "strong" if args.tp else "weak",
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded N(0,1) features, N(0,0.02) weights)",
-        "config": workload_config(cfg),
-        "fps_per_stream": value / world,
+        "config": workload_config(cfg, args, world),
+        "fps_per_stream": value / n_streams,
         "step_latency_ms": {"p50": statistics.median(step_ms), "p5": sorted(step_ms)[int(0.05 * len(step_ms))],
                             "p95": sorted(step_ms)[min(len(step_ms) - 1, int(0.95 * len(step_ms)))]},
         "roofline": {"kernel": "memory attention (attn_sk2_kernel, persistent stream-K, column-split softmax), per block",
@@ -275,6 +286,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C3", choices=["C3", "C3T1"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--tp", action="store_true",
+                    help="one stream with its heads sharded over the N ranks (NCCL all-gather per block)")
     args = ap.parse_args()
     from vi_synth import CONFIGS
     cfg = CONFIGS[args.config]

@@ -82,6 +82,22 @@ typedef struct vi_config {
   int pos_embed;         /* 0 none, 1 additive [P][D] table given in vi_weights.pos */
   int device;            /* CUDA device ordinal */
   void* stream;          /* cudaStream_t to enqueue on (NULL = the context creates one) */
+  /* Head sharding (BASELINE north_star "attention heads are split across
+   * GPUs and the head outputs are all-gathered with NCCL over NVLink before the output
+   * projection").  tp_size G = 1 (or 0): unsharded.  G > 1: this context is rank
+   * tp_rank of G; see vi_tp_layout for which heads / query rows it owns.  Sharded per
+   * rank: the Q/K/V projection of its heads, its K/V memory (memory per GPU / G when
+   * G <= H) and its attention; replicated: everything else (bitwise identical on every
+   * rank).  bf16 path only.
+   *   nccl_id != NULL: 128-byte ncclUniqueId (vi_tp_unique_id on one rank, broadcast by
+   *     the caller); vi_create_ex joins an NCCL communicator of G ranks (collective: all
+   *     ranks must call it) and vi_memory_step all-gathers the head outputs itself.
+   *     G = 1 with an id runs the sharded code path over a 1-rank communicator.
+   *   nccl_id == NULL and G > 1: no communicator; the caller drives the exchange with
+   *     vi_memory_step_attn / vi_tp_local_allgather / vi_memory_step_ffn (several
+   *     contexts of one process, on one or several GPUs). */
+  int tp_size, tp_rank;
+  const void* nccl_id;
 } vi_config;
 
 /* Weights, host fp32 pointers in nn.Linear layout (y = x W^T + b); converted to the
@@ -150,6 +166,35 @@ vi_status vi_soft_split(vi_ctx* ctx, const void* feat, int n, void* out, int pro
  * VI_E_PROTOCOL unless called after a push with layer = 0, 1, ..., L-1 in order. */
 vi_status vi_memory_step(vi_ctx* ctx, int layer, const float* x_in, float* x_out);
 
+/* The two halves of vi_memory_step for head-sharded contexts driven without a
+ * communicator (tp_size > 1, nccl_id == NULL); any context may use them.
+ *   _attn: LN1, Q/K/V projection of the rank's heads, memory write, attention of the
+ *          rank's (heads, query rows) into its chunk of the gathered head-output buffer;
+ *   _ffn : (NCCL all-gather of that buffer if the ctx has a communicator), output
+ *          projection + residual, LN2, FFN + residual.
+ * vi_memory_step(l) == _attn(l) then _ffn(l).  VI_E_PROTOCOL out of that order. */
+vi_status vi_memory_step_attn(vi_ctx* ctx, int layer, const float* x_in);
+vi_status vi_memory_step_ffn(vi_ctx* ctx, int layer, const float* x_in, float* x_out);
+
+/* Partition of the attention over G ranks (CUDA-free, the same function every context
+ * uses).  G <= H: G must divide H; rank r owns heads [r*H/G, (r+1)*H/G), every query
+ * row.  G > H: G must be a multiple of H; q = G/H query parts; rank r owns head r/q and
+ * query rows [(r%q)*Nh, min((r%q+1)*Nh, Nq)), Nh = ceil(T_max*P/q), of the chunk of
+ * Nq = n*P queries.  The gathered head outputs are head-major [H][q*Nh][d] (bf16);
+ * rank r contributes elements [r*chunk, (r+1)*chunk), chunk = (H*q*Nh*d)/G.
+ * Outputs may be NULL.  VI_E_CONFIG for an unsupported (H, G). */
+vi_status vi_tp_layout(int heads, int head_dim, int rows_max, int tp_size, int tp_rank,
+                       int* head0, int* nheads, int* qparts, int* row0, int* rows_per_part,
+                       int64_t* chunk_elems);
+/* ncclGetUniqueId (NCCL loaded at run time): out = 128 bytes.  VI_E_NCCL if NCCL is
+ * unavailable. */
+vi_status vi_tp_unique_id(void* out128);
+/* All-gather of the head outputs among the G contexts of one process (tp_size = G,
+ * ctxs[r] = rank r, no communicator; same or different devices): each rank's chunk is
+ * copied into every other rank's buffer (device-to-device / peer copies), ordered after
+ * every rank's _attn and before any rank's next launch.  Call between _attn and _ffn. */
+vi_status vi_tp_local_allgather(vi_ctx* const* ctxs, int n);
+
 /* Soft composite of n frames into feat [n][H][W][C] (device, ctx dtype).
  * project = 0: in = raw tokens [n][P][kh*kw*C] (ctx dtype);
  * project = 1: in = x [n][P][D] fp32, back-projected with back_w / back_b first.
@@ -158,7 +203,7 @@ vi_status vi_soft_composite(vi_ctx* ctx, const void* in, int n, void* feat, int 
 
 /* Refine commit (Eq. 4's refined memory M-bar): overwrite the memory
  * entries of a past, resident frame for every block with k, v = [L][P][D] (host or
- * device, ctx dtype).  Queued and applied at the next vi_memory_push, so a frame is
+ * device, ctx dtype; a head-sharded context keeps only its heads' columns).  Queued and applied at the next vi_memory_push, so a frame is
  * never torn across blocks; a later commit for the same frame replaces an earlier one.
  * The payload is copied before return (buffers may be reused).  Thread-safe w.r.t.
  * the context's other calls.  VI_E_PROTOCOL / VI_NOT_RESIDENT as vi_memory_evict. */
@@ -201,12 +246,13 @@ vi_status vi_profile_read(vi_ctx* ctx, double* ms /*[VI_PROF_N]*/, int64_t* laun
 /* Test hook: copy an internal buffer to dst (host or device), `bytes` must match.
  *   VI_DBG_TOKENS  raw split tokens of the last split       [n][P][kh*kw*C] ctx dtype
  *   VI_DBG_H       LN output last written                    [n][P][D] ctx dtype
- *   VI_DBG_Q       queries of the last block                 [n][P][D] ctx dtype
+ *   VI_DBG_Q       queries of the last block                 [n][P][Dl] ctx dtype
  *   VI_DBG_O       attention output of the last block        [n][P][D] ctx dtype
+ *                  (head-sharded: the gathered outputs, after _ffn or an all-gather)
  *   VI_DBG_U       FFN1 output of the last block (F3N only)  [n][P][F] fp32
  *   VI_DBG_G       GELU(F3N(u)) of the last block            [n][P][F] ctx dtype
- *   VI_DBG_K, VI_DBG_V   memory rows of (layer, slot)        [P][D] ctx dtype
- * `n` is the chunk size of the last push. */
+ *   VI_DBG_K, VI_DBG_V   memory rows of (layer, slot)        [P][Dl] ctx dtype
+ * `n` is the chunk size of the last push; Dl = D (unsharded) or the rank's heads x d. */
 #define VI_DBG_TOKENS 0
 #define VI_DBG_H      1
 #define VI_DBG_Q      2

@@ -17,6 +17,7 @@ LIB = os.path.join(HERE, "libvi.so")
 
 SOURCES = [
     "ring.cpp",
+    "tp.cpp",
     "engine.cu",
     "kernels/patch.cu",
     "kernels/rows.cu",

@@ -27,6 +27,7 @@
 
 #include "kernels/kernels.h"
 #include "ring.h"
+#include "tp.h"
 #include "vi.h"
 
 using namespace vi;
@@ -96,6 +97,15 @@ struct vi_ctx {
   std::string err = "ok";
   bool poisoned = false;
   int64_t launches = 0;
+  // head sharding (tp.h): Hl local heads, Q/K/V width Dl = Hl * hd; the attention writes
+  // the rank's chunk of the gathered head-major buffer og [H][head_rows][hd]
+  bool sharded = false;
+  TpLayout tp;
+  int Hl = 0, Dl = 0;
+  void* comm = nullptr;           // ncclComm_t (NULL: unsharded, or exchange driven by the caller)
+  void* og = nullptr;
+  int attn_layer = -1;            // layer whose _attn half ran last (its _ffn half pending)
+  cudaEvent_t ev_attn = nullptr, ev_gather = nullptr;   // vi_tp_local_allgather ordering
   Ring ring{0, 1};
   std::mutex mu;
   bool have_weights = false;
@@ -117,7 +127,7 @@ struct vi_ctx {
 
   // tensor maps (bf16 path)
   CUtensorMap tm_tokens, tm_wembed, tm_h, tm_wqkv, tm_o, tm_wo, tm_w1, tm_g, tm_w2, tm_xb, tm_wback;
-  CUtensorMap tm_q, tm_k, tm_vt;
+  CUtensorMap tm_q, tm_k, tm_vt, tm_og;
   // N-tile per GEMM (persistent kernel: ~1-3 tiles per SM at M = 3600; N=64 MMAs run at 2/3 rate)
   int bn_embed = 128, bn_qkv = 128, bn_o = 128, bn_1 = 128, bn_2 = 128, bn_back = 256;
 
@@ -187,6 +197,9 @@ vi_ctx::~vi_ctx() {
     cudaFree(kv.second);
   }
   for (void* p : allocs) cudaFree(p);
+  if (comm) nccl().comm_destroy(comm);
+  if (ev_attn) cudaEventDestroy(ev_attn);
+  if (ev_gather) cudaEventDestroy(ev_gather);
   if (copy_stream) cudaStreamDestroy(copy_stream);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
@@ -247,6 +260,11 @@ static void debug_wait(vi_ctx* c, const char* where) {
   do {                             \
     Prof p_(c, cat);               \
     LAUNCH(call, where);           \
+  } while (0)
+#define CK_C(ctx, call, where)                              \
+  do {                                                      \
+    cudaError_t e_ = (call);                                \
+    if (e_ != cudaSuccess) return (ctx)->cuda_fail(e_, where); \
   } while (0)
 #define LIVE(c)                                                      \
   do {                                                               \
@@ -310,6 +328,14 @@ static vi_status validate(const vi_config* k, std::string* why) {
     if (k->d_model > 1024) return bad("d_model <= 1024");
   }
   if (k->d_model > 1024) return bad("d_model <= 1024 (LayerNorm kernel)");
+  const int G = k->tp_size < 1 ? 1 : k->tp_size;
+  if (G > 1 || k->nccl_id) {
+    TpLayout t;
+    if (k->dtype != VI_DTYPE_BF16) return bad("head sharding: bf16 path only");
+    if (k->tp_rank < 0 || k->tp_rank >= G) return bad("tp_rank out of [0, tp_size)");
+    if (!tp_layout(k->heads, hd, k->max_new_frames * k->tokens_per_frame, G, k->tp_rank, &t))
+      return bad("tp_size must divide heads or be a multiple of heads");
+  }
   return VI_OK;
 }
 
@@ -337,9 +363,10 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_w2, c->w_2, c->F, (uint64_t)c->L * c->D, 64, c->bn_2);
   ok &= make_tmap(&c->tm_xb, c->xb, 2 * c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_wback, c->w_back2, 2 * c->D, c->Pd, 64, c->bn_back);
-  ok &= make_tmap(&c->tm_q, c->q, c->D, rows, 64, 128);
-  ok &= make_tmap(&c->tm_k, c->kslab, c->D, (uint64_t)c->L * c->S * c->P, 64, 128);
-  ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->D, 64, c->hd);
+  ok &= make_tmap(&c->tm_q, c->q, c->Dl, rows, 64, 128);
+  ok &= make_tmap(&c->tm_k, c->kslab, c->Dl, (uint64_t)c->L * c->S * c->P, 64, 128);
+  ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->Dl, 64, c->hd);
+  if (c->sharded) ok &= make_tmap(&c->tm_og, c->og, c->hd, (uint64_t)c->H * c->tp.head_rows, 64, 128);
   return ok ? VI_OK : c->fail(VI_E_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
@@ -367,6 +394,14 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->vt_ld = (c->S * c->P + 63) / 64 * 64;
   c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
   c->ring = Ring(c->M, c->Tmax);
+  {
+    const int G = cfg->tp_size < 1 ? 1 : cfg->tp_size;
+    c->sharded = G > 1 || cfg->nccl_id != nullptr;
+    tp_layout(c->H, c->hd, c->Tmax * c->P, G, c->sharded ? cfg->tp_rank : 0, &c->tp);
+    c->Hl = c->tp.nheads;
+    c->Dl = c->Hl * c->hd;
+    c->cfg.nccl_id = nullptr;   // caller memory: only read here
+  }
   const int oh = (cfg->feat_h + 2 * cfg->ph - cfg->kh) / cfg->sh + 1;
   const int ow = (cfg->feat_w + 2 * cfg->pw - cfg->kw) / cfg->sw + 1;
   c->g = Geom{cfg->feat_h, cfg->feat_w, cfg->feat_c, cfg->kh, cfg->kw, cfg->sh, cfg->sw, cfg->ph, cfg->pw, oh, ow};
@@ -396,14 +431,16 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   };
   c->w_embed = A(D * Pd * es); c->b_embed = (float*)A(D * 4); c->pos = (float*)A(P * D * 4);
   c->ln1_g = (float*)A(L * D * 4); c->ln1_b = (float*)A(L * D * 4);
-  c->w_qkv = A(L * 3 * D * D * es); c->b_qkv = (float*)A(L * 3 * D * 4);
+  const size_t Dl = c->Dl;
+  c->w_qkv = A(L * 3 * Dl * D * es); c->b_qkv = (float*)A(L * 3 * Dl * 4);   // this rank's heads only
   c->w_o = A(L * D * D * es); c->b_o = (float*)A(L * D * 4);
   c->ln2_g = (float*)A(L * D * 4); c->ln2_b = (float*)A(L * D * 4);
   c->w_1 = A(L * F * D * es); c->b_1 = (float*)A(L * F * 4);
   c->w_2 = A(L * D * F * es); c->b_2 = (float*)A(L * D * 4);
   c->w_back = A(Pd * D * es); c->b_back = (float*)A(Pd * 4);
-  c->kslab = A(L * S * P * D * es); c->vtslab = A(L * D * (size_t)c->vt_ld * es);
-  c->tokens = A(rows * Pd * es); c->h = A(rows * D * es); c->q = A(rows * D * es); c->o = A(rows * D * es);
+  c->kslab = A(L * S * P * Dl * es); c->vtslab = A(L * Dl * (size_t)c->vt_ld * es);
+  c->tokens = A(rows * Pd * es); c->h = A(rows * D * es); c->q = A(rows * Dl * es); c->o = A(rows * D * es);
+  if (c->sharded) c->og = A((size_t)c->H * c->tp.head_rows * c->hd * es);
   c->u = A(rows * F * 4);   // FFN1 output kept fp32 for the F3N fold (one rounding less)
   c->gbuf = A(rows * F * es); c->xb = A(rows * 2 * D * es);
   if (c->bf16) {
@@ -427,6 +464,21 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   if (!ok) {
     delete c;
     return VI_E_OOM;
+  }
+  if (cudaEventCreateWithFlags(&c->ev_attn, cudaEventDisableTiming) != cudaSuccess ||
+      cudaEventCreateWithFlags(&c->ev_gather, cudaEventDisableTiming) != cudaSuccess) {
+    delete c;
+    return VI_E_CUDA;
+  }
+  if (cfg->nccl_id) {   // collective: every rank of the group is inside this call
+    const Nccl& nc = nccl();
+    NcclId id;
+    std::memcpy(&id, cfg->nccl_id, sizeof(id));
+    if (!nc.ok || nc.comm_init_rank(&c->comm, c->tp.G, id, c->tp.rank) != 0) {
+      c->comm = nullptr;
+      delete c;
+      return VI_E_NCCL;
+    }
   }
   if (cudaDeviceSynchronize() != cudaSuccess) {
     delete c;
@@ -500,8 +552,20 @@ extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
   if (c->cfg.pos_embed) U(upload_f32(c, c->pos, w->pos, (size_t)c->P * D));
   U(upload_f32(c, c->ln1_g, w->ln1_g, L * D));
   U(upload_f32(c, c->ln1_b, w->ln1_b, L * D));
-  U(upload_mat(c, c->w_qkv, w->wqkv, L * 3 * D * D));
-  U(upload_f32(c, c->b_qkv, w->bqkv, L * 3 * D));
+  if (c->sharded) {   // this rank's heads: rows [part*D + head0*hd, +Dl) of Wq, Wk, Wv
+    const size_t Dl = c->Dl, h0 = (size_t)c->tp.head0 * c->hd;
+    std::vector<float> wl(L * 3 * Dl * D), bl(L * 3 * Dl);
+    for (size_t l = 0; l < L; ++l)
+      for (size_t part = 0; part < 3; ++part) {
+        std::memcpy(&wl[(l * 3 + part) * Dl * D], w->wqkv + (l * 3 * D + part * D + h0) * D, Dl * D * 4);
+        std::memcpy(&bl[(l * 3 + part) * Dl], w->bqkv + l * 3 * D + part * D + h0, Dl * 4);
+      }
+    U(upload_mat(c, c->w_qkv, wl.data(), L * 3 * Dl * D));
+    U(upload_f32(c, c->b_qkv, bl.data(), L * 3 * Dl));
+  } else {
+    U(upload_mat(c, c->w_qkv, w->wqkv, L * 3 * D * D));
+    U(upload_f32(c, c->b_qkv, w->bqkv, L * 3 * D));
+  }
   U(upload_mat(c, c->w_o, w->wo, L * D * D));
   U(upload_f32(c, c->b_o, w->bo, L * D));
   U(upload_f32(c, c->ln2_g, w->ln2_g, L * D));
@@ -528,19 +592,21 @@ extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
 // ------------------------------------------------------------------------------ ring
 
 static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
-  const size_t es = c->es, P = c->P, D = c->D, SP = (size_t)c->S * c->P;
+  const size_t es = c->es, P = c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->S * c->P;
+  const size_t h0 = (size_t)c->tp.head0 * c->hd;   // this rank's columns of the full [P][D] payload
   for (int64_t id : ids) {
     auto it = c->pending_kv.find(id);
     if (it == c->pending_kv.end()) continue;
     const int slot = int(id % c->S);
     for (int l = 0; l < c->L; ++l) {
-      const uint8_t* ksrc = static_cast<const uint8_t*>(it->second.first) + (size_t)l * P * D * es;
-      const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.second) + (size_t)l * P * D * es;
-      uint8_t* kdst = static_cast<uint8_t*>(c->kslab) + ((size_t)l * SP + (size_t)slot * P) * D * es;
-      CK(cudaMemcpyAsync(kdst, ksrc, P * D * es, cudaMemcpyDeviceToDevice, c->stream), "commit K");
-      uint8_t* vt = static_cast<uint8_t*>(c->vtslab) + (size_t)l * D * c->vt_ld * es;
-      PLAUNCH(VI_PROF_ROW, launch_transpose_to_slab(vsrc, vt, c->P, c->D, c->vt_ld, (size_t)slot * P, c->bf16 ? 0 : 1, c->stream),
-             "commit V");
+      const uint8_t* ksrc = static_cast<const uint8_t*>(it->second.first) + ((size_t)l * P * D + h0) * es;
+      const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.second) + ((size_t)l * P * D + h0) * es;
+      uint8_t* kdst = static_cast<uint8_t*>(c->kslab) + ((size_t)l * SP + (size_t)slot * P) * Dl * es;
+      CK(cudaMemcpy2DAsync(kdst, Dl * es, ksrc, D * es, Dl * es, P, cudaMemcpyDeviceToDevice, c->stream), "commit K");
+      uint8_t* vt = static_cast<uint8_t*>(c->vtslab) + (size_t)l * Dl * c->vt_ld * es;
+      PLAUNCH(VI_PROF_ROW,
+              launch_transpose_to_slab(vsrc, vt, c->P, c->Dl, c->vt_ld, (size_t)slot * P, c->bf16 ? 0 : 1, c->stream, c->D),
+              "commit V");
     }
   }
   return VI_OK;
@@ -558,6 +624,7 @@ extern "C" vi_status vi_memory_push(vi_ctx* c, int n, int64_t* first_id, int64_t
   c->pending_kv.clear();
   if (st != VI_OK) return st;
   c->next_layer = 0;
+  c->attn_layer = -1;
   if (first_id) *first_id = f;
   if (evicted)
     for (size_t i = 0; i < ev.size(); ++i) evicted[i] = ev[i];
@@ -699,146 +766,107 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
   return k;
 }
 
-extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, float* x_out) {
-  LIVE(c);
-  g_epi_ctx = c;
-  if (!x_in || !x_out) return c->fail(VI_E_ARG, "vi_memory_step: NULL x");
-  if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_memory_step: weights not set");
-  if (c->next_layer < 0 || layer != c->next_layer || layer >= c->L)
-    return c->fail(VI_E_PROTOCOL, "vi_memory_step: needs a push, then layers 0..L-1 in order");
-  const int l = layer, n = c->ring.cur_n, M = n * c->P, D = c->D, F = c->F;
+// The attention half of block l: LN1, Q/K/V projection (this rank's heads) + memory write,
+// attention over every valid slot.  Output: c->o [M][D] (unsharded) or this rank's chunk
+// of the head-major gathered buffer c->og (head-sharded, tp.h).
+static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
+  const int n = c->ring.cur_n, M = n * c->P, D = c->D, Dl = c->Dl;
   const int dt = c->bf16 ? 0 : 1;
   const size_t es = c->es, SP = (size_t)c->S * c->P;
-  void* kl = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * D * es;
-  void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * c->vt_ld * D * es;
+  void* kl = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * Dl * es;
+  void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * c->vt_ld * Dl * es;
   const uint64_t valid = c->ring.valid_mask();
 
   // a3: LN1
   PLAUNCH(VI_PROF_ROW, launch_layernorm(x_in, c->ln1_g + (size_t)l * D, c->ln1_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln1");
   // a4: QKV projection + memory write
-  Epi eq = epi_base(EPI_QKV, M, 3 * D, c->b_qkv + (size_t)l * 3 * D);
-  eq.D = D; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
+  Epi eq = epi_base(EPI_QKV, M, 3 * Dl, c->b_qkv + (size_t)l * 3 * Dl);
+  eq.D = Dl; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
   eq.S = c->S; eq.P = c->P; eq.vt_ld = c->vt_ld;
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * D, M, 3 * D, D, c->bn_qkv, eq, c->stream), "qkv gemm");
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * Dl, M, 3 * Dl, D, c->bn_qkv, eq, c->stream), "qkv gemm");
   else
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_qkv + (size_t)l * 3 * D * D, M, 3 * D, D, eq,
-                                c->stream),
-           "qkv gemm");
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_qkv + (size_t)l * 3 * Dl * D, M, 3 * Dl, D,
+                                               eq, c->stream),
+            "qkv gemm");
   // a5: memory attention over every valid slot
   const float scale_log2 = float(1.4426950408889634 / std::sqrt(double(c->hd)));
-  if (c->bf16) {
-    AttnTC a;
-    std::memset(&a, 0, sizeof(a));
-    a.Nq = M; a.hd = c->hd; a.D = D; a.H = c->H; a.krow_base = int(l * SP); a.vrow_base = l * D;
-    a.scale_log2 = scale_log2; a.segs = make_segs(c, valid);
-    const int ntiles = a.segs.tile0[a.segs.n];
-    const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
-    choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
-    a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
-    a.o = static_cast<bf16*>(c->o); a.opart = c->opart; a.lse = c->lse;
-    a.timing = (c->prof_mode == 1 || c->prof_mode == 3) ? c->attn_timing : nullptr;
-    static long long* trace_buf = nullptr;
-    static int trace_calls = 0;
-    if (getenv("VI_ATTN_TRACE") && !trace_buf) cudaMalloc(&trace_buf, 32 * 32 * sizeof(long long));
-    if (trace_buf && l == 0 && ++trace_calls == 5) {
-      cudaMemsetAsync(trace_buf, 0, 32 * 32 * sizeof(long long), c->stream);
-      a.trace = trace_buf;
-    }
-    static long long* sk_trace = nullptr;
-    static int sk_calls = 0;
-    const bool sk_tr = getenv("VI_SK_TRACE") && l == 0 && ++sk_calls == 5;
-    if (sk_tr) {
-      if (!sk_trace) cudaMalloc(&sk_trace, 148 * 32 * sizeof(long long));
-      cudaMemsetAsync(sk_trace, 0, 148 * 32 * sizeof(long long), c->stream);
-    }
-    if (!g_attn_v1 && !g_attn_split && !a.trace) {
-      if (sk_tr) a.trace = sk_trace;
-      // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
-      a.npairs = (M + 255) / 256;
-      a.units = a.npairs * c->H;
-      a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
-      const long long work = (long long)a.units * ntiles;
-      int grid = int(work < c->num_sms ? work : c->num_sms);
-      if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
-      if (g_attn_sk == 1)
-        PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-      else
-        PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-      if (sk_tr && g_attn_sk == 2) {
-        std::vector<long long> h(32 * 32);
-        cudaMemcpyAsync(h.data(), sk_trace, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
-        cudaStreamSynchronize(c->stream);
-        const long long t0 = h[24];
-        fprintf(stderr, "[sk2] j | per tile: S_rdy max P_arr(hf0 min..max) P_arr(hf1 min..max) mma_p0 mma_p1 qk_issued\n");
-        for (int j = 0; j < 32 && h[j * 32 + 24]; ++j) {
-          fprintf(stderr, "[sk2] %2d", j);
-          for (int t = 0; t < 2; ++t) {
-            const long long* e = &h[j * 32];
-            long long pm[2][2];
-            for (int hf = 0; hf < 2; ++hf) {
-              pm[hf][0] = LLONG_MAX; pm[hf][1] = 0;
-              for (int q = 0; q < 4; ++q) {
-                pm[hf][0] = std::min(pm[hf][0], e[4 + t * 8 + hf * 4 + q]);
-                pm[hf][1] = std::max(pm[hf][1], e[4 + t * 8 + hf * 4 + q]);
-              }
-            }
-            fprintf(stderr, " | %6lld %6lld %6lld..%-6lld %6lld..%-6lld pv_in %6lld v %6lld p0 %6lld p1 %6lld qk %6lld", e[t] - t0,
-                    e[2 + t] - t0, pm[0][0] - t0, pm[0][1] - t0, pm[1][0] - t0, pm[1][1] - t0, e[28 + t] - t0,
-                    t == 0 ? e[30] - t0 : 0, e[20 + t] - t0, e[26 + t] - t0, e[24 + t] - t0);
-          }
-          fprintf(stderr, "\n");
-        }
-      } else if (sk_tr) {
-        std::vector<long long> h(148 * 32);
-        cudaMemcpyAsync(h.data(), sk_trace, h.size() * 8, cudaMemcpyDeviceToHost, c->stream);
-        cudaStreamSynchronize(c->stream);
-        long long t0 = h[31];
-        for (int i = 0; i < grid; ++i) t0 = std::min(t0, h[i * 32 + 31]);
-        auto T = [&](long long v) { return v ? (v - t0) / 1000.0 : -1.0; };
-        for (int i = 0; i < grid; ++i) {
-          fprintf(stderr, "[sk] cta %3d |", i);
-          for (int k = 0; k < 3 && h[i * 32 + k * 8]; ++k) {
-            const long long* e = &h[i * 32 + k * 8];
-            fprintf(stderr, " u%lld[%lld,%lld) loop %5.1f-%5.1f ld %5.1f wait %5.1f merge %5.1f end %5.1f |", e[3] >> 32,
-                    (e[3] >> 16) & 0xffff, e[3] & 0xffff, T(e[0]), T(e[1]), T(e[4]), T(e[5]), T(e[6]), T(e[2]));
-          }
-          fprintf(stderr, "\n");
-        }
-      }
-    } else {
-      if (g_attn_v1)
-        PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
-      else
-        PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream, g_attn_colsplit), "attention");
-      if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
-    }
-    if (a.trace) {
-      long long h[32 * 32];
-      cudaMemcpyAsync(h, a.trace, sizeof(h), cudaMemcpyDeviceToHost, c->stream);
-      cudaStreamSynchronize(c->stream);
-      const long long t0 = h[0];
-      fprintf(stderr, "[trace] j | t0: S_rdy[4] Ph0[4] Ph1[4] | t1: S_rdy[4] Ph0[4] Ph1[4] | mma t0: wait h0 h1 qk | t1: wait h0 h1 qk\n");
-      for (int j = 0; j < std::min(a.tiles_per_split, 32); ++j) {
-        fprintf(stderr, "[trace] %2d", j);
-        for (int e = 0; e < 32; ++e) fprintf(stderr, "%s%6lld", (e % 4 == 0) ? " |" : " ", h[j * 32 + e] ? h[j * 32 + e] - t0 : -1);
-        fprintf(stderr, "\n");
-      }
-    }
-  } else {
+  if (!c->bf16) {
     AttnArgs a;
     a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->S; a.vt_ld = c->vt_ld; a.valid = valid;
     a.scale_log2 = scale_log2; a.q = c->q; a.kslab = kl; a.vtslab = vl; a.o = c->o;
     PLAUNCH(VI_PROF_ATTN, launch_attn_simt_f32(a, c->stream), "attention");
+    return VI_OK;
+  }
+  AttnTC a;
+  std::memset(&a, 0, sizeof(a));
+  a.Nq = M; a.hd = c->hd; a.D = Dl; a.H = c->Hl; a.krow_base = int(l * SP); a.vrow_base = l * Dl;
+  a.scale_log2 = scale_log2; a.segs = make_segs(c, valid);
+  a.o = static_cast<bf16*>(c->o); a.o_ld = D; a.o_hs = c->hd; a.q_row0 = 0;
+  if (c->sharded) {   // this rank's query rows, written head-major into its chunk of og
+    a.q_row0 = c->tp.row0();
+    a.Nq = c->tp.rows(M);
+    a.o = static_cast<bf16*>(c->og) + (size_t)c->tp.rank * c->tp.chunk_elems;
+    a.o_ld = c->hd;
+    a.o_hs = c->tp.head_rows * c->hd;
+    if (a.Nq == 0) return VI_OK;   // a query part beyond a short chunk: nothing to attend
+  }
+  const int ntiles = a.segs.tile0[a.segs.n];
+  a.opart = c->opart; a.lse = c->lse;
+  a.timing = (c->prof_mode == 1 || c->prof_mode == 3) ? c->attn_timing : nullptr;
+  if ((!g_attn_v1 && !g_attn_split) || c->sharded) {
+    // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
+    a.npairs = (a.Nq + 255) / 256;
+    a.units = a.npairs * a.H;
+    a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
+    const long long work = (long long)a.units * ntiles;
+    int grid = int(work < c->num_sms ? work : c->num_sms);
+    if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
+    if (g_attn_sk == 1)
+      PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+    else
+      PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+  } else {   // A/B variants: fixed KV split + combine kernel
+    const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
+    choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
+    a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
+    if (g_attn_v1)
+      PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
+    else
+      PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream, g_attn_colsplit), "attention");
+    if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
+  }
+  return VI_OK;
+}
+
+// The rest of block l: (all-gather of the head outputs), output projection + residual,
+// LN2, FFN (+ F3N fold/unfold) + residual.
+static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
+  const int n = c->ring.cur_n, M = n * c->P, D = c->D, F = c->F;
+  const int dt = c->bf16 ? 0 : 1;
+  // a6: head all-gather (NCCL, in place: rank r's chunk is already at offset r * chunk)
+  if (c->comm) {
+    const size_t bytes = (size_t)c->tp.chunk_elems * c->es;
+    uint8_t* base = static_cast<uint8_t*>(c->og);
+    const int r = nccl().all_gather(base + (size_t)c->tp.rank * bytes, base, bytes, kNcclUint8, c->comm, c->stream);
+    if (r != 0) {
+      c->poisoned = true;
+      return c->fail(VI_E_NCCL, std::string("ncclAllGather: ") + nccl().error_string(r));
+    }
   }
   // a7: output projection + residual
   Epi eo = epi_base(EPI_RESID, M, D, c->b_o + (size_t)l * D);
   eo.x_in = x_in; eo.x_out = x_out;
+  if (c->sharded) {   // A = concat_h(O_h) read head-major from the gathered buffer
+    eo.a_hs = c->tp.head_rows;
+    eo.a_kpb = c->hd / 64;
+  }
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream), "o gemm");
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->sharded ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream),
+            "o gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->o, (const float*)c->w_o + (size_t)l * D * D, M, D, D, eo, c->stream),
-           "o gemm");
+            "o gemm");
   // a8: LN2
   PLAUNCH(VI_PROF_ROW, launch_layernorm(x_out, c->ln2_g + (size_t)l * D, c->ln2_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln2");
   // a9 / a10: FFN1 (+ F3N fold/unfold) + GELU
@@ -849,7 +877,7 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream), "ffn1 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_1 + (size_t)l * F * D, M, F, D, e1, c->stream),
-           "ffn1 gemm");
+            "ffn1 gemm");
   if (f3n) {
     // g = GELU(unfold(fold(u))) = unfold(GELU(fold(u))): GELU once per folded cell
     PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, dt, n, c->gf, true, c->stream), "f3n fold");
@@ -862,13 +890,93 @@ extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, flo
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, c->tm_w2, l * D, M, D, F, c->bn_2, e2, c->stream), "ffn2 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->gbuf, (const float*)c->w_2 + (size_t)l * D * F, M, D, F, e2,
-                                c->stream),
-           "ffn2 gemm");
+                                               c->stream),
+            "ffn2 gemm");
+  return VI_OK;
+}
+
+static vi_status check_step(vi_ctx* c, int layer, const void* x_in, const void* x_out, const char* who) {
+  if (!x_in || !x_out) return c->fail(VI_E_ARG, std::string(who) + ": NULL x");
+  if (!c->have_weights) return c->fail(VI_E_PROTOCOL, std::string(who) + ": weights not set");
+  if (c->next_layer < 0 || layer != c->next_layer || layer >= c->L)
+    return c->fail(VI_E_PROTOCOL, std::string(who) + ": needs a push, then layers 0..L-1 in order");
+  return VI_OK;
+}
+
+static void layer_done(vi_ctx* c, int layer) {
+  c->attn_layer = -1;
   c->next_layer = layer + 1;
   if (c->next_layer == c->L) {
     std::lock_guard<std::mutex> lk(c->mu);
     c->ring.mark_stepped();
   }
+}
+
+extern "C" vi_status vi_memory_step_attn(vi_ctx* c, int layer, const float* x_in) {
+  LIVE(c);
+  g_epi_ctx = c;
+  vi_status st = check_step(c, layer, x_in, x_in, "vi_memory_step_attn");
+  if (st != VI_OK) return st;
+  if (c->attn_layer == layer) return c->fail(VI_E_PROTOCOL, "vi_memory_step_attn: this layer's _ffn is pending");
+  if ((st = step_attn(c, layer, x_in)) != VI_OK) return st;
+  c->attn_layer = layer;
+  return VI_OK;
+}
+
+extern "C" vi_status vi_memory_step_ffn(vi_ctx* c, int layer, const float* x_in, float* x_out) {
+  LIVE(c);
+  g_epi_ctx = c;
+  vi_status st = check_step(c, layer, x_in, x_out, "vi_memory_step_ffn");
+  if (st != VI_OK) return st;
+  if (c->attn_layer != layer) return c->fail(VI_E_PROTOCOL, "vi_memory_step_ffn: needs vi_memory_step_attn of this layer");
+  if ((st = step_ffn(c, layer, x_in, x_out)) != VI_OK) return st;
+  layer_done(c, layer);
+  return VI_OK;
+}
+
+extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, float* x_out) {
+  LIVE(c);
+  g_epi_ctx = c;
+  vi_status st = check_step(c, layer, x_in, x_out, "vi_memory_step");
+  if (st != VI_OK) return st;
+  if (c->sharded && !c->comm)
+    return c->fail(VI_E_PROTOCOL, "vi_memory_step: head-sharded context without a communicator: use "
+                                  "vi_memory_step_attn / vi_tp_local_allgather / vi_memory_step_ffn");
+  if (c->attn_layer >= 0) return c->fail(VI_E_PROTOCOL, "vi_memory_step: a vi_memory_step_attn is pending");
+  if ((st = step_attn(c, layer, x_in)) != VI_OK) return st;
+  if ((st = step_ffn(c, layer, x_in, x_out)) != VI_OK) return st;
+  layer_done(c, layer);
+  return VI_OK;
+}
+
+extern "C" vi_status vi_tp_local_allgather(vi_ctx* const* ctxs, int n) {
+  if (!ctxs || n < 1) return VI_E_ARG;
+  for (int i = 0; i < n; ++i) {
+    vi_ctx* c = ctxs[i];
+    LIVE(c);
+    if (!c->sharded || c->comm || c->tp.G != n || c->tp.rank != i)
+      return c->fail(VI_E_CONFIG, "vi_tp_local_allgather: ctxs[r] must be rank r of a communicator-less group of n");
+    if (c->tp.chunk_elems != ctxs[0]->tp.chunk_elems || c->H != ctxs[0]->H || c->hd != ctxs[0]->hd)
+      return c->fail(VI_E_SHAPE, "vi_tp_local_allgather: contexts of different shapes");
+    if (c->attn_layer < 0 || c->attn_layer != ctxs[0]->attn_layer)
+      return c->fail(VI_E_PROTOCOL, "vi_tp_local_allgather: every rank must have run _attn of the same layer");
+  }
+  for (int i = 0; i < n; ++i) CK_C(ctxs[i], cudaEventRecord(ctxs[i]->ev_attn, ctxs[i]->stream), "allgather record");
+  const size_t bytes = (size_t)ctxs[0]->tp.chunk_elems * ctxs[0]->es;
+  for (int j = 0; j < n; ++j) {
+    vi_ctx* d = ctxs[j];
+    for (int i = 0; i < n; ++i) CK_C(d, cudaStreamWaitEvent(d->stream, ctxs[i]->ev_attn, 0), "allgather wait");
+    for (int i = 0; i < n; ++i) {
+      if (i == j) continue;
+      uint8_t* dst = static_cast<uint8_t*>(d->og) + i * bytes;
+      const uint8_t* src = static_cast<const uint8_t*>(ctxs[i]->og) + i * bytes;
+      CK_C(d, cudaMemcpyPeerAsync(dst, d->cfg.device, src, ctxs[i]->cfg.device, bytes, d->stream), "allgather copy");
+    }
+    CK_C(d, cudaEventRecord(d->ev_gather, d->stream), "allgather record");
+  }
+  // no rank overwrites its chunk (next layer's attention) before every peer has copied it
+  for (int i = 0; i < n; ++i)
+    for (int j = 0; j < n; ++j) CK_C(ctxs[i], cudaStreamWaitEvent(ctxs[i]->stream, ctxs[j]->ev_gather, 0), "allgather wait");
   return VI_OK;
 }
 
@@ -914,6 +1022,8 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
   LIVE(c);
   if (!feat || !out || n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_run_step: bad argument");
   if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_run_step: weights not set");
+  if (c->sharded && !c->comm)
+    return c->fail(VI_E_PROTOCOL, "vi_run_step: head-sharded context without a communicator");
   const size_t fbytes = (size_t)n * c->g.H * c->g.W * c->g.C * c->es;
   const bool hin = is_host_ptr(feat), hout = is_host_ptr(out);
   const void* fin = feat;
@@ -1035,20 +1145,20 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
   LIVE(c);
   if (!dst) return VI_E_ARG;
   const int n = std::max(c->ring.cur_n, 1);
-  const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, SP = (size_t)c->S * c->P;
+  const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->S * c->P;
   const void* src = nullptr;
   size_t need = 0;
   switch (what) {
     case VI_DBG_TOKENS: src = c->tokens; need = rows * c->Pd * es; break;
     case VI_DBG_H: src = c->h; need = rows * D * es; break;
-    case VI_DBG_Q: src = c->q; need = rows * D * es; break;
+    case VI_DBG_Q: src = c->q; need = rows * Dl * es; break;
     case VI_DBG_O: src = c->o; need = rows * D * es; break;
     case VI_DBG_U:
       if (c->cfg.ffn_kind != VI_FFN_F3N) return c->fail(VI_E_CONFIG, "vi_debug_read: u exists for F3N only");
       src = c->u; need = rows * c->F * 4; break;
     case VI_DBG_G: src = c->gbuf; need = rows * c->F * es; break;
     case VI_DBG_K:
-    case VI_DBG_V: need = (size_t)c->P * D * es; break;
+    case VI_DBG_V: need = (size_t)c->P * Dl * es; break;
     default: return VI_E_ARG;
   }
   if (bytes != need) return c->fail(VI_E_SHAPE, "vi_debug_read: byte count mismatch");
@@ -1056,19 +1166,28 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
     return VI_E_ARG;
   CK(cudaStreamSynchronize(c->stream), "debug sync");
   if (what == VI_DBG_K) {
-    src = static_cast<const uint8_t*>(c->kslab) + ((size_t)layer * SP + (size_t)slot * c->P) * D * es;
+    src = static_cast<const uint8_t*>(c->kslab) + ((size_t)layer * SP + (size_t)slot * c->P) * Dl * es;
     CK(cudaMemcpy(dst, src, need, cudaMemcpyDefault), "debug copy");
   } else if (what == VI_DBG_V) {
-    // Vt [D][S*P] columns slot*P.. -> [P][D]
+    // Vt [Dl][S*P] columns slot*P.. -> [P][Dl]
     std::vector<uint8_t> tmp(need);
     const uint8_t* base =
-        static_cast<const uint8_t*>(c->vtslab) + ((size_t)layer * D * c->vt_ld + (size_t)slot * c->P) * es;
-    CK(cudaMemcpy2D(tmp.data(), c->P * es, base, (size_t)c->vt_ld * es, c->P * es, D, cudaMemcpyDeviceToHost),
+        static_cast<const uint8_t*>(c->vtslab) + ((size_t)layer * Dl * c->vt_ld + (size_t)slot * c->P) * es;
+    CK(cudaMemcpy2D(tmp.data(), c->P * es, base, (size_t)c->vt_ld * es, c->P * es, Dl, cudaMemcpyDeviceToHost),
        "debug copy V");
     std::vector<uint8_t> tr(need);
-    for (size_t d = 0; d < D; ++d)
-      for (int p = 0; p < c->P; ++p) std::memcpy(&tr[((size_t)p * D + d) * es], &tmp[(d * c->P + p) * es], es);
+    for (size_t d = 0; d < Dl; ++d)
+      for (int p = 0; p < c->P; ++p) std::memcpy(&tr[((size_t)p * Dl + d) * es], &tmp[(d * c->P + p) * es], es);
     CK(cudaMemcpy(dst, tr.data(), need, cudaMemcpyDefault), "debug copy V");
+  } else if (what == VI_DBG_O && c->sharded) {
+    // gathered head-major [H][head_rows][hd] -> [rows][D]
+    const size_t hr = c->tp.head_rows, hd = c->hd;
+    std::vector<uint8_t> tmp((size_t)c->H * hr * hd * es), out(need);
+    CK(cudaMemcpy(tmp.data(), c->og, tmp.size(), cudaMemcpyDeviceToHost), "debug copy O");
+    for (int h = 0; h < c->H; ++h)
+      for (size_t r = 0; r < rows; ++r)
+        std::memcpy(&out[(r * D + h * hd) * es], &tmp[((size_t)h * hr + r) * hd * es], hd * es);
+    CK(cudaMemcpy(dst, out.data(), need, cudaMemcpyDefault), "debug copy O");
   } else {
     CK(cudaMemcpy(dst, src, need, cudaMemcpyDefault), "debug copy");
   }

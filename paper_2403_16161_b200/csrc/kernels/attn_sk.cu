@@ -118,7 +118,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
         for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int at = 0; at < HD / 64; ++at)
-            tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, q0 + t * 128);
+            tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, a.q_row0 + q0 + t * 128);
       }
       __syncwarp();
       for (int j = ta; j < tb; ++j, ++jg) {
@@ -325,7 +325,7 @@ attn_sk_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ C
           const int rr = i * 8 + (lane >> 2), part = lane & 3;
           const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 80 + part * 16);
           if (rbase + rr < a.Nq)
-            *reinterpret_cast<uint4*>(a.o + (size_t)(rbase + rr) * a.D + h * HD + c + part * 8) = v;
+            *reinterpret_cast<uint4*>(a.o + (size_t)(rbase + rr) * a.o_ld + (size_t)h * a.o_hs + c + part * 8) = v;
         }
         __syncwarp();
       };

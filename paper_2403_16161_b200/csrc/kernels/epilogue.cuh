@@ -32,6 +32,9 @@ struct Epi {
   int first_slot, S;
   int vt_ld;              // row pitch (elements) of the Vt slab, >= S*P, multiple of 64
   unsigned long long* timing;  // KernelTiming of the GEMM category (profile mode 1) or NULL
+  // A operand stored head-major (head-sharded output projection, tp.h): a_hs > 0 means
+  // A[m][k] = Amap row (k / (64 * a_kpb)) * a_hs + m, column k % (64 * a_kpb)
+  int a_hs, a_kpb;
 };
 
 template <typename T>

@@ -106,10 +106,16 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
           mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
+          int ak = kb * 64, am = m0;
+          if (epi.a_hs > 0) {                   // head-major A: K-block kb of head kb / a_kpb
+            const int hh = kb / epi.a_kpb;
+            ak = (kb - hh * epi.a_kpb) * 64;
+            am = hh * epi.a_hs + m0;
+          }
           if (CN > 1)
-            tma_load_2d_mc(sa + cx * A_SLICE, &tmA, &full[s], kb * 64, m0 + cx * (128 / CN), row_mask);
+            tma_load_2d_mc(sa + cx * A_SLICE, &tmA, &full[s], ak, am + cx * (128 / CN), row_mask);
           else
-            tma_load_2d(sa, &tmA, &full[s], kb * 64, m0);
+            tma_load_2d(sa, &tmA, &full[s], ak, am);
           if (CM > 1)
             tma_load_2d_mc(sa + L::A_BYTES + cy * B_SLICE, &tmB, &full[s], kb * 64, brow0 + n0 + cy * (BN / CM),
                            col_mask);

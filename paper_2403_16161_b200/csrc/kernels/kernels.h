@@ -26,8 +26,9 @@ cudaError_t launch_layernorm(const float* x, const float* g, const float* b, voi
                              int D, cudaStream_t st);
 // x fp32 [rows][D] -> [rows][2D] bf16 (hi | lo) for the extended-precision back projection
 cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaStream_t st);
+// v [P][D] (row pitch src_ld elements) -> vt_slab[d][col0 + p] (row pitch ld)
 cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D, size_t ld, size_t col0, int dtype,
-                                     cudaStream_t st);
+                                     cudaStream_t st, int src_ld = 0);
 
 // ---- GEMMs ---------------------------------------------------------------------------
 // tensor cores (bf16): A [M][K] and W [N][K] described by 2-D TMA maps with 64 x 128 /
@@ -85,6 +86,10 @@ struct AttnTC {
   long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
   unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves
   int H;
+  // stream-K kernels (attn_sk, attn_sk2): query rows start at row q_row0 of the Q map;
+  // output row i of local head h goes to o + i * o_ld + h * o_hs (unsharded: o_ld = D,
+  // o_hs = hd; head-sharded: the rank's chunk of the head-major gathered buffer, tp.h)
+  int q_row0, o_ld, o_hs;
 };
 cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            cudaStream_t st);

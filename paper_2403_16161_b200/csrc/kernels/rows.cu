@@ -127,14 +127,15 @@ cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaSt
   return cudaGetLastError();
 }
 
-// v [P][D] -> vt[d][col0 + p] (row pitch ld elements), 32x32 smem tiles.
+// v [P][D] (row pitch sld) -> vt[d][col0 + p] (row pitch ld elements), 32x32 smem tiles.
 template <typename T>
-__global__ void transpose_kernel(const T* __restrict__ v, T* __restrict__ vt, int P, int D, size_t ld, size_t col0) {
+__global__ void transpose_kernel(const T* __restrict__ v, T* __restrict__ vt, int P, int D, size_t ld, size_t col0,
+                                 int sld) {
   __shared__ T tile[32][33];
   const int p0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
     const int p = p0 + i, d = d0 + threadIdx.x;
-    if (p < P && d < D) tile[i][threadIdx.x] = v[(size_t)p * D + d];
+    if (p < P && d < D) tile[i][threadIdx.x] = v[(size_t)p * sld + d];
   }
   __syncthreads();
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -144,12 +145,13 @@ __global__ void transpose_kernel(const T* __restrict__ v, T* __restrict__ vt, in
 }
 
 cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D, size_t ld, size_t col0, int dtype,
-                                     cudaStream_t st) {
+                                     cudaStream_t st, int src_ld) {
   dim3 grid((P + 31) / 32, (D + 31) / 32), block(32, 8);
+  const int sld = src_ld > 0 ? src_ld : D;
   if (dtype == 0)
-    transpose_kernel<bf16><<<grid, block, 0, st>>>((const bf16*)v, (bf16*)vt_slab, P, D, ld, col0);
+    transpose_kernel<bf16><<<grid, block, 0, st>>>((const bf16*)v, (bf16*)vt_slab, P, D, ld, col0, sld);
   else
-    transpose_kernel<float><<<grid, block, 0, st>>>((const float*)v, (float*)vt_slab, P, D, ld, col0);
+    transpose_kernel<float><<<grid, block, 0, st>>>((const float*)v, (float*)vt_slab, P, D, ld, col0, sld);
   return cudaGetLastError();
 }
 

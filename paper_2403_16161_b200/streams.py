@@ -1,9 +1,13 @@
-"""Multi-GPU host logic: independent live streams split across GPUs (one process per GPU).
+"""Multi-GPU host logic (one process per GPU).
 
-The memory step of different live streams shares nothing (each stream has its own ring
-memory), so N GPUs serve N x streams with no data-path collective (weak scaling); the
-only cross-rank traffic is the timing reduction of the benchmark (max over ranks) and
-barriers.  Works with the NCCL backend on GPUs and with gloo on CPU (tests).
+Two ways the memory step shards:
+* independent live streams split across GPUs: the streams share nothing (each has its own
+  ring memory), so N GPUs serve N streams with no data-path collective (weak scaling);
+* one stream with its attention heads split across GPUs: libvi.so joins an NCCL
+  communicator (its unique id broadcast here) and all-gathers the head outputs inside
+  every block (strong scaling of one stream's step).
+Cross-rank traffic here is only the timing reduction (max over ranks), barriers and the
+id broadcast.  Works with the NCCL backend on GPUs and with gloo on CPU (tests).
 """
 from __future__ import annotations
 
@@ -50,6 +54,15 @@ def max_over_ranks(values: Sequence[float], device: torch.device = None) -> List
     if dist.is_initialized() and dist.get_world_size() > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
     return [float(v) for v in t.cpu()]
+
+
+def broadcast_bytes(payload, device: torch.device = None) -> bytes:
+    """Rank 0's bytes on every rank (the NCCL unique id of a head-sharded group)."""
+    if not (dist.is_initialized() and dist.get_world_size() > 1):
+        return payload
+    obj = [payload]
+    dist.broadcast_object_list(obj, src=0, device=device)
+    return obj[0]
 
 
 def barrier() -> None:

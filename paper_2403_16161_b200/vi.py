@@ -32,14 +32,16 @@ EXPORTS = ["vi_config_default", "vi_create", "vi_create_ex", "vi_destroy", "vi_s
            "vi_memory_evict", "vi_soft_split", "vi_memory_step", "vi_soft_composite", "vi_refine_commit",
            "vi_memory_state", "vi_run_step", "vi_sync", "vi_last_error", "vi_kernel_launches", "vi_num_slots",
            "vi_stream", "vi_debug_read", "vi_ring_create", "vi_ring_destroy", "vi_ring_push", "vi_ring_evict",
-           "vi_ring_commit", "vi_ring_mark_stepped", "vi_ring_state", "vi_version"]
+           "vi_ring_commit", "vi_ring_mark_stepped", "vi_ring_state", "vi_version", "vi_memory_step_attn",
+           "vi_memory_step_ffn", "vi_tp_layout", "vi_tp_unique_id", "vi_tp_local_allgather"]
 
 
 class ViConfig(C.Structure):
     _fields_ = [(n, C.c_int) for n in (
         "layers", "heads", "d_model", "tokens_per_frame", "mem_frames", "max_new_frames",
         "feat_h", "feat_w", "feat_c", "kh", "kw", "sh", "sw", "ph", "pw",
-        "ffn_hidden", "ffn_kind", "dtype", "pos_embed", "device")] + [("stream", C.c_void_p)]
+        "ffn_hidden", "ffn_kind", "dtype", "pos_embed", "device")] + [("stream", C.c_void_p)] + [
+        ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p)]
 
 
 WEIGHT_FIELDS = ("embed_w", "embed_b", "pos", "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b",
@@ -80,6 +82,11 @@ _sig = {
     "vi_ring_mark_stepped": (C.c_int32, [_P]),
     "vi_ring_state": (C.c_int32, [_P, _I64P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),
     "vi_version": (C.c_char_p, []),
+    "vi_memory_step_attn": (C.c_int32, [_P, C.c_int, _P]),
+    "vi_memory_step_ffn": (C.c_int32, [_P, C.c_int, _P, _P]),
+    "vi_tp_layout": (C.c_int32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [C.POINTER(C.c_int)] * 5 + [_I64P]),
+    "vi_tp_unique_id": (C.c_int32, [_P]),
+    "vi_tp_local_allgather": (C.c_int32, [C.POINTER(_P), C.c_int]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -157,6 +164,37 @@ class Ring:
         return list(sid), list(ref), mask.value
 
 
+# ------------------------------------------------------------------ head sharding
+def tp_layout(heads: int, head_dim: int, rows_max: int, tp_size: int, tp_rank: int) -> dict:
+    """vi_tp_layout: which heads / query rows rank `tp_rank` of `tp_size` owns and where its
+    chunk sits in the head-major gathered buffer (CUDA-free)."""
+    v = [C.c_int() for _ in range(5)]
+    chunk = C.c_int64()
+    st = _lib.vi_tp_layout(heads, head_dim, rows_max, tp_size, tp_rank, *[C.byref(x) for x in v], C.byref(chunk))
+    if st != VI_OK:
+        raise ViError(st, f"vi_tp_layout(H={heads}, G={tp_size}, r={tp_rank})")
+    head0, nheads, qparts, row0, part_rows = (x.value for x in v)
+    return dict(head0=head0, nheads=nheads, qparts=qparts, row0=row0, part_rows=part_rows,
+                head_rows=qparts * part_rows, chunk_elems=chunk.value)
+
+
+def tp_unique_id() -> bytes:
+    """ncclGetUniqueId through libvi (128 bytes, to broadcast to the other ranks)."""
+    buf = C.create_string_buffer(128)
+    st = _lib.vi_tp_unique_id(buf)
+    if st != VI_OK:
+        raise ViError(st, "vi_tp_unique_id")
+    return buf.raw
+
+
+def tp_local_allgather(ctxs) -> None:
+    """vi_tp_local_allgather over the contexts of one process (ctxs[r] = rank r)."""
+    arr = (_P * len(ctxs))(*[c.handle for c in ctxs])
+    st = _lib.vi_tp_local_allgather(arr, len(ctxs))
+    if st != VI_OK:
+        raise ViError(st, f"vi_tp_local_allgather: {ctxs[0].error()}")
+
+
 # ------------------------------------------------------------------ context
 class Context:
     """One live stream on one GPU (a vi_ctx)."""
@@ -165,10 +203,14 @@ class Context:
         k = ViConfig()
         _lib.vi_config_default(C.byref(k))
         stream = cfg.pop("stream", None)
+        nccl_id = cfg.pop("nccl_id", None)
         for key, val in cfg.items():
             setattr(k, key, int(val))
         if stream is not None:
             k.stream = stream
+        if nccl_id is not None:
+            self._nccl_id = C.create_string_buffer(bytes(nccl_id), 128)
+            k.nccl_id = C.cast(self._nccl_id, C.c_void_p)
         h = _P()
         st = _lib.vi_create_ex(C.byref(h), C.byref(k))
         if st != VI_OK:
@@ -178,14 +220,15 @@ class Context:
         self.S = _lib.vi_num_slots(h)
 
     @classmethod
-    def from_synth(cls, c, device: int = 0, stream=None, max_new_frames: Optional[int] = None) -> "Context":
-        """Create from a vi_synth.Config."""
+    def from_synth(cls, c, device: int = 0, stream=None, max_new_frames: Optional[int] = None, tp_size: int = 1,
+                   tp_rank: int = 0, nccl_id: Optional[bytes] = None) -> "Context":
+        """Create from a vi_synth.Config (tp_*: head sharding, see vi.h)."""
         return cls(layers=c.layers, heads=c.heads, d_model=c.d_model, tokens_per_frame=c.tokens,
                    mem_frames=c.mem_frames, max_new_frames=max_new_frames or c.t_new, feat_h=c.feat_h,
                    feat_w=c.feat_w, feat_c=c.feat_c, kh=c.kh, kw=c.kw, sh=c.sh, sw=c.sw, ph=c.ph, pw=c.pw,
                    ffn_hidden=c.ffn_hidden, ffn_kind=c.ffn_kind,
                    dtype=DTYPE_BF16 if c.dtype == "bf16" else DTYPE_FP32, pos_embed=c.pos_embed,
-                   device=device, stream=stream)
+                   device=device, stream=stream, tp_size=tp_size, tp_rank=tp_rank, nccl_id=nccl_id)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -242,6 +285,12 @@ class Context:
 
     def memory_step(self, layer: int, x_in, x_out):
         self._check(_lib.vi_memory_step(self._h, layer, _ptr(x_in), _ptr(x_out)), "vi_memory_step")
+
+    def memory_step_attn(self, layer: int, x_in):
+        self._check(_lib.vi_memory_step_attn(self._h, layer, _ptr(x_in)), "vi_memory_step_attn")
+
+    def memory_step_ffn(self, layer: int, x_in, x_out):
+        self._check(_lib.vi_memory_step_ffn(self._h, layer, _ptr(x_in), _ptr(x_out)), "vi_memory_step_ffn")
 
     def soft_composite(self, x, n: int, feat, project: int):
         self._check(_lib.vi_soft_composite(self._h, _ptr(x), n, _ptr(feat), project), "vi_soft_composite")
