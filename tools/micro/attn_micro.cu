@@ -1,0 +1,127 @@
+// Standalone timing of the stream-K memory attention (attn_sk2.cu) at the C3 shape:
+// 3600 queries x 10800 keys (15 full ring slots of 720 tokens), 4 heads, d = 128.
+//
+//   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo --expt-relaxed-constexpr \
+//        -I include -I paper_2403_16161_b200/csrc tools/micro/attn_micro.cu -lcuda -o /tmp/attn_micro
+//   /tmp/attn_micro [iters] [trace]
+//
+// Prints the mean launch time, TFLOP/s (4 Nq Nk D valid-key FLOPs) and, with `trace`, the
+// clock64 timeline of CTA 0's first key tiles (the kernel's VI_SK_TRACE stamps).
+#include <climits>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#include "../../paper_2403_16161_b200/csrc/kernels/attn_sk2.cu"
+using namespace vi;
+
+typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
+                        const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                        CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+static PFN enc() {
+  void* p;
+  cudaDriverEntryPointQueryResult q;
+  cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q);
+  return (PFN)p;
+}
+static CUtensorMap tmap(void* base, uint64_t inner, uint64_t outer, uint32_t bi, uint32_t bo) {
+  CUtensorMap m;
+  cuuint64_t d[2] = {inner, outer};
+  cuuint64_t s[1] = {inner * 2};
+  cuuint32_t b[2] = {bi, bo}, e[2] = {1, 1};
+  enc()(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, base, d, s, b, e, CU_TENSOR_MAP_INTERLEAVE_NONE,
+        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return m;
+}
+
+__global__ void fill_kernel(uint16_t* p, size_t n, uint32_t seed, float scale) {
+  for (size_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    uint32_t h = uint32_t(i) * 2654435761u ^ seed;
+    h ^= h >> 15; h *= 2246822519u; h ^= h >> 13;
+    const float f = (float(h & 0xffff) / 65536.f - 0.5f) * scale;
+    __nv_bfloat16 b = __float2bfloat16(f);
+    p[i] = *reinterpret_cast<uint16_t*>(&b);
+  }
+}
+
+int main(int argc, char** argv) {
+  const int iters = argc > 1 ? atoi(argv[1]) : 50;
+  const bool trace = argc > 2 && argv[2][0] == 't';
+  const int grid_override = argc > 3 ? atoi(argv[3]) : 0;
+  const int Nq = 3600, H = 4, HD = 128, D = H * HD, P = 720, S = 15, SP = S * P, vt_ld = (SP + 63) / 64 * 64;
+  uint16_t *q, *k, *vt, *o;
+  cudaMalloc(&q, (size_t)Nq * D * 2);
+  cudaMalloc(&k, (size_t)SP * D * 2);
+  cudaMalloc(&vt, (size_t)D * vt_ld * 2);
+  cudaMalloc(&o, (size_t)Nq * D * 2);
+  fill_kernel<<<1024, 256>>>(q, (size_t)Nq * D, 1, 4.f);
+  fill_kernel<<<1024, 256>>>(k, (size_t)SP * D, 2, 4.f);
+  fill_kernel<<<1024, 256>>>(vt, (size_t)D * vt_ld, 3, 2.f);
+  int nsm = 0;
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
+  CUtensorMap tq = tmap(q, D, Nq, 64, 128), tk = tmap(k, D, SP, 64, 128), tv = tmap(vt, vt_ld, D, 64, HD);
+  AttnTC a;
+  memset(&a, 0, sizeof(a));
+  a.Nq = Nq; a.hd = HD; a.D = D; a.H = H; a.krow_base = 0; a.vrow_base = 0;
+  a.scale_log2 = 1.4426950408889634f / sqrtf(float(HD));
+  a.segs.n = 1; a.segs.row0[0] = 0; a.segs.lead[0] = 0; a.segs.len[0] = SP; a.segs.tile0[0] = 0;
+  a.segs.tile0[1] = (SP + 127) / 128;
+  a.o = reinterpret_cast<bf16*>(o); a.o_ld = D; a.o_hs = HD; a.q_row0 = 0;
+  a.npairs = (Nq + 255) / 256;
+  a.units = a.npairs * H;
+  cudaMalloc(&a.spart, (size_t)nsm * 256 * HD * 4);
+  cudaMalloc(&a.slse, (size_t)nsm * 256 * 4);
+  cudaMalloc(&a.sflag, (size_t)nsm * 4);
+  cudaMemset(a.sflag, 0, (size_t)nsm * 4);
+  const long long work = (long long)a.units * a.segs.tile0[1];
+  int grid = int(work < nsm ? work : nsm);
+  if (grid_override > 0) grid = grid_override;
+  cudaStream_t st;
+  cudaStreamCreate(&st);
+  for (int i = 0; i < 3; ++i) launch_attn_sk2(tq, tk, tv, a, grid, st);
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  cudaEventRecord(e0, st);
+  for (int i = 0; i < iters; ++i) launch_attn_sk2(tq, tk, tv, a, grid, st);
+  cudaEventRecord(e1, st);
+  cudaError_t err = cudaStreamSynchronize(st);
+  float ms = 0.f;
+  cudaEventElapsedTime(&ms, e0, e1);
+  const double flop = 4.0 * Nq * SP * D, us = 1e3 * ms / iters;
+  printf("attn_sk2 C3: grid %d, %.2f us/launch, %.1f TFLOP/s (%s)\n", grid, us, flop / (us * 1e-6) / 1e12,
+         cudaGetErrorString(err));
+  if (trace) {
+    long long* tb;
+    cudaMalloc(&tb, 32 * 32 * sizeof(long long));
+    cudaMemset(tb, 0, 32 * 32 * sizeof(long long));
+    a.trace = tb;
+    launch_attn_sk2(tq, tk, tv, a, grid, st);
+    cudaStreamSynchronize(st);
+    std::vector<long long> h(32 * 32);
+    cudaMemcpy(h.data(), tb, h.size() * 8, cudaMemcpyDeviceToHost);
+    const long long t0 = h[24];
+    printf("per key tile j and Q tile t: S ready | row max exchanged | P written (half0 min..max, half1 min..max) | "
+           "PV issue (half0, half1) | QK issued   (clk relative to the first QK)\n");
+    for (int j = 0; j < 32 && h[j * 32 + 24]; ++j) {
+      printf("%2d", j);
+      for (int t = 0; t < 2; ++t) {
+        const long long* e = &h[j * 32];
+        long long pm[2][2];
+        for (int hf = 0; hf < 2; ++hf) {
+          pm[hf][0] = LLONG_MAX;
+          pm[hf][1] = 0;
+          for (int qd = 0; qd < 4; ++qd) {
+            pm[hf][0] = std::min(pm[hf][0], e[4 + t * 8 + hf * 4 + qd]);
+            pm[hf][1] = std::max(pm[hf][1], e[4 + t * 8 + hf * 4 + qd]);
+          }
+        }
+        printf(" | t%d S %6lld x %6lld P %6lld..%-6lld %6lld..%-6lld PV %6lld %6lld QK %6lld", t, e[t] - t0,
+               e[2 + t] - t0, pm[0][0] - t0, pm[0][1] - t0, pm[1][0] - t0, pm[1][1] - t0, e[20 + t] - t0,
+               e[26 + t] - t0, e[24 + t] - t0);
+      }
+      printf("\n");
+    }
+  }
+  return 0;
+}
