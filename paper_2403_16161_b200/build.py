@@ -26,6 +26,7 @@ SOURCES = [
     "kernels/attn.cu",
     "kernels/attn_sk.cu",
     "kernels/attn_sk2.cu",
+    "kernels/attn_sk3.cu",
 ]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

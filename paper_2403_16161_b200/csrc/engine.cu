@@ -224,7 +224,8 @@ static const bool g_attn_colsplit = [] {
   const char* e = getenv("VI_ATTN_COLSPLIT");
   return e && e[0] == '1';
 }();
-// VI_ATTN_SK=1|2: stream-K attention with 8 (row-per-thread) or 16 (column-split) softmax warps.
+// VI_ATTN_SK=1|2|3: stream-K attention with 8 (row-per-thread), 16 (column-split) or 16
+// (16x256b layout) softmax warps; sk2 measured fastest (tools/micro/attn_micro).
 static const int g_attn_sk = [] {
   const char* e = getenv("VI_ATTN_SK");
   return e ? atoi(e) : 2;
@@ -824,8 +825,10 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
     if (g_attn_sk == 1)
       PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-    else
+    else if (g_attn_sk == 2)
       PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+    else
+      PLAUNCH(VI_PROF_ATTN, launch_attn_sk3(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
   } else {   // A/B variants: fixed KV split + combine kernel
     const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
     choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);

@@ -103,5 +103,8 @@ cudaError_t launch_attn_sk(const CUtensorMap& tq, const CUtensorMap& tk, const C
 // same with column-split softmax, 16 softmax warps (attn_sk2.cu; the default)
 cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                             int grid, cudaStream_t st);
+// same schedule, softmax warps in the 16x256b TMEM layout (attn_sk3.cu; VI_ATTN_SK=3)
+cudaError_t launch_attn_sk3(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
+                            int grid, cudaStream_t st);
 
 }  // namespace vi

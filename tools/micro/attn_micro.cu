@@ -1,9 +1,9 @@
-// Standalone timing of the stream-K memory attention (attn_sk2.cu) at the C3 shape:
+// Standalone timing of the stream-K memory attention (attn_sk3.cu / attn_sk2.cu) at the C3 shape:
 // 3600 queries x 10800 keys (15 full ring slots of 720 tokens), 4 heads, d = 128.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo --expt-relaxed-constexpr \
 //        -I include -I paper_2403_16161_b200/csrc tools/micro/attn_micro.cu -lcuda -o /tmp/attn_micro
-//   /tmp/attn_micro [iters] [trace]
+//   /tmp/attn_micro [iters] [t(race)|x] [grid (0 = auto)] [kernel version 2|3]
 //
 // Prints the mean launch time, TFLOP/s (4 Nq Nk D valid-key FLOPs) and, with `trace`, the
 // clock64 timeline of CTA 0's first key tiles (the kernel's VI_SK_TRACE stamps).
@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../paper_2403_16161_b200/csrc/kernels/attn_sk2.cu"
+#include "../../paper_2403_16161_b200/csrc/kernels/attn_sk3.cu"
 using namespace vi;
 
 typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -48,6 +49,7 @@ int main(int argc, char** argv) {
   const int iters = argc > 1 ? atoi(argv[1]) : 50;
   const bool trace = argc > 2 && argv[2][0] == 't';
   const int grid_override = argc > 3 ? atoi(argv[3]) : 0;
+  const int ver = argc > 4 ? atoi(argv[4]) : 3;
   const int Nq = 3600, H = 4, HD = 128, D = H * HD, P = 720, S = 15, SP = S * P, vt_ld = (SP + 63) / 64 * 64;
   uint16_t *q, *k, *vt, *o;
   cudaMalloc(&q, (size_t)Nq * D * 2);
@@ -60,6 +62,9 @@ int main(int argc, char** argv) {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   CUtensorMap tq = tmap(q, D, Nq, 64, 128), tk = tmap(k, D, SP, 64, 128), tv = tmap(vt, vt_ld, D, 64, HD);
+  auto launch = [&](const AttnTC& aa, int gr, cudaStream_t s_) {
+    return ver == 2 ? launch_attn_sk2(tq, tk, tv, aa, gr, s_) : launch_attn_sk3(tq, tk, tv, aa, gr, s_);
+  };
   AttnTC a;
   memset(&a, 0, sizeof(a));
   a.Nq = Nq; a.hd = HD; a.D = D; a.H = H; a.krow_base = 0; a.vrow_base = 0;
@@ -78,25 +83,25 @@ int main(int argc, char** argv) {
   if (grid_override > 0) grid = grid_override;
   cudaStream_t st;
   cudaStreamCreate(&st);
-  for (int i = 0; i < 3; ++i) launch_attn_sk2(tq, tk, tv, a, grid, st);
+  for (int i = 0; i < 3; ++i) launch(a, grid, st);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
   cudaEventRecord(e0, st);
-  for (int i = 0; i < iters; ++i) launch_attn_sk2(tq, tk, tv, a, grid, st);
+  for (int i = 0; i < iters; ++i) launch(a, grid, st);
   cudaEventRecord(e1, st);
   cudaError_t err = cudaStreamSynchronize(st);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
   const double flop = 4.0 * Nq * SP * D, us = 1e3 * ms / iters;
-  printf("attn_sk2 C3: grid %d, %.2f us/launch, %.1f TFLOP/s (%s)\n", grid, us, flop / (us * 1e-6) / 1e12,
+  printf("attn_sk%d C3: grid %d, %.2f us/launch, %.1f TFLOP/s (%s)\n", ver, grid, us, flop / (us * 1e-6) / 1e12,
          cudaGetErrorString(err));
   if (trace) {
     long long* tb;
     cudaMalloc(&tb, 32 * 32 * sizeof(long long));
     cudaMemset(tb, 0, 32 * 32 * sizeof(long long));
     a.trace = tb;
-    launch_attn_sk2(tq, tk, tv, a, grid, st);
+    launch(a, grid, st);
     cudaStreamSynchronize(st);
     std::vector<long long> h(32 * 32);
     cudaMemcpy(h.data(), tb, h.size() * 8, cudaMemcpyDeviceToHost);
@@ -116,9 +121,9 @@ int main(int argc, char** argv) {
             pm[hf][1] = std::max(pm[hf][1], e[4 + t * 8 + hf * 4 + qd]);
           }
         }
-        printf(" | t%d S %6lld x %6lld P %6lld..%-6lld %6lld..%-6lld PV %6lld %6lld QK %6lld", t, e[t] - t0,
-               e[2 + t] - t0, pm[0][0] - t0, pm[0][1] - t0, pm[1][0] - t0, pm[1][1] - t0, e[20 + t] - t0,
-               e[26 + t] - t0, e[24 + t] - t0);
+        printf(" | t%d S %6lld ld %+4lld mx %+4lld e0 %+4lld P0 %+4lld..%+4lld e1 %+4lld P1 %+4lld..%+4lld PV %+4lld %+4lld QK %6lld",
+               t, e[t] - t0, e[22 + t] - e[t], e[2 + t] - e[t], e[28 + t] - e[t], pm[0][0] - e[t], pm[0][1] - e[t],
+               e[30 + t] - e[t], pm[1][0] - e[t], pm[1][1] - e[t], e[20 + t] - e[t], e[26 + t] - e[t], e[24 + t] - t0);
       }
       printf("\n");
     }

@@ -45,7 +45,17 @@ static void run(const char* name, int M, int N, int K, int bn, int kind, int cl 
 }
 
 int main(int argc, char** argv) {
-  run("qkvS", 3600, 1536, 512, 128, EPI_STORE, 0);
-  run("qkvN", 3600, 1536, 512, 128, EPI_NONE, 0);
+  // the memory step's GEMMs at C3 (M = 3600 rows = 5 frames x 720 tokens)
+  struct S { const char* name; int N, K, kind; } shapes[] = {
+      {"qkv", 1536, 512, EPI_STORE}, {"oproj", 512, 512, EPI_RESID}, {"ffn1", 1960, 512, EPI_STORE},
+      {"ffn2", 512, 1960, EPI_RESID}, {"embed", 512, 6272, EPI_STORE}, {"back", 6272, 1024, EPI_STORE}};
+  for (auto& sh : shapes) {
+    for (int bn : {128, 256}) {
+      run(sh.name, 3600, sh.N, sh.K, bn, EPI_NONE, 0);
+      run(sh.name, 3600, sh.N, sh.K, bn, sh.kind, 0);
+      for (int cl : {1, 2, 3})
+        run(sh.name, 3600, sh.N, sh.K, bn, sh.kind, cl);
+    }
+  }
   return 0;
 }
