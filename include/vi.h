@@ -98,6 +98,10 @@ typedef struct vi_config {
    *     contexts of one process, on one or several GPUs). */
   int tp_size, tp_rank;
   const void* nccl_id;
+  /* Priority of the stream the context creates (stream == NULL): CUDA convention, lower
+   * = higher priority (cudaDeviceGetStreamPriorityRange); 0 = default.  The Refined
+   * dual-model run gives the online context the high priority and the refiner 0. */
+  int stream_priority;
 } vi_config;
 
 /* Weights, host fp32 pointers in nn.Linear layout (y = x W^T + b); converted to the
@@ -209,6 +213,14 @@ vi_status vi_soft_composite(vi_ctx* ctx, const void* in, int n, void* feat, int 
  * the context's other calls.  VI_E_PROTOCOL / VI_NOT_RESIDENT as vi_memory_evict. */
 vi_status vi_refine_commit(vi_ctx* ctx, int64_t frame_id, const void* k, const void* v);
 
+/* Read the memory entries of a resident past frame for every block into k, v =
+ * [L][P][Dl] (host or device, ctx dtype; Dl = D unless head-sharded): the refiner side of
+ * Eq. 4's hand-off -- a refining context's K/V of a frame, committed into the
+ * online context with vi_refine_commit.  Synchronous: returns once the copies landed.
+ * VI_E_PROTOCOL for a future frame or the current chunk before its step finished;
+ * VI_NOT_RESIDENT if the frame left the memory. */
+vi_status vi_memory_read(vi_ctx* ctx, int64_t frame_id, void* k, void* v);
+
 /* Host snapshot of the ring: slot_id[S] (-1 = empty), refined[S] (0/1), valid bitmask
  * (bit s = slot s holds a resident frame).  Any pointer may be NULL. */
 vi_status vi_memory_state(vi_ctx* ctx, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask);
@@ -225,6 +237,10 @@ vi_status vi_sync(vi_ctx* ctx);
 const char* vi_last_error(const vi_ctx* ctx);
 /* Number of kernels this context has launched so far (test / bench evidence). */
 int64_t vi_kernel_launches(const vi_ctx* ctx);
+/* Device memory of the context (Table 3 analogue): slab_bytes = the K and V
+ * memory of all blocks (2 L S P Dl elements, V rows padded to vt_ld); total_bytes = every
+ * device buffer the context owns (weights, memory, workspaces).  Either may be NULL. */
+vi_status vi_memory_footprint(const vi_ctx* ctx, int64_t* slab_bytes, int64_t* total_bytes);
 /* Ring slot count S and the ctx stream (cudaStream_t). */
 int vi_num_slots(const vi_ctx* ctx);
 void* vi_stream(const vi_ctx* ctx);

@@ -122,6 +122,7 @@ struct vi_ctx {
   float *x_ws = nullptr, *fold_ws = nullptr, *opart = nullptr, *lse = nullptr;
   void *feat_in = nullptr, *feat_out = nullptr;
   std::vector<void*> allocs;
+  size_t device_bytes = 0;   // everything dalloc'd (weights, memory slabs, workspaces)
   std::map<int64_t, std::pair<void*, void*>> pending_kv;  // queued refine commits (device copies)
   std::vector<std::pair<void*, void*>> free_kv;
 
@@ -179,6 +180,7 @@ struct vi_ctx {
     }
     if (zero) cudaMemset(p, 0, bytes ? bytes : 16);
     allocs.push_back(p);
+    device_bytes += bytes;
     return p;
   }
 };
@@ -411,7 +413,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   if (cfg->stream) {
     c->stream = static_cast<cudaStream_t>(cfg->stream);
   } else {
-    if (cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, cfg->stream_priority) != cudaSuccess) {
       delete c;
       return VI_E_CUDA;
     }
@@ -681,6 +683,48 @@ extern "C" vi_status vi_refine_commit(vi_ctx* c, int64_t frame_id, const void* k
   cudaEventDestroy(ev);
   c->pending_kv[frame_id] = buf;
   return VI_OK;
+}
+
+extern "C" vi_status vi_memory_read(vi_ctx* c, int64_t frame_id, void* k, void* v) {
+  LIVE(c);
+  if (!k || !v) return c->fail(VI_E_ARG, "vi_memory_read: NULL buffer");
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    const int32_t st = c->ring.check_past(frame_id);
+    if (st != VI_OK) return st;
+  }
+  const size_t es = c->es, P = c->P, Dl = c->Dl, SP = (size_t)c->S * c->P, per = P * Dl * es;
+  const size_t slot = size_t(frame_id % c->S);
+  const bool hk = is_host_ptr(k), hv = is_host_ptr(v);
+  // V leaves the slab through a transpose kernel: a host destination is staged on the device
+  void* vd = v;
+  if (hv && cudaMalloc(&vd, (size_t)c->L * per) != cudaSuccess) {
+    cudaGetLastError();
+    return c->fail(VI_E_OOM, "vi_memory_read: staging allocation failed");
+  }
+  vi_status st = VI_OK;
+  for (int l = 0; l < c->L && st == VI_OK; ++l) {
+    const uint8_t* ks = static_cast<const uint8_t*>(c->kslab) + ((size_t)l * SP + slot * P) * Dl * es;
+    cudaError_t e = cudaMemcpyAsync(static_cast<uint8_t*>(k) + l * per, ks, per,
+                                    hk ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice, c->stream);
+    if (e != cudaSuccess) st = c->cuda_fail(e, "memory_read K");
+    // Vt [Dl][vt_ld] columns slot*P.. (a [Dl][P] matrix of pitch vt_ld) -> [P][Dl]
+    const uint8_t* vs = static_cast<const uint8_t*>(c->vtslab) + ((size_t)l * Dl * c->vt_ld + slot * P) * es;
+    if (st == VI_OK) {
+      e = launch_transpose_to_slab(vs, static_cast<uint8_t*>(vd) + l * per, c->Dl, c->P, c->Dl, 0, c->bf16 ? 0 : 1,
+                                   c->stream, c->vt_ld);
+      ++c->launches;
+      if (e != cudaSuccess) st = c->cuda_fail(e, "memory_read V");
+    }
+  }
+  if (st == VI_OK && hv) {
+    cudaError_t e = cudaMemcpyAsync(v, vd, (size_t)c->L * per, cudaMemcpyDeviceToHost, c->stream);
+    if (e != cudaSuccess) st = c->cuda_fail(e, "memory_read V d2h");
+  }
+  cudaError_t e = cudaStreamSynchronize(c->stream);
+  if (st == VI_OK && e != cudaSuccess) st = c->cuda_fail(e, "memory_read sync");
+  if (hv) cudaFree(vd);
+  return st;
 }
 
 extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask) {
@@ -1140,6 +1184,12 @@ extern "C" vi_status vi_profile_read(vi_ctx* c, double* ms, int64_t* launches) {
 
 extern "C" const char* vi_last_error(const vi_ctx* c) { return c ? c->err.c_str() : "null context"; }
 extern "C" int64_t vi_kernel_launches(const vi_ctx* c) { return c ? c->launches : 0; }
+extern "C" vi_status vi_memory_footprint(const vi_ctx* c, int64_t* slab_bytes, int64_t* total_bytes) {
+  if (!c) return VI_E_ARG;
+  if (slab_bytes) *slab_bytes = int64_t(c->L) * c->S * c->P * c->Dl * c->es + int64_t(c->L) * c->Dl * c->vt_ld * c->es;
+  if (total_bytes) *total_bytes = int64_t(c->device_bytes);
+  return VI_OK;
+}
 extern "C" int vi_num_slots(const vi_ctx* c) { return c ? c->S : 0; }
 extern "C" void* vi_stream(const vi_ctx* c) { return c ? (void*)c->stream : nullptr; }
 extern "C" const char* vi_version(void) { return "vi-memstep 0.1 (sm_100a)"; }

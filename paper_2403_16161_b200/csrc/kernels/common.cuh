@@ -299,6 +299,14 @@ __device__ __forceinline__ float2 exp2_poly2_deg2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(t.y) << 23)));
 }
 
+// Programmatic dependent launch (kernels launched with pdl_launch): a kernel may be
+// scheduled while its predecessor in the stream is still running; griddep_wait() blocks
+// until the predecessor grid has completed and its writes are visible, so it must precede
+// every access to data the predecessor produces or consumes.  griddep_launch() lets the
+// successor's CTAs be scheduled as SMs free up.
+__device__ __forceinline__ void griddep_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void griddep_launch() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 __device__ __forceinline__ unsigned long long globaltimer() {
   unsigned long long t;
   asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));

@@ -37,7 +37,7 @@ struct GemmSmem {  // (cluster shape does not change the layout)
 };
 
 #ifdef VI_GEMM_TRACE
-__device__ long long g_gemm_trace[16];
+__device__ long long g_gemm_trace[24];
 #define GTR(i) do { if (blockIdx.x == 0) g_gemm_trace[i] = (long long)globaltimer(); } while (0)
 #else
 #define GTR(i) do { } while (0)
@@ -93,6 +93,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // everything above overlaps the previous kernel's tail (programmatic dependent launch)
+  griddep_wait();
+  griddep_launch();
   if (threadIdx.x == 0) GTR(1);
   if (threadIdx.x == 0) time_begin(epi.timing);
 
@@ -149,7 +152,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             umma_commit(&empty[s]);
         }
         umma_commit(&tfull[acc]);
-        if (lt == 0) GTR(3);
+        if (lt < 4) GTR(3 + lt);
       }
     }
   } else if (warp >= 4) {
@@ -167,7 +170,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       gemm_named_bar_sync(1, 256);
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
-      if (lt == 0 && ew == 0 && lane == 0) GTR(4);
+      if (lt < 4 && ew == 0 && lane == 0) GTR(7 + lt);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
 #pragma unroll 1
@@ -186,7 +189,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       }
       tc_fence_before();
       mbar_arrive(&tempty[acc]);
-      if (lt == 0 && ew == 0 && lane == 0) GTR(5);
+      if (lt < 4 && ew == 0 && lane == 0) GTR(11 + lt);
     }
   }
   tc_fence_before();
@@ -196,7 +199,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tc_fence_after();
     tmem_dealloc(tmem, TMEM_COLS);
   }
-  if (threadIdx.x == 0) GTR(6);
+  if (threadIdx.x == 0) GTR(15);
   if (threadIdx.x == 0) time_end(epi.timing, gridDim.x);
 }
 
@@ -240,11 +243,13 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   cfg.blockDim = dim3(384);
   cfg.dynamicSmemBytes = L::TOTAL;
   cfg.stream = st;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[1].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = 2;
   return cudaLaunchKernelEx(&cfg, kfn, a, b, K, brow0, e);
 }
 

@@ -58,6 +58,8 @@ template <> struct Vec<float, 8> {
 // contiguous, so the CTA writes one contiguous run with 16-byte vectors; 32-bit index math.
 template <typename T, int VEC>
 __global__ void __launch_bounds__(256) unfold_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g, int ntok) {
+  griddep_wait();
+  griddep_launch();
   const int CV = g.C / VEC, KK = g.kh * g.kw, P = g.oh * g.ow;
   // a CTA covers tpb consecutive tokens (one contiguous output run); v = (j, cv) per token
   const int per = KK * CV;
@@ -93,6 +95,8 @@ __global__ void __launch_bounds__(256) unfold_kernel(const T* __restrict__ in, T
 // applies its GELU here, once per folded cell.
 template <typename Tin, typename Tout, int VEC, bool GELU>
 __global__ void __launch_bounds__(256) fold_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g) {
+  griddep_wait();
+  griddep_launch();
   constexpr int MAXC = 3;
   const int CV = g.C / VEC, KK = g.kh * g.kw, P = g.oh * g.ow;
   const int y = blockIdx.x % g.H, t = blockIdx.x / g.H;
@@ -147,6 +151,8 @@ __global__ void __launch_bounds__(256) fold_kernel(const Tin* __restrict__ in, T
 template <typename T, int VEC, int CV, int KH, int KW>
 __global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g,
                                                            int ntok) {
+  griddep_wait();
+  griddep_launch();
   constexpr int KK = KH * KW, PER = KK * CV;
   const int P = g.oh * g.ow;
   const int total = ntok * PER;
@@ -173,6 +179,8 @@ __global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__
 template <typename Tin, typename Tout, int VEC, int CV, int KH, int KW, int SH, int SW, bool GELU>
 __global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g,
                                                          int ncell) {
+  griddep_wait();
+  griddep_launch();
   constexpr int KK = KH * KW, C = CV * VEC;
   constexpr int MAXC = (KH + SH - 1) / SH > (KW + SW - 1) / SW ? (KH + SH - 1) / SH : (KW + SW - 1) / SW;
   const int P = g.oh * g.ow;
@@ -246,7 +254,7 @@ cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int d
     const long long total = (long long)ntok * 49 * CV;
 #define UF(T, V, CVV)                                                                                     \
     if (CV == CVV) {                                                                                      \
-      unfold_fixed_kernel<T, V, CVV, 7, 7><<<grid_cap(total), 256, 0, st>>>((const T*)in, (T*)out, g, ntok); \
+      pdl_launch(unfold_fixed_kernel<T, V, CVV, 7, 7>, dim3(grid_cap(total)), dim3(256), 0, st, (const T*)in, (T*)out, g, ntok); \
       return cudaGetLastError();                                                                          \
     }
     if (dtype == 0) { UF(bf16, 8, 16) UF(bf16, 8, 5) UF(bf16, 8, 32) }
@@ -257,9 +265,9 @@ cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int d
   const int tpb = (per >= 512) ? 1 : (512 + per - 1) / per;
   const int blocks = (ntok + tpb - 1) / tpb;
   if (dtype == 0)
-    unfold_kernel<bf16, 8><<<blocks, 256, 0, st>>>((const bf16*)in, (bf16*)out, g, ntok);
+    pdl_launch(unfold_kernel<bf16, 8>, dim3(blocks), dim3(256), 0, st, (const bf16*)in, (bf16*)out, g, ntok);
   else
-    unfold_kernel<float, 4><<<blocks, 256, 0, st>>>((const float*)in, (float*)out, g, ntok);
+    pdl_launch(unfold_kernel<float, 4>, dim3(blocks), dim3(256), 0, st, (const float*)in, (float*)out, g, ntok);
   return cudaGetLastError();
 }
 
@@ -272,9 +280,9 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
     if (g.C == CVV * V) {                                                                                     \
       const long long total = (long long)ncell * CVV;                                                        \
       if (gelu)                                                                                               \
-        fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true><<<grid_cap(total), 256, 0, st>>>((const TI*)in, (TO*)out, g, ncell); \
+        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell); \
       else                                                                                                    \
-        fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false><<<grid_cap(total), 256, 0, st>>>((const TI*)in, (TO*)out, g, ncell); \
+        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell); \
       return cudaGetLastError();                                                                              \
     }
     if (in_dtype == 1 && out_dtype == 0) { FF(float, bf16, 4, 10) FF(float, bf16, 4, 32) }
@@ -283,8 +291,8 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
 #undef FF
   }
 #define FOLD(TI, TO, V)                                                                              \
-  (gelu ? (fold_kernel<TI, TO, V, true><<<blocks, 256, 0, st>>>((const TI*)in, (TO*)out, g), 0)        \
-        : (fold_kernel<TI, TO, V, false><<<blocks, 256, 0, st>>>((const TI*)in, (TO*)out, g), 0))
+  (gelu ? (pdl_launch(fold_kernel<TI, TO, V, true>, dim3(blocks), dim3(256), 0, st, (const TI*)in, (TO*)out, g), 0)        \
+        : (pdl_launch(fold_kernel<TI, TO, V, false>, dim3(blocks), dim3(256), 0, st, (const TI*)in, (TO*)out, g), 0))
   if (in_dtype == 0 && out_dtype == 0) FOLD(bf16, bf16, 8);
   else if (in_dtype == 0) FOLD(bf16, float, 8);
   else if (out_dtype == 1) FOLD(float, float, 4);

@@ -1,13 +1,23 @@
 // Row kernels: pre-norm LayerNorm (reading Q1, eps 1e-5), fp32 -> bf16 cast, and the
 // V transpose used by refine commits (the memory stores V transposed, [D][S*P]).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace vi {
+
+// VI_PDL=0 turns programmatic dependent launch off (A/B measurements)
+int g_pdl = [] {
+  const char* e = getenv("VI_PDL");
+  return (e && e[0] == '0') ? 0 : 1;
+}();
 
 // One warp per row; D <= 1024 and D % 32 == 0.  Two-pass mean / variance in registers.
 template <typename Tout, int PER>
 __global__ void layernorm_kernel(const float* __restrict__ x, const float* __restrict__ g,
                                  const float* __restrict__ b, Tout* __restrict__ out, int rows, int D) {
+  griddep_wait();
+  griddep_launch();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const float* xr = x + (size_t)warp * D;
@@ -46,6 +56,8 @@ template <typename Tout, int NV>
 __global__ void __launch_bounds__(256) layernorm_v4_kernel(const float4* __restrict__ x, const float4* __restrict__ g,
                                                            const float4* __restrict__ b, Tout* __restrict__ out,
                                                            int rows, int D) {
+  griddep_wait();
+  griddep_launch();
   const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (warp >= rows) return;
   const int D4 = D / 4;
@@ -86,16 +98,16 @@ cudaError_t launch_layernorm(const float* x, const float* g, const float* b, voi
                              int D, cudaStream_t st) {
   const int blocks = (rows * 32 + 255) / 256;
   if (D % 128 == 0 && D <= 1024) {
-#define LNV(NV)                                                                                                    if (D == NV * 128) {                                                                                               if (out_dtype == 0)                                                                                                layernorm_v4_kernel<bf16, NV><<<blocks, 256, 0, st>>>((const float4*)x, (const float4*)g, (const float4*)b,                                                             (bf16*)out, rows, D);                                   else                                                                                                               layernorm_v4_kernel<float, NV><<<blocks, 256, 0, st>>>((const float4*)x, (const float4*)g,                                                                              (const float4*)b, (float*)out, rows, D);                return cudaGetLastError();                                                                                     }
+#define LNV(NV)                                                                                                    if (D == NV * 128) {                                                                                               if (out_dtype == 0)                                                                                                pdl_launch(layernorm_v4_kernel<bf16, NV>, dim3(blocks), dim3(256), 0, st, (const float4*)x, (const float4*)g, (const float4*)b,                                                             (bf16*)out, rows, D);                                   else                                                                                                               pdl_launch(layernorm_v4_kernel<float, NV>, dim3(blocks), dim3(256), 0, st, (const float4*)x, (const float4*)g,                                                                              (const float4*)b, (float*)out, rows, D);                return cudaGetLastError();                                                                                     }
     LNV(1) LNV(2) LNV(3) LNV(4) LNV(5) LNV(6) LNV(7) LNV(8)
 #undef LNV
   }
 #define LN_CASE(PER)                                                                                   \
   if (D <= PER * 32) {                                                                                 \
     if (out_dtype == 0)                                                                                \
-      layernorm_kernel<bf16, PER><<<blocks, 256, 0, st>>>(x, g, b, (bf16*)out, rows, D);               \
+      pdl_launch(layernorm_kernel<bf16, PER>, dim3(blocks), dim3(256), 0, st, x, g, b, (bf16*)out, rows, D);               \
     else                                                                                               \
-      layernorm_kernel<float, PER><<<blocks, 256, 0, st>>>(x, g, b, (float*)out, rows, D);             \
+      pdl_launch(layernorm_kernel<float, PER>, dim3(blocks), dim3(256), 0, st, x, g, b, (float*)out, rows, D);             \
     return cudaGetLastError();                                                                         \
   }
   LN_CASE(2) LN_CASE(4) LN_CASE(8) LN_CASE(16) LN_CASE(32)
@@ -106,6 +118,8 @@ cudaError_t launch_layernorm(const float* x, const float* g, const float* b, voi
 // x [rows][D] fp32 -> [rows][2D] bf16 with hi = bf16(x) in columns 0..D-1 and
 // lo = bf16(x - hi) in D..2D-1: a K = 2D GEMM against [W | W] then sees x to ~2^-17.
 __global__ void split_bf16_kernel(const float4* __restrict__ x, uint2* __restrict__ out, int rows, int D4) {
+  griddep_wait();
+  griddep_launch();
   const size_t n4 = (size_t)rows * D4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4; i += (size_t)gridDim.x * blockDim.x) {
     const size_t r = i / D4, c = i - r * D4;
@@ -122,7 +136,7 @@ cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaSt
   size_t blocks = (n4 + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
   if (!blocks) blocks = 1;
-  split_bf16_kernel<<<unsigned(blocks), 256, 0, st>>>(reinterpret_cast<const float4*>(x), reinterpret_cast<uint2*>(out),
+  pdl_launch(split_bf16_kernel, dim3(unsigned(blocks)), dim3(256), 0, st, reinterpret_cast<const float4*>(x), reinterpret_cast<uint2*>(out),
                                                       rows, D / 4);
   return cudaGetLastError();
 }
@@ -131,6 +145,8 @@ cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaSt
 template <typename T>
 __global__ void transpose_kernel(const T* __restrict__ v, T* __restrict__ vt, int P, int D, size_t ld, size_t col0,
                                  int sld) {
+  griddep_wait();
+  griddep_launch();
   __shared__ T tile[32][33];
   const int p0 = blockIdx.x * 32, d0 = blockIdx.y * 32;
   for (int i = threadIdx.y; i < 32; i += 8) {
@@ -149,9 +165,9 @@ cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D,
   dim3 grid((P + 31) / 32, (D + 31) / 32), block(32, 8);
   const int sld = src_ld > 0 ? src_ld : D;
   if (dtype == 0)
-    transpose_kernel<bf16><<<grid, block, 0, st>>>((const bf16*)v, (bf16*)vt_slab, P, D, ld, col0, sld);
+    pdl_launch(transpose_kernel<bf16>, dim3(grid), dim3(block), 0, st, (const bf16*)v, (bf16*)vt_slab, P, D, ld, col0, sld);
   else
-    transpose_kernel<float><<<grid, block, 0, st>>>((const float*)v, (float*)vt_slab, P, D, ld, col0, sld);
+    pdl_launch(transpose_kernel<float>, dim3(grid), dim3(block), 0, st, (const float*)v, (float*)vt_slab, P, D, ld, col0, sld);
   return cudaGetLastError();
 }
 

@@ -33,7 +33,8 @@ EXPORTS = ["vi_config_default", "vi_create", "vi_create_ex", "vi_destroy", "vi_s
            "vi_memory_state", "vi_run_step", "vi_sync", "vi_last_error", "vi_kernel_launches", "vi_num_slots",
            "vi_stream", "vi_debug_read", "vi_ring_create", "vi_ring_destroy", "vi_ring_push", "vi_ring_evict",
            "vi_ring_commit", "vi_ring_mark_stepped", "vi_ring_state", "vi_version", "vi_memory_step_attn",
-           "vi_memory_step_ffn", "vi_tp_layout", "vi_tp_unique_id", "vi_tp_local_allgather"]
+           "vi_memory_step_ffn", "vi_tp_layout", "vi_tp_unique_id", "vi_tp_local_allgather", "vi_memory_footprint",
+           "vi_memory_read"]
 
 
 class ViConfig(C.Structure):
@@ -41,7 +42,7 @@ class ViConfig(C.Structure):
         "layers", "heads", "d_model", "tokens_per_frame", "mem_frames", "max_new_frames",
         "feat_h", "feat_w", "feat_c", "kh", "kw", "sh", "sw", "ph", "pw",
         "ffn_hidden", "ffn_kind", "dtype", "pos_embed", "device")] + [("stream", C.c_void_p)] + [
-        ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p)]
+        ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p), ("stream_priority", C.c_int)]
 
 
 WEIGHT_FIELDS = ("embed_w", "embed_b", "pos", "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b",
@@ -87,6 +88,8 @@ _sig = {
     "vi_tp_layout": (C.c_int32, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int] + [C.POINTER(C.c_int)] * 5 + [_I64P]),
     "vi_tp_unique_id": (C.c_int32, [_P]),
     "vi_tp_local_allgather": (C.c_int32, [C.POINTER(_P), C.c_int]),
+    "vi_memory_footprint": (C.c_int32, [_P, _I64P, _I64P]),
+    "vi_memory_read": (C.c_int32, [_P, C.c_int64, _P, _P]),
 }
 for _name, (_res, _args) in _sig.items():
     _f = getattr(_lib, _name)
@@ -221,14 +224,15 @@ class Context:
 
     @classmethod
     def from_synth(cls, c, device: int = 0, stream=None, max_new_frames: Optional[int] = None, tp_size: int = 1,
-                   tp_rank: int = 0, nccl_id: Optional[bytes] = None) -> "Context":
+                   tp_rank: int = 0, nccl_id: Optional[bytes] = None, stream_priority: int = 0) -> "Context":
         """Create from a vi_synth.Config (tp_*: head sharding, see vi.h)."""
         return cls(layers=c.layers, heads=c.heads, d_model=c.d_model, tokens_per_frame=c.tokens,
                    mem_frames=c.mem_frames, max_new_frames=max_new_frames or c.t_new, feat_h=c.feat_h,
                    feat_w=c.feat_w, feat_c=c.feat_c, kh=c.kh, kw=c.kw, sh=c.sh, sw=c.sw, ph=c.ph, pw=c.pw,
                    ffn_hidden=c.ffn_hidden, ffn_kind=c.ffn_kind,
                    dtype=DTYPE_BF16 if c.dtype == "bf16" else DTYPE_FP32, pos_embed=c.pos_embed,
-                   device=device, stream=stream, tp_size=tp_size, tp_rank=tp_rank, nccl_id=nccl_id)
+                   device=device, stream=stream, tp_size=tp_size, tp_rank=tp_rank, nccl_id=nccl_id,
+                   stream_priority=stream_priority)
 
     def close(self):
         if getattr(self, "_h", None):
@@ -276,6 +280,11 @@ class Context:
         return self._check(_lib.vi_memory_evict(self._h, fid), "vi_memory_evict",
                            allow=(VI_OK, VI_NOT_RESIDENT, VI_E_PROTOCOL, VI_E_ARG))
 
+    def read_kv(self, fid: int, k, v) -> int:
+        """vi_memory_read: this context's K/V of a resident past frame into k, v [L][P][Dl]."""
+        return self._check(_lib.vi_memory_read(self._h, fid, _ptr(k), _ptr(v)), "vi_memory_read",
+                           allow=(VI_OK, VI_NOT_RESIDENT, VI_E_PROTOCOL))
+
     def commit(self, fid: int, k, v) -> int:
         return self._check(_lib.vi_refine_commit(self._h, fid, _ptr(k), _ptr(v)), "vi_refine_commit",
                            allow=(VI_OK, VI_NOT_RESIDENT, VI_E_PROTOCOL, VI_E_ARG))
@@ -312,6 +321,12 @@ class Context:
 
     def launches(self) -> int:
         return int(_lib.vi_kernel_launches(self._h))
+
+    def footprint(self) -> Tuple[int, int]:
+        """(K/V memory bytes, all device bytes owned by the context)."""
+        slab, total = C.c_int64(), C.c_int64()
+        self._check(_lib.vi_memory_footprint(self._h, C.byref(slab), C.byref(total)), "vi_memory_footprint")
+        return slab.value, total.value
 
     def stream(self) -> int:
         return _lib.vi_stream(self._h)

@@ -3,7 +3,11 @@
 #include <vector>
 
 #include "../../paper_2403_16161_b200/csrc/kernels/gemm_tc.cu"
+namespace vi { int g_pdl = 1; }
 using namespace vi;
+#ifdef VI_GEMM_TRACE
+static void* g_gemm_trace_ptr() { void* p; cudaGetSymbolAddress(&p, g_gemm_trace); return p; }
+#endif
 
 typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
                         const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
@@ -41,6 +45,18 @@ static void run(const char* name, int M, int N, int K, int bn, int kind, int cl 
   float ms; cudaEventElapsedTime(&ms, a, b);
   const double us = ms * 1000 / it, tf = 2.0 * M * N * K / (us * 1e-6) / 1e12;
   printf("%-8s M=%d N=%d K=%d BN=%d epi=%d cl=%d: %s %.2f us  %.0f TFLOP/s\n", name, M, N, K, bn, kind, cl, cudaGetErrorString(err), us, tf);
+#ifdef VI_GEMM_TRACE
+  long long tr[24];
+  cudaMemcpyFromSymbol(tr, g_gemm_trace, sizeof(tr));
+  printf("   CTA0 (ns from start): setup %lld first-data %lld | mma-done", tr[1] - tr[0], tr[2] - tr[0]);
+  for (int i = 0; i < 4; ++i) printf(" %lld", tr[3 + i] > tr[0] ? tr[3 + i] - tr[0] : -1);
+  printf(" | epi start");
+  for (int i = 0; i < 4; ++i) printf(" %lld", tr[7 + i] > tr[0] ? tr[7 + i] - tr[0] : -1);
+  printf(" | epi end");
+  for (int i = 0; i < 4; ++i) printf(" %lld", tr[11 + i] > tr[0] ? tr[11 + i] - tr[0] : -1);
+  printf(" | exit %lld\n", tr[15] - tr[0]);
+  cudaMemset(g_gemm_trace_ptr(), 0, sizeof(tr));
+#endif
   cudaFree(A); cudaFree(W); cudaFree(O); cudaFree(bias); cudaFree(x);
 }
 
