@@ -65,6 +65,27 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Output tensor [rows][cols] (fp32 or bf16) for the GEMMs' TMA-store epilogue: box = one
+// 128-byte row segment x 32 rows, 128-byte swizzle (gemm_tc.cu's staging layout).
+bool make_tmap_out(CUtensorMap* m, const void* base, bool f32, uint64_t cols, uint64_t rows) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return false;
+  const uint64_t es = f32 ? 4 : 2;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * es};
+  cuuint32_t box[2] = {uint32_t(128 / es), 32};
+  cuuint32_t e[2] = {1, 1};
+  return fn(m, f32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+            strides, box, e, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// VI_TMA_EPI=0: the GEMMs store from registers instead of through TMA (A/B measurements)
+const bool g_tma_epi = [] {
+  const char* e = getenv("VI_TMA_EPI");
+  return !(e && e[0] == '0');
+}();
+
 uint16_t f2bf(float f) {  // round to nearest even
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -123,12 +144,22 @@ struct vi_ctx {
   void *feat_in = nullptr, *feat_out = nullptr;
   std::vector<void*> allocs;
   size_t device_bytes = 0;   // everything dalloc'd (weights, memory slabs, workspaces)
-  std::map<int64_t, std::pair<void*, void*>> pending_kv;  // queued refine commits (device copies)
-  std::vector<std::pair<void*, void*>> free_kv;
+  // queued refine commits: device copies of the K/V payloads, applied at the next push.  A
+  // consumed buffer returns to free_kv with `released` recorded on the ctx stream after the
+  // copies that read it, so a commit from another thread never touches the ctx stream (which
+  // may be capturing a step graph) and still never overwrites a payload being applied.
+  struct KvBuf {
+    void* k = nullptr;
+    void* v = nullptr;
+    cudaEvent_t released = nullptr;
+  };
+  std::map<int64_t, KvBuf> pending_kv;
+  std::vector<KvBuf> free_kv;
 
   // tensor maps (bf16 path)
   CUtensorMap tm_tokens, tm_wembed, tm_h, tm_wqkv, tm_o, tm_wo, tm_w1, tm_g, tm_w2, tm_xb, tm_wback;
   CUtensorMap tm_q, tm_k, tm_vt, tm_og;
+  CUtensorMap tm_u_out, tm_g_out, tm_yp_out;   // GEMM outputs through the TMA-store epilogue
   // N-tile per GEMM (persistent kernel: ~1-3 tiles per SM at M = 3600; N=64 MMAs run at 2/3 rate)
   int bn_embed = 128, bn_qkv = 128, bn_o = 128, bn_1 = 128, bn_2 = 128, bn_back = 256;
 
@@ -195,8 +226,9 @@ vi_ctx::~vi_ctx() {
   for (auto e : ev_pool) cudaEventDestroy(e);
   for (auto& kv : pending_kv) free_kv.push_back(kv.second);
   for (auto& kv : free_kv) {
-    cudaFree(kv.first);
-    cudaFree(kv.second);
+    cudaFree(kv.k);
+    cudaFree(kv.v);
+    if (kv.released) cudaEventDestroy(kv.released);
   }
   for (void* p : allocs) cudaFree(p);
   if (comm) nccl().comm_destroy(comm);
@@ -274,6 +306,22 @@ static void debug_wait(vi_ctx* c, const char* where) {
     if (!(c)) return VI_E_ARG;                                       \
     if ((c)->poisoned) return VI_E_CUDA;                             \
   } while (0)
+
+// Every entry point runs on its context's device (contexts of one process may live on
+// different GPUs and be driven from different threads, e.g. the Refined model's two).
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    if (cudaGetDevice(&prev) != cudaSuccess || prev == dev) {
+      prev = -1;
+      return;
+    }
+    cudaSetDevice(dev);
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
 
 // Scoped event pair around the launches of one category (vi_profile).
 struct Prof {
@@ -370,6 +418,9 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_k, c->kslab, c->Dl, (uint64_t)c->L * c->S * c->P, 64, 128);
   ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->Dl, 64, c->hd);
   if (c->sharded) ok &= make_tmap(&c->tm_og, c->og, c->hd, (uint64_t)c->H * c->tp.head_rows, 64, 128);
+  ok &= make_tmap_out(&c->tm_u_out, c->u, true, c->F, rows);
+  ok &= make_tmap_out(&c->tm_g_out, c->gbuf, false, c->F, rows);
+  ok &= make_tmap_out(&c->tm_yp_out, c->yp32, true, c->Pd, rows);
   return ok ? VI_OK : c->fail(VI_E_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
@@ -540,6 +591,7 @@ static vi_status upload_f32(vi_ctx* c, float* dst, const float* src, size_t n) {
 
 extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (!w || !w->embed_w || !w->embed_b || !w->ln1_g || !w->ln1_b || !w->wqkv || !w->bqkv || !w->wo || !w->bo ||
       !w->ln2_g || !w->ln2_b || !w->w1 || !w->b1 || !w->w2 || !w->b2 || !w->back_w || !w->back_b)
     return c->fail(VI_E_ARG, "vi_set_weights: NULL weight pointer");
@@ -602,8 +654,8 @@ static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
     if (it == c->pending_kv.end()) continue;
     const int slot = int(id % c->S);
     for (int l = 0; l < c->L; ++l) {
-      const uint8_t* ksrc = static_cast<const uint8_t*>(it->second.first) + ((size_t)l * P * D + h0) * es;
-      const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.second) + ((size_t)l * P * D + h0) * es;
+      const uint8_t* ksrc = static_cast<const uint8_t*>(it->second.k) + ((size_t)l * P * D + h0) * es;
+      const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.v) + ((size_t)l * P * D + h0) * es;
       uint8_t* kdst = static_cast<uint8_t*>(c->kslab) + ((size_t)l * SP + (size_t)slot * P) * Dl * es;
       CK(cudaMemcpy2DAsync(kdst, Dl * es, ksrc, D * es, Dl * es, P, cudaMemcpyDeviceToDevice, c->stream), "commit K");
       uint8_t* vt = static_cast<uint8_t*>(c->vtslab) + (size_t)l * Dl * c->vt_ld * es;
@@ -617,13 +669,20 @@ static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
 
 extern "C" vi_status vi_memory_push(vi_ctx* c, int n, int64_t* first_id, int64_t* evicted, int* n_evicted) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_memory_push: n out of [1, max_new_frames]");
   std::lock_guard<std::mutex> lk(c->mu);
   std::vector<int64_t> ev, apply;
   const int64_t f = c->ring.push(n, &ev, &apply);
   vi_status st = apply_commits(c, apply);
   // all queued payloads are consumed (applied, or dropped because the frame left)
-  for (auto& kv : c->pending_kv) c->free_kv.push_back(kv.second);
+  for (auto& kv : c->pending_kv) {
+    if (st == VI_OK) {
+      cudaError_t e = cudaEventRecord(kv.second.released, c->stream);
+      if (e != cudaSuccess) st = c->cuda_fail(e, "commit release");
+    }
+    c->free_kv.push_back(kv.second);
+  }
   c->pending_kv.clear();
   if (st != VI_OK) return st;
   c->next_layer = 0;
@@ -637,6 +696,7 @@ extern "C" vi_status vi_memory_push(vi_ctx* c, int n, int64_t* first_id, int64_t
 
 extern "C" vi_status vi_memory_evict(vi_ctx* c, int64_t frame_id) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   std::lock_guard<std::mutex> lk(c->mu);
   const vi_status st = c->ring.evict(frame_id);
   if (st == VI_OK) {
@@ -651,42 +711,42 @@ extern "C" vi_status vi_memory_evict(vi_ctx* c, int64_t frame_id) {
 
 extern "C" vi_status vi_refine_commit(vi_ctx* c, int64_t frame_id, const void* k, const void* v) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (!k || !v) return VI_E_ARG;
   std::lock_guard<std::mutex> lk(c->mu);
   const vi_status st = c->ring.commit(frame_id);
   if (st != VI_OK) return st;
   const size_t bytes = (size_t)c->L * c->P * c->D * c->es;
   auto it = c->pending_kv.find(frame_id);
-  std::pair<void*, void*> buf;
+  vi_ctx::KvBuf buf;
   if (it != c->pending_kv.end()) {
-    buf = it->second;
+    buf = it->second;                       // queued, not applied yet: overwrite in place
   } else if (!c->free_kv.empty()) {
     buf = c->free_kv.back();
     c->free_kv.pop_back();
+    // the apply copies that read this buffer at an earlier push must be done
+    CK(cudaStreamWaitEvent(c->copy_stream, buf.released, 0), "commit wait");
   } else {
-    if (cudaMalloc(&buf.first, bytes) != cudaSuccess || cudaMalloc(&buf.second, bytes) != cudaSuccess) {
+    if (cudaMalloc(&buf.k, bytes) != cudaSuccess || cudaMalloc(&buf.v, bytes) != cudaSuccess ||
+        cudaEventCreateWithFlags(&buf.released, cudaEventDisableTiming) != cudaSuccess) {
       cudaGetLastError();
+      if (buf.k) cudaFree(buf.k);
+      if (buf.v) cudaFree(buf.v);
       return c->fail(VI_E_OOM, "vi_refine_commit: staging allocation failed");
     }
   }
   const cudaMemcpyKind kk = is_host_ptr(k) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
   const cudaMemcpyKind kv = is_host_ptr(v) ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
-  // the online stream may still read an older payload of this buffer? no: payloads are
-  // consumed at push (stream-ordered) -- order the copy after the ctx stream's work.
-  cudaEvent_t ev;
-  CK(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming), "commit event");
-  CK(cudaEventRecord(ev, c->stream), "commit event");
-  CK(cudaStreamWaitEvent(c->copy_stream, ev, 0), "commit wait");
-  CK(cudaMemcpyAsync(buf.first, k, bytes, kk, c->copy_stream), "commit copy K");
-  CK(cudaMemcpyAsync(buf.second, v, bytes, kv, c->copy_stream), "commit copy V");
+  CK(cudaMemcpyAsync(buf.k, k, bytes, kk, c->copy_stream), "commit copy K");
+  CK(cudaMemcpyAsync(buf.v, v, bytes, kv, c->copy_stream), "commit copy V");
   CK(cudaStreamSynchronize(c->copy_stream), "commit sync");
-  cudaEventDestroy(ev);
   c->pending_kv[frame_id] = buf;
   return VI_OK;
 }
 
 extern "C" vi_status vi_memory_read(vi_ctx* c, int64_t frame_id, void* k, void* v) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (!k || !v) return c->fail(VI_E_ARG, "vi_memory_read: NULL buffer");
   {
     std::lock_guard<std::mutex> lk(c->mu);
@@ -752,6 +812,7 @@ static Epi epi_base(int kind, int M, int N, const float* bias) {
 
 extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out, int project) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   g_epi_ctx = c;
   if (!feat || !out || n < 1 || n > c->Tmax || (project != 0 && project != 1))
     return c->fail(VI_E_ARG, "vi_soft_split: bad argument");
@@ -763,8 +824,12 @@ extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out
     const int M = n * c->P;
     Epi e = epi_base(EPI_STORE, M, c->D, c->b_embed);
     e.out = out; e.ldo = c->D; e.out_f32 = 1; e.pos = c->cfg.pos_embed ? c->pos : nullptr; e.P = c->P;
+    CUtensorMap tmo;
+    const bool te = c->bf16 && g_tma_epi && make_tmap_out(&tmo, out, true, c->D, M);
     if (c->bf16)
-      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, c->bn_embed, e, c->stream), "embed gemm");
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, c->bn_embed, e, c->stream, 0,
+                                           te ? &tmo : nullptr),
+              "embed gemm");
     else
       PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->tokens, (const float*)c->w_embed, M, c->D, c->Pd, e, c->stream),
              "embed gemm");
@@ -908,8 +973,11 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
     eo.a_hs = c->tp.head_rows;
     eo.a_kpb = c->hd / 64;
   }
+  CUtensorMap tx_in, tx_out;
+  const bool te = c->bf16 && g_tma_epi && make_tmap_out(&tx_in, x_in, true, D, M) && make_tmap_out(&tx_out, x_out, true, D, M);
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->sharded ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream),
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->sharded ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream, 0,
+                                         te ? &tx_out : nullptr, te ? &tx_in : nullptr),
             "o gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->o, (const float*)c->w_o + (size_t)l * D * D, M, D, D, eo, c->stream),
@@ -921,7 +989,9 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   Epi e1 = epi_base(f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
   e1.out = f3n ? c->u : c->gbuf; e1.ldo = F; e1.out_f32 = f3n ? 1 : 0;
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream), "ffn1 gemm");
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream, 0,
+                                         g_tma_epi ? (f3n ? &c->tm_u_out : &c->tm_g_out) : nullptr),
+            "ffn1 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_1 + (size_t)l * F * D, M, F, D, e1, c->stream),
             "ffn1 gemm");
@@ -934,7 +1004,9 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   Epi e2 = epi_base(EPI_RESID, M, D, c->b_2 + (size_t)l * D);
   e2.x_in = x_out; e2.x_out = x_out;
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, c->tm_w2, l * D, M, D, F, c->bn_2, e2, c->stream), "ffn2 gemm");
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, c->tm_w2, l * D, M, D, F, c->bn_2, e2, c->stream, 0,
+                                         te ? &tx_out : nullptr, te ? &tx_out : nullptr),
+            "ffn2 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->gbuf, (const float*)c->w_2 + (size_t)l * D * F, M, D, F, e2,
                                                c->stream),
@@ -961,6 +1033,7 @@ static void layer_done(vi_ctx* c, int layer) {
 
 extern "C" vi_status vi_memory_step_attn(vi_ctx* c, int layer, const float* x_in) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   g_epi_ctx = c;
   vi_status st = check_step(c, layer, x_in, x_in, "vi_memory_step_attn");
   if (st != VI_OK) return st;
@@ -972,6 +1045,7 @@ extern "C" vi_status vi_memory_step_attn(vi_ctx* c, int layer, const float* x_in
 
 extern "C" vi_status vi_memory_step_ffn(vi_ctx* c, int layer, const float* x_in, float* x_out) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   g_epi_ctx = c;
   vi_status st = check_step(c, layer, x_in, x_out, "vi_memory_step_ffn");
   if (st != VI_OK) return st;
@@ -983,6 +1057,7 @@ extern "C" vi_status vi_memory_step_ffn(vi_ctx* c, int layer, const float* x_in,
 
 extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, float* x_out) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   g_epi_ctx = c;
   vi_status st = check_step(c, layer, x_in, x_out, "vi_memory_step");
   if (st != VI_OK) return st;
@@ -1001,6 +1076,7 @@ extern "C" vi_status vi_tp_local_allgather(vi_ctx* const* ctxs, int n) {
   for (int i = 0; i < n; ++i) {
     vi_ctx* c = ctxs[i];
     LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
     if (!c->sharded || c->comm || c->tp.G != n || c->tp.rank != i)
       return c->fail(VI_E_CONFIG, "vi_tp_local_allgather: ctxs[r] must be rank r of a communicator-less group of n");
     if (c->tp.chunk_elems != ctxs[0]->tp.chunk_elems || c->H != ctxs[0]->H || c->hd != ctxs[0]->hd)
@@ -1029,6 +1105,7 @@ extern "C" vi_status vi_tp_local_allgather(vi_ctx* const* ctxs, int n) {
 
 extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* feat, int project) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   g_epi_ctx = c;
   if (!in || !feat || n < 1 || n > c->Tmax || (project != 0 && project != 1))
     return c->fail(VI_E_ARG, "vi_soft_composite: bad argument");
@@ -1044,7 +1121,8 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
       // fp32: the back projection adds no bf16 rounding of its own
       e.out = c->yp32; e.out_f32 = 1;
       PLAUNCH(VI_PROF_ROW, launch_split_bf16((const float*)in, c->xb, M, c->D, c->stream), "cast");
-      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_xb, c->tm_wback, 0, M, c->Pd, 2 * c->D, c->bn_back, e, c->stream),
+      PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_xb, c->tm_wback, 0, M, c->Pd, 2 * c->D, c->bn_back, e, c->stream, 0,
+                                           g_tma_epi ? &c->tm_yp_out : nullptr),
               "back gemm");
     } else {
       PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)in, (const float*)c->w_back, M, c->Pd, c->D, e, c->stream),
@@ -1067,6 +1145,7 @@ static vi_status step_body(vi_ctx* c, const void* fin, int n, void* fout) {
 
 extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, int64_t* first_id) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (!feat || !out || n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_run_step: bad argument");
   if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_run_step: weights not set");
   if (c->sharded && !c->comm)
@@ -1136,12 +1215,14 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
 
 extern "C" vi_status vi_sync(vi_ctx* c) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   CK(cudaStreamSynchronize(c->stream), "vi_sync");
   return VI_OK;
 }
 
 extern "C" vi_status vi_profile(vi_ctx* c, int mode) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (mode < 0 || mode > 3) return VI_E_ARG;
   c->prof_mode = mode;
   return VI_OK;
@@ -1149,6 +1230,7 @@ extern "C" vi_status vi_profile(vi_ctx* c, int mode) {
 
 extern "C" vi_status vi_profile_read(vi_ctx* c, double* ms, int64_t* launches) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   CK(cudaStreamSynchronize(c->stream), "profile sync");
   double acc[VI_PROF_N] = {0, 0, 0, 0};
   int64_t cnt[VI_PROF_N] = {0, 0, 0, 0};
@@ -1196,6 +1278,7 @@ extern "C" const char* vi_version(void) { return "vi-memstep 0.1 (sm_100a)"; }
 
 extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, void* dst, size_t bytes) {
   LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
   if (!dst) return VI_E_ARG;
   const int n = std::max(c->ring.cur_n, 1);
   const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->S * c->P;

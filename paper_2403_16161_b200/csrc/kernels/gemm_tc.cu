@@ -26,13 +26,18 @@ __device__ __forceinline__ void gemm_named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int BN, int STAGES>
+template <int BN, int STAGES, bool TE = false>
 struct GemmSmem {  // (cluster shape does not change the layout)
   static constexpr int A_BYTES = 128 * 64 * 2;
   static constexpr int B_BYTES = BN * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
-  static constexpr int BAR_OFF = STAGES * STAGE_BYTES;
-  static constexpr int BIAS_OFF = BAR_OFF + (2 * STAGES + 4) * 8 + 16;   // [2][BN] fp32
+  // TMA-store epilogue: per epilogue warp two 32-row x 128-byte staging buffers (1 KB aligned
+  // for the 128-byte swizzle of the output tensor maps)
+  static constexpr int STG_OFF = STAGES * STAGE_BYTES;
+  static constexpr int STG_BYTES = TE ? 8 * 2 * 4096 : 0;
+  static constexpr int BAR_OFF = STG_OFF + STG_BYTES;
+  static constexpr int NBAR = 2 * STAGES + 4 + 8;                          // + [8] x_in tile loads
+  static constexpr int BIAS_OFF = BAR_OFF + NBAR * 8 + 16;                 // [2][BN] fp32
   static constexpr int TOTAL = BIAS_OFF + 2 * BN * 4 + 1024;              // +1024 alignment slack
 };
 
@@ -43,11 +48,12 @@ __device__ long long g_gemm_trace[24];
 #define GTR(i) do { } while (0)
 #endif
 
-template <int BN, int STAGES, int CM, int CN>
+template <int BN, int STAGES, int CM, int CN, bool TE>
 __global__ void __launch_bounds__(384, 1)
-gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB, int K, int brow0,
+gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmX, int K, int brow0,
                Epi epi) {
-  using L = GemmSmem<BN, STAGES>;
+  using L = GemmSmem<BN, STAGES, TE>;
   constexpr int CS = CM * CN;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays in .shared
@@ -55,7 +61,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;     // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;         // [2] accumulator drained by the epilogue
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
+  uint64_t* xbar = tempty + 2;          // [8] per epilogue warp: x_in tile landed (TE, EPI_RESID)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GTR(0);
@@ -77,6 +84,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
     tma_prefetch(&tmB);
+    if (TE) {
+      tma_prefetch(&tmO);
+      if (epi.kind == EPI_RESID) tma_prefetch(&tmX);
+    }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], CS);
@@ -85,6 +96,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], 256);
     }
+    for (int w = 0; w < 8; ++w) mbar_init(&xbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
@@ -160,6 +172,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     const int q = ew & 3, hc = ew >> 2;          // TMEM lane quadrant, column half
     const int etid = ew * 32 + lane;             // 0..255
     float* bias_s = reinterpret_cast<float*>(smem + L::BIAS_OFF);
+    uint8_t* stg = smem + L::STG_OFF + ew * 8192;
+    int nchunk = 0;
+    uint32_t xphase = 0;
     int lt = 0;
     for (int st = cid; st < nsuper; st += ncl, ++lt) {
       const int acc = lt & 1;
@@ -173,6 +188,78 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       if (lt < 4 && ew == 0 && lane == 0) GTR(7 + lt);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
+      if constexpr (TE) {
+        // TMA-store epilogue: the warp's 32 rows x (128 B of output) go through a swizzled
+        // staging buffer and leave as one bulk tensor store (coalesced, asynchronous); a
+        // residual tile arrives the same way (TMA load into the buffer it is stored from).
+        const bool resid = epi.kind == EPI_RESID;
+        const int cw = (resid || epi.out_f32) ? 32 : 64;           // columns per 128-byte row
+        const int sw = lane & 7;                                  // 128-byte swizzle phase of this row
+#pragma unroll 1
+        for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += cw, ++nchunk) {
+          if (n0 + c >= epi.N) break;
+          uint8_t* buf = stg + (nchunk & 1) * 4096;
+          if (nchunk >= 2) {                    // the store that used this buffer has read it
+            if (lane == 0) bulk_wait_read<1>();
+            __syncwarp();
+          }
+          if (resid && lane == 0) {
+            mbar_arrive_expect_tx(&xbar[ew], 4096);
+            tma_load_2d(buf, &tmX, &xbar[ew], n0 + c, m0 + q * 32);
+          }
+#pragma unroll 1
+          for (int h2 = 0; h2 < cw; h2 += 32) {
+            float v[32];
+            tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c + h2, reinterpret_cast<uint32_t*>(v));
+            tmem_wait_ld();
+            if (epi.bias) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += bs[c + h2 + i];
+            }
+            if (epi.kind == EPI_GELU) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = gelu_erf(v[i]);
+            } else if (epi.kind == EPI_STORE && epi.pos && m < epi.M) {
+              const float* pr = epi.pos + (size_t)(m % epi.P) * epi.N + n0 + c + h2;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] += (n0 + c + h2 + i < epi.N) ? __ldg(pr + i) : 0.f;
+            }
+            uint8_t* row = buf + lane * 128;
+            if (resid || epi.out_f32) {
+              if (resid) {
+                mbar_wait(&xbar[ew], xphase);
+                xphase ^= 1u;
+              }
+#pragma unroll
+              for (int j = 0; j < 8; ++j) {
+                float4* p4 = reinterpret_cast<float4*>(row + ((j ^ sw) << 4));
+                float4 o = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+                if (resid) {
+                  const float4 xi = *p4;
+                  o.x += xi.x; o.y += xi.y; o.z += xi.z; o.w += xi.w;
+                }
+                *p4 = o;
+              }
+            } else {
+#pragma unroll
+              for (int j = 0; j < 4; ++j)
+                *reinterpret_cast<uint4*>(row + (((h2 / 8 + j) ^ sw) << 4)) =
+                    make_uint4(pack_bf16(v[8 * j], v[8 * j + 1]), pack_bf16(v[8 * j + 2], v[8 * j + 3]),
+                               pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
+            }
+          }
+          fence_proxy_async_smem();
+          __syncwarp();
+          if (lane == 0) {
+            tma_store_2d(&tmO, buf, n0 + c, m0 + q * 32);
+            bulk_commit();
+          }
+        }
+        tc_fence_before();
+        mbar_arrive(&tempty[acc]);
+        if (lt < 4 && ew == 0 && lane == 0) GTR(11 + lt);
+        continue;
+      }
 #pragma unroll 1
       for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += 32) {
         if (n0 + c >= epi.N) break;
@@ -191,6 +278,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_arrive(&tempty[acc]);
       if (lt < 4 && ew == 0 && lane == 0) GTR(11 + lt);
     }
+    if (TE && lane == 0) bulk_wait<0>();        // staging buffers stay valid until stored
   }
   tc_fence_before();
   if (CS > 1) cluster_sync_all();   // no CTA leaves while peers may still multicast into it
@@ -205,12 +293,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
 static int g_num_sms = 0;
 
-template <int BN, int STAGES, int CM, int CN>
+template <int BN, int STAGES, int CM, int CN, bool TE = false>
 static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
-                              const Epi& e, cudaStream_t st) {
-  using L = GemmSmem<BN, STAGES>;
+                              const Epi& e, cudaStream_t st, const CUtensorMap* tmo = nullptr,
+                              const CUtensorMap* tmx = nullptr) {
+  using L = GemmSmem<BN, STAGES, TE>;
   constexpr int CS = CM * CN;
-  auto kfn = gemm_tc_kernel<BN, STAGES, CM, CN>;
+  auto kfn = gemm_tc_kernel<BN, STAGES, CM, CN, TE>;
   static int max_clusters = 0;
   if (!max_clusters) {
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
@@ -250,14 +339,26 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   at[1].val.programmaticStreamSerializationAllowed = g_pdl;
   cfg.attrs = at;
   cfg.numAttrs = 2;
-  return cudaLaunchKernelEx(&cfg, kfn, a, b, K, brow0, e);
+  // unused output maps are passed as copies of the A map (never dereferenced)
+  return cudaLaunchKernelEx(&cfg, kfn, a, b, tmo ? *tmo : a, tmx ? *tmx : a, K, brow0, e);
 }
 
 // cluster (CM x CN): 0 = 1x1, 1 = 2x1 (W tile multicast), 2 = 1x2 (A multicast), 3 = 2x2,
 // 4 = 1x4, 5 = 2x4, 6 = 1x8, 7 = 4x2.  The A map's box must be 64 x (128 / CN), the W map's
 // 64 x (BN / CM).
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K, int bn,
-                           const Epi& e, cudaStream_t st, int cluster) {
+                           const Epi& e, cudaStream_t st, int cluster, const CUtensorMap* tmo,
+                           const CUtensorMap* tmx) {
+  if (tmo) {   // TMA-store epilogue (EPI_STORE / EPI_GELU / EPI_RESID), no clusters
+    if (e.kind != EPI_STORE && e.kind != EPI_GELU && e.kind != EPI_RESID) return cudaErrorInvalidValue;
+    if (e.kind == EPI_RESID && !tmx) return cudaErrorInvalidValue;
+    switch (bn) {
+      case 64: return launch_cfg<64, 6, 1, 1, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      case 128: return launch_cfg<128, 4, 1, 1, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      case 256: return launch_cfg<256, 3, 1, 1, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      default: return cudaErrorInvalidValue;
+    }
+  }
 #define CASES(BN, ST)                                                              \
   switch (cluster) {                                                               \
     case 0: return launch_cfg<BN, ST, 1, 1>(a, b, brow0, M, N, K, e, st);          \

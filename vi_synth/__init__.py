@@ -175,18 +175,43 @@ def _rect_mask(rng: np.random.Generator, h: int, w: int) -> np.ndarray:
     return m
 
 
+def _moving_rect_mask(seed: int, fid: int, h: int, w: int) -> np.ndarray:
+    """One rectangle per stream (10-30% of the grid, aspect U(0.5, 2)) moving with a constant
+    velocity and reflecting at the borders (object-removal style masks)."""
+    rng = rng_for(seed, "moving-mask")
+    area = rng.uniform(0.10, 0.30) * h * w
+    aspect = rng.uniform(0.5, 2.0)
+    rh = int(min(h, max(1, round(np.sqrt(area / aspect)))))
+    rw = int(min(w, max(1, round(area / rh))))
+    y0, x0 = rng.uniform(0, h - rh), rng.uniform(0, w - rw)
+    vy, vx = rng.uniform(-1.5, 1.5), rng.uniform(-1.5, 1.5)
+
+    def reflect(p, span):
+        if span <= 0:
+            return 0
+        q = p % (2 * span)
+        return int(round(q if q <= span else 2 * span - q))
+    y, x = reflect(y0 + vy * fid, h - rh), reflect(x0 + vx * fid, w - rw)
+    m = np.zeros((h, w), dtype=bool)
+    m[y:y + rh, x:x + rw] = True
+    return m
+
+
 def make_features(cfg: Config, n_frames: int, first_frame: int = 0, seed: int = 0,
-                  masked: bool = False) -> np.ndarray:
+                  masked=False) -> np.ndarray:
     """Feature maps [n, H, W, C] (channels-last) ~N(0,1), one independent draw per frame id.
 
     With ``masked`` the cells under a random 10-30% rectangle are zeroed (a stand-in for
-    the encoder seeing X = Y (1-M)).
+    the encoder seeing X = Y (1-M)); ``masked="moving"``: one rectangle per stream
+    moving across the frames with reflecting borders.
     """
     out = np.empty((n_frames, cfg.feat_h, cfg.feat_w, cfg.feat_c), dtype=np.float32)
     for i in range(n_frames):
         fid = first_frame + i
         out[i] = _normal(seed, f"feat{fid}", (cfg.feat_h, cfg.feat_w, cfg.feat_c), 1.0)
-        if masked:
+        if masked == "moving":
+            out[i][_moving_rect_mask(seed, fid, cfg.feat_h, cfg.feat_w)] = 0.0
+        elif masked:
             m = _rect_mask(rng_for(seed, f"mask{fid}"), cfg.feat_h, cfg.feat_w)
             out[i][m] = 0.0
     return round_bf16(out) if cfg.dtype == "bf16" else out
