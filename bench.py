@@ -38,12 +38,18 @@ def peaks():
         return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
 
 
+WORKLOADS = {"C3": "FuseFormer-shaped memory step (BASELINE.json configs[2])",
+             "C3T1": "FuseFormer-shaped memory step, one new frame per step (Eq. 3; configs[2] shape, T=1)",
+             "C2": "STTN-shaped memory step (BASELINE.json configs[1])"}
+
+
 def workload_config(cfg, args=None, world=1):
-    return {"workload": f"{cfg.name}: FuseFormer-shaped memory step (BASELINE.json configs[2])",
+    return {"workload": f"{cfg.name}: {WORKLOADS[cfg.name]}",
             "layers": cfg.layers, "heads": cfg.heads, "d_model": cfg.d_model, "tokens_per_frame": cfg.tokens,
             "new_frames_per_step": cfg.t_new, "mem_frames": cfg.mem_frames,
             "keys_per_block": cfg.slots * cfg.tokens, "queries_per_block": cfg.t_new * cfg.tokens,
-            "feature_map": [cfg.feat_h, cfg.feat_w, cfg.feat_c], "ffn": "F3N 1960",
+            "feature_map": [cfg.feat_h, cfg.feat_w, cfg.feat_c],
+            "ffn": f"F3N {cfg.ffn_hidden}" if cfg.ffn_kind == 1 else f"MLP-GELU {cfg.ffn_hidden}",
             "l2": "flushed between timed steps (256 MiB write)",
             "parallelism": (f"heads sharded over {world} GPUs (NCCL all-gather per block), 1 stream"
                             if args is not None and args.tp else f"{world} independent live streams, 1 per GPU")}
@@ -284,7 +290,7 @@ def main():
     ap.add_argument("--steps", type=int, default=100)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--config", default="C3", choices=["C3", "C3T1"])
+    ap.add_argument("--config", default="C3", choices=sorted(WORKLOADS))
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--tp", action="store_true",
                     help="one stream with its heads sharded over the N ranks (NCCL all-gather per block)")

@@ -102,6 +102,12 @@ typedef struct vi_config {
    * = higher priority (cudaDeviceGetStreamPriorityRange); 0 = default.  The Refined
    * dual-model run gives the online context the high priority and the refiner 0. */
   int stream_priority;
+  /* Reference frames, Eq. 3's M_{1,r}^{f-1}: with ref_rate r > 0, a frame whose
+   * id is a multiple of r stays in the memory after it leaves the span, in one of
+   * max_ref_frames reference slots (its K/V move there at the push; the oldest reference
+   * leaves when the slots are full; reading Q12).  0 = span only.  Slots in total:
+   * mem_frames + max_new_frames + max_ref_frames <= 64 (vi_num_slots). */
+  int ref_rate, max_ref_frames;
 } vi_config;
 
 /* Weights, host fp32 pointers in nn.Linear layout (y = x W^T + b); converted to the
@@ -283,6 +289,9 @@ vi_status vi_debug_read(vi_ctx* ctx, int what, int layer, int slot, void* dst, s
  * For tests of the integer bookkeeping on machines without a GPU. */
 typedef struct vi_ring vi_ring;
 vi_status vi_ring_create(vi_ring** out, int mem_frames, int max_new_frames);
+/* With reference frames (see vi_config.ref_rate / max_ref_frames). */
+vi_status vi_ring_create_ex(vi_ring** out, int mem_frames, int max_new_frames, int ref_rate,
+                            int max_ref_frames);
 vi_status vi_ring_destroy(vi_ring* r);
 vi_status vi_ring_push(vi_ring* r, int n, int64_t* first_id, int64_t* evicted, int* n_evicted);
 vi_status vi_ring_evict(vi_ring* r, int64_t frame_id);

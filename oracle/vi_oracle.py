@@ -266,18 +266,23 @@ def block_memory(x: np.ndarray, mem_kv: Sequence[Tuple[np.ndarray, np.ndarray]],
     return xo, st
 
 
-def joint_forward(feats: np.ndarray, w, cfg, mode: str = "causal") -> Dict[str, object]:
+def joint_forward(feats: np.ndarray, w, cfg, mode: str = "causal",
+                  frame_mask: Optional[np.ndarray] = None) -> Dict[str, object]:
     """Eq. 1/2-style joint pass over a window of frames, all predicted together.
 
     mode "causal": frame i's queries see frames j <= i (frame-level block-causal mask);
-    mode "full": bidirectional (the offline/refiner window of Eq. 1).
+    mode "full": bidirectional (the offline/refiner window of Eq. 1, P:76-82);
+    mode "mask": frame i's queries see the frames j with frame_mask[i, j] (boolean [n, n]).
     Returns per-layer K/V [L][n, P, D] and the composite output [n, H, W, C].
     """
     n = feats.shape[0]
     P, D = cfg.tokens, cfg.d_model
     Tp, X = embed(feats, w, cfg)
     fr = np.repeat(np.arange(n), P)
-    allowed = (fr[None, :] <= fr[:, None]) if mode == "causal" else None
+    if mode == "mask":
+        allowed = np.asarray(frame_mask, bool)[fr[:, None], fr[None, :]]
+    else:
+        allowed = (fr[None, :] <= fr[:, None]) if mode == "causal" else None
     ks, vs, xs = [], [], [X]
     for l in range(cfg.layers):
         h1, Q, K, V = qkv(X, w, l, cfg)
@@ -302,9 +307,14 @@ def joint_forward(feats: np.ndarray, w, cfg, mode: str = "causal") -> Dict[str, 
 class OracleMemory:
     """Resident-set bookkeeping + per-(layer, frame) cache, no slots, no arrays of slots."""
 
-    def __init__(self, mem_frames: int, max_new: int):
+    def __init__(self, mem_frames: int, max_new: int, ref_rate: int = 0, max_refs: int = 0):
         self.M = mem_frames
         self.T_max = max_new
+        # Eq. 3's reference frames M_{1,r}^{f-1} (P:127-130): multiples of r stay after they
+        # leave the span, in R reference slots, the oldest leaving first (DESIGN reading Q12)
+        self.r = ref_rate if max_refs > 0 else 0
+        self.R = max_refs if ref_rate > 0 else 0
+        self.refs: Dict[int, int] = {}     # reference frame id -> its slot (S .. S+R-1)
         self.next_id = 0
         self.cur_first = 0     # first id of the chunk pushed last
         self.cur_n = 0
@@ -318,18 +328,35 @@ class OracleMemory:
 
     @property
     def slots(self) -> int:
-        return self.M + self.T_max
+        return self.M + self.T_max + self.R
 
     def push(self, n: int, on_evict=None, on_commit=None) -> Tuple[int, List[int]]:
         if n < 1 or n > self.T_max:
             raise ValueError("push: n out of range")
         f = self.next_id
-        evicted = sorted(j for j in self.resident if j < f - self.M)
-        for j in evicted:
+        S = self.M + self.T_max
+        evicted = []
+
+        def drop(j):
             self.resident.discard(j)
             self.refined.discard(j)
+            self.pending.pop(j, None)
+            evicted.append(j)
             if on_evict:
                 on_evict(j)
+        for j in sorted(j for j in self.resident if j < f - self.M and j not in self.refs):
+            if self.r > 0 and j % self.r == 0:
+                free = [k for k in range(S, S + self.R) if k not in self.refs.values()]
+                if free:
+                    slot = min(free)
+                else:
+                    oldest = min(self.refs)
+                    slot = self.refs.pop(oldest)
+                    drop(oldest)
+                self.refs[j] = slot
+            else:
+                drop(j)
+        evicted.sort()
         for j in sorted(self.pending):
             if j in self.resident:
                 self.refined.add(j)
@@ -357,6 +384,7 @@ class OracleMemory:
     def evict(self, fid: int, on_evict=None) -> int:
         st = self._check_past(fid)
         if st == VI_OK:
+            self.refs.pop(fid, None)
             self.resident.discard(fid)
             self.refined.discard(fid)
             self.pending.pop(fid, None)
@@ -376,10 +404,10 @@ class OracleMemory:
 
     def state(self) -> Tuple[List[int], List[int], int]:
         """(slot_id[S], refined[S], valid mask) under slot = id mod S."""
-        S = self.slots
-        slot_id, ref, mask = [-1] * S, [0] * S, 0
+        S = self.M + self.T_max
+        slot_id, ref, mask = [-1] * self.slots, [0] * self.slots, 0
         for j in self.resident:
-            s = j % S
+            s = self.refs[j] if j in self.refs else j % S
             assert slot_id[s] == -1, "two resident frames share a slot"
             slot_id[s] = j
             ref[s] = int(j in self.refined)
@@ -393,7 +421,7 @@ class OracleStream:
     def __init__(self, cfg, w: Dict[str, np.ndarray], chunk_causal: bool = False):
         self.cfg = cfg
         self.w = w
-        self.mem = OracleMemory(cfg.mem_frames, cfg.t_new)
+        self.mem = OracleMemory(cfg.mem_frames, cfg.t_new, getattr(cfg, "ref_rate", 0), getattr(cfg, "max_refs", 0))
         self.chunk_causal = chunk_causal
         # (layer, frame id) -> ("x", block input [P, D]) or ("kv", K [P, D], V [P, D])
         self.entries: Dict[Tuple[int, int], tuple] = {}

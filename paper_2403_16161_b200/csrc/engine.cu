@@ -111,6 +111,7 @@ struct vi_ctx {
   vi_config cfg{};
   Geom g{}, gf{};          // split geometry (C = feat_c) and F3N geometry (C = F / (kh*kw))
   int L = 0, H = 0, D = 0, hd = 0, P = 0, M = 0, Tmax = 0, S = 0, F = 0, Pd = 0, es = 2;
+  int ST = 0;              // all memory slots: S span slots + R reference slots (ring.h)
   int vt_ld = 0;           // row pitch of the transposed V slab: S*P rounded up to 64 (TMA: 16-B pitch)
   bool bf16 = true;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -161,7 +162,7 @@ struct vi_ctx {
   CUtensorMap tm_q, tm_k, tm_vt, tm_og;
   CUtensorMap tm_u_out, tm_g_out, tm_yp_out;   // GEMM outputs through the TMA-store epilogue
   // N-tile per GEMM (persistent kernel: ~1-3 tiles per SM at M = 3600; N=64 MMAs run at 2/3 rate)
-  int bn_embed = 128, bn_qkv = 128, bn_o = 128, bn_1 = 128, bn_2 = 128, bn_back = 256;
+  int bn_embed = 128, bn_qkv = 128, bn_o = 128, bn_1 = 256, bn_2 = 128, bn_back = 256;
 
   // profiling (vi_profile)
   int prof_mode = 0;
@@ -350,7 +351,9 @@ static vi_status validate(const vi_config* k, std::string* why) {
   };
   if (k->layers < 1 || k->heads < 1 || k->d_model < 1 || k->mem_frames < 0 || k->max_new_frames < 1)
     return bad("layers, heads, d_model, max_new_frames must be >= 1 and mem_frames >= 0");
-  if (k->mem_frames + k->max_new_frames > 64) return bad("mem_frames + max_new_frames must be <= 64");
+  if (k->ref_rate < 0 || k->max_ref_frames < 0) return bad("ref_rate and max_ref_frames must be >= 0");
+  if (k->mem_frames + k->max_new_frames + (k->ref_rate > 0 ? k->max_ref_frames : 0) > 64)
+    return bad("mem_frames + max_new_frames + max_ref_frames must be <= 64");
   if (k->d_model % k->heads) return bad("d_model must be divisible by heads");
   const int hd = k->d_model / k->heads;
   if (k->dtype != VI_DTYPE_BF16 && k->dtype != VI_DTYPE_FP32) return bad("dtype must be 0 (bf16) or 1 (fp32)");
@@ -406,7 +409,7 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_tokens, c->tokens, c->Pd, rows, 64, 128);
   ok &= make_tmap(&c->tm_wembed, c->w_embed, c->Pd, c->D, 64, c->bn_embed);
   ok &= make_tmap(&c->tm_h, c->h, c->D, rows, 64, 128);
-  ok &= make_tmap(&c->tm_wqkv, c->w_qkv, c->D, (uint64_t)c->L * 3 * c->D, 64, c->bn_qkv);
+  ok &= make_tmap(&c->tm_wqkv, c->w_qkv, c->D, (uint64_t)c->L * 3 * c->Dl, 64, c->bn_qkv);
   ok &= make_tmap(&c->tm_o, c->o, c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_wo, c->w_o, c->D, (uint64_t)c->L * c->D, 64, c->bn_o);
   ok &= make_tmap(&c->tm_w1, c->w_1, c->D, (uint64_t)c->L * c->F, 64, c->bn_1);
@@ -415,7 +418,7 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_xb, c->xb, 2 * c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_wback, c->w_back2, 2 * c->D, c->Pd, 64, c->bn_back);
   ok &= make_tmap(&c->tm_q, c->q, c->Dl, rows, 64, 128);
-  ok &= make_tmap(&c->tm_k, c->kslab, c->Dl, (uint64_t)c->L * c->S * c->P, 64, 128);
+  ok &= make_tmap(&c->tm_k, c->kslab, c->Dl, (uint64_t)c->L * c->ST * c->P, 64, 128);
   ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->Dl, 64, c->hd);
   if (c->sharded) ok &= make_tmap(&c->tm_og, c->og, c->hd, (uint64_t)c->H * c->tp.head_rows, 64, 128);
   ok &= make_tmap_out(&c->tm_u_out, c->u, true, c->F, rows);
@@ -444,10 +447,11 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->cfg = *cfg;
   c->L = cfg->layers; c->H = cfg->heads; c->D = cfg->d_model; c->hd = c->D / c->H;
   c->P = cfg->tokens_per_frame; c->M = cfg->mem_frames; c->Tmax = cfg->max_new_frames; c->S = c->M + c->Tmax;
+  c->ST = c->S + (cfg->ref_rate > 0 ? cfg->max_ref_frames : 0);
   c->F = cfg->ffn_hidden; c->Pd = cfg->kh * cfg->kw * cfg->feat_c;
-  c->vt_ld = (c->S * c->P + 63) / 64 * 64;
+  c->vt_ld = (c->ST * c->P + 63) / 64 * 64;
   c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
-  c->ring = Ring(c->M, c->Tmax);
+  c->ring = Ring(c->M, c->Tmax, cfg->ref_rate, cfg->max_ref_frames);
   {
     const int G = cfg->tp_size < 1 ? 1 : cfg->tp_size;
     c->sharded = G > 1 || cfg->nccl_id != nullptr;
@@ -474,7 +478,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     delete c;
     return VI_E_CUDA;
   }
-  const size_t es = c->es, L = c->L, D = c->D, F = c->F, Pd = c->Pd, S = c->S, P = c->P;
+  const size_t es = c->es, L = c->L, D = c->D, F = c->F, Pd = c->Pd, S = c->ST, P = c->P;
   const size_t rows = (size_t)c->Tmax * P;
   const size_t fmap = (size_t)c->Tmax * cfg->feat_h * cfg->feat_w * cfg->feat_c;
   bool ok = true;
@@ -551,6 +555,30 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   }
   if (c->bf16) {
     if (c->D % 128) c->bn_o = c->bn_2 = 64;
+    // VI_BN="qkv=256,ffn1=256,...": N-tile overrides for A/B measurements (64, 128 or 256)
+    if (const char* e = getenv("VI_BN")) {
+      std::string spec(e);
+      size_t pos = 0;
+      while (pos < spec.size()) {
+        size_t end = spec.find(',', pos);
+        if (end == std::string::npos) end = spec.size();
+        const std::string item = spec.substr(pos, end - pos);
+        const size_t eq = item.find('=');
+        if (eq != std::string::npos) {
+          const std::string k = item.substr(0, eq);
+          const int v = atoi(item.c_str() + eq + 1);
+          if (v == 64 || v == 128 || v == 256) {
+            if (k == "embed") c->bn_embed = v;
+            if (k == "qkv") c->bn_qkv = v;
+            if (k == "o") c->bn_o = v;
+            if (k == "ffn1") c->bn_1 = v;
+            if (k == "ffn2") c->bn_2 = v;
+            if (k == "back") c->bn_back = v;
+          }
+        }
+        pos = end + 1;
+      }
+    }
     if (build_maps(c) != VI_OK) {
       delete c;
       return VI_E_CUDA;
@@ -647,12 +675,13 @@ extern "C" vi_status vi_set_weights(vi_ctx* c, const vi_weights* w) {
 // ------------------------------------------------------------------------------ ring
 
 static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
-  const size_t es = c->es, P = c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->S * c->P;
+  const size_t es = c->es, P = c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->ST * c->P;
   const size_t h0 = (size_t)c->tp.head0 * c->hd;   // this rank's columns of the full [P][D] payload
   for (int64_t id : ids) {
     auto it = c->pending_kv.find(id);
     if (it == c->pending_kv.end()) continue;
-    const int slot = int(id % c->S);
+    const int slot = c->ring.slot_of(id);
+    if (slot < 0) continue;
     for (int l = 0; l < c->L; ++l) {
       const uint8_t* ksrc = static_cast<const uint8_t*>(it->second.k) + ((size_t)l * P * D + h0) * es;
       const uint8_t* vsrc = static_cast<const uint8_t*>(it->second.v) + ((size_t)l * P * D + h0) * es;
@@ -667,14 +696,35 @@ static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
   return VI_OK;
 }
 
+// Frames becoming references (ring.h): their K rows and Vt columns move from the span slot
+// to the reference slot, on the ctx stream before the new chunk's step overwrites the span slot.
+static vi_status apply_moves(vi_ctx* c, const std::vector<Ring::Move>& moves) {
+  const size_t es = c->es, P = c->P, Dl = c->Dl, SP = (size_t)c->ST * c->P, ld = c->vt_ld;
+  for (const auto& mv : moves) {
+    for (int l = 0; l < c->L; ++l) {
+      uint8_t* kb = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * Dl * es;
+      CK(cudaMemcpyAsync(kb + (size_t)mv.dst * P * Dl * es, kb + (size_t)mv.src * P * Dl * es, P * Dl * es,
+                         cudaMemcpyDeviceToDevice, c->stream),
+         "reference move K");
+      uint8_t* vb = static_cast<uint8_t*>(c->vtslab) + (size_t)l * Dl * ld * es;
+      CK(cudaMemcpy2DAsync(vb + (size_t)mv.dst * P * es, ld * es, vb + (size_t)mv.src * P * es, ld * es, P * es, Dl,
+                           cudaMemcpyDeviceToDevice, c->stream),
+         "reference move V");
+    }
+  }
+  return VI_OK;
+}
+
 extern "C" vi_status vi_memory_push(vi_ctx* c, int n, int64_t* first_id, int64_t* evicted, int* n_evicted) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
   if (n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_memory_push: n out of [1, max_new_frames]");
   std::lock_guard<std::mutex> lk(c->mu);
   std::vector<int64_t> ev, apply;
-  const int64_t f = c->ring.push(n, &ev, &apply);
-  vi_status st = apply_commits(c, apply);
+  std::vector<Ring::Move> moves;
+  const int64_t f = c->ring.push(n, &ev, &apply, &moves);
+  vi_status st = apply_moves(c, moves);
+  if (st == VI_OK) st = apply_commits(c, apply);
   // all queued payloads are consumed (applied, or dropped because the frame left)
   for (auto& kv : c->pending_kv) {
     if (st == VI_OK) {
@@ -753,8 +803,12 @@ extern "C" vi_status vi_memory_read(vi_ctx* c, int64_t frame_id, void* k, void* 
     const int32_t st = c->ring.check_past(frame_id);
     if (st != VI_OK) return st;
   }
-  const size_t es = c->es, P = c->P, Dl = c->Dl, SP = (size_t)c->S * c->P, per = P * Dl * es;
-  const size_t slot = size_t(frame_id % c->S);
+  const size_t es = c->es, P = c->P, Dl = c->Dl, SP = (size_t)c->ST * c->P, per = P * Dl * es;
+  size_t slot;
+  {
+    std::lock_guard<std::mutex> lk(c->mu);
+    slot = size_t(c->ring.slot_of(frame_id));
+  }
   const bool hk = is_host_ptr(k), hv = is_host_ptr(v);
   // V leaves the slab through a transpose kernel: a host destination is staged on the device
   void* vd = v;
@@ -790,7 +844,7 @@ extern "C" vi_status vi_memory_read(vi_ctx* c, int64_t frame_id, void* k, void* 
 extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask) {
   if (!c) return VI_E_ARG;
   std::lock_guard<std::mutex> lk(c->mu);
-  for (int s = 0; s < c->S; ++s) {
+  for (int s = 0; s < c->ST; ++s) {
     if (slot_id) slot_id[s] = c->ring.slot_id[s];
     if (refined) refined[s] = c->ring.refined[s];
   }
@@ -858,13 +912,13 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
   KeySegs k;
   std::memset(&k, 0, sizeof(k));
   int s = 0;
-  while (s < c->S) {
+  while (s < c->ST) {
     if (!((valid >> s) & 1)) {
       ++s;
       continue;
     }
     int e = s;
-    while (e + 1 < c->S && ((valid >> (e + 1)) & 1)) ++e;
+    while (e + 1 < c->ST && ((valid >> (e + 1)) & 1)) ++e;
     const int r0 = s * c->P;
     k.row0[k.n] = r0 & ~7;
     k.lead[k.n] = r0 & 7;
@@ -882,7 +936,7 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
 static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   const int n = c->ring.cur_n, M = n * c->P, D = c->D, Dl = c->Dl;
   const int dt = c->bf16 ? 0 : 1;
-  const size_t es = c->es, SP = (size_t)c->S * c->P;
+  const size_t es = c->es, SP = (size_t)c->ST * c->P;
   void* kl = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * Dl * es;
   void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * c->vt_ld * Dl * es;
   const uint64_t valid = c->ring.valid_mask();
@@ -903,7 +957,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   const float scale_log2 = float(1.4426950408889634 / std::sqrt(double(c->hd)));
   if (!c->bf16) {
     AttnArgs a;
-    a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->S; a.vt_ld = c->vt_ld; a.valid = valid;
+    a.Nq = M; a.D = D; a.H = c->H; a.hd = c->hd; a.P = c->P; a.S = c->ST; a.vt_ld = c->vt_ld; a.valid = valid;
     a.scale_log2 = scale_log2; a.q = c->q; a.kslab = kl; a.vtslab = vl; a.o = c->o;
     PLAUNCH(VI_PROF_ATTN, launch_attn_simt_f32(a, c->stream), "attention");
     return VI_OK;
@@ -924,7 +978,13 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   const int ntiles = a.segs.tile0[a.segs.n];
   a.opart = c->opart; a.lse = c->lse;
   a.timing = (c->prof_mode == 1 || c->prof_mode == 3) ? c->attn_timing : nullptr;
-  if ((!g_attn_v1 && !g_attn_split) || c->sharded) {
+  // Stream-K needs enough (query-pair, head) units: with few units (a chunk of one frame:
+  // 720 queries -> 12 units for 148 SMs) every unit splits ~12 ways and its owner merges the
+  // pieces serially, so small chunks take the fixed KV split + parallel combine kernel
+  // (C3, T = 1: 28 us vs 60 us per block; T = 5: stream-K 84 us vs ~93 us).
+  const int sk_units = ((a.Nq + 255) / 256) * a.H;
+  const bool small = sk_units * 4 < c->num_sms;
+  if (!g_attn_v1 && !g_attn_split && !small) {
     // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
     a.npairs = (a.Nq + 255) / 256;
     a.units = a.npairs * a.H;
@@ -938,9 +998,10 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
       PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
     else
       PLAUNCH(VI_PROF_ATTN, launch_attn_sk3(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-  } else {   // A/B variants: fixed KV split + combine kernel
+  } else {   // fixed KV split + combine kernel (small chunks; VI_ATTN_V1 / VI_ATTN_SPLIT A/B variants)
+    if (g_attn_v1 && c->sharded) return c->fail(VI_E_CONFIG, "VI_ATTN_V1 does not support head sharding");
     const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
-    choose_split(((M + qrows - 1) / qrows) * c->H, ntiles, &a.nsplit, &a.tiles_per_split);
+    choose_split(((a.Nq + qrows - 1) / qrows) * a.H, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
     if (g_attn_v1)
       PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
@@ -1268,11 +1329,11 @@ extern "C" const char* vi_last_error(const vi_ctx* c) { return c ? c->err.c_str(
 extern "C" int64_t vi_kernel_launches(const vi_ctx* c) { return c ? c->launches : 0; }
 extern "C" vi_status vi_memory_footprint(const vi_ctx* c, int64_t* slab_bytes, int64_t* total_bytes) {
   if (!c) return VI_E_ARG;
-  if (slab_bytes) *slab_bytes = int64_t(c->L) * c->S * c->P * c->Dl * c->es + int64_t(c->L) * c->Dl * c->vt_ld * c->es;
+  if (slab_bytes) *slab_bytes = int64_t(c->L) * c->ST * c->P * c->Dl * c->es + int64_t(c->L) * c->Dl * c->vt_ld * c->es;
   if (total_bytes) *total_bytes = int64_t(c->device_bytes);
   return VI_OK;
 }
-extern "C" int vi_num_slots(const vi_ctx* c) { return c ? c->S : 0; }
+extern "C" int vi_num_slots(const vi_ctx* c) { return c ? c->ST : 0; }
 extern "C" void* vi_stream(const vi_ctx* c) { return c ? (void*)c->stream : nullptr; }
 extern "C" const char* vi_version(void) { return "vi-memstep 0.1 (sm_100a)"; }
 
@@ -1281,7 +1342,7 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
   DeviceGuard dg_(c->cfg.device);
   if (!dst) return VI_E_ARG;
   const int n = std::max(c->ring.cur_n, 1);
-  const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->S * c->P;
+  const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->ST * c->P;
   const void* src = nullptr;
   size_t need = 0;
   switch (what) {
@@ -1298,7 +1359,7 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
     default: return VI_E_ARG;
   }
   if (bytes != need) return c->fail(VI_E_SHAPE, "vi_debug_read: byte count mismatch");
-  if ((what == VI_DBG_K || what == VI_DBG_V) && (layer < 0 || layer >= c->L || slot < 0 || slot >= c->S))
+  if ((what == VI_DBG_K || what == VI_DBG_V) && (layer < 0 || layer >= c->L || slot < 0 || slot >= c->ST))
     return VI_E_ARG;
   CK(cudaStreamSynchronize(c->stream), "debug sync");
   if (what == VI_DBG_K) {

@@ -448,7 +448,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int at = 0; at < HD / 64; ++at)
-          tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, q0 + t * 128);
+          tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, a.q_row0 + q0 + t * 128);
       for (int jj = 0; jj < n; ++jj) {
         int row0, nv, nskip;
         key_tile(a.segs, t_begin + jj, row0, nv, nskip);
@@ -637,7 +637,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           const float* f = reinterpret_cast<const float*>(r);
           const int col = h * HD + hf * OH + c;
           if (a.nsplit == 1) {
-            uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.D + col);
+            uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.o_ld + (size_t)h * a.o_hs + (col - h * HD));
 #pragma unroll
             for (int i = 0; i < 4; ++i)
               dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv),
@@ -754,7 +754,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         tmem_wait_ld();
         if (q < a.Nq) {
           const float* f = reinterpret_cast<const float*>(r);
-          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.D + h * HD + c);
+          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.o_ld + (size_t)h * a.o_hs + c);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv), pack_bf16(f[8 * i + 2] * inv, f[8 * i + 3] * inv),
@@ -836,7 +836,7 @@ __global__ void attn_combine_kernel(const AttnTC a) {
       acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
     }
     const float inv = 1.f / wsum;
-    uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)q * a.D + h * a.hd + c4 * 4);
+    uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)q * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
     *dst = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   }
   __syncthreads();

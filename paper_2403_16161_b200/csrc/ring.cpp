@@ -8,15 +8,25 @@
 
 namespace vi {
 
-Ring::Ring(int mem_frames, int max_new)
-    : M(mem_frames), T_max(max_new), S(mem_frames + max_new),
-      slot_id(size_t(mem_frames + max_new), -1), refined(size_t(mem_frames + max_new), 0) {}
+Ring::Ring(int mem_frames, int max_new, int ref_rate, int max_refs)
+    : M(mem_frames), T_max(max_new), S(mem_frames + max_new), r(max_refs > 0 ? ref_rate : 0),
+      R(ref_rate > 0 ? max_refs : 0), slot_id(size_t(mem_frames + max_new + (ref_rate > 0 ? max_refs : 0)), -1),
+      refined(slot_id.size(), 0) {}
 
 uint64_t Ring::valid_mask() const {
   uint64_t m = 0;
-  for (int s = 0; s < S; ++s)
+  for (int s = 0; s < slots(); ++s)
     if (slot_id[s] >= 0) m |= (uint64_t(1) << s);
   return m;
+}
+
+int Ring::slot_of(int64_t id) const {
+  if (id < 0) return -1;
+  const int s = int(id % S);
+  if (slot_id[s] == id) return s;
+  for (int k = S; k < S + R; ++k)
+    if (slot_id[k] == id) return k;
+  return -1;
 }
 
 int32_t Ring::check_past(int64_t id) const {
@@ -26,30 +36,55 @@ int32_t Ring::check_past(int64_t id) const {
   return kOk;
 }
 
-int64_t Ring::push(int n, std::vector<int64_t>* evicted, std::vector<int64_t>* commits) {
+int64_t Ring::push(int n, std::vector<int64_t>* evicted, std::vector<int64_t>* commits, std::vector<Move>* moves) {
   const int64_t f = next_id;
-  // 1. leave the window [f-M, f-1]
+  // 1. leave the span [f-M, f-1]: to a reference slot (id a multiple of r) or out
+  std::vector<std::pair<int64_t, int>> leaving;   // (id, span slot), ascending ids
+  for (int s = 0; s < S; ++s)
+    if (slot_id[s] >= 0 && slot_id[s] < f - M) leaving.push_back({slot_id[s], s});
+  std::sort(leaving.begin(), leaving.end());
   std::vector<int64_t> gone;
-  for (int s = 0; s < S; ++s) {
-    if (slot_id[s] >= 0 && slot_id[s] < f - M) {
-      gone.push_back(slot_id[s]);
-      slot_id[s] = -1;
-      refined[s] = 0;
+  for (const auto& lv : leaving) {
+    const int64_t id = lv.first;
+    const int s = lv.second;
+    if (r > 0 && id % r == 0) {
+      int dst = -1;
+      for (int k = S; k < S + R && dst < 0; ++k)
+        if (slot_id[k] < 0) dst = k;
+      if (dst < 0) {                      // all reference slots taken: the oldest leaves
+        int oldest = S;
+        for (int k = S + 1; k < S + R; ++k)
+          if (slot_id[k] < slot_id[oldest]) oldest = k;
+        gone.push_back(slot_id[oldest]);
+        pending.erase(std::remove(pending.begin(), pending.end(), slot_id[oldest]), pending.end());
+        slot_id[oldest] = -1;
+        refined[oldest] = 0;
+        dst = oldest;
+      }
+      slot_id[dst] = id;
+      refined[dst] = refined[s];
+      if (moves) moves->push_back({id, s, dst});
+    } else {
+      gone.push_back(id);
     }
+    slot_id[s] = -1;
+    refined[s] = 0;
   }
   std::sort(gone.begin(), gone.end());
   // 2. queued commits for frames still resident are applied now
   std::vector<int64_t> apply;
   std::sort(pending.begin(), pending.end());
-  for (int64_t id : pending)
-    if (resident(id)) {
+  for (int64_t id : pending) {
+    const int s = slot_of(id);
+    if (s >= 0) {
       apply.push_back(id);
-      refined[slot_of(id)] = 1;
+      refined[s] = 1;
     }
+  }
   pending.clear();
   // 3. the new chunk
   for (int i = 0; i < n; ++i) {
-    const int s = slot_of(f + i);
+    const int s = int((f + i) % S);
     slot_id[s] = f + i;
     refined[s] = 0;
   }
@@ -83,17 +118,23 @@ int32_t Ring::commit(int64_t id) {
 
 struct vi_ring {
   vi::Ring r;
-  vi_ring(int m, int t) : r(m, t) {}
+  vi_ring(int m, int t, int rr, int R) : r(m, t, rr, R) {}
 };
 
 extern "C" {
 
-vi_status vi_ring_create(vi_ring** out, int mem_frames, int max_new_frames) {
+vi_status vi_ring_create_ex(vi_ring** out, int mem_frames, int max_new_frames, int ref_rate, int max_ref_frames) {
   if (!out) return VI_E_ARG;
   *out = nullptr;
-  if (mem_frames < 0 || max_new_frames < 1 || mem_frames + max_new_frames > 64) return VI_E_ARG;
-  *out = new (std::nothrow) vi_ring(mem_frames, max_new_frames);
+  if (mem_frames < 0 || max_new_frames < 1 || ref_rate < 0 || max_ref_frames < 0 ||
+      mem_frames + max_new_frames + (ref_rate > 0 ? max_ref_frames : 0) > 64)
+    return VI_E_ARG;
+  *out = new (std::nothrow) vi_ring(mem_frames, max_new_frames, ref_rate, max_ref_frames);
   return *out ? VI_OK : VI_E_OOM;
+}
+
+vi_status vi_ring_create(vi_ring** out, int mem_frames, int max_new_frames) {
+  return vi_ring_create_ex(out, mem_frames, max_new_frames, 0, 0);
 }
 
 vi_status vi_ring_destroy(vi_ring* r) {
@@ -123,7 +164,7 @@ vi_status vi_ring_mark_stepped(vi_ring* r) {
 
 vi_status vi_ring_state(const vi_ring* r, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask) {
   if (!r) return VI_E_ARG;
-  for (int s = 0; s < r->r.S; ++s) {
+  for (int s = 0; s < r->r.slots(); ++s) {
     if (slot_id) slot_id[s] = r->r.slot_id[s];
     if (refined) refined[s] = r->r.refined[s];
   }

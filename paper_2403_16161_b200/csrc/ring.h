@@ -6,6 +6,12 @@
 // S = M + T_max, which is collision-free because the resident ids always span at most
 // M + n <= S consecutive values.  Refined commits (Eq. 4; reading Q13) are
 // queued and applied at the next push.
+//
+// Reference frames (Eq. 3's M_{1,r}^{f-1}; SPEC select_memory S:458-466,
+// reading Q12): with a sampling rate r > 0, a frame whose id is a multiple of r does not
+// leave the memory when it leaves the span; it moves to one of R reference slots
+// (slots S .. S+R-1; the lowest free one) and stays until R newer references push it out
+// (the oldest goes first).  The K/V rows move with it (the engine copies them at push).
 #pragma once
 #include <cstdint>
 #include <vector>
@@ -15,26 +21,34 @@ namespace vi {
 enum : int32_t { kOk = 0, kNotResident = 1, kEArg = -1, kEProtocol = -4 };
 
 struct Ring {
-  int M = 0, T_max = 1, S = 1;
+  int M = 0, T_max = 1, S = 1;     // span, chunk size, span slots
+  int r = 0, R = 0;                // reference sampling rate (0 = none), reference slots
   int64_t next_id = 0;    // id the next push starts at
   int64_t cur_first = 0;  // first id of the chunk pushed last
   int cur_n = 0;
   bool stepped = false;   // the chunk pushed last has been through every block
-  std::vector<int64_t> slot_id;   // -1 = empty
+  std::vector<int64_t> slot_id;   // [S + R], -1 = empty
   std::vector<uint8_t> refined;
   std::vector<int64_t> pending;   // frame ids with a queued commit (applied at push)
 
-  Ring(int mem_frames, int max_new);
+  struct Move {                    // a frame becoming a reference: its rows go src -> dst slot
+    int64_t id;
+    int src, dst;
+  };
+
+  Ring(int mem_frames, int max_new, int ref_rate = 0, int max_refs = 0);
+  int slots() const { return S + R; }
   uint64_t valid_mask() const;
-  int slot_of(int64_t id) const { return int(id % S); }
-  bool resident(int64_t id) const {
-    return id >= 0 && id < next_id && slot_id[slot_of(id)] == id;
-  }
+  // slot of a resident frame, or -1
+  int slot_of(int64_t id) const;
+  bool resident(int64_t id) const { return id >= 0 && id < next_id && slot_of(id) >= 0; }
   // Status of evict/commit for `id` (kOk = allowed).
   int32_t check_past(int64_t id) const;
-  // push: returns first id; fills evicted ids (ascending) and the commits to apply now
-  // (ascending ids, each still resident).  n must be in [1, T_max] (checked by caller).
-  int64_t push(int n, std::vector<int64_t>* evicted, std::vector<int64_t>* commits_to_apply);
+  // push: returns first id; fills the ids that left the memory (ascending), the commits
+  // to apply now (ascending ids, each still resident) and the reference moves (in order).
+  // n must be in [1, T_max] (checked by caller).
+  int64_t push(int n, std::vector<int64_t>* evicted, std::vector<int64_t>* commits_to_apply,
+               std::vector<Move>* moves = nullptr);
   int32_t evict(int64_t id);
   int32_t commit(int64_t id);
   void mark_stepped() { stepped = true; }

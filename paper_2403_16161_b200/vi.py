@@ -34,7 +34,7 @@ EXPORTS = ["vi_config_default", "vi_create", "vi_create_ex", "vi_destroy", "vi_s
            "vi_stream", "vi_debug_read", "vi_ring_create", "vi_ring_destroy", "vi_ring_push", "vi_ring_evict",
            "vi_ring_commit", "vi_ring_mark_stepped", "vi_ring_state", "vi_version", "vi_memory_step_attn",
            "vi_memory_step_ffn", "vi_tp_layout", "vi_tp_unique_id", "vi_tp_local_allgather", "vi_memory_footprint",
-           "vi_memory_read"]
+           "vi_memory_read", "vi_ring_create_ex"]
 
 
 class ViConfig(C.Structure):
@@ -42,7 +42,8 @@ class ViConfig(C.Structure):
         "layers", "heads", "d_model", "tokens_per_frame", "mem_frames", "max_new_frames",
         "feat_h", "feat_w", "feat_c", "kh", "kw", "sh", "sw", "ph", "pw",
         "ffn_hidden", "ffn_kind", "dtype", "pos_embed", "device")] + [("stream", C.c_void_p)] + [
-        ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p), ("stream_priority", C.c_int)]
+        ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p), ("stream_priority", C.c_int),
+        ("ref_rate", C.c_int), ("max_ref_frames", C.c_int)]
 
 
 WEIGHT_FIELDS = ("embed_w", "embed_b", "pos", "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b",
@@ -76,6 +77,7 @@ _sig = {
     "vi_stream": (_P, [_P]),
     "vi_debug_read": (C.c_int32, [_P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
     "vi_ring_create": (C.c_int32, [C.POINTER(_P), C.c_int, C.c_int]),
+    "vi_ring_create_ex": (C.c_int32, [C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int]),
     "vi_ring_destroy": (C.c_int32, [_P]),
     "vi_ring_push": (C.c_int32, [_P, C.c_int, _I64P, _I64P, C.POINTER(C.c_int)]),
     "vi_ring_evict": (C.c_int32, [_P, C.c_int64]),
@@ -128,13 +130,13 @@ def _ptr(x) -> Optional[int]:
 class Ring:
     """vi_ring_*: the integer ring bookkeeping every context uses, without a GPU."""
 
-    def __init__(self, mem_frames: int, max_new_frames: int):
+    def __init__(self, mem_frames: int, max_new_frames: int, ref_rate: int = 0, max_refs: int = 0):
         h = _P()
-        st = _lib.vi_ring_create(C.byref(h), mem_frames, max_new_frames)
+        st = _lib.vi_ring_create_ex(C.byref(h), mem_frames, max_new_frames, ref_rate, max_refs)
         if st != VI_OK:
-            raise ViError(st, "vi_ring_create")
+            raise ViError(st, "vi_ring_create_ex")
         self._h = h
-        self.S = mem_frames + max_new_frames
+        self.S = mem_frames + max_new_frames + (max_refs if ref_rate > 0 and max_refs > 0 else 0)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -232,7 +234,8 @@ class Context:
                    ffn_hidden=c.ffn_hidden, ffn_kind=c.ffn_kind,
                    dtype=DTYPE_BF16 if c.dtype == "bf16" else DTYPE_FP32, pos_embed=c.pos_embed,
                    device=device, stream=stream, tp_size=tp_size, tp_rank=tp_rank, nccl_id=nccl_id,
-                   stream_priority=stream_priority)
+                   stream_priority=stream_priority, ref_rate=getattr(c, "ref_rate", 0),
+                   max_ref_frames=getattr(c, "max_refs", 0))
 
     def close(self):
         if getattr(self, "_h", None):

@@ -114,3 +114,40 @@ def test_create_validates_config_before_touching_the_gpu(V):
     with pytest.raises(V.ViError) as e:
         V.Context(sh=9, kh=7, feat_h=60, tokens_per_frame=7 * 36)   # stride > kernel: uncovered cells
     assert e.value.status == V.VI_E_CONFIG
+
+
+def test_ring_with_references_matches_oracle_random_traces(V):
+    """Reference slots (Eq. 3 M_{1,r}, reading Q12): slot table, refined bits, moves and
+    evictions bit-exact against the oracle's set model, including explicit evictions and
+    commits of reference frames."""
+    rnd = random.Random(99)
+    for trial in range(300):
+        M, T = rnd.randint(0, 8), rnd.randint(1, 4)
+        rr, R = rnd.randint(1, 6), rnd.randint(1, 4)
+        r, m = V.Ring(M, T, rr, R), O.OracleMemory(M, T, ref_rate=rr, max_refs=R)
+        for step in range(60):
+            x = rnd.random()
+            if x < 0.45:
+                n = rnd.randint(1, T)
+                assert r.push(n) == m.push(n), (trial, step)
+            elif x < 0.6:
+                r.mark_stepped(); m.mark_stepped()
+            elif x < 0.75:
+                fid = rnd.randint(-1, m.next_id + 1)
+                assert r.evict(fid) == m.evict(fid), (trial, step, fid)
+            else:
+                fid = rnd.randint(-1, m.next_id + 1)
+                assert r.commit(fid) == m.commit(fid, None), (trial, step, fid)
+            assert r.state() == tuple(list(x) if isinstance(x, list) else x for x in m.state()), (trial, step)
+
+
+def test_ring_reference_golden_spec(V):
+    """SPEC S:464 select_memory(18, 5, 10): at frame 18 the memory holds 13..17 and the
+    references 0 and 10."""
+    r = V.Ring(5, 1, 10, 2)
+    for f in range(19):
+        r.push(1)
+        r.mark_stepped()
+    sid, _, _ = r.state()
+    assert sorted(x for x in sid if x >= 0) == [0, 10, 13, 14, 15, 16, 17, 18]
+    assert sid[6:] in ([0, 10], [10, 0])          # the two reference slots follow the 6 span slots

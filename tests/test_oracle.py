@@ -472,3 +472,60 @@ def test_round_bf16_is_rne():
     x = np.array([1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -2.5, 3.4e38], np.float32)
     ref = torch.from_numpy(x).to(torch.bfloat16).to(torch.float32).numpy()
     assert np.array_equal(round_bf16(x), ref)
+
+
+# ---------------------------------------------------------------- reference frames (Eq. 3 M_{1,r})
+
+def _select_memory(f, s, r, R):
+    """SPEC select_memory, written out: neighbours [max(0, f-s), f-1]; references =
+    multiples of r in [0, f-1] minus the neighbours -- of which the memory keeps the R most
+    recent (DESIGN reading Q12)."""
+    nb = set(range(max(0, f - s), f))
+    refs = sorted(j for j in range(0, f) if r > 0 and j % r == 0 and j not in nb)
+    return nb, set(refs[-R:] if R > 0 else [])
+
+
+def test_reference_golden_spec_select_memory():
+    """select_memory(18, 5, 10) -> neighbours {13..17}, references {0, 10}."""
+    m = O.OracleMemory(5, 1, ref_rate=10, max_refs=4)
+    for f in range(19):
+        m.push(1)
+        m.mark_stepped()
+    assert m.window() == [0, 10, 13, 14, 15, 16, 17]
+    nb, refs = _select_memory(18, 5, 10, 4)
+    assert set(m.window()) == nb | refs
+
+
+def test_reference_window_matches_spec_sets_and_cap():
+    for s, r, R in ((3, 4, 2), (5, 10, 4), (2, 3, 1), (4, 2, 3)):
+        m = O.OracleMemory(s, 1, ref_rate=r, max_refs=R)
+        for f in range(40):
+            m.push(1)
+            nb, refs = _select_memory(f, s, r, R)
+            assert set(m.window()) == nb | refs, (s, r, R, f)
+            m.mark_stepped()
+
+
+def test_reference_memory_step_equals_masked_joint_pass():
+    """Exact memoisation with references: T=1 memory steps with span s and references every r
+    frames (R kept) == one joint pass where frame i's queries see exactly select_memory(i) and
+    itself (the recurrence of Eq. 3 with M_{f-s}^{f-1} U M_{1,r}^{f-1})."""
+    s, r, R, n = 2, 3, 2, 9
+    cfg = CONFIGS["C1"].replace(layers=2, mem_frames=s, ref_rate=r, max_refs=R)
+    w = make_weights(cfg, seed=7, variant="sensitive")
+    feats = make_features(cfg, n, seed=7)
+    mask = np.zeros((n, n), bool)
+    for i in range(n):
+        nb, refs = _select_memory(i, s, r, R)
+        for j in nb | refs | {i}:
+            mask[i, j] = True
+    joint = O.joint_forward(feats, w, cfg, mode="mask", frame_mask=mask)
+    st = O.OracleStream(cfg, w)
+    for i in range(n):
+        st.push(1)
+        out, _ = st.step(feats[i:i + 1])
+        np.testing.assert_allclose(out[0], joint["out"][i], rtol=1e-9, atol=1e-11)
+    # the references matter: without them frame 8 (refs {0, 3}) differs
+    plain = O.joint_forward(feats, w, cfg, mode="mask",
+                            frame_mask=np.array([[j <= i and j >= i - s for j in range(n)] for i in range(n)]))
+    assert np.abs(plain["out"][8] - joint["out"][8]).max() > 1e-6

@@ -49,6 +49,8 @@ class Config:
     mem_frames: int        # M, the memory span s of Eq. 3
     dtype: str             # "bf16" (tensor-core path) or "fp32" (SIMT path)
     pos_embed: int = 0
+    ref_rate: int = 0      # r of Eq. 3's reference frames M_{1,r} (0 = span only)
+    max_refs: int = 0      # reference slots kept (the oldest reference leaves first)
 
     @property
     def oh(self) -> int:
@@ -72,7 +74,7 @@ class Config:
 
     @property
     def slots(self) -> int:
-        return self.mem_frames + self.t_new
+        return self.mem_frames + self.t_new + (self.max_refs if self.ref_rate > 0 else 0)
 
     def replace(self, **kw) -> "Config":
         return dataclasses.replace(self, **kw)
