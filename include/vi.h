@@ -227,7 +227,8 @@ vi_status vi_refine_commit(vi_ctx* ctx, int64_t frame_id, const void* k, const v
  * VI_NOT_RESIDENT if the frame left the memory. */
 vi_status vi_memory_read(vi_ctx* ctx, int64_t frame_id, void* k, void* v);
 
-/* Host snapshot of the ring: slot_id[S] (-1 = empty), refined[S] (0/1), valid bitmask
+/* Host snapshot of the ring: slot_id[N] (-1 = empty), refined[N] (0/1), N = vi_num_slots
+ * (the S = mem_frames + max_new_frames span slots, then the reference slots), valid bitmask
  * (bit s = slot s holds a resident frame).  Any pointer may be NULL. */
 vi_status vi_memory_state(vi_ctx* ctx, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask);
 
@@ -247,7 +248,7 @@ int64_t vi_kernel_launches(const vi_ctx* ctx);
  * memory of all blocks (2 L S P Dl elements, V rows padded to vt_ld); total_bytes = every
  * device buffer the context owns (weights, memory, workspaces).  Either may be NULL. */
 vi_status vi_memory_footprint(const vi_ctx* ctx, int64_t* slab_bytes, int64_t* total_bytes);
-/* Ring slot count S and the ctx stream (cudaStream_t). */
+/* Ring slot count (span + reference slots) and the ctx stream (cudaStream_t). */
 int vi_num_slots(const vi_ctx* ctx);
 void* vi_stream(const vi_ctx* ctx);
 

@@ -1,0 +1,3 @@
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/t14_build.log 2>&1 || exit 1
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/t14_pytest.log 2>&1; echo "rc=$?" >> gpurun_out/t14_pytest.log
