@@ -43,6 +43,26 @@ WORKLOADS = {"C3": "FuseFormer-shaped memory step (BASELINE.json configs[2])",
              "C2": "STTN-shaped memory step (BASELINE.json configs[1])"}
 
 
+def gemm_flop_per_step(cfg):
+    """Algorithmic GEMM FLOPs of one step (the back-projection's hi/lo split not counted)."""
+    M, D, F, Pd, L = cfg.t_new * cfg.tokens, cfg.d_model, cfg.ffn_hidden, cfg.patch_dim, cfg.layers
+    return 2.0 * M * (D * Pd + L * (3 * D * D + D * D + 2 * F * D) + Pd * D)
+
+
+def patch_bytes_per_step(cfg):
+    """Algorithmic HBM bytes of the patch kernels of one step (bf16 features/tokens, fp32 Yp
+    and F3N hidden): split, composite and, for F3N, the fold/unfold of every block."""
+    T, P, Pd = cfg.t_new, cfg.tokens, cfg.patch_dim
+    fmap = T * cfg.feat_h * cfg.feat_w * cfg.feat_c * 2
+    b = fmap + T * P * Pd * 2                       # split: read features, write tokens
+    b += T * P * Pd * 4 + fmap                      # composite: read fp32 Yp, write features
+    if cfg.ffn_kind == 1:
+        C = cfg.ffn_hidden // (cfg.kh * cfg.kw)
+        fold = T * cfg.feat_h * cfg.feat_w * C * 4
+        b += cfg.layers * ((T * P * cfg.ffn_hidden * 4 + fold) + (fold + T * P * cfg.ffn_hidden * 2))
+    return float(b)
+
+
 def workload_config(cfg, args=None, world=1):
     return {"workload": f"{cfg.name}: {WORKLOADS[cfg.name]}",
             "layers": cfg.layers, "heads": cfg.heads, "d_model": cfg.d_model, "tokens_per_frame": cfg.tokens,
@@ -175,7 +195,8 @@ def run_ours(args, cfg):
     else:
         ctx = vi.Context.from_synth(cfg, device=local)   # one independent live stream per GPU
         n_streams = world
-    ctx.set_weights(make_weights(cfg, seed=0))
+    w = make_weights(cfg, seed=0)
+    ctx.set_weights(w)
     stream = torch.cuda.ExternalStream(ctx.stream())
     dt = torch.bfloat16
     nchunks = 4
@@ -225,6 +246,35 @@ def run_ours(args, cfg):
     e2e_s = time.perf_counter() - t0
     clk = clocks.stop()
 
+    # secondary rooflines and determinism (outside the timed region): the GEMMs' own device
+    # time (self-timing inside the graph), the HBM-bound patch kernels' (CUDA events around
+    # eager launches), and two replays of one step compared bitwise (no atomics anywhere)
+    extra_steps = 20
+    sub = {}
+    for mode in (3, 2):
+        ctx.profile(mode)
+        ctx.profile_read()
+        for k in range(extra_steps):
+            with torch.cuda.stream(stream):
+                flush.fill_(float(k))
+            ctx.run_step(feats[k % nchunks], T, out)
+        sub[mode] = ctx.profile_read()
+    ctx.profile(0)
+    # run-to-run determinism: two fresh contexts, the same weights and frames -> bitwise
+    # identical outputs after the memory is full (no atomics on the path)
+    outs = []
+    for _ in range(2):
+        c2 = vi.Context.from_synth(cfg, device=local, tp_size=world if args.tp else 1, tp_rank=rank if args.tp else 0,
+                                   nccl_id=nccl_id if args.tp else None)
+        c2.set_weights(w)
+        o2 = torch.empty_like(out)
+        for k in range(math.ceil(cfg.mem_frames / T) + 2):
+            c2.run_step(feats[k % nchunks], T, o2)
+        c2.sync()
+        outs.append(o2)
+        c2.close()
+    deterministic = bool(torch.equal(outs[0], outs[1]))
+
     total_ms, e2e_s = streams.max_over_ranks([total_ms, e2e_s], torch.device("cuda", local))
     value = streams.aggregate_fps(T * args.steps, n_streams, total_ms / 1e3)
     e2e_value = streams.aggregate_fps(T * e2e_steps, n_streams, e2e_s)
@@ -262,6 +312,17 @@ def run_ours(args, cfg):
     }
     line["device_time_ms_per_step"] = {"attention": attn_ms / args.steps, "gemm": prof["gemm"][0] / args.steps,
                                        "other": (total_ms - attn_ms - prof["gemm"][0]) / args.steps}
+    gemm_ms = sub[3]["gemm"][0] / extra_steps
+    patch_ms = sub[2]["patch"][0] / extra_steps
+    gflop, pbytes = gemm_flop_per_step(cfg) / (world if args.tp else 1), patch_bytes_per_step(cfg)
+    line["secondary_rooflines"] = {
+        "gemms (embed, QKV, O, FFN1, FFN2, back; self-timed in the graph)": {
+            "bound": "tensor", "achieved": gflop / (gemm_ms * 1e-3) / 1e12, "peak": bf16_peak, "unit": "TFLOP/s",
+            "frac": gflop / (gemm_ms * 1e-3) / 1e12 / bf16_peak, "flop_per_step": gflop, "ms_per_step": gemm_ms},
+        "patch kernels (soft split, F3N fold/unfold, soft composite; eager launches, CUDA events)": {
+            "bound": "hbm", "achieved": pbytes / (patch_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
+            "frac": pbytes / (patch_ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": pbytes, "ms_per_step": patch_ms}}
+    line["deterministic"] = deterministic
     if os.environ.get("VI_PROFILE_MODE") == "2":
         line["profile_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}
         line["profile_launches_per_step"] = {k: v[1] / args.steps for k, v in prof.items()}

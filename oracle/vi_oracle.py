@@ -244,9 +244,22 @@ def qkv(x: np.ndarray, w, l: int, cfg):
 # keys/values = memory frames (span s) + the new frames.
 # ----------------------------------------------------------------------------------
 
+def token_windows(cfg) -> Optional[np.ndarray]:
+    """Window id of every token of a frame for window attention (E2FGVI-style, BASELINE
+    configs[3]: non-overlapping win_h x win_w token windows on the oh x ow token grid, row-major
+    window order), or None for global attention (cfg.win_h = 0)."""
+    wh, ww = getattr(cfg, "win_h", 0), getattr(cfg, "win_w", 0)
+    if not wh:
+        return None
+    oy, ox = np.divmod(np.arange(cfg.tokens), cfg.ow)
+    return (oy // wh) * (cfg.ow // ww) + (ox // ww)
+
+
 def block_memory(x: np.ndarray, mem_kv: Sequence[Tuple[np.ndarray, np.ndarray]], w, l: int, cfg,
                  n_frames: int, chunk_causal: bool = False) -> Tuple[np.ndarray, Dict[str, np.ndarray]]:
-    """x [n*P, D] = block-l input of the chunk; mem_kv = [(K_j, V_j)] in frame-id order."""
+    """x [n*P, D] = block-l input of the chunk; mem_kv = [(K_j, V_j)] in frame-id order.
+    With window attention (cfg.win_h > 0) a query sees only the keys of its own token window,
+    in every frame of the memory and the chunk."""
     P = cfg.tokens
     h1, Q, Kc, Vc = qkv(x, w, l, cfg)
     K = np.concatenate([k for k, _ in mem_kv] + [Kc], axis=0)
@@ -257,6 +270,12 @@ def block_memory(x: np.ndarray, mem_kv: Sequence[Tuple[np.ndarray, np.ndarray]],
         qf = np.repeat(np.arange(n_frames), P)
         kf = np.concatenate([np.full(nm, -1), np.repeat(np.arange(n_frames), P)])
         allowed = kf[None, :] <= qf[:, None]
+    win = token_windows(cfg)
+    if win is not None:
+        wq = np.tile(win, n_frames)
+        wk = np.tile(win, len(mem_kv) + n_frames)
+        same = wq[:, None] == wk[None, :]
+        allowed = same if allowed is None else (allowed & same)
     O, lse = attention(Q, K, V, cfg.heads, allowed=allowed, return_lse=True)
     xa = x + linear(O, w["wo"][l], w["bo"][l])
     h2 = layer_norm(xa, w["ln2_g"][l], w["ln2_b"][l])

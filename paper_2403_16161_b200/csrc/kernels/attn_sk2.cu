@@ -299,8 +299,11 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           }
           tmem_st16(TS + hf * 64 + c * 16, pk);   // P keys [hf*64, +64) -> packed cols [hf*64, +32)
         }
-        // O rescale after P (S registers dead by now); PV(j-1) is complete (s_full implies it)
-        if (__any_sync(0xffffffffu, grow) && j > 0) {   // PV(j-1) done (s_full implies it)
+        // O rescale after P (S registers dead by now); PV(j-1) is complete (s_full implies it).
+        // The PV MMAs of EITHER key half accumulate into all O columns, so both warps of the
+        // pair (same row maxima, same decision) finish their column half before either one
+        // hands its P half over.  Rare (lazy threshold 2^8).
+        if (__any_sync(0xffffffffu, grow) && j > 0) {
 #pragma unroll 1
           for (int c = 0; c < OH; c += 32) {
             uint32_t r[32];
@@ -310,6 +313,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
             tmem_st32(TO + hf * OH + c, r);
           }
+          tmem_wait_st();
+          sk2_named_bar_sync(pair_bar, 64);
         }
         tmem_wait_st();
         tc_fence_before();

@@ -1,22 +1,26 @@
 // tcgen05 GEMM with fused epilogues: C[M][N] = A[M][K] * W[N][K]^T (bf16 in, fp32 acc).
 //
-// Persistent, warp-specialised, in clusters of CM x CN CTAs: a cluster owns CM x CN
-// adjacent 128 x BN output tiles (a "super-tile") and walks super-tiles cid, cid + #clusters,
-// ...  The A tile (128 rows x 64 k) of a cluster row is loaded in CN slices, each CTA of the
-// row loading one slice and TMA-multicasting it to the row; the W tile of a cluster column
-// likewise in CM slices.  At M = 3600 the operands are re-read once per tile from L2, so
-// multicast is what keeps these GEMMs off the L2 bandwidth ceiling.  A stage is refilled
-// only after every CTA of the cluster has consumed it (tcgen05.commit multicast to all).
-// Warp roles (384 threads):
-//   warp 0, lane 0 : TMA producer  (A box 64x128, W box 64xBN, 128-byte swizzle), an
-//                    STAGES-deep smem ring that keeps streaming across tile boundaries
-//   warp 1, lane 0 : MMA issuer    (tcgen05.mma kind::f16, M=128, N=BN, K=16 per instr)
+// Persistent and warp-specialised, in two modes:
+//   single CTA   : a CTA owns 128 x BN output tiles and walks tiles blockIdx.x, +gridDim.x, ...
+//   CTA pair     : a cluster of 2 CTAs owns 256 x BN tiles and computes them with the 2-SM
+//                  MMA (tcgen05.mma.cta_group::2, M = 256): each CTA loads its 128 rows of A
+//                  and HALF of the BN rows of W into its own shared memory, the leader (rank
+//                  0) issues the MMAs, each CTA's TMEM receives its 128 accumulator rows.
+//                  Per SM the operand bytes per MMA cycle drop from (128 + BN)/(2 BN) x 128 B
+//                  to (128 + BN/2)/(2 BN) x 128 B -- the per-SM ingress (~60-80 B/clk
+//                  measured, tools/micro/gemm_micro) bounds the single-CTA K = 512 GEMMs.
+// Warp roles (384 threads per CTA):
+//   warp 0, lane 0 : TMA producer  (A box 64x128, W box 64x(BN or BN/2), 128-byte swizzle),
+//                    a STAGES-deep smem ring that keeps streaming across tile boundaries;
+//                    in pair mode both CTAs load, completion counted on the leader's barrier
+//   warp 1, lane 0 : MMA issuer    (tcgen05.mma kind::f16, M = 128 or 256, N = BN, K = 16)
 //   warp 2         : TMEM allocator (2 x BN fp32 columns: double-buffered accumulator)
 //   warps 4..11    : epilogue      (tcgen05.ld 32x32b, thread = accumulator row; warps w and
 //                    w+4 share a TMEM lane quadrant and split the tile's columns in half)
-// With two accumulators the epilogue of tile i overlaps the mainloop of tile i+1.  The
-// bias of a tile is staged in shared memory (broadcast reads) and residual rows are
-// loaded before the TMEM load is waited on, so the epilogue keeps pace with the MMAs.
+// With two accumulators the epilogue of tile i overlaps the mainloop of tile i+1.  TE: the
+// STORE / GELU / RESID epilogues leave through per-warp swizzled staging buffers and TMA
+// bulk tensor stores (residual tiles arrive by TMA loads); otherwise (the QKV memory
+// scatter) from registers (epilogue.cuh).
 #include "epilogue.cuh"
 #include "kernels.h"
 
@@ -26,10 +30,10 @@ __device__ __forceinline__ void gemm_named_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-template <int BN, int STAGES, bool TE = false>
-struct GemmSmem {  // (cluster shape does not change the layout)
+template <int BN, int STAGES, bool PAIR, bool TE>
+struct GemmSmem {
   static constexpr int A_BYTES = 128 * 64 * 2;
-  static constexpr int B_BYTES = BN * 64 * 2;
+  static constexpr int B_BYTES = (PAIR ? BN / 2 : BN) * 64 * 2;
   static constexpr int STAGE_BYTES = A_BYTES + B_BYTES;
   // TMA-store epilogue: per epilogue warp two 32-row x 128-byte staging buffers (1 KB aligned
   // for the 128-byte swizzle of the output tensor maps)
@@ -48,38 +52,31 @@ __device__ long long g_gemm_trace[24];
 #define GTR(i) do { } while (0)
 #endif
 
-template <int BN, int STAGES, int CM, int CN, bool TE>
+template <int BN, int STAGES, bool PAIR, bool TE>
 __global__ void __launch_bounds__(384, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmX, int K, int brow0,
                Epi epi) {
-  using L = GemmSmem<BN, STAGES, TE>;
-  constexpr int CS = CM * CN;
+  using L = GemmSmem<BN, STAGES, PAIR, TE>;
+  constexpr int TM = PAIR ? 256 : 128;                 // rows of a (pair) tile
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays in .shared
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;     // [2] accumulator ready for the epilogue
-  uint64_t* tempty = tfull + 2;         // [2] accumulator drained by the epilogue
+  uint64_t* tempty = tfull + 2;         // [2] accumulator drained by the epilogue (leader's counts both CTAs)
   uint64_t* xbar = tempty + 2;          // [8] per epilogue warp: x_in tile landed (TE, EPI_RESID)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GTR(0);
-  const int rank = CS > 1 ? int(cluster_ctarank()) : 0;
-  const int cx = rank % CN, cy = rank / CN;           // position inside the cluster
-  const int cid = blockIdx.x / CS, ncl = gridDim.x / CS;
-  const int tiles_m = (epi.M + 127) / 128, tiles_n = (epi.N + BN - 1) / BN;
-  const int super_m = (tiles_m + CM - 1) / CM, super_n = (tiles_n + CN - 1) / CN;
-  const int nsuper = super_m * super_n;
+  const int rank = PAIR ? int(cluster_ctarank()) : 0;
+  const bool leader = rank == 0;
+  const int cid = PAIR ? blockIdx.x / 2 : blockIdx.x, ncl = PAIR ? gridDim.x / 2 : gridDim.x;
+  const int tiles_m = (epi.M + TM - 1) / TM, tiles_n = (epi.N + BN - 1) / BN;
+  const int ntiles = tiles_m * tiles_n;
   const int nk = (K + 63) / 64;
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
-  constexpr int A_SLICE = L::A_BYTES / CN, B_SLICE = L::B_BYTES / CM;
-  const uint16_t row_mask = uint16_t(((1u << CN) - 1) << (cy * CN));
-  uint16_t col_mask = 0;
-#pragma unroll
-  for (int y = 0; y < CM; ++y) col_mask |= uint16_t(1u << (y * CN + cx));
-  const uint16_t all_mask = uint16_t((1u << CS) - 1);
 
   if (warp == 0 && lane == 0) {
     tma_prefetch(&tmA);
@@ -90,18 +87,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&empty[s], CS);
+      mbar_init(&empty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tfull[b], 1);
-      mbar_init(&tempty[b], 256);
+      mbar_init(&tempty[b], PAIR ? 16 : 8);     // one elected arrive per epilogue warp (of both CTAs)
     }
     for (int w = 0; w < 8; ++w) mbar_init(&xbar[w], 1);
     fence_barrier_init();
   }
-  if (warp == 2) tmem_alloc(tmem_slot, TMEM_COLS);
+  if (warp == 2) {
+    if (PAIR) tmem_alloc_pair(tmem_slot, TMEM_COLS);
+    else tmem_alloc(tmem_slot, TMEM_COLS);
+  }
   tc_fence_before();
-  if (CS > 1) cluster_sync_all();   // peers' barriers initialised before any multicast
+  if (PAIR) cluster_sync_all();   // both CTAs' barriers initialised and TMEM allocated
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
@@ -114,36 +114,36 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (warp == 0) {
     if (lane == 0) {
       int it = 0;                               // global k-block counter (ring position)
-      for (int st = cid; st < nsuper; st += ncl) {
-        const int m0 = ((st % super_m) * CM + cy) * 128, n0 = ((st / super_m) * CN + cx) * BN;
+      for (int st = cid; st < ntiles; st += ncl) {
+        const int m0 = (st % tiles_m) * TM + rank * 128, n0 = (st / tiles_m) * BN;
+        const int bn0 = brow0 + n0 + (PAIR ? rank * (BN / 2) : 0);
         for (int kb = 0; kb < nk; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
-          mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
           int ak = kb * 64, am = m0;
           if (epi.a_hs > 0) {                   // head-major A: K-block kb of head kb / a_kpb
             const int hh = kb / epi.a_kpb;
             ak = (kb - hh * epi.a_kpb) * 64;
             am = hh * epi.a_hs + m0;
           }
-          if (CN > 1)
-            tma_load_2d_mc(sa + cx * A_SLICE, &tmA, &full[s], ak, am + cx * (128 / CN), row_mask);
-          else
+          if (PAIR) {
+            if (leader) mbar_arrive_expect_tx(&full[s], 2 * L::STAGE_BYTES);   // both CTAs' bytes
+            tma_load_2d_pair(sa, &tmA, &full[s], ak, am);
+            tma_load_2d_pair(sa + L::A_BYTES, &tmB, &full[s], kb * 64, bn0);
+          } else {
+            mbar_arrive_expect_tx(&full[s], L::STAGE_BYTES);
             tma_load_2d(sa, &tmA, &full[s], ak, am);
-          if (CM > 1)
-            tma_load_2d_mc(sa + L::A_BYTES + cy * B_SLICE, &tmB, &full[s], kb * 64, brow0 + n0 + cy * (BN / CM),
-                           col_mask);
-          else
-            tma_load_2d(sa + L::A_BYTES, &tmB, &full[s], kb * 64, brow0 + n0);
+            tma_load_2d(sa + L::A_BYTES, &tmB, &full[s], kb * 64, bn0);
+          }
         }
       }
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      constexpr uint32_t idesc = idesc_bf16_f32(128, BN);
+    if (lane == 0 && leader) {
+      constexpr uint32_t idesc = idesc_bf16_f32(TM, BN);
       int it = 0, lt = 0;
-      for (int st = cid; st < nsuper; st += ncl, ++lt) {
+      for (int st = cid; st < ntiles; st += ncl, ++lt) {
         const int acc = lt & 1;
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
@@ -156,14 +156,17 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           const uint32_t a = smem_u32(smem + s * L::STAGE_BYTES);
           const uint32_t b = a + L::A_BYTES;
 #pragma unroll
-          for (int k = 0; k < 4; ++k)
-            umma_bf16_ss(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
-          if (CS > 1)
-            umma_commit_mc(&empty[s], all_mask);    // stage free in every CTA that shares it
-          else
-            umma_commit(&empty[s]);
+          for (int k = 0; k < 4; ++k) {
+            if (PAIR)
+              umma_bf16_ss_pair(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
+            else
+              umma_bf16_ss(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
+          }
+          if (PAIR) umma_commit_pair(&empty[s]);    // the stage is free in both CTAs
+          else umma_commit(&empty[s]);
         }
-        umma_commit(&tfull[acc]);
+        if (PAIR) umma_commit_pair(&tfull[acc]);
+        else umma_commit(&tfull[acc]);
         if (lt < 4) GTR(3 + lt);
       }
     }
@@ -176,9 +179,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int nchunk = 0;
     uint32_t xphase = 0;
     int lt = 0;
-    for (int st = cid; st < nsuper; st += ncl, ++lt) {
+    for (int st = cid; st < ntiles; st += ncl, ++lt) {
       const int acc = lt & 1;
-      const int m0 = ((st % super_m) * CM + cy) * 128, n0 = ((st / super_m) * CN + cx) * BN;
+      const int m0 = (st % tiles_m) * TM + rank * 128, n0 = (st / tiles_m) * BN;
       float* bs = bias_s + acc * BN;
       if (epi.bias) {
         for (int i = etid; i < BN; i += 256) bs[i] = n0 + i < epi.N ? __ldg(epi.bias + n0 + i) : 0.f;
@@ -255,37 +258,40 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             bulk_commit();
           }
         }
-        tc_fence_before();
-        mbar_arrive(&tempty[acc]);
-        if (lt < 4 && ew == 0 && lane == 0) GTR(11 + lt);
-        continue;
-      }
+      } else {
 #pragma unroll 1
-      for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += 32) {
-        if (n0 + c >= epi.N) break;
-        uint32_t r[32];
-        tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c, r);
-        float4 xin[8];
-        if (epi.kind == EPI_RESID && m < epi.M && n0 + c + 32 <= epi.N) {
-          const float4* xi = reinterpret_cast<const float4*>(epi.x_in + (size_t)m * epi.N + n0 + c);
+        for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += 32) {
+          if (n0 + c >= epi.N) break;
+          uint32_t r[32];
+          tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c, r);
+          float4 xin[8];
+          if (epi.kind == EPI_RESID && m < epi.M && n0 + c + 32 <= epi.N) {
+            const float4* xi = reinterpret_cast<const float4*>(epi.x_in + (size_t)m * epi.N + n0 + c);
 #pragma unroll
-          for (int i = 0; i < 8; ++i) xin[i] = xi[i];
+            for (int i = 0; i < 8; ++i) xin[i] = xi[i];
+          }
+          tmem_wait_ld();
+          epi_row32_bf16(epi, m, n0 + c, reinterpret_cast<float*>(r), epi.bias ? bs + c : nullptr, xin);
         }
-        tmem_wait_ld();
-        epi_row32_bf16(epi, m, n0 + c, reinterpret_cast<float*>(r), epi.bias ? bs + c : nullptr, xin);
       }
+      // accumulator drained: one arrive per warp on the (leader's) barrier
       tc_fence_before();
-      mbar_arrive(&tempty[acc]);
+      __syncwarp();
+      if (lane == 0) {
+        if (PAIR) mbar_arrive_cluster(&tempty[acc], 0);
+        else mbar_arrive(&tempty[acc]);
+      }
       if (lt < 4 && ew == 0 && lane == 0) GTR(11 + lt);
     }
     if (TE && lane == 0) bulk_wait<0>();        // staging buffers stay valid until stored
   }
   tc_fence_before();
-  if (CS > 1) cluster_sync_all();   // no CTA leaves while peers may still multicast into it
+  if (PAIR) cluster_sync_all();   // no CTA leaves while its peer may still use its smem / TMEM
   else __syncthreads();
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, TMEM_COLS);
+    if (PAIR) tmem_dealloc_pair(tmem, TMEM_COLS);
+    else tmem_dealloc(tmem, TMEM_COLS);
   }
   if (threadIdx.x == 0) GTR(15);
   if (threadIdx.x == 0) time_end(epi.timing, gridDim.x);
@@ -293,23 +299,21 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 
 static int g_num_sms = 0;
 
-template <int BN, int STAGES, int CM, int CN, bool TE = false>
+template <int BN, int STAGES, bool PAIR, bool TE>
 static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
-                              const Epi& e, cudaStream_t st, const CUtensorMap* tmo = nullptr,
-                              const CUtensorMap* tmx = nullptr) {
-  using L = GemmSmem<BN, STAGES, TE>;
-  constexpr int CS = CM * CN;
-  auto kfn = gemm_tc_kernel<BN, STAGES, CM, CN, TE>;
+                              const Epi& e, cudaStream_t st, const CUtensorMap* tmo, const CUtensorMap* tmx) {
+  using L = GemmSmem<BN, STAGES, PAIR, TE>;
+  constexpr int CS = PAIR ? 2 : 1;
+  auto kfn = gemm_tc_kernel<BN, STAGES, PAIR, TE>;
   static int max_clusters = 0;
   if (!max_clusters) {
     cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (err != cudaSuccess) return err;
-    if (CS > 1) cudaFuncSetAttribute(kfn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
     int dev = 0;
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
     max_clusters = g_num_sms / CS;
-    if (CS > 1) {
+    if (PAIR) {
       cudaLaunchConfig_t q = {};
       q.gridDim = dim3(CS * max_clusters);
       q.blockDim = dim3(384);
@@ -324,9 +328,9 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
       cudaGetLastError();
     }
   }
-  const int tiles_m = (M + 127) / 128, tiles_n = (N + BN - 1) / BN;
-  const int nsuper = ((tiles_m + CM - 1) / CM) * ((tiles_n + CN - 1) / CN);
-  const int ncl = nsuper < max_clusters ? nsuper : max_clusters;
+  const int TM = PAIR ? 256 : 128;
+  const int ntiles = ((M + TM - 1) / TM) * ((N + BN - 1) / BN);
+  const int ncl = ntiles < max_clusters ? ntiles : max_clusters;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncl * CS);
   cfg.blockDim = dim3(384);
@@ -343,41 +347,40 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   return cudaLaunchKernelEx(&cfg, kfn, a, b, tmo ? *tmo : a, tmx ? *tmx : a, K, brow0, e);
 }
 
-// cluster (CM x CN): 0 = 1x1, 1 = 2x1 (W tile multicast), 2 = 1x2 (A multicast), 3 = 2x2,
-// 4 = 1x4, 5 = 2x4, 6 = 1x8, 7 = 4x2.  The A map's box must be 64 x (128 / CN), the W map's
-// 64 x (BN / CM).
+// pair = 1: the CTA-pair kernel (M = 256 tiles; the W map's box must be 64 x BN/2).
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K, int bn,
-                           const Epi& e, cudaStream_t st, int cluster, const CUtensorMap* tmo,
+                           const Epi& e, cudaStream_t st, int pair, const CUtensorMap* tmo,
                            const CUtensorMap* tmx) {
-  if (tmo) {   // TMA-store epilogue (EPI_STORE / EPI_GELU / EPI_RESID), no clusters
+  if (tmo) {   // TMA-store epilogue (EPI_STORE / EPI_GELU / EPI_RESID)
     if (e.kind != EPI_STORE && e.kind != EPI_GELU && e.kind != EPI_RESID) return cudaErrorInvalidValue;
     if (e.kind == EPI_RESID && !tmx) return cudaErrorInvalidValue;
+    if (pair) {
+      switch (bn) {
+        case 128: return launch_cfg<128, 6, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+        case 256: return launch_cfg<256, 4, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+        default: return cudaErrorInvalidValue;
+      }
+    }
     switch (bn) {
-      case 64: return launch_cfg<64, 6, 1, 1, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
-      case 128: return launch_cfg<128, 4, 1, 1, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
-      case 256: return launch_cfg<256, 3, 1, 1, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      case 64: return launch_cfg<64, 6, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      case 128: return launch_cfg<128, 4, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      case 256: return launch_cfg<256, 3, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
       default: return cudaErrorInvalidValue;
     }
   }
-#define CASES(BN, ST)                                                              \
-  switch (cluster) {                                                               \
-    case 0: return launch_cfg<BN, ST, 1, 1>(a, b, brow0, M, N, K, e, st);          \
-    case 1: return launch_cfg<BN, ST, 2, 1>(a, b, brow0, M, N, K, e, st);          \
-    case 2: return launch_cfg<BN, ST, 1, 2>(a, b, brow0, M, N, K, e, st);          \
-    case 3: return launch_cfg<BN, ST, 2, 2>(a, b, brow0, M, N, K, e, st);          \
-    case 4: return launch_cfg<BN, ST, 1, 4>(a, b, brow0, M, N, K, e, st);          \
-    case 5: return launch_cfg<BN, ST, 2, 4>(a, b, brow0, M, N, K, e, st);          \
-    case 6: return launch_cfg<BN, ST, 1, 8>(a, b, brow0, M, N, K, e, st);          \
-    case 7: return launch_cfg<BN, ST, 4, 2>(a, b, brow0, M, N, K, e, st);          \
-    default: return cudaErrorInvalidValue;                                         \
+  if (pair) {
+    switch (bn) {
+      case 128: return launch_cfg<128, 8, true, false>(a, b, brow0, M, N, K, e, st, nullptr, nullptr);
+      case 256: return launch_cfg<256, 6, true, false>(a, b, brow0, M, N, K, e, st, nullptr, nullptr);
+      default: return cudaErrorInvalidValue;
+    }
   }
   switch (bn) {
-    case 64: CASES(64, 8)
-    case 128: CASES(128, 6)
-    case 256: CASES(256, 4)
+    case 64: return launch_cfg<64, 8, false, false>(a, b, brow0, M, N, K, e, st, nullptr, nullptr);
+    case 128: return launch_cfg<128, 6, false, false>(a, b, brow0, M, N, K, e, st, nullptr, nullptr);
+    case 256: return launch_cfg<256, 4, false, false>(a, b, brow0, M, N, K, e, st, nullptr, nullptr);
     default: return cudaErrorInvalidValue;
   }
-#undef CASES
 }
 
 }  // namespace vi

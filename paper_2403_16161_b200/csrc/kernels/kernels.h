@@ -55,13 +55,13 @@ cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D,
 // tensor cores (bf16): A [M][K] and W [N][K] described by 2-D TMA maps with 64 x 128 /
 // 64 x BN boxes and 128-byte swizzle.
 // brow0: row offset of this layer's weight block inside the stacked W map.
-// cluster: 0 none, 1 = 2 CTAs along m (W multicast; W box 64 x BN/2), 2 = 2 along n (A
-// multicast; A box 64 x 64), 3 = 2 x 2.
+// pair: 0 = single-CTA 128 x BN tiles (W box 64 x BN); 1 = CTA-pair 256 x BN tiles with the
+// 2-SM MMA (W box 64 x BN/2).
 // tmo (optional): output tensor map (bf16 or fp32 [M][N], box 128 bytes x 32 rows, 128-byte
 // swizzle) -> the TMA-store epilogue for EPI_STORE / EPI_GELU / EPI_RESID (tmx: x_in map of
 // the same shape for EPI_RESID; x_out = the tmo tensor).
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& w, int brow0, int M, int N, int K, int bn,
-                           const Epi& e, cudaStream_t st, int cluster = 0, const CUtensorMap* tmo = nullptr,
+                           const Epi& e, cudaStream_t st, int pair = 0, const CUtensorMap* tmo = nullptr,
                            const CUtensorMap* tmx = nullptr);
 // SIMT (fp32 path): A [M][K], W [N][K] row-major fp32, FFMA accumulate.
 cudaError_t launch_gemm_simt_f32(const float* A, const float* W, int M, int N, int K, const Epi& e, cudaStream_t st);

@@ -529,3 +529,51 @@ def test_reference_memory_step_equals_masked_joint_pass():
     plain = O.joint_forward(feats, w, cfg, mode="mask",
                             frame_mask=np.array([[j <= i and j >= i - s for j in range(n)] for i in range(n)]))
     assert np.abs(plain["out"][8] - joint["out"][8]).max() > 1e-6
+
+
+# ---------------------------------------------------------------- window attention (BASELINE configs[3])
+
+def test_window_ids_partition_the_grid():
+    cfg = CONFIGS["C4"]
+    win = O.token_windows(cfg)
+    assert np.bincount(win).tolist() == [45] * 16                  # 4 x 4 windows of 5 x 9 tokens
+    oy, ox = np.divmod(np.arange(cfg.tokens), cfg.ow)
+    for w in range(16):                                            # each window is a 5 x 9 rectangle
+        ys, xs = oy[win == w], ox[win == w]
+        assert ys.max() - ys.min() == 4 and xs.max() - xs.min() == 8
+
+
+def test_window_attention_equals_per_window_attention():
+    """The masked block == attention run separately on each window's tokens (all frames of the
+    memory and the chunk), O scattered back."""
+    cfg = CONFIGS["C3S"].replace(layers=1, win_h=5, win_w=6)        # 10 x 18 grid -> 2 x 3 windows
+    w = make_weights(cfg, seed=3, variant="sensitive")
+    rng = rng_for(3, "win")
+    P, D, n = cfg.tokens, cfg.d_model, 2
+    x = rng.standard_normal((n * P, D))
+    mem = []
+    for j in range(3):
+        _, _, K, V = O.qkv(rng.standard_normal((P, D)), w, 0, cfg)
+        mem.append((K, V))
+    _, st = O.block_memory(x, mem, w, 0, cfg, n)
+    _, Q, Kc, Vc = O.qkv(x, w, 0, cfg)
+    K = np.concatenate([k for k, _ in mem] + [Kc]); V = np.concatenate([v for _, v in mem] + [Vc])
+    win = O.token_windows(cfg)
+    ref = np.zeros_like(st["o"])
+    for wid in range(win.max() + 1):
+        qi = np.nonzero(np.tile(win, n) == wid)[0]
+        ki = np.nonzero(np.tile(win, len(mem) + n) == wid)[0]
+        ref[qi] = O.attention(Q[qi], K[ki], V[ki], cfg.heads)
+    np.testing.assert_allclose(st["o"], ref, rtol=1e-12, atol=1e-13)
+
+
+def test_window_of_the_whole_grid_is_global_attention():
+    cfg = CONFIGS["C3S"].replace(layers=1)
+    whole = cfg.replace(win_h=cfg.oh, win_w=cfg.ow)
+    w = make_weights(cfg, seed=4, variant="sensitive")
+    rng = rng_for(4, "win")
+    x = rng.standard_normal((cfg.tokens, cfg.d_model))
+    _, _, K, V = O.qkv(rng.standard_normal((cfg.tokens, cfg.d_model)), w, 0, cfg)
+    a, _ = O.block_memory(x, [(K, V)], w, 0, cfg, 1)
+    b, _ = O.block_memory(x, [(K, V)], w, 0, whole, 1)
+    np.testing.assert_array_equal(a, b)

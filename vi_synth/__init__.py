@@ -51,6 +51,8 @@ class Config:
     pos_embed: int = 0
     ref_rate: int = 0      # r of Eq. 3's reference frames M_{1,r} (0 = span only)
     max_refs: int = 0      # reference slots kept (the oldest reference leaves first)
+    win_h: int = 0         # window attention: win_h x win_w token windows (0 = global attention)
+    win_w: int = 0
 
     @property
     def oh(self) -> int:
@@ -89,6 +91,8 @@ CONFIGS: Dict[str, Config] = {
     "C3": Config("C3", 8, 4, 512, 1960, 1, 60, 108, 128, 7, 7, 3, 3, 3, 3, 5, 10, "bf16"),
     # C3 in the paper's strict Eq. 3 mode: one new frame per step (also C5's online model)
     "C3T1": Config("C3T1", 8, 4, 512, 1960, 1, 60, 108, 128, 7, 7, 3, 3, 3, 3, 1, 10, "bf16"),
+    # configs[3]: E2FGVI-shaped, window attention over 5x9-token windows (16 per frame), 16 blocks
+    "C4": Config("C4", 16, 4, 512, 1960, 1, 60, 108, 128, 7, 7, 3, 3, 3, 3, 5, 10, "bf16", win_h=5, win_w=9),
     # a reduced C3 that the fp64 oracle finishes in seconds: 2 blocks, 30x54 map -> 10x18=180 tokens
     "C3S": Config("C3S", 2, 4, 512, 1960, 1, 30, 54, 128, 7, 7, 3, 3, 3, 3, 2, 3, "bf16"),
 }
