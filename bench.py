@@ -40,7 +40,8 @@ def peaks():
 
 WORKLOADS = {"C3": "FuseFormer-shaped memory step (BASELINE.json configs[2])",
              "C3T1": "FuseFormer-shaped memory step, one new frame per step (Eq. 3; configs[2] shape, T=1)",
-             "C2": "STTN-shaped memory step (BASELINE.json configs[1])"}
+             "C2": "STTN-shaped memory step (BASELINE.json configs[1])",
+             "C4": "E2FGVI-shaped memory step, 5x9-token window attention (BASELINE.json configs[3])"}
 
 
 def gemm_flop_per_step(cfg):
@@ -68,6 +69,7 @@ def workload_config(cfg, args=None, world=1):
             "layers": cfg.layers, "heads": cfg.heads, "d_model": cfg.d_model, "tokens_per_frame": cfg.tokens,
             "new_frames_per_step": cfg.t_new, "mem_frames": cfg.mem_frames,
             "keys_per_block": cfg.slots * cfg.tokens, "queries_per_block": cfg.t_new * cfg.tokens,
+            "keys_per_query": cfg.slots * (cfg.win_h * cfg.win_w if cfg.win_h else cfg.tokens),
             "feature_map": [cfg.feat_h, cfg.feat_w, cfg.feat_c],
             "ffn": f"F3N {cfg.ffn_hidden}" if cfg.ffn_kind == 1 else f"MLP-GELU {cfg.ffn_hidden}",
             "l2": "flushed between timed steps (256 MiB write)",
@@ -281,7 +283,7 @@ def run_ours(args, cfg):
     bf16_peak, hbm_peak, peak_src = peaks()
     attn_ms, attn_recs = prof["attention"]
     per_block_ms = attn_ms / (args.steps * cfg.layers) if attn_ms > 0 else float("nan")
-    nq, nk = T * P, cfg.slots * P
+    nq, nk = T * P, cfg.slots * (cfg.win_h * cfg.win_w if cfg.win_h else P)   # keys a query sees
     attn_flop = 4.0 * nq * nk * D / (world if args.tp else 1)   # this rank's share when head-sharded
     achieved = attn_flop / (per_block_ms * 1e-3) / 1e12 if attn_ms > 0 else float("nan")
     traffic = None

@@ -108,6 +108,11 @@ typedef struct vi_config {
    * leaves when the slots are full; reading Q12).  0 = span only.  Slots in total:
    * mem_frames + max_new_frames + max_ref_frames <= 64 (vi_num_slots). */
   int ref_rate, max_ref_frames;
+  /* Window attention (E2FGVI-shaped, BASELINE configs[3]): a query sees only the keys of
+   * its own win_h x win_w token window (non-overlapping, tiling the token grid), in every
+   * frame of the memory and the chunk.  0 = global attention.  bf16 path; no head sharding,
+   * reference frames, refine commits or memory reads (the memory is window-major). */
+  int win_h, win_w;
 } vi_config;
 
 /* Weights, host fp32 pointers in nn.Linear layout (y = x W^T + b); converted to the

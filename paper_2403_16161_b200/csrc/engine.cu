@@ -112,6 +112,11 @@ struct vi_ctx {
   Geom g{}, gf{};          // split geometry (C = feat_c) and F3N geometry (C = F / (kh*kw))
   int L = 0, H = 0, D = 0, hd = 0, P = 0, M = 0, Tmax = 0, S = 0, F = 0, Pd = 0, es = 2;
   int ST = 0;              // all memory slots: S span slots + R reference slots (ring.h)
+  // window attention (vi_config.win_h / win_w): win_n windows of win_real tokens, padded to
+  // win_pad rows; the memory and Q are window-major (epilogue.cuh qkv_rows)
+  int win_n = 0, win_real = 0, win_pad = 0, win_cols = 0;
+  int KR = 0;              // key rows per block in the slabs: ST*P, or win_n*ST*win_pad
+  int QR = 0;              // rows of the Q buffer: T_max*P, or win_n*T_max*win_pad
   int vt_ld = 0;           // row pitch of the transposed V slab: S*P rounded up to 64 (TMA: 16-B pitch)
   bool bf16 = true;
   cudaStream_t stream = nullptr, copy_stream = nullptr;
@@ -382,6 +387,13 @@ static vi_status validate(const vi_config* k, std::string* why) {
     if (k->d_model > 1024) return bad("d_model <= 1024");
   }
   if (k->d_model > 1024) return bad("d_model <= 1024 (LayerNorm kernel)");
+  if (k->win_h < 0 || k->win_w < 0 || (k->win_h > 0) != (k->win_w > 0)) return bad("win_h / win_w: both 0 or both > 0");
+  if (k->win_h > 0) {
+    if (k->dtype != VI_DTYPE_BF16) return bad("window attention: bf16 path only");
+    if (oh % k->win_h || ow % k->win_w) return bad("window attention: windows must tile the token grid");
+    if (k->tp_size > 1 || k->nccl_id || k->ref_rate > 0)
+      return bad("window attention: no head sharding or reference frames (not built)");
+  }
   const int G = k->tp_size < 1 ? 1 : k->tp_size;
   if (G > 1 || k->nccl_id) {
     TpLayout t;
@@ -417,8 +429,8 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_w2, c->w_2, c->F, (uint64_t)c->L * c->D, 64, c->bn_2);
   ok &= make_tmap(&c->tm_xb, c->xb, 2 * c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_wback, c->w_back2, 2 * c->D, c->Pd, 64, c->bn_back);
-  ok &= make_tmap(&c->tm_q, c->q, c->Dl, rows, 64, 128);
-  ok &= make_tmap(&c->tm_k, c->kslab, c->Dl, (uint64_t)c->L * c->ST * c->P, 64, 128);
+  ok &= make_tmap(&c->tm_q, c->q, c->Dl, (uint64_t)c->QR, 64, 128);
+  ok &= make_tmap(&c->tm_k, c->kslab, c->Dl, (uint64_t)c->L * c->KR, 64, 128);
   ok &= make_tmap(&c->tm_vt, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->Dl, 64, c->hd);
   if (c->sharded) ok &= make_tmap(&c->tm_og, c->og, c->hd, (uint64_t)c->H * c->tp.head_rows, 64, 128);
   ok &= make_tmap_out(&c->tm_u_out, c->u, true, c->F, rows);
@@ -449,7 +461,19 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->P = cfg->tokens_per_frame; c->M = cfg->mem_frames; c->Tmax = cfg->max_new_frames; c->S = c->M + c->Tmax;
   c->ST = c->S + (cfg->ref_rate > 0 ? cfg->max_ref_frames : 0);
   c->F = cfg->ffn_hidden; c->Pd = cfg->kh * cfg->kw * cfg->feat_c;
-  c->vt_ld = (c->ST * c->P + 63) / 64 * 64;
+  if (cfg->win_h > 0) {
+    const int oh = (cfg->feat_h + 2 * cfg->ph - cfg->kh) / cfg->sh + 1, ow = (cfg->feat_w + 2 * cfg->pw - cfg->kw) / cfg->sw + 1;
+    c->win_cols = ow / cfg->win_w;
+    c->win_n = (oh / cfg->win_h) * c->win_cols;
+    c->win_real = cfg->win_h * cfg->win_w;
+    c->win_pad = (c->win_real + 15) / 16 * 16;   // 16-row TMA/MMA granularity
+    c->KR = c->win_n * c->ST * c->win_pad;
+    c->QR = c->win_n * c->Tmax * c->win_pad;
+  } else {
+    c->KR = c->ST * c->P;
+    c->QR = c->Tmax * c->P;
+  }
+  c->vt_ld = (c->KR + 63) / 64 * 64;
   c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
   c->ring = Ring(c->M, c->Tmax, cfg->ref_rate, cfg->max_ref_frames);
   {
@@ -496,8 +520,8 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->w_1 = A(L * F * D * es); c->b_1 = (float*)A(L * F * 4);
   c->w_2 = A(L * D * F * es); c->b_2 = (float*)A(L * D * 4);
   c->w_back = A(Pd * D * es); c->b_back = (float*)A(Pd * 4);
-  c->kslab = A(L * S * P * Dl * es); c->vtslab = A(L * Dl * (size_t)c->vt_ld * es);
-  c->tokens = A(rows * Pd * es); c->h = A(rows * D * es); c->q = A(rows * Dl * es); c->o = A(rows * D * es);
+  c->kslab = A(L * (size_t)c->KR * Dl * es); c->vtslab = A(L * Dl * (size_t)c->vt_ld * es);
+  c->tokens = A(rows * Pd * es); c->h = A(rows * D * es); c->q = A((size_t)c->QR * Dl * es); c->o = A(rows * D * es);
   if (c->sharded) c->og = A((size_t)c->H * c->tp.head_rows * c->hd * es);
   c->u = A(rows * F * 4);   // FFN1 output kept fp32 for the F3N fold (one rounding less)
   c->gbuf = A(rows * F * es); c->xb = A(rows * 2 * D * es);
@@ -508,8 +532,8 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->x_ws = (float*)A(rows * D * 4);
   c->fold_ws = (float*)A((size_t)c->Tmax * cfg->feat_h * cfg->feat_w * std::max(c->gf.C, 1) * 4);
   if (c->bf16) {
-    c->opart = (float*)A((size_t)kMaxSplit * rows * D * 4);
-    c->lse = (float*)A((size_t)kMaxSplit * c->H * rows * 4);
+    c->opart = (float*)A((size_t)kMaxSplit * std::max(rows, (size_t)c->QR) * D * 4);
+    c->lse = (float*)A((size_t)kMaxSplit * c->H * std::max(rows, (size_t)c->QR) * 4);
   }
   c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);
   c->attn_timing = (unsigned long long*)A(2 * sizeof(KernelTiming));   // [0] attention, [1] GEMMs
@@ -763,6 +787,7 @@ extern "C" vi_status vi_refine_commit(vi_ctx* c, int64_t frame_id, const void* k
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
   if (!k || !v) return VI_E_ARG;
+  if (c->win_n) return c->fail(VI_E_CONFIG, "vi_refine_commit: not built for window attention (window-major memory)");
   std::lock_guard<std::mutex> lk(c->mu);
   const vi_status st = c->ring.commit(frame_id);
   if (st != VI_OK) return st;
@@ -798,6 +823,7 @@ extern "C" vi_status vi_memory_read(vi_ctx* c, int64_t frame_id, void* k, void* 
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
   if (!k || !v) return c->fail(VI_E_ARG, "vi_memory_read: NULL buffer");
+  if (c->win_n) return c->fail(VI_E_CONFIG, "vi_memory_read: not built for window attention (window-major memory)");
   {
     std::lock_guard<std::mutex> lk(c->mu);
     const int32_t st = c->ring.check_past(frame_id);
@@ -919,10 +945,11 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
     }
     int e = s;
     while (e + 1 < c->ST && ((valid >> (e + 1)) & 1)) ++e;
-    const int r0 = s * c->P;
+    const int rows_per_slot = c->win_n ? c->win_pad : c->P;   // windows: rows within the window's region
+    const int r0 = s * rows_per_slot;
     k.row0[k.n] = r0 & ~7;
     k.lead[k.n] = r0 & 7;
-    k.len[k.n] = (e - s + 1) * c->P + k.lead[k.n];
+    k.len[k.n] = (e - s + 1) * rows_per_slot + k.lead[k.n];
     k.tile0[k.n + 1] = k.tile0[k.n] + (k.len[k.n] + 127) / 128;
     ++k.n;
     s = e + 1;
@@ -936,7 +963,7 @@ static KeySegs make_segs(const vi_ctx* c, uint64_t valid) {
 static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   const int n = c->ring.cur_n, M = n * c->P, D = c->D, Dl = c->Dl;
   const int dt = c->bf16 ? 0 : 1;
-  const size_t es = c->es, SP = (size_t)c->ST * c->P;
+  const size_t es = c->es, SP = (size_t)c->KR;
   void* kl = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * Dl * es;
   void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * c->vt_ld * Dl * es;
   const uint64_t valid = c->ring.valid_mask();
@@ -947,6 +974,10 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   Epi eq = epi_base(EPI_QKV, M, 3 * Dl, c->b_qkv + (size_t)l * 3 * Dl);
   eq.D = Dl; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
   eq.S = c->S; eq.P = c->P; eq.vt_ld = c->vt_ld;
+  if (c->win_n) {
+    eq.win_pad = c->win_pad; eq.win_h = c->cfg.win_h; eq.win_w = c->cfg.win_w; eq.win_cols = c->win_cols;
+    eq.ow = c->g.ow; eq.win_qstride = c->Tmax * c->win_pad; eq.win_kstride = c->ST * c->win_pad;
+  }
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * Dl, M, 3 * Dl, D, c->bn_qkv, eq, c->stream), "qkv gemm");
   else
@@ -967,6 +998,13 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   a.Nq = M; a.hd = c->hd; a.D = Dl; a.H = c->Hl; a.krow_base = int(l * SP); a.vrow_base = l * Dl;
   a.scale_log2 = scale_log2; a.segs = make_segs(c, valid);
   a.o = static_cast<bf16*>(c->o); a.o_ld = D; a.o_hs = c->hd; a.q_row0 = 0;
+  if (c->win_n) {   // window attention: the fixed KV split over (window, 256 queries) units
+    a.win_n = c->win_n; a.win_qstride = c->Tmax * c->win_pad; a.win_kstride = c->ST * c->win_pad;
+    a.win_pad = c->win_pad; a.win_real = c->win_real; a.win_h = c->cfg.win_h; a.win_w = c->cfg.win_w;
+    a.win_cols = c->win_cols; a.ow = c->g.ow; a.P = c->P; a.win_nq = n * c->win_pad;
+    a.win_npw = (a.win_nq + 255) / 256;
+    a.Nq = c->win_n * a.win_qstride;   // rows of the KV-split partials (window-major)
+  }
   if (c->sharded) {   // this rank's query rows, written head-major into its chunk of og
     a.q_row0 = c->tp.row0();
     a.Nq = c->tp.rows(M);
@@ -984,7 +1022,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   // (C3, T = 1: 28 us vs 60 us per block; T = 5: stream-K 84 us vs ~93 us).
   const int sk_units = ((a.Nq + 255) / 256) * a.H;
   const bool small = sk_units * 4 < c->num_sms;
-  if (!g_attn_v1 && !g_attn_split && !small) {
+  if (!g_attn_v1 && !g_attn_split && !small && !c->win_n) {
     // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
     a.npairs = (a.Nq + 255) / 256;
     a.units = a.npairs * a.H;
@@ -1001,7 +1039,10 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   } else {   // fixed KV split + combine kernel (small chunks; VI_ATTN_V1 / VI_ATTN_SPLIT A/B variants)
     if (g_attn_v1 && c->sharded) return c->fail(VI_E_CONFIG, "VI_ATTN_V1 does not support head sharding");
     const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
-    choose_split(((a.Nq + qrows - 1) / qrows) * a.H, ntiles, &a.nsplit, &a.tiles_per_split);
+    if (c->win_n && (g_attn_v1 || g_attn_colsplit))
+      return c->fail(VI_E_CONFIG, "window attention runs on the attn_tc2 row-per-thread kernel only");
+    const int units = c->win_n ? c->win_n * a.win_npw * a.H : ((a.Nq + qrows - 1) / qrows) * a.H;
+    choose_split(units, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
     if (g_attn_v1)
       PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
@@ -1345,6 +1386,8 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
   const size_t es = c->es, rows = (size_t)n * c->P, D = c->D, Dl = c->Dl, SP = (size_t)c->ST * c->P;
   const void* src = nullptr;
   size_t need = 0;
+  if (c->win_n && (what == VI_DBG_Q || what == VI_DBG_K || what == VI_DBG_V))
+    return c->fail(VI_E_CONFIG, "vi_debug_read: Q / K / V are window-major under window attention");
   switch (what) {
     case VI_DBG_TOKENS: src = c->tokens; need = rows * c->Pd * es; break;
     case VI_DBG_H: src = c->h; need = rows * D * es; break;

@@ -81,6 +81,16 @@ struct AttnSmem {
 
 // Tile g of the valid key space: keys row0 .. row0+127 of the slab, of which
 // [nskip, nvalid) belong to valid slots (the rest is masked to -inf).
+// window attention: output token row of local query q of window w, or -1 for padding /
+// rows beyond the chunk
+__device__ __forceinline__ int win_out_row(const AttnTC& a, int w, int q) {
+  if (q >= a.win_nq) return -1;
+  const int t = q / a.win_pad, i = q - t * a.win_pad;
+  if (i >= a.win_real) return -1;
+  const int oy = (w / a.win_cols) * a.win_h + i / a.win_w, ox = (w % a.win_cols) * a.win_w + i % a.win_w;
+  return t * a.P + oy * a.ow + ox;
+}
+
 __device__ __forceinline__ void key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
   int i = 0;
   while (i + 1 < s.n && g >= s.tile0[i + 1]) ++i;
@@ -408,7 +418,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = blockIdx.x * 256, h = blockIdx.y, z = blockIdx.z;
+  const int win = a.win_n ? int(blockIdx.x) / a.win_npw : 0;                   // window (0 if global)
+  const int q0 = (a.win_n ? int(blockIdx.x) % a.win_npw : int(blockIdx.x)) * 256, h = blockIdx.y, z = blockIdx.z;
+  const int wq = win * a.win_qstride, wk = win * a.win_kstride;                  // window row offsets
   const int ntiles = a.segs.tile0[a.segs.n];
   const int t_begin = z * a.tiles_per_split;
   int t_end = t_begin + a.tiles_per_split;
@@ -448,7 +460,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       for (int t = 0; t < 2; ++t)
 #pragma unroll
         for (int at = 0; at < HD / 64; ++at)
-          tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, a.q_row0 + q0 + t * 128);
+          tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64,
+                      a.q_row0 + wq + q0 + t * 128);
       for (int jj = 0; jj < n; ++jj) {
         int row0, nv, nskip;
         key_tile(a.segs, t_begin + jj, row0, nv, nskip);
@@ -459,13 +472,13 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         mbar_arrive_expect_tx(&k_full[st], L::KB);
 #pragma unroll
         for (int at = 0; at < HD / 64; ++at)
-          tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + row0);
+          tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + wk + row0);
         if (jj >= ST) mbar_wait(&v_empty[st], par);
         uint8_t* sv = smem + L::V_OFF + st * L::VB;
         mbar_arrive_expect_tx(&v_full[st], L::VB);
 #pragma unroll
         for (int at = 0; at < 2; ++at)
-          tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], row0 + at * 64, a.vrow_base + h * HD);
+          tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], wk + row0 + at * 64, a.vrow_base + h * HD);
       }
     }
   } else if (warp == 9) {
@@ -577,6 +590,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
             tmem_st32(TO + hf * OH + c, r);
           }
+          tmem_wait_st();
+          named_bar_sync(1 + qd, 64);                 // both O halves rescaled before any PV
         }
         const float2 mm = make_float2(-m_use[t], -m_use[t]);
         float2 sum[4];
@@ -680,6 +695,14 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         for (int i = 0; i < 128; ++i)
           if (i >= nv || i < nskip) s[i] = -INFINITY;
       }
+      if (a.win_n) {                                  // window padding keys (index % pad >= real)
+        uint32_t pm[4] = {0u, 0u, 0u, 0u};
+        for (int k = a.win_real - row0 % a.win_pad; k < 128; k += a.win_pad)
+          for (int e = k < 0 ? 0 : k; e < k + a.win_pad - a.win_real && e < 128; ++e) pm[e >> 5] |= 1u << (e & 31);
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if ((pm[i >> 5] >> (i & 31)) & 1u) s[i] = -INFINITY;
+      }
 #pragma unroll
       for (int i = 0; i < 128; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
       const float rmax = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
@@ -741,6 +764,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     }
     // epilogue
     const int q = q0 + t * 128 + qd * 32 + lane;
+    // output row (global: q itself; windows: the token row of (frame, window index), -1 = none)
+    const int orow = a.win_n ? win_out_row(a, win, q) : (q < a.Nq ? q : -1);
+    const int qp = wq + q;                            // row of the KV-split partials
     if (n > 0) {
       mbar_wait(&o_final[t], 0);
       tc_fence_after();
@@ -752,9 +778,9 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         uint32_t r[32];
         tmem_ld32(TO + c, r);
         tmem_wait_ld();
-        if (q < a.Nq) {
+        if (orow >= 0) {
           const float* f = reinterpret_cast<const float*>(r);
-          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.o_ld + (size_t)h * a.o_hs + c);
+          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c);
 #pragma unroll
           for (int i = 0; i < 4; ++i)
             dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv), pack_bf16(f[8 * i + 2] * inv, f[8 * i + 3] * inv),
@@ -762,7 +788,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
       }
     } else {
-      float* op = a.opart + ((size_t)z * a.Nq + q) * a.D + h * HD;
+      float* op = a.opart + ((size_t)z * a.Nq + qp) * a.D + h * HD;
 #pragma unroll 1
       for (int c = 0; c < HD; c += 32) {
         uint32_t r[32];
@@ -770,7 +796,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           tmem_ld32(TO + c, r);
           tmem_wait_ld();
         }
-        if (q < a.Nq) {
+        if (orow >= 0) {
           float4* dst = reinterpret_cast<float4*>(op + c);
 #pragma unroll
           for (int i = 0; i < 8; ++i)
@@ -779,7 +805,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
                            : make_float4(0.f, 0.f, 0.f, 0.f);
         }
       }
-      if (q < a.Nq) a.lse[((size_t)z * a.H + h) * a.Nq + q] = n > 0 ? m_use + __log2f(l) : -INFINITY;
+      if (orow >= 0) a.lse[((size_t)z * a.H + h) * a.Nq + qp] = n > 0 ? m_use + __log2f(l) : -INFINITY;
     }
   }
   tc_fence_before();
@@ -802,7 +828,7 @@ static cudaError_t launch2_hd(const CUtensorMap& tq, const CUtensorMap& tk, cons
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  dim3 grid((a.Nq + 255) / 256, a.H, a.nsplit);
+  dim3 grid(a.win_n ? a.win_n * a.win_npw : (a.Nq + 255) / 256, a.H, a.nsplit);
   attn_tc2_kernel<HD, CS><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
   return cudaGetLastError();
 }
@@ -823,7 +849,9 @@ __global__ void attn_combine_kernel(const AttnTC a) {
     const int c4 = int(i % hd4);
     const size_t r = i / hd4;
     const int h = int(r % a.H);
-    const int q = int(r / a.H);
+    const int q = int(r / a.H);             // KV-split partial row (windows: window-major)
+    const int orow = a.win_n ? win_out_row(a, q / a.win_qstride, q % a.win_qstride) : q;
+    if (orow < 0) continue;
     float mx = -INFINITY;
     for (int z = 0; z < a.nsplit; ++z) mx = fmaxf(mx, a.lse[((size_t)z * a.H + h) * a.Nq + q]);
     float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
@@ -836,7 +864,7 @@ __global__ void attn_combine_kernel(const AttnTC a) {
       acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
     }
     const float inv = 1.f / wsum;
-    uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)q * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
+    uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
     *dst = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   }
   __syncthreads();

@@ -35,7 +35,28 @@ struct Epi {
   // A operand stored head-major (head-sharded output projection, tp.h): a_hs > 0 means
   // A[m][k] = Amap row (k / (64 * a_kpb)) * a_hs + m, column k % (64 * a_kpb)
   int a_hs, a_kpb;
+  // EPI_QKV with window attention (win_pad > 0): token p = (oy, ox) of frame t belongs to
+  // window w = (oy / win_h) * win_cols + ox / win_w at index i = (oy % win_h) * win_w + ox % win_w;
+  // Q goes to row w * win_qstride + t * win_pad + i, K / Vt to row / column
+  // w * win_kstride + slot * win_pad + i (window-major memory, pad rows never written)
+  int win_pad, win_h, win_w, win_cols, ow, win_qstride, win_kstride;
 };
+
+// QKV destinations of row m (token p of chunk frame t): Q row and memory (K row / Vt column)
+__device__ __forceinline__ void qkv_rows(const Epi& e, int m, size_t& qrow, size_t& krow) {
+  const int t = m / e.P, p = m - t * e.P;
+  const int slot = (e.first_slot + t) % e.S;
+  if (e.win_pad) {
+    const int oy = p / e.ow, ox = p - oy * e.ow;
+    const int w = (oy / e.win_h) * e.win_cols + ox / e.win_w;
+    const int i = (oy % e.win_h) * e.win_w + ox % e.win_w;
+    qrow = (size_t)w * e.win_qstride + (size_t)t * e.win_pad + i;
+    krow = (size_t)w * e.win_kstride + (size_t)slot * e.win_pad + i;
+  } else {
+    qrow = (size_t)m;
+    krow = (size_t)slot * e.P + p;
+  }
+}
 
 template <typename T>
 __device__ __forceinline__ void epi_one(const Epi& e, int m, int n, float acc) {
@@ -55,10 +76,10 @@ __device__ __forceinline__ void epi_one(const Epi& e, int m, int n, float acc) {
       e.x_out[(size_t)m * e.N + n] = e.x_in[(size_t)m * e.N + n] + v;
       break;
     default: {
-      const int t = m / e.P, p = m - t * e.P;
-      const size_t row = (size_t)((e.first_slot + t) % e.S) * e.P + p;
+      size_t qrow, row;
+      qkv_rows(e, m, qrow, row);
       if (n < e.D) {
-        reinterpret_cast<T*>(e.q)[(size_t)m * e.D + n] = from_f<T>(v);
+        reinterpret_cast<T*>(e.q)[qrow * e.D + n] = from_f<T>(v);
       } else if (n < 2 * e.D) {
         reinterpret_cast<T*>(e.kslab)[row * e.D + (n - e.D)] = from_f<T>(v);
       } else {
@@ -121,10 +142,10 @@ __device__ __forceinline__ void epi_row32_bf16(const Epi& e, int m, int n0, floa
       break;
     }
     default: {  // EPI_QKV; a 32-column group never straddles Q/K/V (D % 32 == 0)
-      const int t = m / e.P, p = m - t * e.P;
-      const size_t row = (size_t)((e.first_slot + t) % e.S) * e.P + p;
+      size_t qrow, row;
+      qkv_rows(e, m, qrow, row);
       if (n0 < 2 * e.D) {
-        bf16* base = (n0 < e.D) ? reinterpret_cast<bf16*>(e.q) + (size_t)m * e.D + n0
+        bf16* base = (n0 < e.D) ? reinterpret_cast<bf16*>(e.q) + qrow * e.D + n0
                                 : reinterpret_cast<bf16*>(e.kslab) + row * e.D + (n0 - e.D);
         uint4* dst = reinterpret_cast<uint4*>(base);
 #pragma unroll

@@ -115,6 +115,12 @@ struct AttnTC {
   // output row i of local head h goes to o + i * o_ld + h * o_hs (unsharded: o_ld = D,
   // o_hs = hd; head-sharded: the rank's chunk of the head-major gathered buffer, tp.h)
   int q_row0, o_ld, o_hs;
+  // window attention (win_n > 0; attn_tc2 + combine only): win_npw CTAs (256 query rows
+  // each) per window; window w's queries are rows w * win_qstride + [0, win_nq) of the Q map
+  // (frame t's token i of the window at t * win_pad + i), its keys rows w * win_kstride + the
+  // key segments (slot s at s * win_pad); rows with index % win_pad >= win_real are padding
+  // (keys masked, queries not written); output row of (t, i) = t * P + token(w, i)
+  int win_n, win_npw, win_qstride, win_kstride, win_pad, win_real, win_h, win_w, win_cols, ow, P, win_nq;
 };
 cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            cudaStream_t st);

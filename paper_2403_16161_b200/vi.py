@@ -43,7 +43,7 @@ class ViConfig(C.Structure):
         "feat_h", "feat_w", "feat_c", "kh", "kw", "sh", "sw", "ph", "pw",
         "ffn_hidden", "ffn_kind", "dtype", "pos_embed", "device")] + [("stream", C.c_void_p)] + [
         ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p), ("stream_priority", C.c_int),
-        ("ref_rate", C.c_int), ("max_ref_frames", C.c_int)]
+        ("ref_rate", C.c_int), ("max_ref_frames", C.c_int), ("win_h", C.c_int), ("win_w", C.c_int)]
 
 
 WEIGHT_FIELDS = ("embed_w", "embed_b", "pos", "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b",
@@ -235,7 +235,8 @@ class Context:
                    dtype=DTYPE_BF16 if c.dtype == "bf16" else DTYPE_FP32, pos_embed=c.pos_embed,
                    device=device, stream=stream, tp_size=tp_size, tp_rank=tp_rank, nccl_id=nccl_id,
                    stream_priority=stream_priority, ref_rate=getattr(c, "ref_rate", 0),
-                   max_ref_frames=getattr(c, "max_refs", 0))
+                   max_ref_frames=getattr(c, "max_refs", 0), win_h=getattr(c, "win_h", 0),
+                   win_w=getattr(c, "win_w", 0))
 
     def close(self):
         if getattr(self, "_h", None):

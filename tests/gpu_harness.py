@@ -53,7 +53,9 @@ class GpuStream:
             ctx.memory_step(l, x, x)
             if stages:
                 d = {}
-                names = [("q", cfg.d_model, dt), ("o", cfg.d_model, dt), ("g", cfg.ffn_hidden, dt)]
+                names = [("o", cfg.d_model, dt), ("g", cfg.ffn_hidden, dt)]
+                if not getattr(cfg, "win_h", 0):      # Q is window-major under window attention
+                    names.append(("q", cfg.d_model, dt))
                 if cfg.ffn_kind == 1:
                     names.append(("u", cfg.ffn_hidden, torch.float32))
                 for name, width, bdt in names:
