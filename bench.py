@@ -266,8 +266,11 @@ def run_ours(args, cfg):
     # identical outputs after the memory is full (no atomics on the path)
     outs = []
     for _ in range(2):
+        nid = None
+        if args.tp:           # an NCCL id serves one communicator: a fresh one per context
+            nid = streams.broadcast_bytes(vi.tp_unique_id() if rank == 0 else None, torch.device("cuda", local))
         c2 = vi.Context.from_synth(cfg, device=local, tp_size=world if args.tp else 1, tp_rank=rank if args.tp else 0,
-                                   nccl_id=nccl_id if args.tp else None)
+                                   nccl_id=nid)
         c2.set_weights(w)
         o2 = torch.empty_like(out)
         for k in range(math.ceil(cfg.mem_frames / T) + 2):
