@@ -80,6 +80,26 @@ bool make_tmap_out(CUtensorMap* m, const void* base, bool f32, uint64_t cols, ui
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// General 2-D bf16 map [rows][cols] with an arbitrary box, 128-byte swizzle or none
+bool make_tmap_box(CUtensorMap* m, const void* base, uint64_t cols, uint64_t rows, uint32_t box_cols, uint32_t box_rows,
+                   bool swizzle128) {
+  PFN_encodeTiled_t fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {cols * 2};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t e[2] = {1, 1};
+  return fn(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims, strides, box, e,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle128 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
+// VI_PAIR=0: the FFN2 GEMM (K = F) on single-CTA tiles instead of CTA pairs (A/B measurements)
+const bool g_pair_ffn2 = [] {
+  const char* e = getenv("VI_PAIR");
+  return !(e && e[0] == '0');
+}();
+
 // VI_TMA_EPI=0: the GEMMs store from registers instead of through TMA (A/B measurements)
 const bool g_tma_epi = [] {
   const char* e = getenv("VI_TMA_EPI");
@@ -164,8 +184,11 @@ struct vi_ctx {
 
   // tensor maps (bf16 path)
   CUtensorMap tm_tokens, tm_wembed, tm_h, tm_wqkv, tm_o, tm_wo, tm_w1, tm_g, tm_w2, tm_xb, tm_wback;
+  CUtensorMap tm_w2_pair;    // W2 with a 64-row box: the CTA-pair FFN2 (256 x 128 tiles)
   CUtensorMap tm_q, tm_k, tm_vt, tm_og;
   CUtensorMap tm_u_out, tm_g_out, tm_yp_out;   // GEMM outputs through the TMA-store epilogue
+  CUtensorMap tm_q_out, tm_k_out, tm_vt_out;   // QKV epilogue: Q rows, K slab rows (8-row boxes), Vt columns
+  bool qkv_te = false;
   // N-tile per GEMM (persistent kernel: ~1-3 tiles per SM at M = 3600; N=64 MMAs run at 2/3 rate)
   int bn_embed = 128, bn_qkv = 128, bn_o = 128, bn_1 = 256, bn_2 = 128, bn_back = 256;
 
@@ -427,6 +450,7 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_w1, c->w_1, c->D, (uint64_t)c->L * c->F, 64, c->bn_1);
   ok &= make_tmap(&c->tm_g, c->gbuf, c->F, rows, 64, 128);
   ok &= make_tmap(&c->tm_w2, c->w_2, c->F, (uint64_t)c->L * c->D, 64, c->bn_2);
+  ok &= make_tmap(&c->tm_w2_pair, c->w_2, c->F, (uint64_t)c->L * c->D, 64, 64);
   ok &= make_tmap(&c->tm_xb, c->xb, 2 * c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_wback, c->w_back2, 2 * c->D, c->Pd, 64, c->bn_back);
   ok &= make_tmap(&c->tm_q, c->q, c->Dl, (uint64_t)c->QR, 64, 128);
@@ -436,6 +460,12 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap_out(&c->tm_u_out, c->u, true, c->F, rows);
   ok &= make_tmap_out(&c->tm_g_out, c->gbuf, false, c->F, rows);
   ok &= make_tmap_out(&c->tm_yp_out, c->yp32, true, c->Pd, rows);
+  c->qkv_te = !c->win_n && c->P % 8 == 0 && c->Dl % 64 == 0;
+  if (c->qkv_te) {
+    ok &= make_tmap_out(&c->tm_q_out, c->q, false, c->Dl, (uint64_t)c->QR);
+    ok &= make_tmap_box(&c->tm_k_out, c->kslab, c->Dl, (uint64_t)c->L * c->KR, 64, 8, true);
+    ok &= make_tmap_box(&c->tm_vt_out, c->vtslab, (uint64_t)c->vt_ld, (uint64_t)c->L * c->Dl, 8, 64, false);
+  }
   return ok ? VI_OK : c->fail(VI_E_CUDA, "cuTensorMapEncodeTiled failed");
 }
 
@@ -978,8 +1008,14 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     eq.win_pad = c->win_pad; eq.win_h = c->cfg.win_h; eq.win_w = c->cfg.win_w; eq.win_cols = c->win_cols;
     eq.ow = c->g.ow; eq.win_qstride = c->Tmax * c->win_pad; eq.win_kstride = c->ST * c->win_pad;
   }
+  eq.qkv_krow0 = int(l * SP);
+  eq.qkv_vrow0 = l * Dl;
+  const bool qte = c->bf16 && g_tma_epi && c->qkv_te;
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * Dl, M, 3 * Dl, D, c->bn_qkv, eq, c->stream), "qkv gemm");
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * Dl, M, 3 * Dl, D, c->bn_qkv, eq, c->stream, 0,
+                                         qte ? &c->tm_q_out : nullptr, qte ? &c->tm_k_out : nullptr,
+                                         qte ? &c->tm_vt_out : nullptr),
+            "qkv gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_qkv + (size_t)l * 3 * Dl * D, M, 3 * Dl, D,
                                                eq, c->stream),
@@ -1105,9 +1141,11 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   // a11: FFN2 + residual
   Epi e2 = epi_base(EPI_RESID, M, D, c->b_2 + (size_t)l * D);
   e2.x_in = x_out; e2.x_out = x_out;
+  // FFN2 (K = F = 1960) on CTA-pair tiles 256 x 128 (tools/micro/gemm_micro: 16.9 vs 18.3 us)
+  const bool pair2 = te && g_pair_ffn2;
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, c->tm_w2, l * D, M, D, F, c->bn_2, e2, c->stream, 0,
-                                         te ? &tx_out : nullptr, te ? &tx_out : nullptr),
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, pair2 ? c->tm_w2_pair : c->tm_w2, l * D, M, D, F, pair2 ? 128 : c->bn_2, e2,
+                                         c->stream, pair2 ? 1 : 0, te ? &tx_out : nullptr, te ? &tx_out : nullptr),
             "ffn2 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->gbuf, (const float*)c->w_2 + (size_t)l * D * F, M, D, F, e2,

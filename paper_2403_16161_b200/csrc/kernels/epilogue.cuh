@@ -40,6 +40,9 @@ struct Epi {
   // Q goes to row w * win_qstride + t * win_pad + i, K / Vt to row / column
   // w * win_kstride + slot * win_pad + i (window-major memory, pad rows never written)
   int win_pad, win_h, win_w, win_cols, ow, win_qstride, win_kstride;
+  // EPI_QKV through the TMA-store epilogue: rows of this layer's block in the K map (l * S * P)
+  // and in the Vt map (l * D)
+  int qkv_krow0, qkv_vrow0;
 };
 
 // QKV destinations of row m (token p of chunk frame t): Q row and memory (K row / Vt column)

@@ -55,8 +55,8 @@ __device__ long long g_gemm_trace[24];
 template <int BN, int STAGES, bool PAIR, bool TE>
 __global__ void __launch_bounds__(384, 1)
 gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
-               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmX, int K, int brow0,
-               Epi epi) {
+               const __grid_constant__ CUtensorMap tmO, const __grid_constant__ CUtensorMap tmX,
+               const __grid_constant__ CUtensorMap tmV, int K, int brow0, Epi epi) {
   using L = GemmSmem<BN, STAGES, PAIR, TE>;
   constexpr int TM = PAIR ? 256 : 128;                 // rows of a (pair) tile
   extern __shared__ uint8_t smem_raw[];
@@ -83,7 +83,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     tma_prefetch(&tmB);
     if (TE) {
       tma_prefetch(&tmO);
-      if (epi.kind == EPI_RESID) tma_prefetch(&tmX);
+      if (epi.kind == EPI_RESID || epi.kind == EPI_QKV) tma_prefetch(&tmX);
+      if (epi.kind == EPI_QKV) tma_prefetch(&tmV);
     }
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
@@ -195,7 +196,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         // TMA-store epilogue: the warp's 32 rows x (128 B of output) go through a swizzled
         // staging buffer and leave as one bulk tensor store (coalesced, asynchronous); a
         // residual tile arrives the same way (TMA load into the buffer it is stored from).
-        const bool resid = epi.kind == EPI_RESID;
+        const bool resid = epi.kind == EPI_RESID, qkv = epi.kind == EPI_QKV;
         const int cw = (resid || epi.out_f32) ? 32 : 64;           // columns per 128-byte row
         const int sw = lane & 7;                                  // 128-byte swizzle phase of this row
 #pragma unroll 1
@@ -211,6 +212,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             tma_load_2d(buf, &tmX, &xbar[ew], n0 + c, m0 + q * 32);
           }
 #pragma unroll 1
+          // QKV: a 64-column chunk lies in one of Q / K / V (D % 64 == 0); V leaves transposed
+          const int region = qkv ? (n0 + c) / epi.D : 0;
           for (int h2 = 0; h2 < cw; h2 += 32) {
             float v[32];
             tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c + h2, reinterpret_cast<uint32_t*>(v));
@@ -228,7 +231,13 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               for (int i = 0; i < 32; ++i) v[i] += (n0 + c + h2 + i < epi.N) ? __ldg(pr + i) : 0.f;
             }
             uint8_t* row = buf + lane * 128;
-            if (resid || epi.out_f32) {
+            if (region == 2) {
+              // Vt boxes: 4 x [64 d][8 tokens] (1 KB each, token group lane / 8)
+              uint8_t* vb = buf + (lane >> 3) * 1024 + (lane & 7) * 2;
+#pragma unroll
+              for (int i = 0; i < 32; ++i)
+                *reinterpret_cast<bf16*>(vb + (h2 + i) * 16) = __float2bfloat16_rn(v[i]);
+            } else if (resid || epi.out_f32) {
               if (resid) {
                 mbar_wait(&xbar[ew], xphase);
                 xphase ^= 1u;
@@ -254,7 +263,22 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
-            tma_store_2d(&tmO, buf, n0 + c, m0 + q * 32);
+            if (region == 0) {
+              tma_store_2d(&tmO, buf, n0 + c, m0 + q * 32);
+            } else {
+              // K rows / Vt columns of the frame's memory slot, 8 tokens at a time (P % 8 == 0:
+              // a group never straddles two frames); rows past the chunk are not stored
+              for (int g8 = 0; g8 < 4; ++g8) {
+                const int r0 = m0 + q * 32 + g8 * 8;
+                if (r0 >= epi.M) break;
+                const int t = r0 / epi.P, p = r0 - t * epi.P;
+                const int krow = ((epi.first_slot + t) % epi.S) * epi.P + p;
+                if (region == 1)
+                  tma_store_2d(&tmX, buf + g8 * 1024, n0 + c - epi.D, epi.qkv_krow0 + krow);
+                else
+                  tma_store_2d(&tmV, buf + g8 * 1024, krow, epi.qkv_vrow0 + n0 + c - 2 * epi.D);
+              }
+            }
             bulk_commit();
           }
         }
@@ -301,7 +325,8 @@ static int g_num_sms = 0;
 
 template <int BN, int STAGES, bool PAIR, bool TE>
 static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
-                              const Epi& e, cudaStream_t st, const CUtensorMap* tmo, const CUtensorMap* tmx) {
+                              const Epi& e, cudaStream_t st, const CUtensorMap* tmo, const CUtensorMap* tmx,
+                              const CUtensorMap* tmv = nullptr) {
   using L = GemmSmem<BN, STAGES, PAIR, TE>;
   constexpr int CS = PAIR ? 2 : 1;
   auto kfn = gemm_tc_kernel<BN, STAGES, PAIR, TE>;
@@ -344,27 +369,28 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   cfg.attrs = at;
   cfg.numAttrs = 2;
   // unused output maps are passed as copies of the A map (never dereferenced)
-  return cudaLaunchKernelEx(&cfg, kfn, a, b, tmo ? *tmo : a, tmx ? *tmx : a, K, brow0, e);
+  return cudaLaunchKernelEx(&cfg, kfn, a, b, tmo ? *tmo : a, tmx ? *tmx : a, tmv ? *tmv : a, K, brow0, e);
 }
 
 // pair = 1: the CTA-pair kernel (M = 256 tiles; the W map's box must be 64 x BN/2).
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K, int bn,
                            const Epi& e, cudaStream_t st, int pair, const CUtensorMap* tmo,
-                           const CUtensorMap* tmx) {
-  if (tmo) {   // TMA-store epilogue (EPI_STORE / EPI_GELU / EPI_RESID)
-    if (e.kind != EPI_STORE && e.kind != EPI_GELU && e.kind != EPI_RESID) return cudaErrorInvalidValue;
-    if (e.kind == EPI_RESID && !tmx) return cudaErrorInvalidValue;
+                           const CUtensorMap* tmx, const CUtensorMap* tmv) {
+  if (tmo) {   // TMA-store epilogue (EPI_STORE / EPI_GELU / EPI_RESID / EPI_QKV)
+    if (e.kind == EPI_NONE) return cudaErrorInvalidValue;
+    if ((e.kind == EPI_RESID || e.kind == EPI_QKV) && !tmx) return cudaErrorInvalidValue;
+    if (e.kind == EPI_QKV && (!tmv || e.out_f32 || e.win_pad || e.P % 8 || e.D % 64)) return cudaErrorInvalidValue;
     if (pair) {
       switch (bn) {
-        case 128: return launch_cfg<128, 6, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
-        case 256: return launch_cfg<256, 4, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+        case 128: return launch_cfg<128, 6, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx, tmv);
+        case 256: return launch_cfg<256, 4, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx, tmv);
         default: return cudaErrorInvalidValue;
       }
     }
     switch (bn) {
-      case 64: return launch_cfg<64, 6, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
-      case 128: return launch_cfg<128, 4, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
-      case 256: return launch_cfg<256, 3, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx);
+      case 64: return launch_cfg<64, 6, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx, tmv);
+      case 128: return launch_cfg<128, 4, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx, tmv);
+      case 256: return launch_cfg<256, 3, false, true>(a, b, brow0, M, N, K, e, st, tmo, tmx, tmv);
       default: return cudaErrorInvalidValue;
     }
   }

@@ -59,10 +59,12 @@ cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D,
 // 2-SM MMA (W box 64 x BN/2).
 // tmo (optional): output tensor map (bf16 or fp32 [M][N], box 128 bytes x 32 rows, 128-byte
 // swizzle) -> the TMA-store epilogue for EPI_STORE / EPI_GELU / EPI_RESID (tmx: x_in map of
-// the same shape for EPI_RESID; x_out = the tmo tensor).
+// the same shape for EPI_RESID; x_out = the tmo tensor).  EPI_QKV: tmo = Q (box 64 x 32,
+// swizzled), tmx = the K slabs (box 64 x 8, swizzled), tmv = the Vt slabs (box 8 x 64, no
+// swizzle); global attention with P % 8 == 0 only.
 cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& w, int brow0, int M, int N, int K, int bn,
                            const Epi& e, cudaStream_t st, int pair = 0, const CUtensorMap* tmo = nullptr,
-                           const CUtensorMap* tmx = nullptr);
+                           const CUtensorMap* tmx = nullptr, const CUtensorMap* tmv = nullptr);
 // SIMT (fp32 path): A [M][K], W [N][K] row-major fp32, FFMA accumulate.
 cudaError_t launch_gemm_simt_f32(const float* A, const float* W, int M, int N, int K, const Epi& e, cudaStream_t st);
 
