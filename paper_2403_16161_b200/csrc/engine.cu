@@ -414,8 +414,8 @@ static vi_status validate(const vi_config* k, std::string* why) {
   if (k->win_h > 0) {
     if (k->dtype != VI_DTYPE_BF16) return bad("window attention: bf16 path only");
     if (oh % k->win_h || ow % k->win_w) return bad("window attention: windows must tile the token grid");
-    if (k->tp_size > 1 || k->nccl_id || k->ref_rate > 0)
-      return bad("window attention: no head sharding or reference frames (not built)");
+    if (k->ref_rate > 0) return bad("window attention: no reference frames (not built)");
+    if (k->tp_size > k->heads) return bad("window attention: head sharding needs tp_size <= heads");
   }
   const int G = k->tp_size < 1 ? 1 : k->tp_size;
   if (G > 1 || k->nccl_id) {
@@ -1042,12 +1042,14 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.Nq = c->win_n * a.win_qstride;   // rows of the KV-split partials (window-major)
   }
   if (c->sharded) {   // this rank's query rows, written head-major into its chunk of og
-    a.q_row0 = c->tp.row0();
-    a.Nq = c->tp.rows(M);
+    if (!c->win_n) {  // (windows: tp_size <= heads, every query row of the rank's heads)
+      a.q_row0 = c->tp.row0();
+      a.Nq = c->tp.rows(M);
+      if (a.Nq == 0) return VI_OK;   // a query part beyond a short chunk: nothing to attend
+    }
     a.o = static_cast<bf16*>(c->og) + (size_t)c->tp.rank * c->tp.chunk_elems;
     a.o_ld = c->hd;
     a.o_hs = c->tp.head_rows * c->hd;
-    if (a.Nq == 0) return VI_OK;   // a query part beyond a short chunk: nothing to attend
   }
   const int ntiles = a.segs.tile0[a.segs.n];
   a.opart = c->opart; a.lse = c->lse;

@@ -222,3 +222,11 @@ def test_split_phase_equals_memory_step_and_protocol():
     with pytest.raises(vi.ViError) as e:
         s.memory_step_ffn(0, xa, xa)               # _ffn before _attn
     assert e.value.status == vi.VI_E_PROTOCOL
+
+
+@pytest.mark.parametrize("G", [2, 4])
+def test_head_sharded_window_attention(G):
+    """Window attention (BASELINE configs[3]: heads sharded across GPUs with an all-gather of
+    the head outputs) on the reduced map: 10 x 18 tokens in 5 x 6 windows."""
+    cfg = CONFIGS["C3S"].replace(win_h=5, win_w=6)
+    _run_group(cfg, make_weights(cfg, seed=5, variant="sensitive"), G, ns=[2, 1, 2, 2])
