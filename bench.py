@@ -238,13 +238,17 @@ def run_ours(args, cfg):
     total_ms = sum(step_ms)
 
     # end to end through the public API with host (pinned) buffers, copies inside
-    host_in = [f.cpu().pin_memory() for f in feats]
-    host_out = torch.empty(out.shape, dtype=dt).pin_memory()
+    # (vi_run_step_async: the copies of a step overlap the neighbouring steps' compute, the
+    # way a live stream feeds the library; every step's H2D and D2H are inside the timed region)
     e2e_steps = max(3, min(args.steps, 50))
+    host_in = [f.cpu().pin_memory() for f in feats]
+    host_out = [torch.empty(out.shape, dtype=dt).pin_memory() for _ in range(e2e_steps)]
+    ctx.sync()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
     for k in range(e2e_steps):
-        ctx.run_step(host_in[k % nchunks], T, host_out)     # returns after the D2H landed
+        ctx.run_step_async(host_in[k % nchunks], T, host_out[k])
+    ctx.sync()                                           # every result has landed in host memory
     e2e_s = time.perf_counter() - t0
     clk = clocks.stop()
 
@@ -311,7 +315,8 @@ def run_ours(args, cfg):
                      "peak_source": f"{peak_src} bf16 dense (burst)",
                      "share_of_step": attn_ms / total_ms},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_in[0].numel() * 2,
-                "d2h_bytes_per_step": host_out.numel() * 2, "api": "vi_run_step (host buffers)"},
+                "d2h_bytes_per_step": host_out[0].numel() * 2,
+                "api": "vi_run_step_async (pinned host buffers; copies overlap neighbouring steps)"},
         "gpu_launches": launches,
         "clocks": clk,
     }

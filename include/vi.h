@@ -244,7 +244,14 @@ vi_status vi_memory_state(vi_ctx* ctx, int64_t* slot_id, uint8_t* refined, uint6
  * returns after the output has landed in host memory). */
 vi_status vi_run_step(vi_ctx* ctx, const void* feat, int n, void* out, int64_t* first_id);
 
-/* Wait for all work enqueued on the context stream. */
+/* vi_run_step, pipelined for live streams: returns after enqueue.  Host inputs are copied in
+ * and results copied out on a second stream through two device staging slots, so the
+ * copies of one step overlap the compute of the previous / next one.  The host buffers
+ * must stay valid (and out unread) until a later vi_sync; consecutive calls may reuse a
+ * buffer only after vi_sync.  Device buffers work as in vi_run_step (no copies). */
+vi_status vi_run_step_async(vi_ctx* ctx, const void* feat, int n, void* out, int64_t* first_id);
+
+/* Wait for all work enqueued on the context's streams. */
 vi_status vi_sync(vi_ctx* ctx);
 /* Last error message of this context (static storage inside the ctx; never NULL). */
 const char* vi_last_error(const vi_ctx* ctx);

@@ -168,6 +168,12 @@ struct vi_ctx {
   void *tokens = nullptr, *yp32 = nullptr, *w_back2 = nullptr, *h = nullptr, *q = nullptr, *o = nullptr, *u = nullptr, *gbuf = nullptr, *xb = nullptr;
   float *x_ws = nullptr, *fold_ws = nullptr, *opart = nullptr, *lse = nullptr;
   void *feat_in = nullptr, *feat_out = nullptr;
+  // vi_run_step_async: a copy stream and two staging slots (frames in, result out)
+  cudaStream_t io_stream = nullptr;
+  void *async_in[2] = {nullptr, nullptr}, *async_out[2] = {nullptr, nullptr};
+  cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
+  bool async_used[2] = {false, false};
+  int async_slot = 0;
   std::vector<void*> allocs;
   size_t device_bytes = 0;   // everything dalloc'd (weights, memory slabs, workspaces)
   // queued refine commits: device copies of the K/V payloads, applied at the next push.  A
@@ -247,6 +253,7 @@ struct vi_ctx {
 
 vi_ctx::~vi_ctx() {
   if (stream) cudaStreamSynchronize(stream);
+  if (io_stream) cudaStreamSynchronize(io_stream);
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   for (auto& r : prof_recs) {
     cudaEventDestroy(r.a);
@@ -264,6 +271,13 @@ vi_ctx::~vi_ctx() {
   if (ev_attn) cudaEventDestroy(ev_attn);
   if (ev_gather) cudaEventDestroy(ev_gather);
   if (copy_stream) cudaStreamDestroy(copy_stream);
+  if (io_stream) {
+    cudaStreamSynchronize(io_stream);
+    cudaStreamDestroy(io_stream);
+  }
+  for (int k = 0; k < 2; ++k)
+    for (cudaEvent_t e : {ev_h2d[k], ev_done[k], ev_d2h[k]})
+      if (e) cudaEventDestroy(e);
   if (own_stream && stream) cudaStreamDestroy(stream);
 }
 
@@ -1285,13 +1299,69 @@ static vi_status step_body(vi_ctx* c, const void* fin, int n, void* fout) {
   return vi_soft_composite(c, c->x_ws, n, fout, 1);
 }
 
+// Enqueue the device part of a step (after the push) on the ctx stream: replay of the step's
+// CUDA graph, captured on first use for this (shape, ring state, buffers, weights, profiling).
+static vi_status step_graph(vi_ctx* c, const void* fin, int n, void* fout) {
+  vi_status st;
+  const bool graphs = c->use_graphs && !g_debug_sync && c->prof_mode != 2 && !getenv("VI_ATTN_TRACE");
+  if (!graphs) return step_body(c, fin, n, fout);
+  // everything a replay bakes in: shapes, ring state, buffers, weights, profiling mode
+  std::vector<uint64_t> key = {uint64_t(n), uint64_t(c->ring.cur_first % c->S), c->ring.valid_mask(),
+                               uint64_t(reinterpret_cast<uintptr_t>(fin)), uint64_t(reinterpret_cast<uintptr_t>(fout)),
+                               uint64_t(c->prof_mode), uint64_t(c->weights_gen)};
+  vi_ctx::GraphEntry* hit = nullptr;
+  for (auto& g : c->graphs)
+    if (g.key == key) hit = &g;
+  if (!hit) {
+    const int64_t l0 = c->launches;
+    cudaGraph_t graph = nullptr;
+    CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+    st = step_body(c, fin, n, fout);
+    cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
+    if (st != VI_OK) {
+      if (graph) cudaGraphDestroy(graph);
+      return st;
+    }
+    if (ce != cudaSuccess) return c->cuda_fail(ce, "graph capture end");
+    cudaGraphExec_t exec = nullptr;
+    ce = cudaGraphInstantiate(&exec, graph, 0);
+    cudaGraphDestroy(graph);
+    if (ce != cudaSuccess) return c->cuda_fail(ce, "graph instantiate");
+    if (c->graphs.size() >= 32) {   // evict the least recently used
+      auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
+                                  [](const vi_ctx::GraphEntry& a, const vi_ctx::GraphEntry& b) {
+                                    return a.last_use < b.last_use;
+                                  });
+      cudaGraphExecDestroy(lru->exec);
+      c->graphs.erase(lru);
+    }
+    c->graphs.push_back({key, exec, c->launches - l0, 0});
+    c->launches = l0;
+    hit = &c->graphs.back();
+  } else {
+    c->next_layer = c->L;               // the host-side protocol state a replay skips
+    std::lock_guard<std::mutex> lk(c->mu);
+    c->ring.mark_stepped();
+  }
+  hit->last_use = ++c->graph_clock;
+  c->launches += hit->launches;
+  CK(cudaGraphLaunch(hit->exec, c->stream), "graph launch");
+  return VI_OK;
+}
+
+static vi_status check_run_step(vi_ctx* c, const void* feat, int n, const void* out, const char* who) {
+  if (!feat || !out || n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, std::string(who) + ": bad argument");
+  if (!c->have_weights) return c->fail(VI_E_PROTOCOL, std::string(who) + ": weights not set");
+  if (c->sharded && !c->comm)
+    return c->fail(VI_E_PROTOCOL, std::string(who) + ": head-sharded context without a communicator");
+  return VI_OK;
+}
+
 extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, int64_t* first_id) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  if (!feat || !out || n < 1 || n > c->Tmax) return c->fail(VI_E_ARG, "vi_run_step: bad argument");
-  if (!c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_run_step: weights not set");
-  if (c->sharded && !c->comm)
-    return c->fail(VI_E_PROTOCOL, "vi_run_step: head-sharded context without a communicator");
+  vi_status st = check_run_step(c, feat, n, out, "vi_run_step");
+  if (st != VI_OK) return st;
   const size_t fbytes = (size_t)n * c->g.H * c->g.W * c->g.C * c->es;
   const bool hin = is_host_ptr(feat), hout = is_host_ptr(out);
   const void* fin = feat;
@@ -1299,55 +1369,10 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
     CK(cudaMemcpyAsync(c->feat_in, feat, fbytes, cudaMemcpyHostToDevice, c->stream), "run_step h2d");
     fin = c->feat_in;
   }
-  vi_status st = vi_memory_push(c, n, first_id, nullptr, nullptr);   // host bookkeeping + queued commits
+  st = vi_memory_push(c, n, first_id, nullptr, nullptr);   // host bookkeeping + queued commits
   if (st != VI_OK) return st;
   void* fout = hout ? c->feat_out : out;
-  const bool graphs = c->use_graphs && !g_debug_sync && c->prof_mode != 2 && !getenv("VI_ATTN_TRACE");
-  if (!graphs) {
-    if ((st = step_body(c, fin, n, fout)) != VI_OK) return st;
-  } else {
-    // everything a replay bakes in: shapes, ring state, buffers, weights, profiling mode
-    std::vector<uint64_t> key = {uint64_t(n), uint64_t(c->ring.cur_first % c->S), c->ring.valid_mask(),
-                                 uint64_t(reinterpret_cast<uintptr_t>(fin)), uint64_t(reinterpret_cast<uintptr_t>(fout)),
-                                 uint64_t(c->prof_mode), uint64_t(c->weights_gen)};
-    vi_ctx::GraphEntry* hit = nullptr;
-    for (auto& g : c->graphs)
-      if (g.key == key) hit = &g;
-    if (!hit) {
-      const int64_t l0 = c->launches;
-      cudaGraph_t graph = nullptr;
-      CK(cudaStreamBeginCapture(c->stream, cudaStreamCaptureModeThreadLocal), "graph capture");
-      st = step_body(c, fin, n, fout);
-      cudaError_t ce = cudaStreamEndCapture(c->stream, &graph);
-      if (st != VI_OK) {
-        if (graph) cudaGraphDestroy(graph);
-        return st;
-      }
-      if (ce != cudaSuccess) return c->cuda_fail(ce, "graph capture end");
-      cudaGraphExec_t exec = nullptr;
-      ce = cudaGraphInstantiate(&exec, graph, 0);
-      cudaGraphDestroy(graph);
-      if (ce != cudaSuccess) return c->cuda_fail(ce, "graph instantiate");
-      if (c->graphs.size() >= 32) {   // evict the least recently used
-        auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
-                                    [](const vi_ctx::GraphEntry& a, const vi_ctx::GraphEntry& b) {
-                                      return a.last_use < b.last_use;
-                                    });
-        cudaGraphExecDestroy(lru->exec);
-        c->graphs.erase(lru);
-      }
-      c->graphs.push_back({key, exec, c->launches - l0, 0});
-      c->launches = l0;
-      hit = &c->graphs.back();
-    } else {
-      c->next_layer = c->L;               // the host-side protocol state a replay skips
-      std::lock_guard<std::mutex> lk(c->mu);
-      c->ring.mark_stepped();
-    }
-    hit->last_use = ++c->graph_clock;
-    c->launches += hit->launches;
-    CK(cudaGraphLaunch(hit->exec, c->stream), "graph launch");
-  }
+  if ((st = step_graph(c, fin, n, fout)) != VI_OK) return st;
   if (hout) {
     CK(cudaMemcpyAsync(out, c->feat_out, fbytes, cudaMemcpyDeviceToHost, c->stream), "run_step d2h");
     CK(cudaStreamSynchronize(c->stream), "run_step sync");
@@ -1355,10 +1380,62 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
   return VI_OK;
 }
 
+extern "C" vi_status vi_run_step_async(vi_ctx* c, const void* feat, int n, void* out, int64_t* first_id) {
+  LIVE(c);
+  DeviceGuard dg_(c->cfg.device);
+  vi_status st = check_run_step(c, feat, n, out, "vi_run_step_async");
+  if (st != VI_OK) return st;
+  if (!c->io_stream) {
+    if (cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking) != cudaSuccess) {
+      cudaGetLastError();
+      return c->fail(VI_E_CUDA, "vi_run_step_async: stream creation failed");
+    }
+    const size_t fmap = (size_t)c->Tmax * c->g.H * c->g.W * c->g.C * c->es;
+    for (int k = 0; k < 2; ++k) {
+      c->async_in[k] = c->dalloc(fmap, false);
+      c->async_out[k] = c->dalloc(fmap, false);
+      if (!c->async_in[k] || !c->async_out[k]) return c->fail(VI_E_OOM, "vi_run_step_async: staging allocation failed");
+      for (cudaEvent_t* e : {&c->ev_h2d[k], &c->ev_done[k], &c->ev_d2h[k]})
+        if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
+          return c->fail(VI_E_CUDA, "vi_run_step_async: event creation failed");
+    }
+  }
+  const size_t fbytes = (size_t)n * c->g.H * c->g.W * c->g.C * c->es;
+  const int k = c->async_slot;
+  c->async_slot ^= 1;
+  const bool hin = is_host_ptr(feat), hout = is_host_ptr(out);
+  // io stream: this slot's input staging is free once the step that read it (two calls ago)
+  // is done; copy the frames in
+  const void* fin = feat;
+  if (hin) {
+    if (c->async_used[k]) CK(cudaStreamWaitEvent(c->io_stream, c->ev_done[k], 0), "async wait");
+    CK(cudaMemcpyAsync(c->async_in[k], feat, fbytes, cudaMemcpyHostToDevice, c->io_stream), "async h2d");
+    CK(cudaEventRecord(c->ev_h2d[k], c->io_stream), "async record");
+    CK(cudaStreamWaitEvent(c->stream, c->ev_h2d[k], 0), "async wait");
+    fin = c->async_in[k];
+  }
+  // compute stream: the output staging is free once its previous copy-out is done
+  if (hout && c->async_used[k]) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[k], 0), "async wait");
+  st = vi_memory_push(c, n, first_id, nullptr, nullptr);
+  if (st != VI_OK) return st;
+  void* fout = hout ? c->async_out[k] : out;
+  if ((st = step_graph(c, fin, n, fout)) != VI_OK) return st;
+  CK(cudaEventRecord(c->ev_done[k], c->stream), "async record");
+  // io stream: copy the result out while the next step computes
+  if (hout) {
+    CK(cudaStreamWaitEvent(c->io_stream, c->ev_done[k], 0), "async wait");
+    CK(cudaMemcpyAsync(out, c->async_out[k], fbytes, cudaMemcpyDeviceToHost, c->io_stream), "async d2h");
+    CK(cudaEventRecord(c->ev_d2h[k], c->io_stream), "async record");
+  }
+  c->async_used[k] = true;
+  return VI_OK;
+}
+
 extern "C" vi_status vi_sync(vi_ctx* c) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
   CK(cudaStreamSynchronize(c->stream), "vi_sync");
+  if (c->io_stream) CK(cudaStreamSynchronize(c->io_stream), "vi_sync");
   return VI_OK;
 }
 

@@ -34,7 +34,7 @@ EXPORTS = ["vi_config_default", "vi_create", "vi_create_ex", "vi_destroy", "vi_s
            "vi_stream", "vi_debug_read", "vi_ring_create", "vi_ring_destroy", "vi_ring_push", "vi_ring_evict",
            "vi_ring_commit", "vi_ring_mark_stepped", "vi_ring_state", "vi_version", "vi_memory_step_attn",
            "vi_memory_step_ffn", "vi_tp_layout", "vi_tp_unique_id", "vi_tp_local_allgather", "vi_memory_footprint",
-           "vi_memory_read", "vi_ring_create_ex"]
+           "vi_memory_read", "vi_ring_create_ex", "vi_run_step_async"]
 
 
 class ViConfig(C.Structure):
@@ -70,6 +70,7 @@ _sig = {
     "vi_refine_commit": (C.c_int32, [_P, C.c_int64, _P, _P]),
     "vi_memory_state": (C.c_int32, [_P, _I64P, C.POINTER(C.c_uint8), C.POINTER(C.c_uint64)]),
     "vi_run_step": (C.c_int32, [_P, _P, C.c_int, _P, _I64P]),
+    "vi_run_step_async": (C.c_int32, [_P, _P, C.c_int, _P, _I64P]),
     "vi_sync": (C.c_int32, [_P]),
     "vi_last_error": (C.c_char_p, [_P]),
     "vi_kernel_launches": (C.c_int64, [_P]),
@@ -160,6 +161,12 @@ class Ring:
 
     def mark_stepped(self):
         _lib.vi_ring_mark_stepped(self._h)
+
+    def run_step_async(self, feat, n: int, out) -> int:
+        """vi_run_step_async: enqueue only; host buffers valid / unread until sync()."""
+        first = C.c_int64()
+        self._check(_lib.vi_run_step_async(self._h, _ptr(feat), n, _ptr(out), C.byref(first)), "vi_run_step_async")
+        return first.value
 
     def state(self):
         sid = (C.c_int64 * self.S)()

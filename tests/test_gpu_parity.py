@@ -412,3 +412,26 @@ def test_window_attention_c4_full_shape_step():
         _, ost = o.step(feats)
         _, gst = g.step(feats, stages=(i == 3))
     compare_step(cfg, ost, gst, 2e-2)
+
+
+def test_run_step_async_pipelined_equals_run_step():
+    """vi_run_step_async (copies on a second stream, two staging slots) == vi_run_step, bitwise,
+    over a sequence long enough to reuse both slots and wrap the ring."""
+    cfg = CONFIGS["C3S"].replace(layers=1)
+    w = make_weights(cfg, seed=14)
+    from paper_2403_16161_b200 import vi
+    a, b = vi.Context.from_synth(cfg), vi.Context.from_synth(cfg)
+    for c in (a, b):
+        c.set_weights(w)
+    steps = 7
+    host_in = [torch.from_numpy(make_features(cfg, cfg.t_new, first_frame=i * cfg.t_new, seed=14)).to(
+        torch.bfloat16).contiguous().pin_memory() for i in range(steps)]
+    outs_a = [torch.empty_like(h).pin_memory() for h in host_in]
+    outs_b = [torch.empty_like(h) for h in host_in]
+    for i in range(steps):
+        a.run_step_async(host_in[i], cfg.t_new, outs_a[i])
+        b.run_step(host_in[i], cfg.t_new, outs_b[i])
+    a.sync()
+    for i in range(steps):
+        assert torch.equal(outs_a[i], outs_b[i]), f"step {i}"
+    assert a.state() == b.state()
