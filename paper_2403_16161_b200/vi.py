@@ -162,12 +162,6 @@ class Ring:
     def mark_stepped(self):
         _lib.vi_ring_mark_stepped(self._h)
 
-    def run_step_async(self, feat, n: int, out) -> int:
-        """vi_run_step_async: enqueue only; host buffers valid / unread until sync()."""
-        first = C.c_int64()
-        self._check(_lib.vi_run_step_async(self._h, _ptr(feat), n, _ptr(out), C.byref(first)), "vi_run_step_async")
-        return first.value
-
     def state(self):
         sid = (C.c_int64 * self.S)()
         ref = (C.c_uint8 * self.S)()
@@ -314,6 +308,12 @@ class Context:
 
     def soft_composite(self, x, n: int, feat, project: int):
         self._check(_lib.vi_soft_composite(self._h, _ptr(x), n, _ptr(feat), project), "vi_soft_composite")
+
+    def run_step_async(self, feat, n: int, out) -> int:
+        """vi_run_step_async: enqueue only; host buffers valid / unread until sync()."""
+        first = C.c_int64()
+        self._check(_lib.vi_run_step_async(self._h, _ptr(feat), n, _ptr(out), C.byref(first)), "vi_run_step_async")
+        return first.value
 
     def run_step(self, feat, n: int, out) -> int:
         first = C.c_int64()
