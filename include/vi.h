@@ -245,7 +245,7 @@ vi_status vi_memory_state(vi_ctx* ctx, int64_t* slot_id, uint8_t* refined, uint6
 vi_status vi_run_step(vi_ctx* ctx, const void* feat, int n, void* out, int64_t* first_id);
 
 /* vi_run_step, pipelined for live streams: returns after enqueue.  Host inputs are copied in
- * and results copied out on a second stream through two device staging slots, so the
+ * and results copied out on two copy streams (in, out) through two device staging slots, so the
  * copies of one step overlap the compute of the previous / next one.  The host buffers
  * must stay valid (and out unread) until a later vi_sync; consecutive calls may reuse a
  * buffer only after vi_sync.  Device buffers work as in vi_run_step (no copies). */

@@ -168,8 +168,9 @@ struct vi_ctx {
   void *tokens = nullptr, *yp32 = nullptr, *w_back2 = nullptr, *h = nullptr, *q = nullptr, *o = nullptr, *u = nullptr, *gbuf = nullptr, *xb = nullptr;
   float *x_ws = nullptr, *fold_ws = nullptr, *opart = nullptr, *lse = nullptr;
   void *feat_in = nullptr, *feat_out = nullptr;
-  // vi_run_step_async: a copy stream and two staging slots (frames in, result out)
-  cudaStream_t io_stream = nullptr;
+  // vi_run_step_async: copy streams (frames in / results out: one stream for both would order
+  // step k+1's input copy behind step k's output copy, i.e. behind step k) and two staging slots
+  cudaStream_t io_stream = nullptr, io_out = nullptr;
   void *async_in[2] = {nullptr, nullptr}, *async_out[2] = {nullptr, nullptr};
   cudaEvent_t ev_h2d[2] = {nullptr, nullptr}, ev_done[2] = {nullptr, nullptr}, ev_d2h[2] = {nullptr, nullptr};
   bool async_used[2] = {false, false};
@@ -254,6 +255,7 @@ struct vi_ctx {
 vi_ctx::~vi_ctx() {
   if (stream) cudaStreamSynchronize(stream);
   if (io_stream) cudaStreamSynchronize(io_stream);
+  if (io_out) cudaStreamSynchronize(io_out);
   for (auto& g : graphs) cudaGraphExecDestroy(g.exec);
   for (auto& r : prof_recs) {
     cudaEventDestroy(r.a);
@@ -271,10 +273,8 @@ vi_ctx::~vi_ctx() {
   if (ev_attn) cudaEventDestroy(ev_attn);
   if (ev_gather) cudaEventDestroy(ev_gather);
   if (copy_stream) cudaStreamDestroy(copy_stream);
-  if (io_stream) {
-    cudaStreamSynchronize(io_stream);
-    cudaStreamDestroy(io_stream);
-  }
+  if (io_stream) cudaStreamDestroy(io_stream);
+  if (io_out) cudaStreamDestroy(io_out);
   for (int k = 0; k < 2; ++k)
     for (cudaEvent_t e : {ev_h2d[k], ev_done[k], ev_d2h[k]})
       if (e) cudaEventDestroy(e);
@@ -307,6 +307,13 @@ static const int g_attn_sk = [] {
   const char* e = getenv("VI_ATTN_SK");
   return e ? atoi(e) : 2;
 }();
+// VI_SK_TAIL_W: cost of a tail pair's key tile in 16ths of a full pair's (sk2 work split);
+// read when a step is recorded, so a sweep can change it between contexts
+static int sk_tail_weight() {
+  const char* e = getenv("VI_SK_TAIL_W");
+  const int w = e ? atoi(e) : 16;
+  return w < 1 ? 1 : (w > 64 ? 64 : w);
+}
 static void debug_wait(vi_ctx* c, const char* where) {
   for (int i = 0; i < 20000; ++i) {
     cudaError_t e = cudaStreamQuery(c->stream);
@@ -1080,6 +1087,15 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.units = a.npairs * a.H;
     a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
     const long long work = (long long)a.units * ntiles;
+    // sk2: a last pair with an empty second tile (C3: 3600 = 14 x 256 + 16) skips tile 1's
+    // MMAs and the dead softmax quadrants, but its key tiles still cost about a full pair's
+    // (the per-tile chain QK -> softmax -> PV is the bound, not the work): VI_SK_TAIL_W = 16
+    // (measured: 8 -> +46 % attention time, 10 -> +22 %)
+    const int rem = a.Nq % 256;
+    a.sk_tail = (g_attn_sk == 2 && rem > 0 && rem <= 128) ? 1 : 0;
+    a.sk_tail_w = 16;
+    if (a.sk_tail) a.sk_tail_w = sk_tail_weight();
+    a.sk_wfull = (long long)(a.npairs - a.sk_tail) * a.H * ntiles;
     int grid = int(work < c->num_sms ? work : c->num_sms);
     if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
     if (g_attn_sk == 1)
@@ -1386,7 +1402,8 @@ extern "C" vi_status vi_run_step_async(vi_ctx* c, const void* feat, int n, void*
   vi_status st = check_run_step(c, feat, n, out, "vi_run_step_async");
   if (st != VI_OK) return st;
   if (!c->io_stream) {
-    if (cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking) != cudaSuccess) {
+    if (cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking) != cudaSuccess ||
+        cudaStreamCreateWithFlags(&c->io_out, cudaStreamNonBlocking) != cudaSuccess) {
       cudaGetLastError();
       return c->fail(VI_E_CUDA, "vi_run_step_async: stream creation failed");
     }
@@ -1423,9 +1440,9 @@ extern "C" vi_status vi_run_step_async(vi_ctx* c, const void* feat, int n, void*
   CK(cudaEventRecord(c->ev_done[k], c->stream), "async record");
   // io stream: copy the result out while the next step computes
   if (hout) {
-    CK(cudaStreamWaitEvent(c->io_stream, c->ev_done[k], 0), "async wait");
-    CK(cudaMemcpyAsync(out, c->async_out[k], fbytes, cudaMemcpyDeviceToHost, c->io_stream), "async d2h");
-    CK(cudaEventRecord(c->ev_d2h[k], c->io_stream), "async record");
+    CK(cudaStreamWaitEvent(c->io_out, c->ev_done[k], 0), "async wait");
+    CK(cudaMemcpyAsync(out, c->async_out[k], fbytes, cudaMemcpyDeviceToHost, c->io_out), "async d2h");
+    CK(cudaEventRecord(c->ev_d2h[k], c->io_out), "async record");
   }
   c->async_used[k] = true;
   return VI_OK;
@@ -1436,6 +1453,7 @@ extern "C" vi_status vi_sync(vi_ctx* c) {
   DeviceGuard dg_(c->cfg.device);
   CK(cudaStreamSynchronize(c->stream), "vi_sync");
   if (c->io_stream) CK(cudaStreamSynchronize(c->io_stream), "vi_sync");
+  if (c->io_out) CK(cudaStreamSynchronize(c->io_out), "vi_sync");
   return VI_OK;
 }
 

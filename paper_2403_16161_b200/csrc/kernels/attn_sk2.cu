@@ -11,6 +11,12 @@
 // = w % 4), warp 16 TMA producer, warp 17 TMEM allocator + MMA issuer.
 #include "kernels.h"
 
+// SK2_EXPERIMENT (micro-benchmark builds only): 1 = softmax warps skip the math (MMA + TMA
+// pipeline alone), 2 = no MMAs issued (softmax chain alone)
+#ifndef SK2_EXPERIMENT
+#define SK2_EXPERIMENT 0
+#endif
+
 namespace vi {
 
 template <int HD>
@@ -46,8 +52,26 @@ __device__ __forceinline__ void sk2_bar_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-// slice of the flattened work [0, W) owned by CTA c of G
-__device__ __forceinline__ long long sk2_begin(long long W, int G, int c) { return W * c / G; }
+// slice of the flattened work [0, W) owned by CTA c of G: an even split of the COST, where
+// the work items of the tail units (ordered last) cost sk_tail_w / 16 of a full unit's
+__device__ __forceinline__ long long sk2_begin(const AttnTC& a, long long W, int G, int c) {
+  const long long wf = a.sk_wfull, tw = a.sk_tail_w;
+  const long long cost = (wf * 16 + (W - wf) * tw) * c / G;
+  return cost <= wf * 16 ? cost / 16 : wf + (cost - wf * 16) / tw;
+}
+
+// unit u -> (head, first query row of its pair); tail units (if any) are the last H
+__device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0) {
+  const int full = a.npairs - a.sk_tail;     // full pairs per head
+  const int uf = full * a.H;
+  if (u < uf) {
+    h = u / full;
+    q0 = (u - h * full) * 256;
+  } else {
+    h = u - uf;
+    q0 = full * 256;
+  }
+}
 
 template <int HD>
 __global__ void __launch_bounds__(576, 1)
@@ -74,7 +98,12 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   const int NT = a.segs.tile0[a.segs.n];
   const long long W = (long long)a.units * NT;
   const int G = gridDim.x, cta = blockIdx.x;
-  const long long w_begin = sk2_begin(W, G, cta), w_end = sk2_begin(W, G, cta + 1);
+  const long long w_begin = sk2_begin(a, W, G, cta), w_end = sk2_begin(a, W, G, cta + 1);
+  // per-CTA stamps (micro-benchmarks): 0 entry, 1 setup done, 2 first QK issued, 3 last
+  // o_final committed, 4 last epilogue start, 5 owner flags seen, 6 exit, 7 segments,
+  // 8..11 MMA warp: each segment's o_final commit (first 4)
+  long long* const ct = a.cta_trace ? a.cta_trace + (size_t)cta * 16 : nullptr;
+  if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
 
   if (warp == 16 && lane == 0) {
     tma_prefetch(&tq);
@@ -103,6 +132,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   if (threadIdx.x == 0) time_begin(a.timing);
+  if (ct && threadIdx.x == 0) ct[1] = (long long)globaltimer();
   // debug timeline (VI_SK_TRACE): CTA 0, first segment's first 32 key tiles, 32 clock64 stamps per tile
   long long* const trc = (a.trace && cta == 0) ? a.trace : nullptr;
 
@@ -112,7 +142,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     for (long long w = w_begin; w < w_end; ++sg) {
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
-      const int h = u / a.npairs, q0 = (u - h * a.npairs) * 256;
+      int h, q0;
+      sk2_unit(a, u, h, q0);
       if (sg > 0) mbar_wait(q_empty, (sg - 1) & 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(q_full, 2 * L::QB);
@@ -162,6 +193,10 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
+      int h_, q0;
+      sk2_unit(a, u, h_, q0);
+      const bool t1_live = q0 + 128 < a.Nq && SK2_EXPERIMENT != 2;   // tile 1 of a tail pair: commits only
+      const bool t0_live = SK2_EXPERIMENT != 2;
       mbar_wait(q_full, sg & 1);
       auto issue_pv = [&](int t, int j) {          // O_t (+)= P_t(j) V(j), j local to the segment
         const int g = jg + j, st = g % ST;
@@ -174,10 +209,12 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           tc_fence_after();
           if (elect_one()) {
             if (trc && g < 32) trc[g * 32 + 20 + hh * 6 + t] = clock64();
+            if (t == 0 ? t0_live : t1_live) {
 #pragma unroll
-            for (int k4 = 0; k4 < 4; ++k4)
-              umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + hh * 64 + k4 * 8,
-                           dv + uint64_t((hh * (HD * 128) + k4 * 32) >> 4), idesc_o, (j | hh | k4) != 0);
+              for (int k4 = 0; k4 < 4; ++k4)
+                umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + hh * 64 + k4 * 8,
+                             dv + uint64_t((hh * (HD * 128) + k4 * 32) >> 4), idesc_o, (j | hh | k4) != 0);
+            }
             if (hh == 1 && t == 1) umma_commit(&v_empty[st]);
           }
           __syncwarp();
@@ -191,13 +228,16 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         const uint64_t dk = dk0 + uint64_t((st * L::KB) >> 4), dq = dq0 + uint64_t((t * L::QB) >> 4);
         if (elect_one()) {
+          if (t == 0 ? t0_live : t1_live) {
 #pragma unroll
-          for (int kk = 0; kk < HD / 16; ++kk) {
-            const uint64_t off = uint64_t(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
-            umma_bf16_ss(tmem + t * 128, dq + off, dk + off, idesc_s, kk > 0);
+            for (int kk = 0; kk < HD / 16; ++kk) {
+              const uint64_t off = uint64_t(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+              umma_bf16_ss(tmem + t * 128, dq + off, dk + off, idesc_s, kk > 0);
+            }
           }
           umma_commit(&s_full[t]);
           if (trc && g < 32) trc[g * 32 + 24 + t] = clock64();
+          if (ct && g == 0 && t == 0) ct[2] = (long long)globaltimer();
           if (t == 1) umma_commit(&k_empty[st]);
         }
         __syncwarp();
@@ -213,6 +253,12 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         issue_pv(t, n - 1);
         if (elect_one()) umma_commit(&o_final[t]);
         __syncwarp();
+      }
+      if (ct && lane == 0) {
+        const long long now = (long long)globaltimer();
+        ct[3] = now;
+        if (sg < 4) ct[8 + sg] = now;
+        ct[7] = sg + 1;
       }
       jg += n;
       w += n;
@@ -242,13 +288,21 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
-      const int h = u / a.npairs, q0 = (u - h * a.npairs) * 256;
+      int h, q0;
+      sk2_unit(a, u, h, q0);
+      // all 32 rows of this warp past Nq (a tail pair): keep the barrier phases, skip the math
+      // (their P / O lanes hold garbage that only reaches rows never stored)
+      const bool dead = q0 + t * 128 + qd * 32 >= a.Nq || SK2_EXPERIMENT == 1;
       float m_use = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         const int g = jg + j;
+        mbar_wait(&s_full[t], g & 1);
+        if (dead) {
+          mbar_arrive(&p_full[2 * t + hf]);
+          continue;
+        }
         int row0, nv, nskip;
         sk2_key_tile(a.segs, ta + j, row0, nv, nskip);
-        mbar_wait(&s_full[t], g & 1);
         tc_fence_after();
         const bool tr = trc && lane == 0 && g < 32;
         if (tr && hf == 0 && qd == 0) trc[g * 32 + 0 + t] = clock64();
@@ -326,6 +380,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       // ---- segment epilogue: each warp owns O columns [hf*64, +64) of its 32 rows
       mbar_wait(&o_final[t], sg & 1);
       tc_fence_after();
+      if (ct && warp == 0 && lane == 0) ct[4] = (long long)globaltimer();
       l += exchange(l);                             // row sum over both key halves
       const int r256 = t * 128 + row;               // row in the CTA's 256-row slot
       const float lse_own = m_use + __log2f(l);
@@ -377,7 +432,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         // CTAs cta+1 .. (the unit's last tile) in CTA order
         const long long unit_end = (long long)(u + 1) * NT;
         int last = cta + 1;
-        while (last + 1 < G && sk2_begin(W, G, last + 1) < unit_end) ++last;
+        while (last + 1 < G && sk2_begin(a, W, G, last + 1) < unit_end) ++last;
         const int np = last - cta;
         for (int k = lane; k < np; k += 32) {
           const int* fl = a.sflag + cta + 1 + k;
@@ -385,6 +440,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         __syncwarp();
         __threadfence();
+        if (ct && warp == 0 && lane == 0) ct[5] = (long long)globaltimer();
         float mx = lse_own;
         for (int k = 0; k < np; ++k) mx = fmaxf(mx, __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256));
         const float wown = ex2(lse_own - mx);
@@ -456,6 +512,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   tc_fence_before();
   __syncthreads();
   if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
+  if (ct && threadIdx.x == 0) ct[6] = (long long)globaltimer();
   if (warp == 17) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);

@@ -107,10 +107,17 @@ struct AttnTC {
   // split evenly over the persistent grid; partial results of split units go through
   // spart/slse/sflag (one slot per CTA) and are merged by the unit's first CTA.
   int npairs, units;
+  // attn_sk2 only: when the last query pair of every head has an empty second tile
+  // (Nq mod 256 in (0, 128]), those H "tail" units are ordered last (sk_tail = 1) and the
+  // work split weights their key tiles sk_tail_w / 16 of a full pair's (tile 1 and the
+  // softmax quadrants past Nq are skipped); sk_wfull = work items of the full units.
+  int sk_tail, sk_tail_w;
+  long long sk_wfull;
   float* spart;             // [grid][256][hd]
   float* slse;              // [grid][256]
   int* sflag;               // [grid], 0 between launches
   long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
+  long long* cta_trace;     // attn_sk2: [grid][16] globaltimer stamps per CTA (micro-benchmarks; NULL = off)
   unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves
   int H;
   // stream-K kernels (attn_sk, attn_sk2): query rows start at row q_row0 of the Q map;

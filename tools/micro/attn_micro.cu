@@ -74,11 +74,16 @@ int main(int argc, char** argv) {
   a.o = reinterpret_cast<bf16*>(o); a.o_ld = D; a.o_hs = HD; a.q_row0 = 0;
   a.npairs = (Nq + 255) / 256;
   a.units = a.npairs * H;
-  cudaMalloc(&a.spart, (size_t)nsm * 256 * HD * 4);
-  cudaMalloc(&a.slse, (size_t)nsm * 256 * 4);
-  cudaMalloc(&a.sflag, (size_t)nsm * 4);
-  cudaMemset(a.sflag, 0, (size_t)nsm * 4);
+  cudaMalloc(&a.spart, (size_t)nsm * 2 * 256 * HD * 4);
+  cudaMalloc(&a.slse, (size_t)nsm * 2 * 256 * 4);
+  cudaMalloc(&a.sflag, (size_t)(nsm * 2 + a.units + 8) * 4);
+  cudaMemset(a.sflag, 0, (size_t)(nsm * 2 + a.units + 8) * 4);
   const long long work = (long long)a.units * a.segs.tile0[1];
+  // sk2 tail ordering (engine.cu): the last pair of each head has an empty second tile
+  const int rem = Nq % 256;
+  a.sk_tail = (ver == 2 && rem > 0 && rem <= 128) ? 1 : 0;
+  a.sk_tail_w = a.sk_tail && getenv("VI_SK_TAIL_W") ? atoi(getenv("VI_SK_TAIL_W")) : 16;
+  a.sk_wfull = (long long)(a.npairs - a.sk_tail) * H * a.segs.tile0[1];
   int grid = int(work < nsm ? work : nsm);
   if (grid_override > 0) grid = grid_override;
   cudaStream_t st;
@@ -96,6 +101,29 @@ int main(int argc, char** argv) {
   const double flop = 4.0 * Nq * SP * D, us = 1e3 * ms / iters;
   printf("attn_sk%d C3: grid %d, %.2f us/launch, %.1f TFLOP/s (%s)\n", ver, grid, us, flop / (us * 1e-6) / 1e12,
          cudaGetErrorString(err));
+  if (getenv("CTA_TRACE")) {   // per-CTA globaltimer stamps of one launch
+    long long* ctb;
+    cudaMalloc(&ctb, (size_t)grid * 16 * 8);
+    cudaMemset(ctb, 0, (size_t)grid * 16 * 8);
+    a.cta_trace = ctb;
+    launch(a, grid, st);
+    cudaStreamSynchronize(st);
+    a.cta_trace = nullptr;
+    std::vector<long long> h((size_t)grid * 16);
+    cudaMemcpy(h.data(), ctb, h.size() * 8, cudaMemcpyDeviceToHost);
+    long long t0 = LLONG_MAX;
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 16]);
+    printf("cta: entry setup firstQK lastOfinal lastEpi ownerFlags exit nseg | segment o_final (ns from first entry)\n");
+    for (int c = 0; c < grid; ++c) {
+      const long long* e = &h[c * 16];
+      printf("%3d:", c);
+      for (int i = 0; i < 7; ++i) printf(" %6lld", e[i] ? e[i] - t0 : -1);
+      printf(" %lld |", e[7]);
+      for (int i = 0; i < e[7] && i < 4; ++i) printf(" %6lld", e[8 + i] - t0);
+      printf(" | piece published %6lld owner staged %6lld", e[12] ? e[12] - t0 : -1, e[13] ? e[13] - t0 : -1);
+      printf("\n");
+    }
+  }
   if (trace) {
     long long* tb;
     cudaMalloc(&tb, 32 * 32 * sizeof(long long));
