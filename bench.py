@@ -220,9 +220,15 @@ def run_ours(args, cfg):
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ctx.profile(int(os.environ.get("VI_PROFILE_MODE", "1")))   # attention kernels timed with events
+    ctx.run_step(feats[0], T, out)     # untimed: records + uploads this profile mode's step graph
+    ctx.profile_read()                 # (and resets the kernel self-timing)
     l0 = ctx.launches()
     streams.barrier()
     torch.cuda.synchronize()
+    # an untimed ~25 ms device sleep lets the host queue the steps ahead of the GPU, so a host
+    # hiccup (the clock sampler's process, GC) never leaves the stream idle inside a step
+    with torch.cuda.stream(stream):
+        torch.cuda._sleep(int(5e7))
     for k in range(args.steps):
         with torch.cuda.stream(stream):
             flush.fill_(float(k))                   # untimed L2 flush
@@ -307,7 +313,8 @@ def run_ours(args, cfg):
         "config": workload_config(cfg, args, world),
         "fps_per_stream": value / n_streams,
         "step_latency_ms": {"p50": statistics.median(step_ms), "p5": sorted(step_ms)[int(0.05 * len(step_ms))],
-                            "p95": sorted(step_ms)[min(len(step_ms) - 1, int(0.95 * len(step_ms)))]},
+                            "p95": sorted(step_ms)[min(len(step_ms) - 1, int(0.95 * len(step_ms)))],
+                            "max": max(step_ms)},
         "roofline": {"kernel": "memory attention (attn_sk2_kernel, persistent stream-K, column-split softmax), per block",
                      "bound": "tensor", "achieved": achieved, "peak": bf16_peak, "unit": "TFLOP/s",
                      "frac": achieved / bf16_peak, "traffic": traffic,

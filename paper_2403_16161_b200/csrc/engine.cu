@@ -314,6 +314,13 @@ static int sk_tail_weight() {
   const int w = e ? atoi(e) : 16;
   return w < 1 ? 1 : (w > 64 ? 64 : w);
 }
+// VI_SK_UNIT_COST: split cost of a unit's start in 16ths of a pair key tile (the CTA that
+// begins a unit switches segments and merges the unit's pieces at the end)
+static int sk_unit_cost() {
+  const char* e = getenv("VI_SK_UNIT_COST");
+  const int b = e ? atoi(e) : 32;   // measured: 0 -> 86.9 us, 32 -> 85.5, 64 -> 85.9, 96 -> 87.6 (C3 micro)
+  return b < 0 ? 0 : (b > 4096 ? 4096 : b);
+}
 static void debug_wait(vi_ctx* c, const char* where) {
   for (int i = 0; i < 20000; ++i) {
     cudaError_t e = cudaStreamQuery(c->stream);
@@ -1095,6 +1102,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.sk_tail = (g_attn_sk == 2 && rem > 0 && rem <= 128) ? 1 : 0;
     a.sk_tail_w = 16;
     if (a.sk_tail) a.sk_tail_w = sk_tail_weight();
+    a.sk_ucost = sk_unit_cost();
     a.sk_wfull = (long long)(a.npairs - a.sk_tail) * a.H * ntiles;
     int grid = int(work < c->num_sms ? work : c->num_sms);
     if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));

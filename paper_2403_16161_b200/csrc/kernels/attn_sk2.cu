@@ -29,7 +29,7 @@ struct AttnSk2Smem {
   static constexpr int K_OFF = 2 * QB;
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
-  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2;
+  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2 + 2;   // + merge_full[2]
   static constexpr int STG_OFF = BAR_OFF + NBAR * 8 + 16;      // [16 warps][32 rows][48 B] output staging
   static constexpr int XCH_OFF = STG_OFF + 16 * 32 * 48;        // [2 phases][2 tiles][2 halves][128] fp32
   static constexpr int TOTAL = XCH_OFF + 2 * 2 * 2 * 128 * 4 + 1024;
@@ -53,11 +53,21 @@ __device__ __forceinline__ void sk2_bar_sync(int id, int n) {
 }
 
 // slice of the flattened work [0, W) owned by CTA c of G: an even split of the COST, where
-// the work items of the tail units (ordered last) cost sk_tail_w / 16 of a full unit's
+// a unit costs sk_ucost (its start: the owner's segment switch and merge) + 16 per key tile,
+// and the key tiles of the tail units (ordered last) sk_tail_w each
 __device__ __forceinline__ long long sk2_begin(const AttnTC& a, long long W, int G, int c) {
-  const long long wf = a.sk_wfull, tw = a.sk_tail_w;
-  const long long cost = (wf * 16 + (W - wf) * tw) * c / G;
-  return cost <= wf * 16 ? cost / 16 : wf + (cost - wf * 16) / tw;
+  if (c >= G) return W;
+  const long long NT = W / a.units, B = a.sk_ucost, tw = a.sk_tail_w;
+  const long long uf = a.sk_wfull / NT;                 // full units
+  const long long ucf = B + 16 * NT, uct = B + tw * NT;
+  const long long cf = uf * ucf;
+  const long long x = (cf + (a.units - uf) * uct) * c / G;
+  if (x < cf) {
+    const long long u = x / ucf, r = x - u * ucf;
+    return u * NT + (r <= B ? 0 : (r - B) / 16);
+  }
+  const long long u = (x - cf) / uct, r = x - cf - u * uct;
+  return (uf + u) * NT + (r <= B ? 0 : (r - B) / tw);
 }
 
 // unit u -> (head, first query row of its pair); tail units (if any) are the last H
@@ -92,7 +102,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint64_t* p_full = s_full + 2;      // [2 tiles][2 key halves]
   uint64_t* o_final = p_full + 4;     // [2] all PV of a segment done
   uint64_t* o_free = o_final + 2;     // [2] O read out by the epilogue
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
+  uint64_t* merge_full = o_free + 2;  // [2] bulk loads of a split unit's pieces, per O column half
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_full + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NT = a.segs.tile0[a.segs.n];
@@ -101,7 +112,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   const long long w_begin = sk2_begin(a, W, G, cta), w_end = sk2_begin(a, W, G, cta + 1);
   // per-CTA stamps (micro-benchmarks): 0 entry, 1 setup done, 2 first QK issued, 3 last
   // o_final committed, 4 last epilogue start, 5 owner flags seen, 6 exit, 7 segments,
-  // 8..11 MMA warp: each segment's o_final commit (first 4)
+  // 8..11 MMA warp: each segment's o_final commit (first 4), 12 continuation piece
+  // published, 13 owner's merge done
   long long* const ct = a.cta_trace ? a.cta_trace + (size_t)cta * 16 : nullptr;
   if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
 
@@ -123,6 +135,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       mbar_init(&p_full[2 * t + 1], 128);
       mbar_init(&o_final[t], 1);
       mbar_init(&o_free[t], 256);
+      mbar_init(&merge_full[t], 1);
     }
     fence_barrier_init();
   }
@@ -406,10 +419,20 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         __syncwarp();
       };
+      // the CTA's last segment: the K/V stages are idle -> staging for the owner's bulk loads of
+      // the pieces, one 64 KB buffer per O column half (K stages: half 0, V stages: half 1),
+      // [col/4][256] float4 like the slots (bulk stores of the pieces measured slower than
+      // direct stores: 3.2 us for 128 KB per SM with ~90 CTAs storing at once)
+      const bool last_seg = w + n == w_end;
+      uint8_t* const hbuf = smem + (hf == 0 ? L::K_OFF : L::V_OFF);
+      constexpr uint32_t HBYTES = (HD / 2) * 256 * 4;     // one column half of a 256-row partial
+      const bool hissuer = (warp & 11) == 0 && lane == 0;  // warp 0 (half 0) / warp 4 (half 1)
+      // (the other Q tile's last PV may still be reading a V stage: both tiles done first)
+      if (last_seg && ta == 0 && tb < NT) mbar_wait(&o_final[t ^ 1], sg & 1);
       if (ta > 0) {
         // continuation piece: normalised partial -> this CTA's slot, then raise the flag
-        float4* dst = reinterpret_cast<float4*>(a.spart) + (size_t)cta * (HD / 4) * 256 + r256;
         const float inv = 1.f / l;
+        float4* dst = reinterpret_cast<float4*>(a.spart) + (size_t)cta * (HD / 4) * 256 + r256;
 #pragma unroll 1
         for (int c = 0; c < OH; c += 32) {
           float f[32];
@@ -426,6 +449,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         if (threadIdx.x == 0) {                      // ... then one cumulative gpu-scope release
           __threadfence();
           atomicExch(&a.sflag[cta], 1);
+          if (ct) ct[12] = (long long)globaltimer();
         }
       } else if (tb < NT) {
         // owner of a split unit (always the last segment of this CTA): merge the pieces of
@@ -440,29 +464,30 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         __syncwarp();
         __threadfence();
+        fence_proxy_async_global();                  // the pieces are read through the async proxy
         if (ct && warp == 0 && lane == 0) ct[5] = (long long)globaltimer();
+        // bulk-load piece k's column half of this thread group into its staging buffer
+        auto load_piece = [&](int k) {
+          const uint8_t* src = reinterpret_cast<const uint8_t*>(a.spart) +
+                               ((size_t)(cta + 1 + k) * (HD / 4) * 256 + (size_t)hf * (OH / 4) * 256) * 16;
+          fence_proxy_async_smem();
+          mbar_arrive_expect_tx(&merge_full[hf], HBYTES);
+          for (uint32_t off = 0; off < HBYTES; off += 32768)
+            bulk_g2s(hbuf + off, src + off, HBYTES - off < 32768 ? HBYTES - off : 32768, &merge_full[hf]);
+        };
+        if (hissuer) load_piece(0);
         float mx = lse_own;
         for (int k = 0; k < np; ++k) mx = fmaxf(mx, __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256));
         const float wown = ex2(lse_own - mx);
         float wsum = wown;
         for (int k = 0; k < np; ++k) wsum += ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
         const float inv_w = 1.f / wsum;
-        float4* stage = reinterpret_cast<float4*>(smem + L::K_OFF);   // idle K/V stages (128 KB)
+        const float4* stage = reinterpret_cast<const float4*>(hbuf);   // this half's columns
         float scale = wown / l;
-        const int etid = threadIdx.x;               // 0..511 (softmax warps)
 #pragma unroll 1
         for (int k = 0; k < np; ++k) {
-          const float4* src = reinterpret_cast<const float4*>(a.spart) + (size_t)(cta + 1 + k) * (HD / 4) * 256;
-#pragma unroll 1
-          for (int i0 = 0; i0 < (HD / 4) * 256; i0 += 512 * 8) {
-            float4 r[8];
-#pragma unroll
-            for (int e = 0; e < 8; ++e) r[e] = __ldcg(src + i0 + e * 512 + etid);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) stage[i0 + e * 512 + etid] = r[e];
-          }
-          sk2_bar_sync(10, 512);
           const float wk = ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
+          mbar_wait(&merge_full[hf], k & 1);
 #pragma unroll 1
           for (int c = 0; c < OH; c += 32) {
             float f[32];
@@ -470,7 +495,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             tmem_wait_ld();
 #pragma unroll
             for (int q4 = 0; q4 < 8; ++q4) {
-              const float4 v = stage[((hf * OH + c) / 4 + q4) * 256 + r256];
+              const float4 v = stage[(c / 4 + q4) * 256 + r256];
               f[4 * q4] = f[4 * q4] * scale + wk * v.x;
               f[4 * q4 + 1] = f[4 * q4 + 1] * scale + wk * v.y;
               f[4 * q4 + 2] = f[4 * q4 + 2] * scale + wk * v.z;
@@ -480,8 +505,12 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             tmem_wait_st();
           }
           scale = 1.f;
-          sk2_bar_sync(10, 512);                     // stage free for the next slot
+          if (k + 1 < np) {                          // this half's buffer read: load the next piece
+            sk2_named_bar_sync(13 + hf, 256);
+            if (hissuer) load_piece(k + 1);
+          }
         }
+        if (ct && warp == 0 && lane == 0) ct[13] = (long long)globaltimer();
 #pragma unroll 1
         for (int c = 0; c < OH; c += 16) {
           float f[16];

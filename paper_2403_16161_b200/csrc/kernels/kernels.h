@@ -112,6 +112,7 @@ struct AttnTC {
   // work split weights their key tiles sk_tail_w / 16 of a full pair's (tile 1 and the
   // softmax quadrants past Nq are skipped); sk_wfull = work items of the full units.
   int sk_tail, sk_tail_w;
+  int sk_ucost;              // attn_sk2 split cost of a unit's start (16 = one key tile of a pair)
   long long sk_wfull;
   float* spart;             // [grid][256][hd]
   float* slse;              // [grid][256]

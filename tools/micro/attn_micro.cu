@@ -84,6 +84,7 @@ int main(int argc, char** argv) {
   a.sk_tail = (ver == 2 && rem > 0 && rem <= 128) ? 1 : 0;
   a.sk_tail_w = a.sk_tail && getenv("VI_SK_TAIL_W") ? atoi(getenv("VI_SK_TAIL_W")) : 16;
   a.sk_wfull = (long long)(a.npairs - a.sk_tail) * H * a.segs.tile0[1];
+  a.sk_ucost = getenv("VI_SK_UNIT_COST") ? atoi(getenv("VI_SK_UNIT_COST")) : 0;
   int grid = int(work < nsm ? work : nsm);
   if (grid_override > 0) grid = grid_override;
   cudaStream_t st;
