@@ -29,10 +29,14 @@ struct AttnSk2Smem {
   static constexpr int K_OFF = 2 * QB;
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
-  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2 + 2;   // + merge_full[2]
+  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2 + 12;   // + merge_full / merge_empty [2 halves][3]
   static constexpr int STG_OFF = BAR_OFF + NBAR * 8 + 16;      // [16 warps][32 rows][48 B] output staging
   static constexpr int XCH_OFF = STG_OFF + 16 * 32 * 48;        // [2 phases][2 tiles][2 halves][128] fp32
-  static constexpr int TOTAL = XCH_OFF + 2 * 2 * 2 * 128 * 4 + 1024;
+  static constexpr int LSE_OFF = XCH_OFF + 2 * 2 * 2 * 128 * 4;   // [2 halves][2 piece parities][256] fp32 (merge)
+  static constexpr int TOTAL = LSE_OFF + 2 * 2 * 256 * 4 + 1024;
+  // owner merge: 32 KB chunk buffers over the idle Q / K / V smem, NBH per O column half
+  static constexpr int NBH = (3 * 512 * HD / 32768) / 2 > 3 ? 3 : (3 * 512 * HD / 32768) / 2;
+  static constexpr int CPP = HD / 64;                           // 32-column chunks per piece half
 };
 
 __device__ __forceinline__ void sk2_key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
@@ -102,8 +106,9 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint64_t* p_full = s_full + 2;      // [2 tiles][2 key halves]
   uint64_t* o_final = p_full + 4;     // [2] all PV of a segment done
   uint64_t* o_free = o_final + 2;     // [2] O read out by the epilogue
-  uint64_t* merge_full = o_free + 2;  // [2] bulk loads of a split unit's pieces, per O column half
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_full + 2);
+  uint64_t* merge_full = o_free + 2;  // [2 halves][3 buffers] bulk loads of a split unit's pieces
+  uint64_t* merge_empty = merge_full + 6;   // [2 halves][3 buffers] chunk consumed (256 arrivals)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_empty + 6);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NT = a.segs.tile0[a.segs.n];
@@ -135,7 +140,10 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       mbar_init(&p_full[2 * t + 1], 128);
       mbar_init(&o_final[t], 1);
       mbar_init(&o_free[t], 256);
-      mbar_init(&merge_full[t], 1);
+    }
+    for (int b = 0; b < 6; ++b) {
+      mbar_init(&merge_full[b], 1);
+      mbar_init(&merge_empty[b], 256);
     }
     fence_barrier_init();
   }
@@ -192,6 +200,50 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         __syncwarp();
       }
       w += tb - ta;
+    }
+    // Owner merge of a split unit (this CTA's last segment starts a unit it does not finish):
+    // once both Q tiles' last PVs are done (Q / K / V smem idle), bulk-load the pieces of CTAs
+    // cta+1 .. cta+np, LAST CTA first (its piece is that CTA's first segment, published long
+    // before the end), 32-column chunks per O half into NBH buffers each; a piece's first
+    // chunk also brings its 256 lse values.  The flag of a piece is acquired before its loads.
+    if (w_end > w_begin) {
+      const long long wl = w_end - 1;
+      const int u = int(wl / NT);
+      const long long ub = (long long)u * NT;
+      if (w_begin <= ub && w_end < ub + NT) {       // last segment = [ub, w_end): owner
+        // o_final phases complete once per segment; the MMA warp may still be one segment
+        // behind (never two: this warp's last Q load waited for its QKs), so wait in order
+        const int sgl = sg - 1;
+        for (int s2 = sgl > 0 ? sgl - 1 : 0; s2 <= sgl; ++s2) {
+          mbar_wait(&o_final[0], s2 & 1);
+          mbar_wait(&o_final[1], s2 & 1);
+        }
+        int last = cta + 1;
+        while (last + 1 < G && sk2_begin(a, W, G, last + 1) < ub + NT) ++last;
+        const int np = last - cta, items = np * L::CPP;
+        for (int i = 0; i < items; ++i) {
+          const int c = cta + np - i / L::CPP, cc = i % L::CPP, b = i % L::NBH;
+          if (cc == 0 && lane == 0) {
+            while (ld_acquire_gpu(a.sflag + c) == 0) __nanosleep(32);
+            fence_proxy_async_global();                // the piece is read through the async proxy
+          }
+          __syncwarp();
+          for (int hf = 0; hf < 2; ++hf) {
+            if (i >= L::NBH) mbar_wait(&merge_empty[hf * 3 + b], ((i / L::NBH) - 1) & 1);
+            if (lane == 0) {
+              uint64_t* bar = &merge_full[hf * 3 + b];
+              mbar_arrive_expect_tx(bar, 32768u + (cc == 0 ? 1024u : 0u));
+              bulk_g2s(smem + (size_t)(hf * L::NBH + b) * 32768,
+                       reinterpret_cast<const uint8_t*>(a.spart) +
+                           ((size_t)c * (HD / 4) * 256 + (size_t)((hf * (HD / 2) + cc * 32) / 4) * 256) * 16,
+                       32768u, bar);
+              if (cc == 0)
+                bulk_g2s(smem + L::LSE_OFF + (hf * 2 + ((i / L::CPP) & 1)) * 1024, a.slse + (size_t)c * 256, 1024u, bar);
+            }
+            __syncwarp();
+          }
+        }
+      }
     }
   } else if (warp == 17) {
     // The whole warp walks the schedule (warp-uniform control flow keeps the descriptors in
@@ -419,16 +471,6 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         __syncwarp();
       };
-      // the CTA's last segment: the K/V stages are idle -> staging for the owner's bulk loads of
-      // the pieces, one 64 KB buffer per O column half (K stages: half 0, V stages: half 1),
-      // [col/4][256] float4 like the slots (bulk stores of the pieces measured slower than
-      // direct stores: 3.2 us for 128 KB per SM with ~90 CTAs storing at once)
-      const bool last_seg = w + n == w_end;
-      uint8_t* const hbuf = smem + (hf == 0 ? L::K_OFF : L::V_OFF);
-      constexpr uint32_t HBYTES = (HD / 2) * 256 * 4;     // one column half of a 256-row partial
-      const bool hissuer = (warp & 11) == 0 && lane == 0;  // warp 0 (half 0) / warp 4 (half 1)
-      // (the other Q tile's last PV may still be reading a V stage: both tiles done first)
-      if (last_seg && ta == 0 && tb < NT) mbar_wait(&o_final[t ^ 1], sg & 1);
       if (ta > 0) {
         // continuation piece: normalised partial -> this CTA's slot, then raise the flag
         const float inv = 1.f / l;
@@ -452,72 +494,52 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           if (ct) ct[12] = (long long)globaltimer();
         }
       } else if (tb < NT) {
-        // owner of a split unit (always the last segment of this CTA): merge the pieces of
-        // CTAs cta+1 .. (the unit's last tile) in CTA order
+        // owner of a split unit (always the last segment of this CTA): the producer warp
+        // streams the pieces in (see above); online-rescaled merge in that order: A <- A
+        // 2^(m - m') + 2^(lse_k - m') O_k, W likewise, out = A / W (own O enters normalised)
         const long long unit_end = (long long)(u + 1) * NT;
         int last = cta + 1;
         while (last + 1 < G && sk2_begin(a, W, G, last + 1) < unit_end) ++last;
         const int np = last - cta;
-        for (int k = lane; k < np; k += 32) {
-          const int* fl = a.sflag + cta + 1 + k;
-          while (*reinterpret_cast<const volatile int*>(fl) == 0) __nanosleep(32);
-        }
-        __syncwarp();
-        __threadfence();
-        fence_proxy_async_global();                  // the pieces are read through the async proxy
+        const int items = np * L::CPP;
         if (ct && warp == 0 && lane == 0) ct[5] = (long long)globaltimer();
-        // bulk-load piece k's column half of this thread group into its staging buffer
-        auto load_piece = [&](int k) {
-          const uint8_t* src = reinterpret_cast<const uint8_t*>(a.spart) +
-                               ((size_t)(cta + 1 + k) * (HD / 4) * 256 + (size_t)hf * (OH / 4) * 256) * 16;
-          fence_proxy_async_smem();
-          mbar_arrive_expect_tx(&merge_full[hf], HBYTES);
-          for (uint32_t off = 0; off < HBYTES; off += 32768)
-            bulk_g2s(hbuf + off, src + off, HBYTES - off < 32768 ? HBYTES - off : 32768, &merge_full[hf]);
-        };
-        if (hissuer) load_piece(0);
-        float mx = lse_own;
-        for (int k = 0; k < np; ++k) mx = fmaxf(mx, __ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256));
-        const float wown = ex2(lse_own - mx);
-        float wsum = wown;
-        for (int k = 0; k < np; ++k) wsum += ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
-        const float inv_w = 1.f / wsum;
-        const float4* stage = reinterpret_cast<const float4*>(hbuf);   // this half's columns
-        float scale = wown / l;
+        float m = lse_own, wsum = 1.f, alpha = 1.f, wk = 0.f;
+        const float sfirst = 1.f / l;
 #pragma unroll 1
-        for (int k = 0; k < np; ++k) {
-          const float wk = ex2(__ldcg(a.slse + (size_t)(cta + 1 + k) * 256 + r256) - mx);
-          mbar_wait(&merge_full[hf], k & 1);
-#pragma unroll 1
-          for (int c = 0; c < OH; c += 32) {
-            float f[32];
-            tmem_ld32(TOh + c, reinterpret_cast<uint32_t*>(f));
-            tmem_wait_ld();
-#pragma unroll
-            for (int q4 = 0; q4 < 8; ++q4) {
-              const float4 v = stage[(c / 4 + q4) * 256 + r256];
-              f[4 * q4] = f[4 * q4] * scale + wk * v.x;
-              f[4 * q4 + 1] = f[4 * q4 + 1] * scale + wk * v.y;
-              f[4 * q4 + 2] = f[4 * q4 + 2] * scale + wk * v.z;
-              f[4 * q4 + 3] = f[4 * q4 + 3] * scale + wk * v.w;
-            }
-            tmem_st32(TOh + c, reinterpret_cast<uint32_t*>(f));
-            tmem_wait_st();
+        for (int i = 0; i < items; ++i) {
+          const int cc = i % L::CPP, b = i % L::NBH;
+          mbar_wait(&merge_full[hf * 3 + b], (i / L::NBH) & 1);
+          if (cc == 0) {                               // a new piece: its weight, rescale A
+            const float lk = reinterpret_cast<const float*>(smem + L::LSE_OFF + (hf * 2 + ((i / L::CPP) & 1)) * 1024)[r256];
+            const float mn = fmaxf(m, lk);
+            const float am = ex2(m - mn);
+            alpha = am * (i == 0 ? sfirst : 1.f);
+            wk = ex2(lk - mn);
+            wsum = wsum * am + wk;
+            m = mn;
           }
-          scale = 1.f;
-          if (k + 1 < np) {                          // this half's buffer read: load the next piece
-            sk2_named_bar_sync(13 + hf, 256);
-            if (hissuer) load_piece(k + 1);
+          const float4* stage = reinterpret_cast<const float4*>(smem + (size_t)(hf * L::NBH + b) * 32768);
+          float f[32];
+          tmem_ld32(TOh + cc * 32, reinterpret_cast<uint32_t*>(f));
+          tmem_wait_ld();
+#pragma unroll
+          for (int q4 = 0; q4 < 8; ++q4) {
+            const float4 v = stage[q4 * 256 + r256];
+            f[4 * q4] = f[4 * q4] * alpha + wk * v.x;
+            f[4 * q4 + 1] = f[4 * q4 + 1] * alpha + wk * v.y;
+            f[4 * q4 + 2] = f[4 * q4 + 2] * alpha + wk * v.z;
+            f[4 * q4 + 3] = f[4 * q4 + 3] * alpha + wk * v.w;
+          }
+          mbar_arrive(&merge_empty[hf * 3 + b]);       // chunk buffer (and lse slot reads) done
+          if (i + L::CPP >= items) {                   // last piece: normalise and write out
+            write_out16(cc * 32, f, 1.f / wsum);
+            write_out16(cc * 32 + 16, f + 16, 1.f / wsum);
+          } else {
+            tmem_st32(TOh + cc * 32, reinterpret_cast<uint32_t*>(f));
+            tmem_wait_st();
           }
         }
         if (ct && warp == 0 && lane == 0) ct[13] = (long long)globaltimer();
-#pragma unroll 1
-        for (int c = 0; c < OH; c += 16) {
-          float f[16];
-          tmem_ld16(TOh + c, reinterpret_cast<uint32_t*>(f));
-          tmem_wait_ld();
-          write_out16(c, f, scale * inv_w);
-        }
         tc_fence_before();
         mbar_arrive(&o_free[t]);
         sk2_bar_sync(11, 512);                       // every row has read the slots
