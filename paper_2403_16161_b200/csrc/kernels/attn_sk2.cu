@@ -29,8 +29,8 @@ struct AttnSk2Smem {
   static constexpr int K_OFF = 2 * QB;
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
-  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2 + 12;   // + merge_full / merge_empty [2 halves][3]
-  static constexpr int STG_OFF = BAR_OFF + NBAR * 8 + 16;      // [16 warps][32 rows][48 B] output staging
+  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2 + 12 + 1;   // + merge_full / merge_empty [2][3], merge_go
+  static constexpr int STG_OFF = (BAR_OFF + NBAR * 8 + 16 + 127) / 128 * 128;   // [16 warps][32 rows][48 B] output staging
   static constexpr int XCH_OFF = STG_OFF + 16 * 32 * 48;        // [2 phases][2 tiles][2 halves][128] fp32
   static constexpr int LSE_OFF = XCH_OFF + 2 * 2 * 2 * 128 * 4;   // [2 halves][2 piece parities][256] fp32 (merge)
   static constexpr int TOTAL = LSE_OFF + 2 * 2 * 256 * 4 + 1024;
@@ -108,7 +108,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint64_t* o_free = o_final + 2;     // [2] O read out by the epilogue
   uint64_t* merge_full = o_free + 2;  // [2 halves][3 buffers] bulk loads of a split unit's pieces
   uint64_t* merge_empty = merge_full + 6;   // [2 halves][3 buffers] chunk consumed (256 arrivals)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_empty + 6);
+  uint64_t* merge_go = merge_empty + 6;     // the owner's 512 softmax threads are past both tiles' last PV
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_go + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NT = a.segs.tile0[a.segs.n];
@@ -145,6 +146,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       mbar_init(&merge_full[b], 1);
       mbar_init(&merge_empty[b], 256);
     }
+    mbar_init(merge_go, 512);
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc(tmem_slot, 512);
@@ -211,20 +213,26 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int u = int(wl / NT);
       const long long ub = (long long)u * NT;
       if (w_begin <= ub && w_end < ub + NT) {       // last segment = [ub, w_end): owner
-        // o_final phases complete once per segment; the MMA warp may still be one segment
-        // behind (never two: this warp's last Q load waited for its QKs), so wait in order
-        const int sgl = sg - 1;
-        for (int s2 = sgl > 0 ? sgl - 1 : 0; s2 <= sgl; ++s2) {
-          mbar_wait(&o_final[0], s2 & 1);
-          mbar_wait(&o_final[1], s2 & 1);
-        }
+        // (not o_final: this warp may reach here before or after the MMA warp finishes either
+        // of the last two segments, and a parity wait cannot tell those phases apart)
+        mbar_wait(merge_go, 0);
         int last = cta + 1;
         while (last + 1 < G && sk2_begin(a, W, G, last + 1) < ub + NT) ++last;
         const int np = last - cta, items = np * L::CPP;
         for (int i = 0; i < items; ++i) {
           const int c = cta + np - i / L::CPP, cc = i % L::CPP, b = i % L::NBH;
           if (cc == 0 && lane == 0) {
+#ifdef VI_MBAR_TIMEOUT
+            for (long long it = 0; ld_acquire_gpu(a.sflag + c) == 0; ++it) {
+              __nanosleep(32);
+              if (it > (1ll << 22)) {
+                printf("[flag timeout] block %d waits for piece of CTA %d\n", cta, c);
+                __trap();
+              }
+            }
+#else
             while (ld_acquire_gpu(a.sflag + c) == 0) __nanosleep(32);
+#endif
             fence_proxy_async_global();                // the piece is read through the async proxy
           }
           __syncwarp();
@@ -502,6 +510,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         while (last + 1 < G && sk2_begin(a, W, G, last + 1) < unit_end) ++last;
         const int np = last - cta;
         const int items = np * L::CPP;
+        mbar_arrive(merge_go);                       // this tile's MMAs are done: smem free for the pieces
         if (ct && warp == 0 && lane == 0) ct[5] = (long long)globaltimer();
         float m = lse_own, wsum = 1.f, alpha = 1.f, wk = 0.f;
         const float sfirst = 1.f / l;

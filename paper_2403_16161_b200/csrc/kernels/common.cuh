@@ -53,7 +53,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(a), "r"(parity) : "memory");
-    if (n > (1ll << 26)) __trap();
+    if (n > (1ll << 21)) {
+      printf("[mbar timeout] block %d warp %d lane %d smem %u parity %u\n", blockIdx.x, threadIdx.x >> 5,
+             threadIdx.x & 31, a, parity);
+      __trap();
+    }
   }
 #else
   asm volatile(
