@@ -249,6 +249,8 @@ def run_ours(args, cfg):
     e2e_steps = max(3, min(args.steps, 50))
     host_in = [f.cpu().pin_memory() for f in feats]
     host_out = [torch.empty(out.shape, dtype=dt).pin_memory() for _ in range(e2e_steps)]
+    for k in range(2):                 # untimed: creates the copy streams and staging slots
+        ctx.run_step_async(host_in[k % nchunks], T, host_out[k])
     ctx.sync()
     torch.cuda.synchronize()
     t0 = time.perf_counter()
