@@ -110,9 +110,9 @@ typedef struct vi_config {
   int ref_rate, max_ref_frames;
   /* Window attention (E2FGVI-shaped, BASELINE configs[3]): a query sees only the keys of
    * its own win_h x win_w token window (non-overlapping, tiling the token grid), in every
-   * frame of the memory and the chunk.  0 = global attention.  bf16 path; head sharding with
-   * tp_size <= heads; no reference frames, refine commits or memory reads (the memory is
-   * window-major). */
+   * frame of the memory and the chunk (reference frames included).  0 = global attention.
+   * bf16 path; head sharding with tp_size <= heads; no refine commits or memory reads (the
+   * memory is window-major). */
   int win_h, win_w;
 } vi_config;
 

@@ -132,10 +132,11 @@ struct vi_ctx {
   Geom g{}, gf{};          // split geometry (C = feat_c) and F3N geometry (C = F / (kh*kw))
   int L = 0, H = 0, D = 0, hd = 0, P = 0, M = 0, Tmax = 0, S = 0, F = 0, Pd = 0, es = 2;
   int ST = 0;              // all memory slots: S span slots + R reference slots (ring.h)
-  // window attention (vi_config.win_h / win_w): win_n windows of win_real tokens, padded to
-  // win_pad rows; the memory and Q are window-major (epilogue.cuh qkv_rows)
-  int win_n = 0, win_real = 0, win_pad = 0, win_cols = 0;
-  int KR = 0;              // key rows per block in the slabs: ST*P, or win_n*ST*win_pad
+  // window attention (vi_config.win_h / win_w): win_n windows of win_real tokens (win_pad =
+  // win_real rows per frame); the memory and Q are window-major (epilogue.cuh qkv_rows), a
+  // window's key region win_kstride = ST*win_pad rounded up to 8 rows
+  int win_n = 0, win_real = 0, win_pad = 0, win_cols = 0, win_kstride = 0;
+  int KR = 0;              // key rows per block in the slabs: ST*P, or win_n*win_kstride
   int QR = 0;              // rows of the Q buffer: T_max*P, or win_n*T_max*win_pad
   int vt_ld = 0;           // row pitch of the transposed V slab: S*P rounded up to 64 (TMA: 16-B pitch)
   bool bf16 = true;
@@ -442,7 +443,6 @@ static vi_status validate(const vi_config* k, std::string* why) {
   if (k->win_h > 0) {
     if (k->dtype != VI_DTYPE_BF16) return bad("window attention: bf16 path only");
     if (oh % k->win_h || ow % k->win_w) return bad("window attention: windows must tile the token grid");
-    if (k->ref_rate > 0) return bad("window attention: no reference frames (not built)");
     if (k->tp_size > k->heads) return bad("window attention: head sharding needs tp_size <= heads");
   }
   const int G = k->tp_size < 1 ? 1 : k->tp_size;
@@ -524,8 +524,11 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     c->win_cols = ow / cfg->win_w;
     c->win_n = (oh / cfg->win_h) * c->win_cols;
     c->win_real = cfg->win_h * cfg->win_w;
-    c->win_pad = (c->win_real + 15) / 16 * 16;   // 16-row TMA/MMA granularity
-    c->KR = c->win_n * c->ST * c->win_pad;
+    // rows per (window, frame): no padding (pad rows cost a per-key mask in the softmax); a
+    // window's key region is padded to 8 rows so every V^T box starts 16-byte aligned
+    c->win_pad = c->win_real;
+    c->win_kstride = (c->ST * c->win_pad + 7) / 8 * 8;
+    c->KR = c->win_n * c->win_kstride;
     c->QR = c->win_n * c->Tmax * c->win_pad;
   } else {
     c->KR = c->ST * c->P;
@@ -781,7 +784,25 @@ static vi_status apply_commits(vi_ctx* c, const std::vector<int64_t>& ids) {
 // Frames becoming references (ring.h): their K rows and Vt columns move from the span slot
 // to the reference slot, on the ctx stream before the new chunk's step overwrites the span slot.
 static vi_status apply_moves(vi_ctx* c, const std::vector<Ring::Move>& moves) {
-  const size_t es = c->es, P = c->P, Dl = c->Dl, SP = (size_t)c->ST * c->P, ld = c->vt_ld;
+  const size_t es = c->es, P = c->P, Dl = c->Dl, SP = (size_t)c->KR, ld = c->vt_ld;
+  if (c->win_n) {   // window-major memory: a slot is win_pad rows inside every window's region
+    const size_t wp = c->win_pad, ks = c->win_kstride;
+    for (const auto& mv : moves) {
+      for (int l = 0; l < c->L; ++l) {
+        uint8_t* kb = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * Dl * es;
+        CK(cudaMemcpy2DAsync(kb + (size_t)mv.dst * wp * Dl * es, ks * Dl * es, kb + (size_t)mv.src * wp * Dl * es,
+                             ks * Dl * es, wp * Dl * es, c->win_n, cudaMemcpyDeviceToDevice, c->stream),
+           "reference move K");
+        uint8_t* vb = static_cast<uint8_t*>(c->vtslab) + (size_t)l * Dl * ld * es;
+        for (int w = 0; w < c->win_n; ++w)
+          CK(cudaMemcpy2DAsync(vb + ((size_t)w * ks + (size_t)mv.dst * wp) * es, ld * es,
+                               vb + ((size_t)w * ks + (size_t)mv.src * wp) * es, ld * es, wp * es, Dl,
+                               cudaMemcpyDeviceToDevice, c->stream),
+             "reference move V");
+      }
+    }
+    return VI_OK;
+  }
   for (const auto& mv : moves) {
     for (int l = 0; l < c->L; ++l) {
       uint8_t* kb = static_cast<uint8_t*>(c->kslab) + (size_t)l * SP * Dl * es;
@@ -1034,7 +1055,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   eq.S = c->S; eq.P = c->P; eq.vt_ld = c->vt_ld;
   if (c->win_n) {
     eq.win_pad = c->win_pad; eq.win_h = c->cfg.win_h; eq.win_w = c->cfg.win_w; eq.win_cols = c->win_cols;
-    eq.ow = c->g.ow; eq.win_qstride = c->Tmax * c->win_pad; eq.win_kstride = c->ST * c->win_pad;
+    eq.ow = c->g.ow; eq.win_qstride = c->Tmax * c->win_pad; eq.win_kstride = c->win_kstride;
   }
   eq.qkv_krow0 = int(l * SP);
   eq.qkv_vrow0 = l * Dl;
@@ -1063,7 +1084,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   a.scale_log2 = scale_log2; a.segs = make_segs(c, valid);
   a.o = static_cast<bf16*>(c->o); a.o_ld = D; a.o_hs = c->hd; a.q_row0 = 0;
   if (c->win_n) {   // window attention: the fixed KV split over (window, 256 queries) units
-    a.win_n = c->win_n; a.win_qstride = c->Tmax * c->win_pad; a.win_kstride = c->ST * c->win_pad;
+    a.win_n = c->win_n; a.win_qstride = c->Tmax * c->win_pad; a.win_kstride = c->win_kstride;
     a.win_pad = c->win_pad; a.win_real = c->win_real; a.win_h = c->cfg.win_h; a.win_w = c->cfg.win_w;
     a.win_cols = c->win_cols; a.ow = c->g.ow; a.P = c->P; a.win_nq = n * c->win_pad;
     a.win_npw = (a.win_nq + 255) / 256;
@@ -1088,6 +1109,23 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   // (C3, T = 1: 28 us vs 60 us per block; T = 5: stream-K 84 us vs ~93 us).
   const int sk_units = ((a.Nq + 255) / 256) * a.H;
   const bool small = sk_units * 4 < c->num_sms;
+  // window attention: sk2 over (head, window, query pair) units, stream-K split over up to
+  // VI_WIN_SPLIT CTAs per unit (C4: 64 units of 6 key tiles; attn_tc2's KV split + combine
+  // kernel measured 28 us/block)
+  const int win_units = c->win_n ? c->win_n * a.win_npw * a.H : 0;
+  if (c->win_n && g_attn_sk == 2 && !g_attn_split && win_units <= c->num_sms) {
+    a.npairs = a.win_npw;
+    a.units = win_units;
+    a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
+    a.sk_tail = 0; a.sk_tail_w = 16; a.sk_ucost = 0;
+    a.sk_wfull = (long long)a.units * ntiles;
+    const char* ws = getenv("VI_WIN_SPLIT");
+    const int split = std::max(1, ws ? atoi(ws) : 2);
+    const long long work = (long long)a.units * ntiles;
+    const int grid = int(std::min<long long>(std::min<long long>((long long)a.units * split, work), c->num_sms));
+    PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+    return VI_OK;
+  }
   if (!g_attn_v1 && !g_attn_split && !small && !c->win_n) {
     // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
     a.npairs = (a.Nq + 255) / 256;

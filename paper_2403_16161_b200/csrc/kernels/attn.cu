@@ -695,7 +695,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         for (int i = 0; i < 128; ++i)
           if (i >= nv || i < nskip) s[i] = -INFINITY;
       }
-      if (a.win_n) {                                  // window padding keys (index % pad >= real)
+      if (a.win_pad > a.win_real) {                   // window padding keys (index % pad >= real)
         uint32_t pm[4] = {0u, 0u, 0u, 0u};
         for (int k = a.win_real - row0 % a.win_pad; k < 128; k += a.win_pad)
           for (int e = k < 0 ? 0 : k; e < k + a.win_pad - a.win_real && e < 128; ++e) pm[e >> 5] |= 1u << (e & 31);

@@ -74,8 +74,20 @@ __device__ __forceinline__ long long sk2_begin(const AttnTC& a, long long W, int
   return (uf + u) * NT + (r <= B ? 0 : (r - B) / tw);
 }
 
-// unit u -> (head, first query row of its pair); tail units (if any) are the last H
-__device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0) {
+// unit u -> (head, first query row of its pair, window); tail units (if any) are the last H.
+// Window attention (win_n > 0): units = (head, window, query pair of the window), one CTA per
+// unit (the launch never splits them); query / key rows are offsets into the window-major
+// buffers (win_qstride / win_kstride rows per window).
+__device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0, int& win) {
+  win = 0;
+  if (a.win_n) {
+    const int per_h = a.win_n * a.win_npw;
+    h = u / per_h;
+    const int r = u - h * per_h;
+    win = r / a.win_npw;
+    q0 = (r - win * a.win_npw) * 256;
+    return;
+  }
   const int full = a.npairs - a.sk_tail;     // full pairs per head
   const int uf = full * a.H;
   if (u < uf) {
@@ -85,6 +97,16 @@ __device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0
     h = u - uf;
     q0 = full * 256;
   }
+}
+
+// window attention: output token row of local query q of window w, or -1 for padding rows
+// and rows beyond the chunk (window-major rows: frame t, index i < win_real in the window)
+__device__ __forceinline__ int sk2_win_out_row(const AttnTC& a, int w, int q) {
+  if (q >= a.win_nq) return -1;
+  const int t = q / a.win_pad, i = q - t * a.win_pad;
+  if (i >= a.win_real) return -1;
+  const int oy = (w / a.win_cols) * a.win_h + i / a.win_w, ox = (w % a.win_cols) * a.win_w + i % a.win_w;
+  return t * a.P + oy * a.ow + ox;
 }
 
 template <int HD>
@@ -165,8 +187,9 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     for (long long w = w_begin; w < w_end; ++sg) {
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
-      int h, q0;
-      sk2_unit(a, u, h, q0);
+      int h, q0, win;
+      sk2_unit(a, u, h, q0, win);
+      const int wq = win * a.win_qstride, wk = win * a.win_kstride;   // window row offsets
       if (sg > 0) mbar_wait(q_empty, (sg - 1) & 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(q_full, 2 * L::QB);
@@ -174,7 +197,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         for (int t = 0; t < 2; ++t)
 #pragma unroll
           for (int at = 0; at < HD / 64; ++at)
-            tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, a.q_row0 + q0 + t * 128);
+            tma_load_2d(smem + L::Q_OFF + t * L::QB + at * 16384, &tq, q_full, h * HD + at * 64, a.q_row0 + wq + q0 + t * 128);
       }
       __syncwarp();
       for (int j = ta; j < tb; ++j, ++jg) {
@@ -188,7 +211,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           mbar_arrive_expect_tx(&k_full[st], L::KB);
 #pragma unroll
           for (int at = 0; at < HD / 64; ++at)
-            tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + row0);
+            tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + wk + row0);
         }
         __syncwarp();
         if (jg >= ST) mbar_wait(&v_empty[st], par);
@@ -197,7 +220,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           mbar_arrive_expect_tx(&v_full[st], L::VB);
 #pragma unroll
           for (int at = 0; at < 2; ++at)
-            tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], row0 + at * 64, a.vrow_base + h * HD);
+            tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], wk + row0 + at * 64, a.vrow_base + h * HD);
         }
         __syncwarp();
       }
@@ -266,9 +289,10 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
-      int h_, q0;
-      sk2_unit(a, u, h_, q0);
-      const bool t1_live = q0 + 128 < a.Nq && SK2_EXPERIMENT != 2;   // tile 1 of a tail pair: commits only
+      int h_, q0, win_;
+      sk2_unit(a, u, h_, q0, win_);
+      const int nq = a.win_n ? a.win_nq : a.Nq;
+      const bool t1_live = q0 + 128 < nq && SK2_EXPERIMENT != 2;   // tile 1 of a tail pair: commits only
       const bool t0_live = SK2_EXPERIMENT != 2;
       mbar_wait(q_full, sg & 1);
       auto issue_pv = [&](int t, int j) {          // O_t (+)= P_t(j) V(j), j local to the segment
@@ -361,11 +385,12 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
-      int h, q0;
-      sk2_unit(a, u, h, q0);
+      int h, q0, win;
+      sk2_unit(a, u, h, q0, win);
+      const int nq = a.win_n ? a.win_nq : a.Nq;       // query rows of the unit's row space
       // all 32 rows of this warp past Nq (a tail pair): keep the barrier phases, skip the math
       // (their P / O lanes hold garbage that only reaches rows never stored)
-      const bool dead = q0 + t * 128 + qd * 32 >= a.Nq || SK2_EXPERIMENT == 1;
+      const bool dead = q0 + t * 128 + qd * 32 >= nq || SK2_EXPERIMENT == 1;
       float m_use = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         const int g = jg + j;
@@ -388,6 +413,18 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
 #pragma unroll
           for (int i = 0; i < 64; ++i)
             if (i < lo || i >= hi) s[i] = -INFINITY;
+        }
+        if (a.win_pad > a.win_real) {                 // window padding keys (row % pad >= real)
+          uint32_t pm0 = 0u, pm1 = 0u;
+          const int base = row0 + hf * 64;
+          for (int k = a.win_real - base % a.win_pad; k < 64; k += a.win_pad)
+            for (int e = k < 0 ? 0 : k; e < k + a.win_pad - a.win_real && e < 64; ++e) {
+              if (e < 32) pm0 |= 1u << e;
+              else pm1 |= 1u << (e - 32);
+            }
+#pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if ((((i < 32 ? pm0 : pm1) >> (i & 31)) & 1u) != 0u) s[i] = -INFINITY;
         }
         float mx[4] = {-INFINITY, -INFINITY, -INFINITY, -INFINITY};
 #pragma unroll
@@ -474,8 +511,9 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         for (int i = 0; i < 2; ++i) {
           const int rr = i * 16 + (lane >> 1), part = lane & 1;
           const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 48 + part * 16);
-          if (rbase + rr < a.Nq)
-            *reinterpret_cast<uint4*>(a.o + (size_t)(rbase + rr) * a.o_ld + (size_t)h * a.o_hs + hf * OH + c + part * 8) = v;
+          const int orow = a.win_n ? sk2_win_out_row(a, win, rbase + rr) : (rbase + rr < a.Nq ? rbase + rr : -1);
+          if (orow >= 0)
+            *reinterpret_cast<uint4*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + hf * OH + c + part * 8) = v;
         }
         __syncwarp();
       };

@@ -399,6 +399,14 @@ def test_window_attention_c3s_ragged():
     run_pair(cfg, w, steps=5, ns=[3, 1, 2, 3, 2])
 
 
+def test_window_attention_with_reference_frames():
+    """Window attention over a memory with reference frames: a reference move copies the slot's
+    rows inside every window's key region (window-major memory); 10 one-frame steps."""
+    cfg = CONFIGS["C3S"].replace(layers=2, t_new=1, mem_frames=2, ref_rate=3, max_refs=2, win_h=5, win_w=6)
+    w = make_weights(cfg, seed=14, variant="sensitive")
+    run_pair(cfg, w, steps=10, masked="moving")
+
+
 def test_window_attention_c4_full_shape_step():
     """BASELINE configs[3] shape (2 of its 16 blocks): 720 tokens/frame in 16 windows of 5 x 9,
     5 new frames over a 10-frame memory; the 4th step compared stage by stage."""
