@@ -497,6 +497,9 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       uint8_t* stg = smem + L::STG_OFF + warp * (32 * 48);
       const int rbase = q0 + t * 128 + qd * 32;
       const uint32_t TOh = TO + hf * OH;
+      // output row of this lane's accumulator row (-1: none); write_out16 fetches the rows it
+      // stores by shuffle (the window mapping costs a few integer divisions: once per segment)
+      const int my_orow = a.win_n ? sk2_win_out_row(a, win, rbase + lane) : (rbase + lane < a.Nq ? rbase + lane : -1);
       // 16 O columns -> bf16 output rows via the per-warp stage (16 rows x 32 B per store)
       auto write_out16 = [&](int c, const float* f, float scale) {   // c: column within the half
         uint4* my = reinterpret_cast<uint4*>(stg + lane * 48);
@@ -511,7 +514,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         for (int i = 0; i < 2; ++i) {
           const int rr = i * 16 + (lane >> 1), part = lane & 1;
           const uint4 v = *reinterpret_cast<const uint4*>(stg + rr * 48 + part * 16);
-          const int orow = a.win_n ? sk2_win_out_row(a, win, rbase + rr) : (rbase + rr < a.Nq ? rbase + rr : -1);
+          const int orow = __shfl_sync(0xffffffffu, my_orow, rr);
           if (orow >= 0)
             *reinterpret_cast<uint4*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + hf * OH + c + part * 8) = v;
         }

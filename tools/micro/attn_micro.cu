@@ -50,7 +50,12 @@ int main(int argc, char** argv) {
   const bool trace = argc > 2 && argv[2][0] == 't';
   const int grid_override = argc > 3 ? atoi(argv[3]) : 0;
   const int ver = argc > 4 ? atoi(argv[4]) : 3;
-  const int Nq = 3600, H = 4, HD = 128, D = H * HD, P = 720, S = 15, SP = S * P, vt_ld = (SP + 63) / 64 * 64;
+  // argv[5] == 'w': the C4 window shape (16 windows of 5 x 9 tokens, window-major rows,
+  // 225 queries and 675 keys per window, key regions padded to 680 rows)
+  const bool win = argc > 5 && argv[5][0] == 'w';
+  const int WN = 16, WREAL = 45, WKS = (15 * WREAL + 7) / 8 * 8;
+  const int Nq = 3600, H = 4, HD = 128, D = H * HD, P = 720, S = 15, SP = win ? WN * WKS : S * P,
+            vt_ld = (SP + 63) / 64 * 64;
   uint16_t *q, *k, *vt, *o;
   cudaMalloc(&q, (size_t)Nq * D * 2);
   cudaMalloc(&k, (size_t)SP * D * 2);
@@ -74,6 +79,15 @@ int main(int argc, char** argv) {
   a.o = reinterpret_cast<bf16*>(o); a.o_ld = D; a.o_hs = HD; a.q_row0 = 0;
   a.npairs = (Nq + 255) / 256;
   a.units = a.npairs * H;
+  if (win) {
+    a.win_n = WN; a.win_pad = WREAL; a.win_real = WREAL; a.win_h = 5; a.win_w = 9; a.win_cols = 4;
+    a.ow = 36; a.P = P; a.win_nq = 5 * WREAL; a.win_qstride = 5 * WREAL; a.win_kstride = WKS;
+    a.win_npw = 1;
+    a.segs.len[0] = 15 * WREAL;
+    a.segs.tile0[1] = (15 * WREAL + 127) / 128;
+    a.npairs = 1;
+    a.units = WN * H;
+  }
   cudaMalloc(&a.spart, (size_t)nsm * 2 * 256 * HD * 4);
   cudaMalloc(&a.slse, (size_t)nsm * 2 * 256 * 4);
   cudaMalloc(&a.sflag, (size_t)(nsm * 2 + a.units + 8) * 4);
@@ -81,7 +95,7 @@ int main(int argc, char** argv) {
   const long long work = (long long)a.units * a.segs.tile0[1];
   // sk2 tail ordering (engine.cu): the last pair of each head has an empty second tile
   const int rem = Nq % 256;
-  a.sk_tail = (ver == 2 && rem > 0 && rem <= 128) ? 1 : 0;
+  a.sk_tail = (ver == 2 && rem > 0 && rem <= 128 && !win) ? 1 : 0;
   a.sk_tail_w = a.sk_tail && getenv("VI_SK_TAIL_W") ? atoi(getenv("VI_SK_TAIL_W")) : 16;
   a.sk_wfull = (long long)(a.npairs - a.sk_tail) * H * a.segs.tile0[1];
   a.sk_ucost = getenv("VI_SK_UNIT_COST") ? atoi(getenv("VI_SK_UNIT_COST")) : 0;
@@ -99,7 +113,7 @@ int main(int argc, char** argv) {
   cudaError_t err = cudaStreamSynchronize(st);
   float ms = 0.f;
   cudaEventElapsedTime(&ms, e0, e1);
-  const double flop = 4.0 * Nq * SP * D, us = 1e3 * ms / iters;
+  const double flop = 4.0 * Nq * (win ? 15.0 * WREAL : double(SP)) * D, us = 1e3 * ms / iters;
   printf("attn_sk%d C3: grid %d, %.2f us/launch, %.1f TFLOP/s (%s)\n", ver, grid, us, flop / (us * 1e-6) / 1e12,
          cudaGetErrorString(err));
   if (getenv("CTA_TRACE")) {   // per-CTA globaltimer stamps of one launch
@@ -121,7 +135,8 @@ int main(int argc, char** argv) {
       for (int i = 0; i < 7; ++i) printf(" %6lld", e[i] ? e[i] - t0 : -1);
       printf(" %lld |", e[7]);
       for (int i = 0; i < e[7] && i < 4; ++i) printf(" %6lld", e[8 + i] - t0);
-      printf(" | piece published %6lld owner staged %6lld", e[12] ? e[12] - t0 : -1, e[13] ? e[13] - t0 : -1);
+      printf(" | piece published %6lld owner staged %6lld | direct %6lld %6lld", e[12] ? e[12] - t0 : -1, e[13] ? e[13] - t0 : -1,
+             e[14] ? e[14] - t0 : -1, e[15] ? e[15] - t0 : -1);
       printf("\n");
     }
   }
