@@ -341,8 +341,8 @@ def run_ours(args, cfg):
     }
     line["device_time_ms_per_step"] = {"attention": attn_ms / args.steps, "gemm": prof["gemm"][0] / args.steps,
                                        "other": (total_ms - attn_ms - prof["gemm"][0]) / args.steps}
-    gemm_ms = sub[3]["gemm"][0] / extra_steps
-    patch_ms = sub[2]["patch"][0] / extra_steps
+    gemm_ms = max(sub[3]["gemm"][0] / extra_steps, 1e-9)    # (> 0 even when a VI_ABLATE run skips them)
+    patch_ms = max(sub[2]["patch"][0] / extra_steps, 1e-9)
     gflop, pbytes = gemm_flop_per_step(cfg) / (world if args.tp else 1), patch_bytes_per_step(cfg)
     line["secondary_rooflines"] = {
         "gemms (embed, QKV, O, FFN1, FFN2, back; self-timed in the graph)": {
