@@ -349,10 +349,19 @@ static void debug_wait(vi_ctx* c, const char* where) {
     CK((call), where);             \
     if (g_debug_sync) debug_wait(c, where); \
   } while (0)
-#define PLAUNCH(cat, call, where) \
-  do {                             \
-    Prof p_(c, cat);               \
-    LAUNCH(call, where);           \
+// VI_ABLATE=<mask> (timing experiments only, results are garbage): skip the launches of the
+// profile categories whose bit is set (1 attention, 2 GEMMs, 4 patch, 8 row kernels), to
+// measure each class's marginal cost inside the step graph
+static const int g_ablate = [] {
+  const char* e = getenv("VI_ABLATE");
+  return e ? atoi(e) : 0;
+}();
+#define PLAUNCH(cat, call, where)                  \
+  do {                                             \
+    if (!((g_ablate >> (cat)) & 1)) {              \
+      Prof p_(c, cat);                             \
+      LAUNCH(call, where);                         \
+    }                                              \
   } while (0)
 #define CK_C(ctx, call, where)                              \
   do {                                                      \
