@@ -334,6 +334,54 @@ def test_c3_full_shape_step():
     compare_step(cfg, ost, gst, 2e-2)
 
 
+def _run_steps(cfg, w, steps, seed):
+    from paper_2403_16161_b200 import vi
+    ctx = vi.Context.from_synth(cfg)
+    ctx.set_weights(w)
+    outs = []
+    for i in range(steps):
+        f = torch.from_numpy(make_features(cfg, cfg.t_new, first_frame=i * cfg.t_new, seed=seed)).to(torch.bfloat16).cuda()
+        out = torch.empty_like(f)
+        ctx.run_step(f, cfg.t_new, out)
+        outs.append(out.float())
+    ctx.sync()
+    ctx.close()
+    return outs
+
+
+@pytest.mark.parametrize("env", [{"VI_SK_UNIT_COST": "0"}, {"VI_SK_UNIT_COST": "400"},
+                                 {"VI_SK_UNIT_COST": "96", "VI_SK_TAIL_W": "6"}, {"VI_SK_TAIL_W": "40"}])
+def test_stream_k_partition_invariance(env, monkeypatch):
+    """The stream-K attention at the C3 shape under other work splits (unit-start cost, tail
+    weight): different CTA boundaries, pieces, owners and merge orders (a split that once hung
+    is among them) give the default split's output up to merge rounding.  The default split is
+    the one test_c3_full_shape_step pins to the oracle."""
+    cfg = CONFIGS["C3"].replace(layers=1)
+    w = make_weights(cfg, seed=21)
+    ref = _run_steps(cfg, w, 4, seed=21)
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got = _run_steps(cfg, w, 4, seed=21)
+    for i in (2, 3):           # memory full: every unit spans 85 key tiles
+        scale = ref[i].abs().max().item()
+        err = (got[i] - ref[i]).abs().max().item() / scale
+        assert err < 1e-2, f"step {i}: {err:.3g} under {env}"
+
+
+@pytest.mark.parametrize("split", ["1", "3"])
+def test_window_split_invariance(split, monkeypatch):
+    """Window attention (C4 shape, 1 block) with 1 or 3 CTAs per (head, window, query pair)
+    unit instead of the default 2: same output up to merge rounding."""
+    cfg = CONFIGS["C4"].replace(layers=1)
+    w = make_weights(cfg, seed=22)
+    ref = _run_steps(cfg, w, 4, seed=22)
+    monkeypatch.setenv("VI_WIN_SPLIT", split)
+    got = _run_steps(cfg, w, 4, seed=22)
+    scale = ref[3].abs().max().item()
+    err = (got[3] - ref[3]).abs().max().item() / scale
+    assert err < 1e-2, f"window split {split}: {err:.3g}"
+
+
 def test_c2_full_shape_step():
     """BASELINE configs[1] at full size (STTN-shaped: 8 blocks, 4 heads of d 64, D 256,
     5x9-cell patches of a 60x108x256 map -> 144 tokens/frame, MLP-GELU 1024, T=5, M=10):
