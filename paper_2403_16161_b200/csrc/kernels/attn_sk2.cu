@@ -78,9 +78,10 @@ __device__ __forceinline__ long long sk2_begin(const AttnTC& a, long long W, int
 // Window attention (win_n > 0): units = (head, window, query pair of the window), one CTA per
 // unit (the launch never splits them); query / key rows are offsets into the window-major
 // buffers (win_qstride / win_kstride rows per window).
+template <bool WIN>
 __device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0, int& win) {
   win = 0;
-  if (a.win_n) {
+  if (WIN) {
     const int per_h = a.win_n * a.win_npw;
     h = u / per_h;
     const int r = u - h * per_h;
@@ -109,7 +110,9 @@ __device__ __forceinline__ int sk2_win_out_row(const AttnTC& a, int w, int q) {
   return t * a.P + oy * a.ow + ox;
 }
 
-template <int HD>
+// WIN: window attention compiled in (a separate instantiation, so the global-attention kernel
+// carries none of the window code: it measurably cost the C3 softmax loop registers)
+template <int HD, bool WIN>
 __global__ void __launch_bounds__(576, 1)
 attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
@@ -188,7 +191,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int u = int(w / NT), ta = int(w - (long long)u * NT);
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       int h, q0, win;
-      sk2_unit(a, u, h, q0, win);
+      sk2_unit<WIN>(a, u, h, q0, win);
       const int wq = win * a.win_qstride, wk = win * a.win_kstride;   // window row offsets
       if (sg > 0) mbar_wait(q_empty, (sg - 1) & 1);
       if (elect_one()) {
@@ -290,8 +293,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
       int h_, q0, win_;
-      sk2_unit(a, u, h_, q0, win_);
-      const int nq = a.win_n ? a.win_nq : a.Nq;
+      sk2_unit<WIN>(a, u, h_, q0, win_);
+      const int nq = WIN ? a.win_nq : a.Nq;
       const bool t1_live = q0 + 128 < nq && SK2_EXPERIMENT != 2;   // tile 1 of a tail pair: commits only
       const bool t0_live = SK2_EXPERIMENT != 2;
       mbar_wait(q_full, sg & 1);
@@ -386,8 +389,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int tb = (int)((long long)NT < ta + (w_end - w) ? NT : ta + (w_end - w));
       const int n = tb - ta;
       int h, q0, win;
-      sk2_unit(a, u, h, q0, win);
-      const int nq = a.win_n ? a.win_nq : a.Nq;       // query rows of the unit's row space
+      sk2_unit<WIN>(a, u, h, q0, win);
+      const int nq = WIN ? a.win_nq : a.Nq;       // query rows of the unit's row space
       // all 32 rows of this warp past Nq (a tail pair): keep the barrier phases, skip the math
       // (their P / O lanes hold garbage that only reaches rows never stored)
       const bool dead = q0 + t * 128 + qd * 32 >= nq || SK2_EXPERIMENT == 1;
@@ -414,7 +417,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           for (int i = 0; i < 64; ++i)
             if (i < lo || i >= hi) s[i] = -INFINITY;
         }
-        if (a.win_pad > a.win_real) {                 // window padding keys (row % pad >= real)
+        if (WIN && a.win_pad > a.win_real) {         // window padding keys (row % pad >= real)
           uint32_t pm0 = 0u, pm1 = 0u;
           const int base = row0 + hf * 64;
           for (int k = a.win_real - base % a.win_pad; k < 64; k += a.win_pad)
@@ -499,7 +502,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const uint32_t TOh = TO + hf * OH;
       // output row of this lane's accumulator row (-1: none); write_out16 fetches the rows it
       // stores by shuffle (the window mapping costs a few integer divisions: once per segment)
-      const int my_orow = a.win_n ? sk2_win_out_row(a, win, rbase + lane) : (rbase + lane < a.Nq ? rbase + lane : -1);
+      const int my_orow = WIN ? sk2_win_out_row(a, win, rbase + lane) : (rbase + lane < a.Nq ? rbase + lane : -1);
       // 16 O columns -> bf16 output rows via the per-warp stage (16 rows x 32 B per store)
       auto write_out16 = [&](int c, const float* f, float scale) {   // c: column within the half
         uint4* my = reinterpret_cast<uint4*>(stg + lane * 48);
@@ -620,13 +623,13 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   }
 }
 
-template <int HD>
+template <int HD, bool WIN>
 static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
                                 const AttnTC& a, int grid, cudaStream_t st) {
   using L = AttnSk2Smem<HD>;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sk2_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
+    cudaError_t e = cudaFuncSetAttribute(attn_sk2_kernel<HD, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
     if (e != cudaSuccess) return e;
     configured = true;
   }
@@ -640,13 +643,18 @@ static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, c
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_sk2_kernel<HD>, tq, tk, tvt, a);
+  return cudaLaunchKernelEx(&cfg, attn_sk2_kernel<HD, WIN>, tq, tk, tvt, a);
 }
 
 cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            int grid, cudaStream_t st) {
-  if (a.hd == 128) return launch_sk2_hd<128>(tq, tk, tvt, a, grid, st);
-  if (a.hd == 64) return launch_sk2_hd<64>(tq, tk, tvt, a, grid, st);
+  if (a.win_n) {
+    if (a.hd == 128) return launch_sk2_hd<128, true>(tq, tk, tvt, a, grid, st);
+    if (a.hd == 64) return launch_sk2_hd<64, true>(tq, tk, tvt, a, grid, st);
+    return cudaErrorInvalidValue;
+  }
+  if (a.hd == 128) return launch_sk2_hd<128, false>(tq, tk, tvt, a, grid, st);
+  if (a.hd == 64) return launch_sk2_hd<64, false>(tq, tk, tvt, a, grid, st);
   return cudaErrorInvalidValue;
 }
 
