@@ -16,6 +16,11 @@
 #ifndef SK2_EXPERIMENT
 #define SK2_EXPERIMENT 0
 #endif
+// SK2_TRACE=1 (micro-benchmark builds): compile in the clock64 / globaltimer stamps of
+// AttnTC::trace and ::cta_trace; the library's kernel carries none of that code
+#ifndef SK2_TRACE
+#define SK2_TRACE 0
+#endif
 
 namespace vi {
 
@@ -145,7 +150,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   // o_final committed, 4 last epilogue start, 5 owner flags seen, 6 exit, 7 segments,
   // 8..11 MMA warp: each segment's o_final commit (first 4), 12 continuation piece
   // published, 13 owner's merge done
-  long long* const ct = a.cta_trace ? a.cta_trace + (size_t)cta * 16 : nullptr;
+  long long* const ct = (SK2_TRACE && a.cta_trace) ? a.cta_trace + (size_t)cta * 16 : nullptr;
   if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
 
   if (warp == 16 && lane == 0) {
@@ -182,7 +187,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   if (threadIdx.x == 0) time_begin(a.timing);
   if (ct && threadIdx.x == 0) ct[1] = (long long)globaltimer();
   // debug timeline (VI_SK_TRACE): CTA 0, first segment's first 32 key tiles, 32 clock64 stamps per tile
-  long long* const trc = (a.trace && cta == 0) ? a.trace : nullptr;
+  long long* const trc = (SK2_TRACE && a.trace && cta == 0) ? a.trace : nullptr;
 
   if (warp == 16) {
     // TMA producer: the whole warp walks the schedule, one elected lane issues

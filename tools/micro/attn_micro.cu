@@ -12,6 +12,9 @@
 #include <cstdlib>
 #include <vector>
 
+#ifndef SK2_TRACE
+#define SK2_TRACE 1   // per-CTA / per-tile stamps compiled in (-DSK2_TRACE=0 for the library's code)
+#endif
 #include "../../paper_2403_16161_b200/csrc/kernels/attn_sk2.cu"
 #include "../../paper_2403_16161_b200/csrc/kernels/attn_sk3.cu"
 using namespace vi;
