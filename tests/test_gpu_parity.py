@@ -382,6 +382,21 @@ def test_window_split_invariance(split, monkeypatch):
     assert err < 1e-2, f"window split {split}: {err:.3g}"
 
 
+def test_stream_k_headdim64_c3_shape():
+    """Head dim 64 through the stream-K kernel (attn_sk2<64>): the C3 token grid (3600
+    queries x 10800 keys, 60 units) with D = 256; the 4th step compared stage by stage."""
+    cfg = CONFIGS["C3"].replace(layers=1, d_model=256)
+    w = make_weights(cfg, seed=23)
+    g = H().GpuStream(cfg, w)
+    o = O.OracleStream(cfg, w)
+    for i in range(4):
+        feats = make_features(cfg, 5, first_frame=5 * i, seed=23)
+        o.push(5)
+        _, ost = o.step(feats)
+        _, gst = g.step(feats, stages=(i == 3))
+    compare_step(cfg, ost, gst, 2e-2)
+
+
 def test_c2_full_shape_step():
     """BASELINE configs[1] at full size (STTN-shaped: 8 blocks, 4 heads of d 64, D 256,
     5x9-cell patches of a 60x108x256 map -> 144 tokens/frame, MLP-GELU 1024, T=5, M=10):
