@@ -319,7 +319,9 @@ static int sk_tail_weight() {
 // begins a unit switches segments and merges the unit's pieces at the end)
 static int sk_unit_cost() {
   const char* e = getenv("VI_SK_UNIT_COST");
-  const int b = e ? atoi(e) : 32;   // measured: 0 -> 86.9 us, 32 -> 85.5, 64 -> 85.9, 96 -> 87.6 (C3 micro)
+  // measured (C3 micro, same box): 0 -> 85.5 us, 16 -> 83.7, 32 -> 83.9, 48 -> 82.2,
+  // 56 -> 81.7, 58-60 -> 81.5, 62 -> 83.0, 64 -> 83.0 (partition-dependent steps)
+  const int b = e ? atoi(e) : 56;
   return b < 0 ? 0 : (b > 4096 ? 4096 : b);
 }
 static void debug_wait(vi_ctx* c, const char* where) {
