@@ -21,6 +21,15 @@
 #ifndef SK2_TRACE
 #define SK2_TRACE 0
 #endif
+// exp2 pairs k with k % MOD >= GE go to the degree-3 polynomial on the FMA pipe, the rest
+// to MUFU (C3 micro, same box: 5 of 16 pairs (3/2) 80.8 us, 4/16 (4/3) 81.4, 6/16 (5/3) 81.7,
+// none 82.9, 8/16 85.8; 3/2 moved one bf16-bar test to 2.04 % > 2 %: 4/3 kept)
+#ifndef SK2_POLY_MOD
+#define SK2_POLY_MOD 4
+#endif
+#ifndef SK2_POLY_GE
+#define SK2_POLY_GE 3
+#endif
 
 namespace vi {
 
@@ -459,7 +468,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             const int i = c * 16 + k;
             const float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
             float2 p;
-            if (k % 5 >= 3) {
+            if (k % SK2_POLY_MOD >= SK2_POLY_GE) {   // these exp2 pairs on the FMA pipe (polynomial)
               p = exp2_poly2(x);
             } else {
               p.x = ex2(x.x);
