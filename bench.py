@@ -30,12 +30,14 @@ UNIT = "frames/s"
 
 
 def peaks():
+    """Roofline denominators: the driver-measured MEASURED_PEAKS.json (bf16 dense burst, HBM
+    copy); without it the profiling guide's fallback figures, labelled "fallback"."""
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
             p = json.load(f)
-        return float(p["bf16_tflops"]), float(p["hbm_gbs"]), "measured"
+        return float(p["bf16_tflops"]), float(p["hbm_gbs"]), "measured (MEASURED_PEAKS.json)"
     except Exception:
-        return 1590.0, 6650.0, "fallback (B200_PROFILING.md)"
+        return 1590.0, 6650.0, "fallback (B200_PROFILING.md: no MEASURED_PEAKS.json)"
 
 
 WORKLOADS = {"C3": "FuseFormer-shaped memory step (BASELINE.json configs[2])",
@@ -127,53 +129,87 @@ def cpu_threads():
         return len(os.sched_getaffinity(0))
 
 
-def oracle_sample(cfg, seed=0):
-    """Time the fp64 oracle on a bounded sample of one step: split+embed of the 5-frame
-    chunk, ONE of the 8 blocks against a full 10-frame memory, composite.  Returns the
-    extrapolated seconds per step (embed + L * block + composite) and the sample time."""
-    import numpy as np
+def oracle_memory(cfg, seed=0):
+    """A full memory for the oracle: per block, the K/V of cfg.mem_frames resident frames,
+    projected (oracle.qkv) from seeded random block inputs (the values do not change the
+    work; the oracle's own stream would need mem_frames / T extra steps to fill it)."""
     from oracle import vi_oracle as O
-    from vi_synth import make_features, make_weights, rng_for
+    from vi_synth import make_weights, rng_for
     w = make_weights(cfg, seed=seed)
-    feats = make_features(cfg, cfg.t_new, first_frame=cfg.mem_frames, seed=seed)
     rng = rng_for(seed, "oracle-mem")
     mem = []
-    for j in range(cfg.mem_frames):          # K/V of the resident frames of block 0
-        _, _, K, V = O.qkv(rng.standard_normal((cfg.tokens, cfg.d_model)), w, 0, cfg)
-        mem.append((K, V))
+    for l in range(cfg.layers):
+        kv = []
+        for j in range(cfg.mem_frames):
+            _, _, K, V = O.qkv(rng.standard_normal((cfg.tokens, cfg.d_model)), w, l, cfg)
+            kv.append((K, V))
+        mem.append(kv)
+    return w, mem
+
+
+def oracle_step(cfg, w, mem, seed=0, layers=None):
+    """One WHOLE memory step of the fp64 oracle (no extrapolation): soft split + embedding of
+    the T new frames, every block against its full memory, back-projection + composite.
+    `layers` < cfg.layers runs only the first blocks (used for the 1-core sample).  Returns
+    the seconds it took."""
+    from oracle import vi_oracle as O
+    from vi_synth import make_features
+    feats = make_features(cfg, cfg.t_new, first_frame=cfg.mem_frames, seed=seed)
     t0 = time.perf_counter()
     _, X = O.embed(feats, w, cfg)
-    t1 = time.perf_counter()
-    X, _ = O.block_memory(X, mem, w, 0, cfg, cfg.t_new)
-    t2 = time.perf_counter()
+    for l in range(cfg.layers if layers is None else layers):
+        X, _ = O.block_memory(X, mem[l], w, l, cfg, cfg.t_new)
     O.compose(X, w, cfg, cfg.t_new)
-    t3 = time.perf_counter()
-    step = (t1 - t0) + cfg.layers * (t2 - t1) + (t3 - t2)
-    return step, t3 - t0
+    return time.perf_counter() - t0
 
 
 def run_reference(args, cfg):
+    """--impl reference: the fp64 oracle as it stands, on the host cores, on this arm's config
+    and metric.  Every timed step is a whole oracle memory step (5 frames through all blocks
+    against a full memory); the run is bounded in time: it stops after the step that crosses
+    REF_BUDGET_S seconds (at least one step), and prints the steps it actually timed."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    for _ in range(args.warmup):
-        oracle_sample(cfg)
+    budget = float(os.environ.get("REF_BUDGET_S", "90"))
+    w, mem = oracle_memory(cfg)
+    warm = min(args.warmup, 1)                   # nothing to warm up in NumPy beyond one step
+    for _ in range(warm):
+        oracle_step(cfg, w, mem)
     steps = []
-    for _ in range(args.steps):
-        s, _ = oracle_sample(cfg)
-        steps.append(s)
+    while len(steps) < args.steps and (not steps or sum(steps) < budget):
+        steps.append(oracle_step(cfg, w, mem, seed=len(steps)))
     total = sum(steps)
-    value = args.steps * cfg.t_new / total
+    value = len(steps) * cfg.t_new / total
     cores = cpu_threads()
-    sample = (f"per step: soft split + embedding of {cfg.t_new} frames, 1 of {cfg.layers} blocks against a full "
-              f"{cfg.mem_frames}-frame memory, composite; block time x{cfg.layers} (extrapolated)")
-    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": 1000 * total / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+    sample = (f"{len(steps)} whole oracle steps (of {args.steps} requested; time budget {budget:.0f} s): soft split + "
+              f"embedding of {cfg.t_new} frames, all {cfg.layers} blocks against a full {cfg.mem_frames}-frame "
+              f"memory, composite; {warm} untimed warm-up step")
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus, "steps": len(steps),
+            "steps_requested": args.steps, "warmup": warm, "ms_per_step": 1000 * total / len(steps),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
             "config": workload_config(cfg, args, args.gpus), "impl": "reference",
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def cpu_baseline(cfg):
+    """The oracle timed beside the GPU (rank 0, N = 1): one whole step on all host cores, and
+    one block (+ split/embedding + composite) on ONE core, scaled to a step (stated)."""
+    from threadpoolctl import threadpool_limits
+    w, mem = oracle_memory(cfg)
+    t_all = oracle_step(cfg, w, mem)
+    with threadpool_limits(limits=1):
+        t1_block = oracle_step(cfg, w, mem, layers=1)
+        t1_embed = oracle_step(cfg, w, mem, layers=0)
+    t1_step = t1_embed + cfg.layers * (t1_block - t1_embed)
+    return {"value": cfg.t_new / t_all, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
+            "sample": f"1 whole step ({cfg.t_new} frames, {cfg.layers} blocks against a full {cfg.mem_frames}-frame "
+                      f"memory, split/embed and composite): {t_all:.1f} s on all cores",
+            "one_core": {"value": cfg.t_new / t1_step, "unit": UNIT, "cores": 1,
+                         "sample": f"split/embed + 1 block + composite on 1 core ({t1_block:.1f} s), the block time "
+                                   f"x{cfg.layers} (scaled, not run)"}}
 
 
 def run_ours(args, cfg):
@@ -336,12 +372,23 @@ def run_ours(args, cfg):
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_in[0].numel() * 2,
                 "d2h_bytes_per_step": host_out[0].numel() * 2,
                 "api": "vi_run_step_async (pinned host buffers; copies overlap neighbouring steps)"},
+        # per-frame latency of a live source: frame i of a T-frame chunk waits for the T-1-i
+        # frames after it (batching delay), then for the step; at a 25 fps source and at a source
+        # delivering frames as fast as this run processes them
+        "frame_latency_ms": {
+            "step_p50": statistics.median(step_ms),
+            "source_25fps": {"first_frame": (T - 1) * 40.0 + statistics.median(step_ms),
+                             "mean": (T - 1) / 2 * 40.0 + statistics.median(step_ms)},
+            "source_at_processing_rate": {
+                "first_frame": (T - 1) * total_ms / (args.steps * T) + statistics.median(step_ms),
+                "mean": (T - 1) / 2 * total_ms / (args.steps * T) + statistics.median(step_ms)}},
         "gpu_launches": launches,
         "clocks": clk,
     }
-    line["device_time_ms_per_step"] = {"attention": attn_ms / args.steps, "gemm": prof["gemm"][0] / args.steps,
-                                       "other": (total_ms - attn_ms - prof["gemm"][0]) / args.steps}
-    gemm_ms = max(sub[3]["gemm"][0] / extra_steps, 1e-9)    # (> 0 even when a VI_ABLATE run skips them)
+    gemm_ms = max(sub[3]["gemm"][0] / extra_steps, 1e-9)    # GEMMs' own device time (profile mode 3 sub-run)
+    line["device_time_ms_per_step"] = {"attention": attn_ms / args.steps, "gemm": gemm_ms,
+                                       "other": total_ms / args.steps - attn_ms / args.steps - gemm_ms,
+                                       "gemm_source": "self-timed in a separate 20-step sub-run (profile mode 3)"}
     patch_ms = max(sub[2]["patch"][0] / extra_steps, 1e-9)
     gflop, pbytes = gemm_flop_per_step(cfg) / (world if args.tp else 1), patch_bytes_per_step(cfg)
     line["secondary_rooflines"] = {
@@ -356,17 +403,7 @@ def run_ours(args, cfg):
         line["profile_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}
         line["profile_launches_per_step"] = {k: v[1] / args.steps for k, v in prof.items()}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        est, spent, reps = [], 0.0, 0
-        while spent < 10.0 and reps < 8:          # a bounded ~10 s sample of CPU work
-            s, sample_s = oracle_sample(cfg, seed=reps)
-            est.append(s)
-            spent += sample_s
-            reps += 1
-        step_s = statistics.median(est)
-        line["cpu_baseline"] = {"value": T / step_s, "unit": UNIT, "cores": cpu_threads(), "kind": "oracle",
-                                "sample": f"{reps} x (split/embed of one {T}-frame chunk + 1 of {cfg.layers} blocks "
-                                          f"against a full {cfg.mem_frames}-frame memory + composite) = "
-                                          f"{spent:.1f} s of CPU work; block time x{cfg.layers}, median"}
+        line["cpu_baseline"] = cpu_baseline(cfg)
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

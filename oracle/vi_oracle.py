@@ -204,14 +204,16 @@ def f3n_mix(u: np.ndarray, cfg) -> np.ndarray:
     return soft_split(folded, *g)
 
 
-def ffn(h2: np.ndarray, w: Dict[str, np.ndarray], l: int, cfg, n_frames: int) -> Tuple[np.ndarray, np.ndarray]:
-    """FFN of block l on LN2 output h2 [n*P, D]; returns (u, g) and the caller adds W2."""
+def ffn(h2: np.ndarray, w: Dict[str, np.ndarray], l: int, cfg, n_frames: int,
+        store=None) -> Tuple[np.ndarray, np.ndarray]:
+    """FFN of block l on LN2 output h2 [n*P, D]; returns (u, g) and the caller adds W2.
+    (``store``: the emulation's rounding of the stored hidden g, see ``qkv``.)"""
     u = linear(h2, w["w1"][l], w["b1"][l])
     if cfg.ffn_kind == 1:
         g = gelu(f3n_mix(u.reshape(n_frames, cfg.tokens, -1), cfg).reshape(u.shape))
     else:
         g = gelu(u)
-    return u, g
+    return u, _st(store, g)
 
 
 def embed(feats: np.ndarray, w: Dict[str, np.ndarray], cfg) -> Tuple[np.ndarray, np.ndarray]:
@@ -232,11 +234,22 @@ def compose(X: np.ndarray, w: Dict[str, np.ndarray], cfg, n_frames: int) -> Tupl
     return Yp, out
 
 
-def qkv(x: np.ndarray, w, l: int, cfg):
-    h = layer_norm(x, w["ln1_g"][l], w["ln1_b"][l])
+def _st(store, a):
+    return a if store is None else store(a)
+
+
+def qkv(x: np.ndarray, w, l: int, cfg, store=None):
+    """LN1 and the Q/K/V projection of block l.  ``store`` (default None: plain fp64) is a
+    storage-rounding function applied where the bf16 design stores a tensor (here the LN1
+    output h and Q, K, V) -- the bf16-storage EMULATION used only to derive logit-scaled
+    tolerance bars (see ``emulate_bf16_storage``); never the oracle itself."""
+    h = _st(store, layer_norm(x, w["ln1_g"][l], w["ln1_b"][l]))
     D = cfg.d_model
     y = linear(h, w["wqkv"][l], w["bqkv"][l])
-    return h, y[:, :D], y[:, D:2 * D], y[:, 2 * D:]
+    Q, K, V = y[:, :D], y[:, D:2 * D], y[:, 2 * D:]
+    if store is not None:
+        Q, K, V = store(Q), store(K), store(V)
+    return h, Q, K, V
 
 
 # ----------------------------------------------------------------------------------
@@ -256,12 +269,12 @@ def token_windows(cfg) -> Optional[np.ndarray]:
 
 
 def block_memory(x: np.ndarray, mem_kv: Sequence[Tuple[np.ndarray, np.ndarray]], w, l: int, cfg,
-                 n_frames: int, chunk_causal: bool = False) -> Tuple[np.ndarray, Dict[str, np.ndarray]]:
+                 n_frames: int, chunk_causal: bool = False, store=None) -> Tuple[np.ndarray, Dict[str, np.ndarray]]:
     """x [n*P, D] = block-l input of the chunk; mem_kv = [(K_j, V_j)] in frame-id order.
     With window attention (cfg.win_h > 0) a query sees only the keys of its own token window,
     in every frame of the memory and the chunk."""
     P = cfg.tokens
-    h1, Q, Kc, Vc = qkv(x, w, l, cfg)
+    h1, Q, Kc, Vc = qkv(x, w, l, cfg, store)
     K = np.concatenate([k for k, _ in mem_kv] + [Kc], axis=0)
     V = np.concatenate([v for _, v in mem_kv] + [Vc], axis=0)
     allowed = None
@@ -277,9 +290,10 @@ def block_memory(x: np.ndarray, mem_kv: Sequence[Tuple[np.ndarray, np.ndarray]],
         same = wq[:, None] == wk[None, :]
         allowed = same if allowed is None else (allowed & same)
     O, lse = attention(Q, K, V, cfg.heads, allowed=allowed, return_lse=True)
+    O = _st(store, O)
     xa = x + linear(O, w["wo"][l], w["bo"][l])
-    h2 = layer_norm(xa, w["ln2_g"][l], w["ln2_b"][l])
-    u, g = ffn(h2, w, l, cfg, n_frames)
+    h2 = _st(store, layer_norm(xa, w["ln2_g"][l], w["ln2_b"][l]))
+    u, g = ffn(h2, w, l, cfg, n_frames, store)
     xo = xa + linear(g, w["w2"][l], w["b2"][l])
     st = dict(h1=h1, q=Q, k=Kc, v=Vc, o=O, lse=lse, x_attn=xa, h2=h2, u=u, g=g, x=xo)
     return xo, st
@@ -437,9 +451,10 @@ class OracleMemory:
 class OracleStream:
     """A live stream through the Memory model (Eq. 3), one chunk of n new frames per step."""
 
-    def __init__(self, cfg, w: Dict[str, np.ndarray], chunk_causal: bool = False):
+    def __init__(self, cfg, w: Dict[str, np.ndarray], chunk_causal: bool = False, store=None):
         self.cfg = cfg
         self.w = w
+        self.store = store     # None: the oracle; a rounding function: the bf16-storage emulation
         self.mem = OracleMemory(cfg.mem_frames, cfg.t_new, getattr(cfg, "ref_rate", 0), getattr(cfg, "max_refs", 0))
         self.chunk_causal = chunk_causal
         # (layer, frame id) -> ("x", block input [P, D]) or ("kv", K [P, D], V [P, D])
@@ -473,7 +488,7 @@ class OracleStream:
             if e[0] == "kv":
                 out.append((e[1], e[2]))
             else:
-                _, _, K, V = qkv(e[1], self.w, l, self.cfg)
+                _, _, K, V = qkv(e[1], self.w, l, self.cfg, self.store)
                 out.append((K, V))
         return out
 
@@ -490,7 +505,7 @@ class OracleStream:
             mem = self.memory_kv(l)
             for i in range(n):   # cache this block's input for the chunk's frames
                 self.entries[(l, self.mem.cur_first + i)] = ("x", X[i * P:(i + 1) * P].copy())
-            X, st = block_memory(X, mem, self.w, l, cfg, n, self.chunk_causal)
+            X, st = block_memory(X, mem, self.w, l, cfg, n, self.chunk_causal, self.store)
             stages["layers"].append(st)
         Yp, out = compose(X, self.w, cfg, n)
         stages["x"] = X
@@ -504,8 +519,34 @@ class OracleStream:
         e = self.entries[(l, fid)]
         if e[0] == "kv":
             return e[1], e[2]
-        _, _, K, V = qkv(e[1], self.w, l, self.cfg)
+        _, _, K, V = qkv(e[1], self.w, l, self.cfg, self.store)
         return K, V
+
+
+def bf16_round(a: np.ndarray) -> np.ndarray:
+    """Round fp64 values to the nearest bf16 (round-to-nearest-even), returned as fp64.
+    Two steps: fp64 -> fp32 (RNE) -> bf16 (RNE on the fp32 bit pattern); this double
+    rounding is what a GPU storing an fp32 accumulator as bf16 does."""
+    a32 = np.ascontiguousarray(np.asarray(a, np.float64).astype(np.float32))
+    u = a32.view(np.uint32).astype(np.uint64)
+    r = (((u + 0x7FFF + ((u >> 16) & 1)) >> 16) << 16).astype(np.uint32).view(np.float32)
+    r = np.where(np.isnan(a32), np.float32(np.nan), r)
+    return r.astype(np.float64)
+
+
+def emulate_bf16_storage(cfg, w: Dict[str, np.ndarray], chunk_causal: bool = False) -> "OracleStream":
+    """The bf16-STORAGE EMULATION (GPU-free, test infrastructure for tolerance bars only):
+    the oracle stream with every tensor the bf16 design STORES in bf16 rounded to bf16 at
+    that point -- the GEMM A operands h = LN1(x), O (attention output), h2 = LN2(x) and the
+    FFN hidden g, and Q, K, V (the query buffer and the K/V ring-buffer memory; BASELINE
+    north_star "in bf16 with fp32 accumulate", reading Q15).  The softmax
+    probabilities P (bf16 in the GPU's TMEM) are NOT rounded: that rounding, the fp32
+    accumulation order and the exp2 approximations are the GPU's own arithmetic, which the
+    tests hold to the plain bar against this emulation.  Everything else stays exact fp64.
+    Its distance from the plain oracle is the error storage alone causes at the given logit
+    scale (a logit s moves by ~|s| 2^-8); tests derive the bars of the logit-sensitive
+    weight variants from it."""
+    return OracleStream(cfg, w, chunk_causal=chunk_causal, store=bf16_round)
 
 
 def mac_counts(P: int, n_mem: int, n_new: int, D: int) -> int:
@@ -513,9 +554,12 @@ def mac_counts(P: int, n_mem: int, n_new: int, D: int) -> int:
     return (n_new * P) * ((n_mem + n_new) * P) * D
 
 
-def rel_err(got: np.ndarray, ref: np.ndarray) -> float:
-    """Tolerance metric (reading Q18): max_i |g_i - o_i| / max(|o_i|, rms(o))."""
+def rel_err(got: np.ndarray, ref: np.ndarray, den_ref: Optional[np.ndarray] = None) -> float:
+    """Tolerance metric (reading Q18): max_i |g_i - o_i| / max(|d_i|, rms(d)), d = ref (or
+    ``den_ref``: distances to an emulation are normalised by the oracle's values, so that
+    rel_err(g, o) <= rel_err(g, e; den_ref=o) + rel_err(e, o) holds element by element)."""
     got = np.asarray(got, np.float64); ref = np.asarray(ref, np.float64)
-    rms = math.sqrt(float(np.mean(ref * ref))) if ref.size else 0.0
-    den = np.maximum(np.abs(ref), rms if rms > 0 else 1e-300)
+    d = ref if den_ref is None else np.asarray(den_ref, np.float64)
+    rms = math.sqrt(float(np.mean(d * d))) if d.size else 0.0
+    den = np.maximum(np.abs(d), rms if rms > 0 else 1e-300)
     return float(np.max(np.abs(got - ref) / den)) if ref.size else 0.0

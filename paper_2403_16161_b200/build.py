@@ -19,14 +19,13 @@ SOURCES = [
     "ring.cpp",
     "tp.cpp",
     "engine.cu",
+    "kernels/setup.cu",
     "kernels/patch.cu",
     "kernels/rows.cu",
     "kernels/gemm_simt.cu",
     "kernels/gemm_tc.cu",
     "kernels/attn.cu",
-    "kernels/attn_sk.cu",
     "kernels/attn_sk2.cu",
-    "kernels/attn_sk3.cu",
 ]
 
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")

@@ -94,18 +94,6 @@ bool make_tmap_box(CUtensorMap* m, const void* base, uint64_t cols, uint64_t row
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
-// VI_PAIR=0: the FFN2 GEMM (K = F) on single-CTA tiles instead of CTA pairs (A/B measurements)
-const bool g_pair_ffn2 = [] {
-  const char* e = getenv("VI_PAIR");
-  return !(e && e[0] == '0');
-}();
-
-// VI_TMA_EPI=0: the GEMMs store from registers instead of through TMA (A/B measurements)
-const bool g_tma_epi = [] {
-  const char* e = getenv("VI_TMA_EPI");
-  return !(e && e[0] == '0');
-}();
-
 uint16_t f2bf(float f) {  // round to nearest even
   uint32_t u;
   std::memcpy(&u, &f, 4);
@@ -287,27 +275,6 @@ static const bool g_debug_sync = [] {
   const char* e = getenv("VI_DEBUG_SYNC");
   return e && e[0] == '1';
 }();
-// VI_ATTN_V1=1 selects the one-Q-tile attention kernel (A/B comparisons).
-static const bool g_attn_v1 = [] {
-  const char* e = getenv("VI_ATTN_V1");
-  return e && e[0] == '1';
-}();
-// VI_ATTN_SPLIT=1: attention v2 with a fixed KV split + combine kernel instead of stream-K.
-static const bool g_attn_split = [] {
-  const char* e = getenv("VI_ATTN_SPLIT");
-  return e && e[0] == '1';
-}();
-// VI_ATTN_COLSPLIT=1: attention v2 with the column-split softmax (A/B experiments).
-static const bool g_attn_colsplit = [] {
-  const char* e = getenv("VI_ATTN_COLSPLIT");
-  return e && e[0] == '1';
-}();
-// VI_ATTN_SK=1|2|3: stream-K attention with 8 (row-per-thread), 16 (column-split) or 16
-// (16x256b layout) softmax warps; sk2 measured fastest (tools/micro/attn_micro).
-static const int g_attn_sk = [] {
-  const char* e = getenv("VI_ATTN_SK");
-  return e ? atoi(e) : 2;
-}();
 // VI_SK_TAIL_W: cost of a tail pair's key tile in 16ths of a full pair's (sk2 work split);
 // read when a step is recorded, so a sweep can change it between contexts
 static int sk_tail_weight() {
@@ -351,9 +318,11 @@ static void debug_wait(vi_ctx* c, const char* where) {
     CK((call), where);             \
     if (g_debug_sync) debug_wait(c, where); \
   } while (0)
-// VI_ABLATE=<mask> (timing experiments only, results are garbage): skip the launches of the
-// profile categories whose bit is set (1 attention, 2 GEMMs, 4 patch, 8 row kernels), to
-// measure each class's marginal cost inside the step graph
+// VI_ABLATE_BUILD (a separate timing-experiment build, never the product library: its
+// results are garbage): VI_ABLATE=<mask> skips the launches of the profile categories whose
+// bit is set (1 attention, 2 GEMMs, 4 patch, 8 row kernels), to measure each class's
+// marginal cost inside the step graph
+#ifdef VI_ABLATE_BUILD
 static const int g_ablate = [] {
   const char* e = getenv("VI_ABLATE");
   return e ? atoi(e) : 0;
@@ -365,6 +334,13 @@ static const int g_ablate = [] {
       LAUNCH(call, where);                         \
     }                                              \
   } while (0)
+#else
+#define PLAUNCH(cat, call, where)                  \
+  do {                                             \
+    Prof p_(c, cat);                               \
+    LAUNCH(call, where);                           \
+  } while (0)
+#endif
 #define CK_C(ctx, call, where)                              \
   do {                                                      \
     cudaError_t e_ = (call);                                \
@@ -651,30 +627,6 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   }
   if (c->bf16) {
     if (c->D % 128) c->bn_o = c->bn_2 = 64;
-    // VI_BN="qkv=256,ffn1=256,...": N-tile overrides for A/B measurements (64, 128 or 256)
-    if (const char* e = getenv("VI_BN")) {
-      std::string spec(e);
-      size_t pos = 0;
-      while (pos < spec.size()) {
-        size_t end = spec.find(',', pos);
-        if (end == std::string::npos) end = spec.size();
-        const std::string item = spec.substr(pos, end - pos);
-        const size_t eq = item.find('=');
-        if (eq != std::string::npos) {
-          const std::string k = item.substr(0, eq);
-          const int v = atoi(item.c_str() + eq + 1);
-          if (v == 64 || v == 128 || v == 256) {
-            if (k == "embed") c->bn_embed = v;
-            if (k == "qkv") c->bn_qkv = v;
-            if (k == "o") c->bn_o = v;
-            if (k == "ffn1") c->bn_1 = v;
-            if (k == "ffn2") c->bn_2 = v;
-            if (k == "back") c->bn_back = v;
-          }
-        }
-        pos = end + 1;
-      }
-    }
     if (build_maps(c) != VI_OK) {
       delete c;
       return VI_E_CUDA;
@@ -970,20 +922,18 @@ extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refin
 
 // ------------------------------------------------------------------------------ compute
 
-static vi_ctx* g_epi_ctx = nullptr;   // set by the launching entry point (single-threaded per ctx)
-static Epi epi_base(int kind, int M, int N, const float* bias) {
+static Epi epi_base(const vi_ctx* c, int kind, int M, int N, const float* bias) {
   Epi e;
   std::memset(&e, 0, sizeof(e));
   e.kind = kind; e.M = M; e.N = N; e.bias = bias; e.P = 1; e.S = 1;
-  if (g_epi_ctx && g_epi_ctx->prof_mode == 3)
-    e.timing = g_epi_ctx->attn_timing + sizeof(KernelTiming) / sizeof(unsigned long long);
+  if (c->prof_mode == 3)   // the GEMMs' self-timing slot (vi_profile mode 3)
+    e.timing = c->attn_timing + sizeof(KernelTiming) / sizeof(unsigned long long);
   return e;
 }
 
 extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out, int project) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  g_epi_ctx = c;
   if (!feat || !out || n < 1 || n > c->Tmax || (project != 0 && project != 1))
     return c->fail(VI_E_ARG, "vi_soft_split: bad argument");
   if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_split: weights not set");
@@ -992,10 +942,10 @@ extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out
   PLAUNCH(VI_PROF_PATCH, launch_unfold(feat, tok, n, c->g, dt, c->stream), "unfold");
   if (project) {
     const int M = n * c->P;
-    Epi e = epi_base(EPI_STORE, M, c->D, c->b_embed);
+    Epi e = epi_base(c, EPI_STORE, M, c->D, c->b_embed);
     e.out = out; e.ldo = c->D; e.out_f32 = 1; e.pos = c->cfg.pos_embed ? c->pos : nullptr; e.P = c->P;
     CUtensorMap tmo;
-    const bool te = c->bf16 && g_tma_epi && make_tmap_out(&tmo, out, true, c->D, M);
+    const bool te = c->bf16 && make_tmap_out(&tmo, out, true, c->D, M);
     if (c->bf16)
       PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, c->bn_embed, e, c->stream, 0,
                                            te ? &tmo : nullptr),
@@ -1061,7 +1011,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   // a3: LN1
   PLAUNCH(VI_PROF_ROW, launch_layernorm(x_in, c->ln1_g + (size_t)l * D, c->ln1_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln1");
   // a4: QKV projection + memory write
-  Epi eq = epi_base(EPI_QKV, M, 3 * Dl, c->b_qkv + (size_t)l * 3 * Dl);
+  Epi eq = epi_base(c, EPI_QKV, M, 3 * Dl, c->b_qkv + (size_t)l * 3 * Dl);
   eq.D = Dl; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
   eq.S = c->S; eq.P = c->P; eq.vt_ld = c->vt_ld;
   if (c->win_n) {
@@ -1070,7 +1020,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   }
   eq.qkv_krow0 = int(l * SP);
   eq.qkv_vrow0 = l * Dl;
-  const bool qte = c->bf16 && g_tma_epi && c->qkv_te;
+  const bool qte = c->bf16 && c->qkv_te;
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_wqkv, l * 3 * Dl, M, 3 * Dl, D, c->bn_qkv, eq, c->stream, 0,
                                          qte ? &c->tm_q_out : nullptr, qte ? &c->tm_k_out : nullptr,
@@ -1124,7 +1074,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   // VI_WIN_SPLIT CTAs per unit (C4: 64 units of 6 key tiles; attn_tc2's KV split + combine
   // kernel measured 28 us/block)
   const int win_units = c->win_n ? c->win_n * a.win_npw * a.H : 0;
-  if (c->win_n && g_attn_sk == 2 && !g_attn_split && win_units <= c->num_sms) {
+  if (c->win_n && win_units <= c->num_sms) {
     a.npairs = a.win_npw;
     a.units = win_units;
     a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
@@ -1137,42 +1087,29 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
     return VI_OK;
   }
-  if (!g_attn_v1 && !g_attn_split && !small && !c->win_n) {
+  if (!small && !c->win_n) {
     // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
     a.npairs = (a.Nq + 255) / 256;
     a.units = a.npairs * a.H;
     a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
     const long long work = (long long)a.units * ntiles;
-    // sk2: a last pair with an empty second tile (C3: 3600 = 14 x 256 + 16) skips tile 1's
-    // MMAs and the dead softmax quadrants, but its key tiles still cost about a full pair's
-    // (the per-tile chain QK -> softmax -> PV is the bound, not the work): VI_SK_TAIL_W = 16
+    // a last pair with an empty second tile (C3: 3600 = 14 x 256 + 16) skips tile 1's MMAs
+    // and the dead softmax quadrants, but its key tiles still cost about a full pair's (the
+    // per-tile chain QK -> softmax -> PV is the bound, not the work): VI_SK_TAIL_W = 16
     // (measured: 8 -> +46 % attention time, 10 -> +22 %)
     const int rem = a.Nq % 256;
-    a.sk_tail = (g_attn_sk == 2 && rem > 0 && rem <= 128) ? 1 : 0;
+    a.sk_tail = (rem > 0 && rem <= 128) ? 1 : 0;
     a.sk_tail_w = 16;
     if (a.sk_tail) a.sk_tail_w = sk_tail_weight();
     a.sk_ucost = sk_unit_cost();
     a.sk_wfull = (long long)(a.npairs - a.sk_tail) * a.H * ntiles;
-    int grid = int(work < c->num_sms ? work : c->num_sms);
-    if (const char* gs = getenv("VI_SK_GRID")) grid = std::max(1, std::min(grid, atoi(gs)));
-    if (g_attn_sk == 1)
-      PLAUNCH(VI_PROF_ATTN, launch_attn_sk(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-    else if (g_attn_sk == 2)
-      PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-    else
-      PLAUNCH(VI_PROF_ATTN, launch_attn_sk3(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
-  } else {   // fixed KV split + combine kernel (small chunks; VI_ATTN_V1 / VI_ATTN_SPLIT A/B variants)
-    if (g_attn_v1 && c->sharded) return c->fail(VI_E_CONFIG, "VI_ATTN_V1 does not support head sharding");
-    const int qrows = g_attn_v1 ? 128 : 256;       // queries per CTA (v2: two 128-row tiles)
-    if (c->win_n && (g_attn_v1 || g_attn_colsplit))
-      return c->fail(VI_E_CONFIG, "window attention runs on the attn_tc2 row-per-thread kernel only");
-    const int units = c->win_n ? c->win_n * a.win_npw * a.H : ((a.Nq + qrows - 1) / qrows) * a.H;
+    const int grid = int(work < c->num_sms ? work : c->num_sms);
+    PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
+  } else {   // small chunks (and windows beyond one wave): fixed KV split + combine kernel
+    const int units = c->win_n ? c->win_n * a.win_npw * a.H : ((a.Nq + 255) / 256) * a.H;
     choose_split(units, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
-    if (g_attn_v1)
-      PLAUNCH(VI_PROF_ATTN, launch_attn_tc(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
-    else
-      PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream, g_attn_colsplit), "attention");
+    PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
     if (a.nsplit > 1) PLAUNCH(VI_PROF_ATTN, launch_attn_combine(a, c->stream), "attention combine");
   }
   return VI_OK;
@@ -1194,14 +1131,14 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
     }
   }
   // a7: output projection + residual
-  Epi eo = epi_base(EPI_RESID, M, D, c->b_o + (size_t)l * D);
+  Epi eo = epi_base(c, EPI_RESID, M, D, c->b_o + (size_t)l * D);
   eo.x_in = x_in; eo.x_out = x_out;
   if (c->sharded) {   // A = concat_h(O_h) read head-major from the gathered buffer
     eo.a_hs = c->tp.head_rows;
     eo.a_kpb = c->hd / 64;
   }
   CUtensorMap tx_in, tx_out;
-  const bool te = c->bf16 && g_tma_epi && make_tmap_out(&tx_in, x_in, true, D, M) && make_tmap_out(&tx_out, x_out, true, D, M);
+  const bool te = c->bf16 && make_tmap_out(&tx_in, x_in, true, D, M) && make_tmap_out(&tx_out, x_out, true, D, M);
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->sharded ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream, 0,
                                          te ? &tx_out : nullptr, te ? &tx_in : nullptr),
@@ -1213,11 +1150,11 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   PLAUNCH(VI_PROF_ROW, launch_layernorm(x_out, c->ln2_g + (size_t)l * D, c->ln2_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln2");
   // a9 / a10: FFN1 (+ F3N fold/unfold) + GELU
   const bool f3n = c->cfg.ffn_kind == VI_FFN_F3N;
-  Epi e1 = epi_base(f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
+  Epi e1 = epi_base(c, f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
   e1.out = f3n ? c->u : c->gbuf; e1.ldo = F; e1.out_f32 = f3n ? 1 : 0;
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream, 0,
-                                         g_tma_epi ? (f3n ? &c->tm_u_out : &c->tm_g_out) : nullptr),
+                                         f3n ? &c->tm_u_out : &c->tm_g_out),
             "ffn1 gemm");
   else
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->h, (const float*)c->w_1 + (size_t)l * F * D, M, F, D, e1, c->stream),
@@ -1228,10 +1165,10 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
     PLAUNCH(VI_PROF_PATCH, launch_unfold(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream), "f3n unfold");
   }
   // a11: FFN2 + residual
-  Epi e2 = epi_base(EPI_RESID, M, D, c->b_2 + (size_t)l * D);
+  Epi e2 = epi_base(c, EPI_RESID, M, D, c->b_2 + (size_t)l * D);
   e2.x_in = x_out; e2.x_out = x_out;
   // FFN2 (K = F = 1960) on CTA-pair tiles 256 x 128 (tools/micro/gemm_micro: 16.9 vs 18.3 us)
-  const bool pair2 = te && g_pair_ffn2;
+  const bool pair2 = te;
   if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, pair2 ? c->tm_w2_pair : c->tm_w2, l * D, M, D, F, pair2 ? 128 : c->bn_2, e2,
                                          c->stream, pair2 ? 1 : 0, te ? &tx_out : nullptr, te ? &tx_out : nullptr),
@@ -1263,7 +1200,6 @@ static void layer_done(vi_ctx* c, int layer) {
 extern "C" vi_status vi_memory_step_attn(vi_ctx* c, int layer, const float* x_in) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  g_epi_ctx = c;
   vi_status st = check_step(c, layer, x_in, x_in, "vi_memory_step_attn");
   if (st != VI_OK) return st;
   if (c->attn_layer == layer) return c->fail(VI_E_PROTOCOL, "vi_memory_step_attn: this layer's _ffn is pending");
@@ -1275,7 +1211,6 @@ extern "C" vi_status vi_memory_step_attn(vi_ctx* c, int layer, const float* x_in
 extern "C" vi_status vi_memory_step_ffn(vi_ctx* c, int layer, const float* x_in, float* x_out) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  g_epi_ctx = c;
   vi_status st = check_step(c, layer, x_in, x_out, "vi_memory_step_ffn");
   if (st != VI_OK) return st;
   if (c->attn_layer != layer) return c->fail(VI_E_PROTOCOL, "vi_memory_step_ffn: needs vi_memory_step_attn of this layer");
@@ -1287,7 +1222,6 @@ extern "C" vi_status vi_memory_step_ffn(vi_ctx* c, int layer, const float* x_in,
 extern "C" vi_status vi_memory_step(vi_ctx* c, int layer, const float* x_in, float* x_out) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  g_epi_ctx = c;
   vi_status st = check_step(c, layer, x_in, x_out, "vi_memory_step");
   if (st != VI_OK) return st;
   if (c->sharded && !c->comm)
@@ -1335,7 +1269,6 @@ extern "C" vi_status vi_tp_local_allgather(vi_ctx* const* ctxs, int n) {
 extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* feat, int project) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  g_epi_ctx = c;
   if (!in || !feat || n < 1 || n > c->Tmax || (project != 0 && project != 1))
     return c->fail(VI_E_ARG, "vi_soft_composite: bad argument");
   if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_composite: weights not set");
@@ -1343,7 +1276,7 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
   const void* tok = in;
   if (project) {
     const int M = n * c->P;
-    Epi e = epi_base(EPI_STORE, M, c->Pd, c->b_back);
+    Epi e = epi_base(c, EPI_STORE, M, c->Pd, c->b_back);
     e.out = c->tokens; e.ldo = c->Pd;
     if (c->bf16) {
       // x enters the GEMM as bf16 hi + lo (K = 2D against [Wb | Wb]) and Yp leaves it in
@@ -1351,7 +1284,7 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
       e.out = c->yp32; e.out_f32 = 1;
       PLAUNCH(VI_PROF_ROW, launch_split_bf16((const float*)in, c->xb, M, c->D, c->stream), "cast");
       PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_xb, c->tm_wback, 0, M, c->Pd, 2 * c->D, c->bn_back, e, c->stream, 0,
-                                           g_tma_epi ? &c->tm_yp_out : nullptr),
+                                           &c->tm_yp_out),
               "back gemm");
     } else {
       PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)in, (const float*)c->w_back, M, c->Pd, c->D, e, c->stream),
@@ -1376,7 +1309,7 @@ static vi_status step_body(vi_ctx* c, const void* fin, int n, void* fout) {
 // CUDA graph, captured on first use for this (shape, ring state, buffers, weights, profiling).
 static vi_status step_graph(vi_ctx* c, const void* fin, int n, void* fout) {
   vi_status st;
-  const bool graphs = c->use_graphs && !g_debug_sync && c->prof_mode != 2 && !getenv("VI_ATTN_TRACE");
+  const bool graphs = c->use_graphs && !g_debug_sync && c->prof_mode != 2;
   if (!graphs) return step_body(c, fin, n, fout);
   // everything a replay bakes in: shapes, ring state, buffers, weights, profiling mode
   std::vector<uint64_t> key = {uint64_t(n), uint64_t(c->ring.cur_first % c->S), c->ring.valid_mask(),
@@ -1435,6 +1368,8 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
   DeviceGuard dg_(c->cfg.device);
   vi_status st = check_run_step(c, feat, n, out, "vi_run_step");
   if (st != VI_OK) return st;
+  st = vi_memory_push(c, n, first_id, nullptr, nullptr);   // host bookkeeping + queued commits
+  if (st != VI_OK) return st;
   const size_t fbytes = (size_t)n * c->g.H * c->g.W * c->g.C * c->es;
   const bool hin = is_host_ptr(feat), hout = is_host_ptr(out);
   const void* fin = feat;
@@ -1442,8 +1377,6 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
     CK(cudaMemcpyAsync(c->feat_in, feat, fbytes, cudaMemcpyHostToDevice, c->stream), "run_step h2d");
     fin = c->feat_in;
   }
-  st = vi_memory_push(c, n, first_id, nullptr, nullptr);   // host bookkeeping + queued commits
-  if (st != VI_OK) return st;
   void* fout = hout ? c->feat_out : out;
   if ((st = step_graph(c, fin, n, fout)) != VI_OK) return st;
   if (hout) {
@@ -1453,27 +1386,52 @@ extern "C" vi_status vi_run_step(vi_ctx* c, const void* feat, int n, void* out, 
   return VI_OK;
 }
 
+// First use of vi_run_step_async: the copy streams, staging slots and events, created into
+// locals and published only when all of them exist (a failure leaves the context unchanged).
+static vi_status async_init(vi_ctx* c) {
+  cudaStream_t in_s = nullptr, out_s = nullptr;
+  void* bufs[4] = {nullptr, nullptr, nullptr, nullptr};
+  cudaEvent_t evs[6] = {nullptr, nullptr, nullptr, nullptr, nullptr, nullptr};
+  const size_t fmap = (size_t)c->Tmax * c->g.H * c->g.W * c->g.C * c->es;
+  bool ok = cudaStreamCreateWithFlags(&in_s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&out_s, cudaStreamNonBlocking) == cudaSuccess;
+  for (int i = 0; i < 4 && ok; ++i) ok = cudaMalloc(&bufs[i], fmap) == cudaSuccess;
+  for (int i = 0; i < 6 && ok; ++i) ok = cudaEventCreateWithFlags(&evs[i], cudaEventDisableTiming) == cudaSuccess;
+  if (!ok) {
+    cudaGetLastError();
+    for (void* b : bufs)
+      if (b) cudaFree(b);
+    for (cudaEvent_t e : evs)
+      if (e) cudaEventDestroy(e);
+    if (in_s) cudaStreamDestroy(in_s);
+    if (out_s) cudaStreamDestroy(out_s);
+    return c->fail(VI_E_OOM, "vi_run_step_async: staging streams / buffers / events could not be created");
+  }
+  for (int k = 0; k < 2; ++k) {
+    c->async_in[k] = bufs[2 * k];
+    c->async_out[k] = bufs[2 * k + 1];
+    c->allocs.push_back(bufs[2 * k]);
+    c->allocs.push_back(bufs[2 * k + 1]);
+    c->device_bytes += 2 * fmap;
+    c->ev_h2d[k] = evs[3 * k];
+    c->ev_done[k] = evs[3 * k + 1];
+    c->ev_d2h[k] = evs[3 * k + 2];
+  }
+  c->io_out = out_s;
+  c->io_stream = in_s;       // published last: io_stream != NULL <=> everything above exists
+  return VI_OK;
+}
+
 extern "C" vi_status vi_run_step_async(vi_ctx* c, const void* feat, int n, void* out, int64_t* first_id) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
   vi_status st = check_run_step(c, feat, n, out, "vi_run_step_async");
   if (st != VI_OK) return st;
-  if (!c->io_stream) {
-    if (cudaStreamCreateWithFlags(&c->io_stream, cudaStreamNonBlocking) != cudaSuccess ||
-        cudaStreamCreateWithFlags(&c->io_out, cudaStreamNonBlocking) != cudaSuccess) {
-      cudaGetLastError();
-      return c->fail(VI_E_CUDA, "vi_run_step_async: stream creation failed");
-    }
-    const size_t fmap = (size_t)c->Tmax * c->g.H * c->g.W * c->g.C * c->es;
-    for (int k = 0; k < 2; ++k) {
-      c->async_in[k] = c->dalloc(fmap, false);
-      c->async_out[k] = c->dalloc(fmap, false);
-      if (!c->async_in[k] || !c->async_out[k]) return c->fail(VI_E_OOM, "vi_run_step_async: staging allocation failed");
-      for (cudaEvent_t* e : {&c->ev_h2d[k], &c->ev_done[k], &c->ev_d2h[k]})
-        if (cudaEventCreateWithFlags(e, cudaEventDisableTiming) != cudaSuccess)
-          return c->fail(VI_E_CUDA, "vi_run_step_async: event creation failed");
-    }
-  }
+  if (!c->io_stream && (st = async_init(c)) != VI_OK) return st;
+  // the push first: the only call here that can fail without poisoning the context, and its
+  // device work (queued commits, reference moves) is on the ctx stream ahead of the step
+  st = vi_memory_push(c, n, first_id, nullptr, nullptr);
+  if (st != VI_OK) return st;
   const size_t fbytes = (size_t)n * c->g.H * c->g.W * c->g.C * c->es;
   const int k = c->async_slot;
   c->async_slot ^= 1;
@@ -1490,8 +1448,6 @@ extern "C" vi_status vi_run_step_async(vi_ctx* c, const void* feat, int n, void*
   }
   // compute stream: the output staging is free once its previous copy-out is done
   if (hout && c->async_used[k]) CK(cudaStreamWaitEvent(c->stream, c->ev_d2h[k], 0), "async wait");
-  st = vi_memory_push(c, n, first_id, nullptr, nullptr);
-  if (st != VI_OK) return st;
   void* fout = hout ? c->async_out[k] : out;
   if ((st = step_graph(c, fin, n, fout)) != VI_OK) return st;
   CK(cudaEventRecord(c->ev_done[k], c->stream), "async record");

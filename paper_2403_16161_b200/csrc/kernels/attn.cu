@@ -5,19 +5,10 @@
 // resident frames f-M .. f-1 (Eq. 3).  Softmax is exact (max-subtracted,
 // online over key tiles; reading Q14), key order = slot order (permutation invariant).
 //
-// attn_tc_kernel (bf16, sm_100a tensor cores), one CTA = (128-query tile, head, KV split):
-//   warp 0 lane 0 : TMA producer -- Q tile once, then K tiles [128 keys][d] and
-//                   transposed-V tiles [d][128 keys] through a 2-stage ring
-//   warp 1 lane 0 : MMA issuer -- S_b = Q K^T (tcgen05, M=128 N=128, TMEM, double-
-//                   buffered b = 0/1) and O += P V (M=128, N=d, TMEM)
-//   warp 2        : TMEM allocator (512 columns: S0 | S1 | O)
-//   warps 4..7    : softmax -- thread i owns query row i (TMEM lane i): tcgen05.ld of
-//                   its S row, mask, running max / sum in the log2 domain (ex2), P to
-//                   shared memory in the 128B-swizzled K-major layout the MMA reads,
-//                   O rescale in TMEM when the running max grows, final 1/l epilogue.
-// QK^T of tile j+1 runs on the tensor core while the softmax of tile j runs.
-// KV splits write normalised fp32 partials + log2-sum-exp; attn_combine_kernel merges
-// them in a fixed order (deterministic, no atomics).
+// Kernels here: the fp32 SIMT path (attn_simt_f32_kernel, BASELINE configs[0]) and the
+// small-chunk tensor-core path (attn_tc2_kernel: fixed KV split, partials merged by
+// attn_combine_kernel in a fixed order -- deterministic, no atomics).  The large-chunk
+// default is the persistent stream-K kernel of attn_sk2.cu.
 #include "kernels.h"
 
 namespace vi {
@@ -63,21 +54,6 @@ cudaError_t launch_attn_simt_f32(const AttnArgs& a, cudaStream_t st) {
 }
 
 // ------------------------------------------------------------------ tcgen05 bf16 path
-template <int HD>
-struct AttnSmem {
-  static constexpr int ST = 2;
-  static constexpr int QB = 128 * HD * 2;       // Q tile: HD/64 atoms of [128 rows][128 B]
-  static constexpr int KB = 128 * HD * 2;       // K tile: same layout (128 key rows)
-  static constexpr int VB = HD * 128 * 2;       // Vt tile: 2 atoms (keys 0-63 | 64-127) of [HD rows][128 B]
-  static constexpr int PB = 128 * 128 * 2;      // P tile: 2 atoms of [128 rows][128 B]
-  static constexpr int Q_OFF = 0;
-  static constexpr int K_OFF = QB;
-  static constexpr int V_OFF = K_OFF + ST * KB;
-  static constexpr int P_OFF = V_OFF + ST * VB;
-  static constexpr int BAR_OFF = P_OFF + PB;
-  static constexpr int NBAR = 1 + 2 * ST + 2 * ST + 2 + 2 + 1 + 1;
-  static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
-};
 
 // Tile g of the valid key space: keys row0 .. row0+127 of the slab, of which
 // [nskip, nvalid) belong to valid slots (the rest is masked to -inf).
@@ -101,264 +77,6 @@ __device__ __forceinline__ void key_tile(const KeySegs& s, int g, int& row0, int
   nskip = off == 0 ? s.lead[i] : 0;
 }
 
-template <int HD>
-__global__ void __launch_bounds__(256, 1)
-attn_tc_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
-               const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
-  using L = AttnSmem<HD>;
-  constexpr int ST = L::ST;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);  // 1 KB aligned, stays in .shared
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + L::BAR_OFF);
-  uint64_t* q_full = bars;
-  uint64_t* k_full = bars + 1;
-  uint64_t* k_empty = k_full + ST;
-  uint64_t* v_full = k_empty + ST;
-  uint64_t* v_empty = v_full + ST;
-  uint64_t* s_full = v_empty + ST;
-  uint64_t* s_empty = s_full + 2;
-  uint64_t* p_full = s_empty + 2;
-  uint64_t* o_done = p_full + 1;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_done + 1);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int q0 = blockIdx.x * 128, h = blockIdx.y, z = blockIdx.z;
-  const int ntiles = a.segs.tile0[a.segs.n];
-  const int t_begin = z * a.tiles_per_split;
-  int t_end = t_begin + a.tiles_per_split;
-  if (t_end > ntiles) t_end = ntiles;
-  const int n = t_end > t_begin ? t_end - t_begin : 0;
-
-  if (warp == 0 && lane == 0) {
-    tma_prefetch(&tq);
-    tma_prefetch(&tk);
-    tma_prefetch(&tvt);
-    mbar_init(q_full, 1);
-    for (int s = 0; s < ST; ++s) {
-      mbar_init(&k_full[s], 1);
-      mbar_init(&k_empty[s], 1);
-      mbar_init(&v_full[s], 1);
-      mbar_init(&v_empty[s], 1);
-    }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&s_full[b], 1);
-      mbar_init(&s_empty[b], 128);
-    }
-    mbar_init(p_full, 128);
-    mbar_init(o_done, 1);
-    fence_barrier_init();
-  }
-  if (warp == 2) tmem_alloc(tmem_slot, 512);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  const uint32_t tmem = *tmem_slot;
-  const uint32_t TM_S = tmem, TM_O = tmem + 256;
-
-  if (warp == 0) {
-    if (lane == 0 && n > 0) {
-      uint8_t* sq = smem + L::Q_OFF;
-      mbar_arrive_expect_tx(q_full, L::QB);
-#pragma unroll
-      for (int at = 0; at < HD / 64; ++at) tma_load_2d(sq + at * 16384, &tq, q_full, h * HD + at * 64, q0);
-      for (int jj = 0; jj < n; ++jj) {
-        int row0, nv, nskip;
-        key_tile(a.segs, t_begin + jj, row0, nv, nskip);
-        const int st = jj % ST;
-        const uint32_t par = ((jj / ST) & 1) ^ 1;
-        if (jj >= ST) mbar_wait(&k_empty[st], par);
-        uint8_t* sk = smem + L::K_OFF + st * L::KB;
-        mbar_arrive_expect_tx(&k_full[st], L::KB);
-#pragma unroll
-        for (int at = 0; at < HD / 64; ++at)
-          tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + row0);
-        if (jj >= ST) mbar_wait(&v_empty[st], par);
-        uint8_t* sv = smem + L::V_OFF + st * L::VB;
-        mbar_arrive_expect_tx(&v_full[st], L::VB);
-#pragma unroll
-        for (int at = 0; at < 2; ++at)
-          tma_load_2d(sv + at * (HD * 128), &tvt, &v_full[st], row0 + at * 64, a.vrow_base + h * HD);
-      }
-    }
-  } else if (warp == 1) {
-    if (lane == 0 && n > 0) {
-      constexpr uint32_t idesc_s = idesc_bf16_f32(128, 128);
-      constexpr uint32_t idesc_o = idesc_bf16_f32(128, HD);
-      const uint32_t sq = smem_u32(smem + L::Q_OFF);
-      const uint32_t sp = smem_u32(smem + L::P_OFF);
-      mbar_wait(q_full, 0);
-      auto issue_qk = [&](int t) {
-        const int st = t % ST, b = t & 1;
-        mbar_wait(&k_full[st], (t / ST) & 1);
-        if (t >= 2) mbar_wait(&s_empty[b], ((t >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t sk = smem_u32(smem + L::K_OFF + st * L::KB);
-#pragma unroll
-        for (int kk = 0; kk < HD / 16; ++kk) {
-          const uint32_t off = (kk >> 2) * 16384 + (kk & 3) * 32;
-          umma_bf16_ss(TM_S + b * 128, sdesc_k_sw128(sq + off), sdesc_k_sw128(sk + off), idesc_s, kk > 0);
-        }
-        umma_commit(&k_empty[st]);
-        umma_commit(&s_full[b]);
-      };
-      issue_qk(0);
-      for (int jj = 0; jj < n; ++jj) {
-        if (jj + 1 < n) issue_qk(jj + 1);
-        const int st = jj % ST;
-        mbar_wait(p_full, jj & 1);
-        mbar_wait(&v_full[st], (jj / ST) & 1);
-        tc_fence_after();
-        const uint32_t sv = smem_u32(smem + L::V_OFF + st * L::VB);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t offp = (kk >> 2) * 16384 + (kk & 3) * 32;
-          const uint32_t offv = (kk >> 2) * (HD * 128) + (kk & 3) * 32;
-          umma_bf16_ss(TM_O, sdesc_k_sw128(sp + offp), sdesc_k_sw128(sv + offv), idesc_o, (jj | kk) != 0);
-        }
-        umma_commit(&v_empty[st]);
-        umma_commit(o_done);
-      }
-    }
-  } else if (warp >= 4) {
-    const int qd = warp - 4;
-    const int row = qd * 32 + lane;                 // query row inside the tile == TMEM lane
-    const uint32_t lane_off = uint32_t(qd * 32) << 16;
-    uint8_t* sp = smem + L::P_OFF;
-    float m = -INFINITY, l = 0.f;
-    for (int jj = 0; jj < n; ++jj) {
-      const int b = jj & 1;
-      int row0, nv, nskip;
-      key_tile(a.segs, t_begin + jj, row0, nv, nskip);
-      mbar_wait(&s_full[b], (jj >> 1) & 1);
-      tc_fence_after();
-      float s[128];
-#pragma unroll
-      for (int c = 0; c < 4; ++c) tmem_ld32(TM_S + lane_off + b * 128 + c * 32, reinterpret_cast<uint32_t*>(s + c * 32));
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(&s_empty[b]);
-      float mx = -INFINITY;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        if (i >= nv || i < nskip) s[i] = -INFINITY;
-        mx = fmaxf(mx, s[i]);
-      }
-      const float m_new = fmaxf(m, mx * a.scale_log2);
-      const float alpha = ex2(m - m_new);
-      // the row sum is taken over the bf16-rounded P the PV MMA actually multiplies
-      float sum = 0.f;
-#pragma unroll
-      for (int i = 0; i < 128; ++i) {
-        const float p = __bfloat162float(__float2bfloat16_rn(ex2(fmaf(s[i], a.scale_log2, -m_new))));
-        s[i] = p;
-        sum += p;
-      }
-      l = l * alpha + sum;
-      if (jj > 0) {
-        mbar_wait(o_done, (jj - 1) & 1);              // PV(jj-1) done: O stable, P buffer free
-        tc_fence_after();
-        // tcgen05.ld/st are warp-collective: rescale if any row of this warp needs it
-        if (__any_sync(0xffffffffu, alpha < 1.f)) {
-#pragma unroll 1
-          for (int c = 0; c < HD; c += 16) {
-            uint32_t r[16];
-            tmem_ld16(TM_O + lane_off + c, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 16; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st16(TM_O + lane_off + c, r);
-          }
-          tmem_wait_st();
-        }
-      }
-      // P row -> smem, K-major, 128-byte swizzle: 16-byte chunk c of row r sits at c ^ (r & 7)
-#pragma unroll
-      for (int at = 0; at < 2; ++at) {
-        uint8_t* base = sp + at * 16384 + row * 128;
-#pragma unroll
-        for (int c = 0; c < 8; ++c) {
-          const float* p = s + at * 64 + c * 8;
-          *reinterpret_cast<uint4*>(base + ((c ^ (row & 7)) << 4)) =
-              make_uint4(pack_bf16(p[0], p[1]), pack_bf16(p[2], p[3]), pack_bf16(p[4], p[5]), pack_bf16(p[6], p[7]));
-        }
-      }
-      fence_proxy_async_smem();
-      tc_fence_before();
-      mbar_arrive(p_full);
-      m = m_new;
-    }
-    // epilogue
-    const int q = q0 + row;
-    if (n > 0) {
-      mbar_wait(o_done, (n - 1) & 1);
-      tc_fence_after();
-    }
-    const float inv = n > 0 ? 1.f / l : 0.f;
-    if (a.nsplit == 1) {
-#pragma unroll 1
-      for (int c = 0; c < HD; c += 16) {
-        uint32_t r[16];
-        tmem_ld16(TM_O + lane_off + c, r);
-        tmem_wait_ld();
-        if (q < a.Nq) {
-          float* f = reinterpret_cast<float*>(r);
-          uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.D + h * HD + c);
-          dst[0] = make_uint4(pack_bf16(f[0] * inv, f[1] * inv), pack_bf16(f[2] * inv, f[3] * inv),
-                              pack_bf16(f[4] * inv, f[5] * inv), pack_bf16(f[6] * inv, f[7] * inv));
-          dst[1] = make_uint4(pack_bf16(f[8] * inv, f[9] * inv), pack_bf16(f[10] * inv, f[11] * inv),
-                              pack_bf16(f[12] * inv, f[13] * inv), pack_bf16(f[14] * inv, f[15] * inv));
-        }
-      }
-    } else {
-      float* op = a.opart + ((size_t)z * a.Nq + q) * a.D + h * HD;
-#pragma unroll 1
-      for (int c = 0; c < HD; c += 16) {
-        uint32_t r[16];
-        if (n > 0) {
-          tmem_ld16(TM_O + lane_off + c, r);
-          tmem_wait_ld();
-        }
-        if (q < a.Nq) {
-          float4* dst = reinterpret_cast<float4*>(op + c);
-#pragma unroll
-          for (int i = 0; i < 4; ++i)
-            dst[i] = n > 0 ? make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
-                                         __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
-        }
-      }
-      if (q < a.Nq) a.lse[((size_t)z * a.H + h) * a.Nq + q] = n > 0 ? m + __log2f(l) : -INFINITY;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    tc_fence_after();
-    tmem_dealloc(tmem, 512);
-  }
-}
-
-template <int HD>
-static cudaError_t launch_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                             cudaStream_t st) {
-  using L = AttnSmem<HD>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<HD>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
-  dim3 grid((a.Nq + 127) / 128, a.H, a.nsplit);
-  attn_tc_kernel<HD><<<grid, 256, L::TOTAL, st>>>(tq, tk, tvt, a);
-  return cudaGetLastError();
-}
-
-cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                           cudaStream_t st) {
-  if (a.hd == 128) return launch_hd<128>(tq, tk, tvt, a, st);
-  if (a.hd == 64) return launch_hd<64>(tq, tk, tvt, a, st);
-  return cudaErrorInvalidValue;
-}
 
 // ------------------------------------------------------------------ v2: two Q tiles per CTA
 // attn_tc2_kernel: one CTA = (pair of 128-query tiles, head, KV split), 384 threads:
@@ -385,20 +103,11 @@ struct Attn2Smem {
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
   static constexpr int NBAR = 1 + 4 * ST + 2 + 4 + 2;
-  static constexpr int XCH_OFF = BAR_OFF + NBAR * 8 + 16;      // [2 phases][2 halves][128 rows] fp32
-  static constexpr int TOTAL = XCH_OFF + 2 * 2 * 128 * 4 + 1024;
+  static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
 };
 
-__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
-}
-
-// CS = false: one softmax warpgroup per Q tile (thread = row, all 128 keys);
-// CS = true : column split -- all 8 softmax warps work on each Q tile in turn, warp w and
-//             w+4 own the same 32 rows and keys [0,64) / [64,128) of the tile; the row max
-//             is exchanged through shared memory (named barrier per warp pair).  Halves
-//             the per-tile softmax latency that sits on the tensor core's critical path.
-template <int HD, bool CS>
+// One softmax warpgroup per Q tile (thread = row, all 128 keys).
+template <int HD>
 __global__ void __launch_bounds__(384, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                 const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
@@ -535,140 +244,6 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         issue_pv(t, n - 1);
         umma_commit(&o_final[t]);
       }
-    }
-  } else if (warp < 8 && CS) {
-    const int qd = warp & 3, hf = warp >> 2;          // lane quadrant, key half
-    const int row = qd * 32 + lane;
-    const uint32_t lane_off = uint32_t(qd * 32) << 16;
-    float* xch = reinterpret_cast<float*>(smem + L::XCH_OFF);
-    constexpr int OH = HD / 2;                        // O columns owned by this half
-    float m_use[2] = {-INFINITY, -INFINITY}, l[2] = {0.f, 0.f};
-    int phase = 0;
-    const float2 cc = make_float2(a.scale_log2, a.scale_log2);
-    for (int jj = 0; jj < n; ++jj) {
-      int row0, nv, nskip;
-      key_tile(a.segs, t_begin + jj, row0, nv, nskip);
-      const int lo = nskip - hf * 64, hi = nv - hf * 64;   // valid local keys [lo, hi)
-#pragma unroll 1
-      for (int t = 0; t < 2; ++t, ++phase) {
-        const uint32_t TS = tmem + t * 128 + lane_off, TO = tmem + 256 + t * 128 + lane_off;
-        mbar_wait(&s_full[t], jj & 1);
-        tc_fence_after();
-        float s[64];
-        tmem_ld32(TS + hf * 64, reinterpret_cast<uint32_t*>(s));
-        tmem_ld32(TS + hf * 64 + 32, reinterpret_cast<uint32_t*>(s + 32));
-        tmem_wait_ld();
-        if (lo > 0 || hi < 64) {
-#pragma unroll
-          for (int i = 0; i < 64; ++i)
-            if (i < lo || i >= hi) s[i] = -INFINITY;
-        }
-        float mx[8];
-#pragma unroll
-        for (int i = 0; i < 8; ++i) mx[i] = -INFINITY;
-#pragma unroll
-        for (int i = 0; i < 64; ++i) mx[i & 7] = fmaxf(mx[i & 7], s[i]);
-        const float lm = fmaxf(fmaxf(fmaxf(mx[0], mx[1]), fmaxf(mx[2], mx[3])),
-                               fmaxf(fmaxf(mx[4], mx[5]), fmaxf(mx[6], mx[7])));
-        float* xb = xch + (phase & 1) * 256;
-        xb[hf * 128 + row] = lm;
-        named_bar_sync(1 + qd, 64);                   // both halves loaded S and posted a max
-        const float rmax = fmaxf(lm, xb[(hf ^ 1) * 128 + row]) * a.scale_log2;
-        const bool grow = rmax > m_use[t] + 8.f;      // lazy rescale (identical in both halves)
-        float alpha = 1.f;
-        if (grow) {
-          alpha = ex2(m_use[t] - rmax);
-          m_use[t] = rmax;
-        }
-        if (__any_sync(0xffffffffu, grow) && jj > 0) {
-#pragma unroll 1
-          for (int c = 0; c < OH; c += 32) {
-            uint32_t r[32];
-            tmem_ld32(TO + hf * OH + c, r);
-            tmem_wait_ld();
-#pragma unroll
-            for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * alpha);
-            tmem_st32(TO + hf * OH + c, r);
-          }
-          tmem_wait_st();
-          named_bar_sync(1 + qd, 64);                 // both O halves rescaled before any PV
-        }
-        const float2 mm = make_float2(-m_use[t], -m_use[t]);
-        float2 sum[4];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) sum[i] = make_float2(0.f, 0.f);
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-          uint32_t pk[16];
-#pragma unroll
-          for (int k = 0; k < 16; ++k) {
-            const int i = c * 16 + k;
-            const float2 x = ffma2(make_float2(s[2 * i], s[2 * i + 1]), cc, mm);
-            float2 p;
-            if ((k & 3) == 3) {
-              p = exp2_poly2(x);
-            } else {
-              p.x = ex2(x.x);
-              p.y = ex2(x.y);
-            }
-            __nv_bfloat162 b = __floats2bfloat162_rn(p.x, p.y);
-            pk[k] = *reinterpret_cast<uint32_t*>(&b);
-            sum[k & 3] = fadd2(sum[k & 3], p);
-          }
-          tmem_st16(TS + hf * 32 + c * 16, pk);     // P keys [hf*64, +64) -> packed cols [hf*32, +32)
-        }
-        const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
-        l[t] = l[t] * alpha + (s01.x + s01.y);
-        tmem_wait_st();
-        tc_fence_before();
-        mbar_arrive(&p_full[2 * t + hf]);
-      }
-    }
-    // epilogue: combine the two halves' row sums, each warp writes its O column half
-#pragma unroll 1
-    for (int t = 0; t < 2; ++t, ++phase) {
-      float* xb = xch + (phase & 1) * 256;
-      xb[hf * 128 + row] = l[t];
-      named_bar_sync(1 + qd, 64);
-      const float lt = l[t] + xb[(hf ^ 1) * 128 + row];
-      const uint32_t TO = tmem + 256 + t * 128 + lane_off + hf * OH;
-      const int q = q0 + t * 128 + row;
-      if (n > 0) {
-        mbar_wait(&o_final[t], 0);
-        tc_fence_after();
-      }
-      const float inv = n > 0 ? 1.f / lt : 0.f;
-#pragma unroll 1
-      for (int c = 0; c < OH; c += 32) {
-        uint32_t r[32];
-        if (n > 0) {
-          tmem_ld32(TO + c, r);
-          tmem_wait_ld();
-        } else {
-#pragma unroll
-          for (int i = 0; i < 32; ++i) r[i] = 0u;
-        }
-        if (q < a.Nq) {
-          const float* f = reinterpret_cast<const float*>(r);
-          const int col = h * HD + hf * OH + c;
-          if (a.nsplit == 1) {
-            uint4* dst = reinterpret_cast<uint4*>(a.o + (size_t)q * a.o_ld + (size_t)h * a.o_hs + (col - h * HD));
-#pragma unroll
-            for (int i = 0; i < 4; ++i)
-              dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv),
-                                  pack_bf16(f[8 * i + 2] * inv, f[8 * i + 3] * inv),
-                                  pack_bf16(f[8 * i + 4] * inv, f[8 * i + 5] * inv),
-                                  pack_bf16(f[8 * i + 6] * inv, f[8 * i + 7] * inv));
-          } else {
-            float4* dst = reinterpret_cast<float4*>(a.opart + ((size_t)z * a.Nq + q) * a.D + col);
-#pragma unroll
-            for (int i = 0; i < 8; ++i)
-              dst[i] = make_float4(f[4 * i] * inv, f[4 * i + 1] * inv, f[4 * i + 2] * inv, f[4 * i + 3] * inv);
-          }
-        }
-      }
-      if (a.nsplit > 1 && hf == 0 && q < a.Nq)
-        a.lse[((size_t)z * a.H + h) * a.Nq + q] = n > 0 ? m_use[t] + __log2f(lt) : -INFINITY;
     }
   } else if (warp < 8) {
     const int t = warp >> 2;                          // Q tile of this warpgroup
@@ -817,26 +392,21 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   }
 }
 
-template <int HD, bool CS>
+template <int HD>
 static cudaError_t launch2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                               cudaStream_t st) {
   using L = Attn2Smem<HD>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_tc2_kernel<HD, CS>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(attn_tc2_kernel<HD>), L::TOTAL);
+  if (e != cudaSuccess) return e;
   dim3 grid(a.win_n ? a.win_n * a.win_npw : (a.Nq + 255) / 256, a.H, a.nsplit);
-  attn_tc2_kernel<HD, CS><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
+  attn_tc2_kernel<HD><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
   return cudaGetLastError();
 }
 
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                            cudaStream_t st, bool colsplit) {
-  if (a.hd == 128) return colsplit ? launch2_hd<128, true>(tq, tk, tvt, a, st) : launch2_hd<128, false>(tq, tk, tvt, a, st);
-  if (a.hd == 64) return colsplit ? launch2_hd<64, true>(tq, tk, tvt, a, st) : launch2_hd<64, false>(tq, tk, tvt, a, st);
+                            cudaStream_t st) {
+  if (a.hd == 128) return launch2_hd<128>(tq, tk, tvt, a, st);
+  if (a.hd == 64) return launch2_hd<64>(tq, tk, tvt, a, st);
   return cudaErrorInvalidValue;
 }
 

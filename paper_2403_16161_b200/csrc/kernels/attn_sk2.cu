@@ -641,12 +641,8 @@ template <int HD, bool WIN>
 static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
                                 const AttnTC& a, int grid, cudaStream_t st) {
   using L = AttnSk2Smem<HD>;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(attn_sk2_kernel<HD, WIN>, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(attn_sk2_kernel<HD, WIN>), L::TOTAL);
+  if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(576);

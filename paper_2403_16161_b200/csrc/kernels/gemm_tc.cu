@@ -321,8 +321,6 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   if (threadIdx.x == 0) time_end(epi.timing, gridDim.x);
 }
 
-static int g_num_sms = 0;
-
 template <int BN, int STAGES, bool PAIR, bool TE>
 static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int brow0, int M, int N, int K,
                               const Epi& e, cudaStream_t st, const CUtensorMap* tmo, const CUtensorMap* tmx,
@@ -330,29 +328,9 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   using L = GemmSmem<BN, STAGES, PAIR, TE>;
   constexpr int CS = PAIR ? 2 : 1;
   auto kfn = gemm_tc_kernel<BN, STAGES, PAIR, TE>;
-  static int max_clusters = 0;
-  if (!max_clusters) {
-    cudaError_t err = cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, L::TOTAL);
-    if (err != cudaSuccess) return err;
-    int dev = 0;
-    cudaGetDevice(&dev);
-    cudaDeviceGetAttribute(&g_num_sms, cudaDevAttrMultiProcessorCount, dev);
-    max_clusters = g_num_sms / CS;
-    if (PAIR) {
-      cudaLaunchConfig_t q = {};
-      q.gridDim = dim3(CS * max_clusters);
-      q.blockDim = dim3(384);
-      q.dynamicSmemBytes = L::TOTAL;
-      cudaLaunchAttribute at[1];
-      at[0].id = cudaLaunchAttributeClusterDimension;
-      at[0].val.clusterDim.x = CS; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
-      q.attrs = at;
-      q.numAttrs = 1;
-      int n = 0;
-      if (cudaOccupancyMaxActiveClusters(&n, kfn, &q) == cudaSuccess && n > 0) max_clusters = n;
-      cudaGetLastError();
-    }
-  }
+  int max_clusters = 0;
+  cudaError_t err = ensure_kernel_setup(reinterpret_cast<const void*>(kfn), L::TOTAL, CS, 384, &max_clusters);
+  if (err != cudaSuccess) return err;
   const int TM = PAIR ? 256 : 128;
   const int ntiles = ((M + TM - 1) / TM) * ((N + BN - 1) / BN);
   const int ncl = ntiles < max_clusters ? ntiles : max_clusters;

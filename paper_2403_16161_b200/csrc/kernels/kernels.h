@@ -29,6 +29,12 @@ cudaError_t pdl_launch(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t s
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 
+// Per-device, thread-safe one-time setup of a kernel (setup.cu): the dynamic shared memory
+// opt-in on the CURRENT device, and (cluster > 1) the number of clusters of `cluster` CTAs
+// of `block` threads that fit at once (else the SM count); returned in *max_clusters.
+cudaError_t ensure_kernel_setup(const void* fn, int smem_bytes, int cluster = 1, int block = 0,
+                                int* max_clusters = nullptr);
+
 struct Geom {
   int H, W, C, kh, kw, sh, sw, ph, pw, oh, ow;
 };
@@ -132,20 +138,12 @@ struct AttnTC {
   // (keys masked, queries not written); output row of (t, i) = t * P + token(w, i)
   int win_n, win_npw, win_qstride, win_kstride, win_pad, win_real, win_h, win_w, win_cols, ow, P, win_nq;
 };
-cudaError_t launch_attn_tc(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                           cudaStream_t st);
-// two 128-query tiles per CTA, P kept in TMEM (see attn.cu)
+// two 128-query tiles per CTA, P kept in TMEM, fixed KV split (small chunks; attn.cu)
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                            cudaStream_t st, bool colsplit);
+                            cudaStream_t st);
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st);
-// persistent stream-K variant (one CTA per SM, no combine kernel)
-cudaError_t launch_attn_sk(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                           int grid, cudaStream_t st);
-// same with column-split softmax, 16 softmax warps (attn_sk2.cu; the default)
+// persistent stream-K, column-split softmax, 16 softmax warps (attn_sk2.cu; the default)
 cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
-                            int grid, cudaStream_t st);
-// same schedule, softmax warps in the 16x256b TMEM layout (attn_sk3.cu; VI_ATTN_SK=3)
-cudaError_t launch_attn_sk3(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                             int grid, cudaStream_t st);
 
 }  // namespace vi

@@ -4,6 +4,9 @@ seeded inputs.  Bars (BASELINE.json north_star; metric = reading Q18, oracle.rel
   * fp32 SIMT path: rel_err <= 1e-4 on every stage and output;
   * bf16 tensor-core path: rel_err <= 2e-2 on every stage and output.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 import torch
@@ -37,59 +40,94 @@ def assert_close(got, ref, tol, what):
     return e
 
 
-def logit_scale(cfg, ol):
-    """rms of the scaled attention logits of a block (oracle values).  On the bf16 path the
-    queries and the K memory are stored in bf16, so a logit s carries an error ~|s| 2^-8
-    and the attention output's error grows linearly with the logit scale (DESIGN.md,
-    "Tolerances"); the output stage keeps the plain 2e-2 bar."""
-    d = cfg.head_dim
-    q, k = ol["q"], ol["k"]
-    vals = []
-    for h in range(cfg.heads):
-        sl = slice(h * d, (h + 1) * d)
-        vals.append((q[:256, sl] @ k[:256, sl].T).ravel() / np.sqrt(d))
-    return float(np.sqrt(np.mean(np.concatenate(vals) ** 2)))
+# Per-test worst error / bar ratios (headroom record): VI_PARITY_LOG=<file> appends one JSON
+# line per compared stage group, so a GPU run documents how close every test is to its bar.
+PARITY_LOG = os.environ.get("VI_PARITY_LOG")
 
 
-# Worst element over ~10^5 outputs of one input vs the emulated typical maximum (DESIGN.md §5):
-# the same kernels measured 3.01 % at sigma = 0.99 where the emulation gave 2.7 %.
-ATTN_STAGE_MARGIN = 1.25
+def log_parity(tag, errs, bars, emu=None):
+    if not PARITY_LOG:
+        return
+    worst = max(errs, key=lambda k: errs[k] / bars[k])
+    rec = {"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "tag": tag,
+           "worst_stage": worst, "err": errs[worst], "bar": bars[worst], "ratio": errs[worst] / bars[worst]}
+    if emu:
+        we = max(emu, key=emu.get)
+        rec["vs_emulation"] = {"stage": we, "err": emu[we]}
+    with open(PARITY_LOG, "a") as f:
+        f.write(json.dumps(rec) + "\n")
 
 
-def attn_stage_factor(cfg, ol):
-    """Bar multiplier of the block-internal stages after the attention: 1.25 max(1, 1.5 sigma)."""
-    return ATTN_STAGE_MARGIN * max(1.0, 1.5 * logit_scale(cfg, ol))
+def stage_pairs(cfg, ost, gst, est=None):
+    """(name, gpu, oracle, emulation) for every compared stage of one step."""
+    out = [("x0", gst["x0"], ost["x0"], est["x0"] if est else None)]
+    for l, (ol, gl) in enumerate(zip(ost["layers"], gst["layers"])):
+        el = est["layers"][l] if est else None
+        names = (("q",) if "q" in gl else ()) + (("o", "u", "g") if cfg.ffn_kind == 1 else ("o", "g")) + ("x",)
+        for k in names:
+            out.append((f"{k}{l}", gl[k], ol[k], el[k] if el else None))
+    out.append(("out", gst["out"], ost["out"], est["out"] if est else None))
+    return out
 
 
-def compare_step(cfg, ost, gst, tol, tag="", sharp=False):
-    """Stage-by-stage parity.  Outputs (x after every block, the composite) are held to the
-    north_star bar `tol`.  On the bf16 path the block-internal stages after the attention
-    (o, u, g) are held to tol * 1.25 max(1, 1.5 sigma), sigma = rms attention logit: the
-    memory stores Q/K/V in bf16, so a logit s carries an error ~|s| 2^-8 that exact
-    arithmetic on the bf16-stored operands already shows (DESIGN.md "Tolerances";
-    emulated: sigma 0.2 -> 1.0%, 1 -> 2.7%, 5 -> 8.5%).  `sharp` applies the same factor
-    to the outputs (logits ~5x larger than a trained model's)."""
-    errs = {}
+def compare_step(cfg, ost, gst, tol, tag="", est=None):
+    """Stage-by-stage parity against the fp64 oracle (BASELINE north_star bars; metric =
+    reading Q18).  Without `est` (the metric config's N(0, 0.02) weights, the fp32 path)
+    every stage and output is held to `tol` as it stands.
+
+    With `est` = the same step through ``oracle.emulate_bf16_storage`` (the oracle with every
+    tensor the design stores in bf16 -- h, Q, K, V, O, h2, g -- rounded there; GPU-free,
+    computed in this test from the same inputs): the logit-sensitive weight variants, whose
+    attention amplifies the storage rounding of Q/K (a logit s moves by ~|s| 2^-8), hold every
+    stage to rel_err(gpu, oracle) <= tol + E with E = rel_err(emulation, oracle) -- the
+    storage error at this logit scale plus the plain bar for the GPU's own arithmetic (triangle
+    inequality), no constant fitted to a GPU measurement.  The GPU's distance
+    to the emulation itself is logged, not asserted: the two round h / Q / K of slightly
+    different fp32-vs-fp64 values, so ~2.5 % of the stored elements sit one ulp apart at a
+    rounding boundary, and sharp logits amplify exactly that (tools/parity_diag.py).  The
+    attention kernel's own arithmetic (bf16 P, exp2 approximations) is held to `tol`
+    separately against fp64 attention of the GPU's own Q/K/V (check_attention_kernel)."""
+    errs, bars, emu = {}, {}, {}
     if "tp" in gst:
         assert np.array_equal(gst["tp"].float().cpu().numpy().astype(np.float64), ost["tp"]), "soft split not bit-exact"
-    errs["x0"] = assert_close(gst["x0"], ost["x0"], tol, tag + "x0")
-    fmax = 1.0
-    for l, (ol, gl) in enumerate(zip(ost["layers"], gst["layers"])):
-        f = attn_stage_factor(cfg, ol) if tol > 1e-3 else 1.0
-        fmax = max(fmax, f)
-        if "q" in gl:
-            errs[f"q{l}"] = assert_close(gl["q"], ol["q"], tol, f"{tag}layer {l} q")
-        for k in (("o", "u", "g") if cfg.ffn_kind == 1 else ("o", "g")):
-            errs[f"{k}{l}"] = assert_close(gl[k], ol[k], tol * f, f"{tag}layer {l} {k}") / f
-        errs[f"x{l}"] = assert_close(gl["x"], ol["x"], tol * (fmax if sharp else 1.0), f"{tag}layer {l} x")
-    errs["out"] = assert_close(gst["out"], ost["out"], tol * (fmax if sharp else 1.0), tag + "out")
+    for name, g, o, e in stage_pairs(cfg, ost, gst, est):
+        g = g.float().cpu().numpy() if isinstance(g, torch.Tensor) else g
+        assert np.isfinite(g).all(), f"{tag}{name}: non-finite values"
+        if e is None:
+            errs[name], bars[name] = O.rel_err(g, o), tol
+        else:
+            emu[name] = O.rel_err(g, e, den_ref=o)
+            errs[name], bars[name] = O.rel_err(g, o), tol + O.rel_err(e, o)
+        assert errs[name] <= bars[name], f"{tag}{name}: rel_err {errs[name]:.3e} > {bars[name]:.3e}"
+    log_parity(tag, errs, bars, emu)
     return errs
 
 
-def run_pair(cfg, w, steps, ns=None, seed=0, masked=False, sharp=False):
-    """Free-running oracle and GPU streams over the same frames; compare every step."""
+def check_attention_kernel(g, cfg, gl, layer, fids, tol, tag=""):
+    """The attention kernel's own arithmetic: the GPU's attention output of block `layer`
+    against fp64 attention (oracle.attention) of the GPU's OWN stored Q and K/V memory rows
+    (frames `fids`, read back through vi_debug_read) -- isolates the bf16 P, the exp2
+    approximations and the split merges from everything upstream; held to the plain bar."""
+    ks, vs = [], []
+    slot_ids = list(g.ctx.state()[0])
+    for fid in fids:
+        k, v = g.kv(layer, slot_ids.index(fid))
+        ks.append(k.float().cpu().numpy().astype(np.float64))
+        vs.append(v.float().cpu().numpy().astype(np.float64))
+    q = gl["q"].float().cpu().numpy().astype(np.float64)
+    ref = O.attention(q, np.concatenate(ks), np.concatenate(vs), cfg.heads)
+    e = O.rel_err(gl["o"].float().cpu().numpy(), ref)
+    assert e <= tol, f"{tag}attention kernel vs fp64 attention of its own Q/K/V: {e:.3e} > {tol}"
+    log_parity(tag + "attention-kernel", {"o_kernel": e}, {"o_kernel": tol})
+    return e
+
+
+def run_pair(cfg, w, steps, ns=None, seed=0, masked=False, emulate=False):
+    """Free-running oracle and GPU streams over the same frames; compare every step.
+    `emulate`: also run the bf16-storage emulation (logit-sensitive weight variants)."""
     g = H().GpuStream(cfg, w)
     o = O.OracleStream(cfg, w)
+    e = O.emulate_bf16_storage(cfg, w) if emulate else None
     fid = 0
     worst = 0.0
     for i in range(steps):
@@ -98,12 +136,44 @@ def run_pair(cfg, w, steps, ns=None, seed=0, masked=False, sharp=False):
         fid += n
         f_o, ev_o = o.push(n)
         _, ost = o.step(feats)
+        est = None
+        if e is not None:
+            e.push(n)
+            _, est = e.step(feats)
         _, gst = g.step(feats)
         assert (gst["first"], gst["evicted"]) == (f_o, ev_o)
         assert g.ctx.state() == tuple(o.mem.state()), "ring state differs"
-        errs = compare_step(cfg, ost, gst, TOL[cfg.dtype], tag=f"step {i}: ", sharp=sharp)
+        errs = compare_step(cfg, ost, gst, TOL[cfg.dtype], tag=f"step {i}: ", est=est)
+        if cfg.dtype == "bf16" and not cfg.win_h:
+            fids = o.mem.window() + list(range(o.mem.cur_first, o.mem.next_id))
+            check_attention_kernel(g, cfg, gst["layers"][-1], cfg.layers - 1, fids, TOL["bf16"], tag=f"step {i}: ")
         worst = max(worst, max(errs.values()))
     return g, o, worst
+
+
+def full_shape_step(cfg, w, steps, seed, masked=False, emulate=False, n=None):
+    """Run `steps` chunks of n frames through the oracle, the GPU (eager, stage by stage) and,
+    for logit-sensitive weights, the bf16-storage emulation; compare the last step (memory
+    full) stage by stage.  Returns the GPU stream."""
+    n = n or cfg.t_new
+    g = H().GpuStream(cfg, w)
+    o = O.OracleStream(cfg, w)
+    e = O.emulate_bf16_storage(cfg, w) if emulate else None
+    for i in range(steps):
+        feats = make_features(cfg, n, first_frame=n * i, seed=seed, masked=masked)
+        last = i == steps - 1
+        o.push(n)
+        _, ost = o.step(feats)
+        est = None
+        if e is not None:
+            e.push(n)
+            _, est = e.step(feats)
+        _, gst = g.step(feats, stages=last)
+    compare_step(cfg, ost, gst, TOL[cfg.dtype], tag=f"step {steps - 1}: ", est=est)
+    if cfg.dtype == "bf16" and not cfg.win_h:
+        fids = o.mem.window() + list(range(o.mem.cur_first, o.mem.next_id))
+        check_attention_kernel(g, cfg, gst["layers"][-1], cfg.layers - 1, fids, TOL["bf16"], tag=f"step {steps - 1}: ")
+    return g
 
 
 # ---------------------------------------------------------------- soft split / composite
@@ -269,25 +339,25 @@ def test_c3s_bf16_stream_per_stage():
 def test_c3s_bf16_sensitive_and_ragged_chunks():
     cfg = CONFIGS["C3S"].replace(t_new=3)
     w = make_weights(cfg, seed=1, variant="sensitive")
-    run_pair(cfg, w, steps=5, ns=[3, 1, 2, 3, 1])
+    run_pair(cfg, w, steps=5, ns=[3, 1, 2, 3, 1], emulate=True)
 
 
 def test_c3s_bf16_sharp_logits_online_softmax():
     cfg = CONFIGS["C3S"].replace(layers=1)
     w = make_weights(cfg, seed=2, variant="sharp")
-    run_pair(cfg, w, steps=4, sharp=True)
+    run_pair(cfg, w, steps=4, emulate=True)
 
 
 def test_c2_shape_headdim64_mlp():
     cfg = CONFIGS["C2"].replace(layers=1, mem_frames=2, t_new=2, feat_h=30, feat_w=54)
     w = make_weights(cfg, seed=3, variant="sensitive")
-    run_pair(cfg, w, steps=3)
+    run_pair(cfg, w, steps=3, emulate=True)
 
 
 def test_bf16_kv_rows_and_determinism():
     cfg = CONFIGS["C3S"].replace(layers=1)
     w = make_weights(cfg, seed=4, variant="sensitive")
-    g1, o, _ = run_pair(cfg, w, steps=3)
+    g1, o, _ = run_pair(cfg, w, steps=3, emulate=True)
     for fid in o.mem.window() + list(range(o.mem.cur_first, o.mem.next_id)):
         K, V = o.frame_kv(0, fid)
         gk, gv = g1.kv(0, fid % g1.ctx.S)
@@ -322,16 +392,68 @@ def test_c3_full_shape_step():
     """The metric config (BASELINE configs[2]) at full size: 3 steps of 5 frames fill the
     10-frame memory, the 4th step (3600 queries x 10800 keys) is compared stage by stage."""
     cfg = CONFIGS["C3"].replace(layers=2)
-    w = make_weights(cfg, seed=0)
-    g = H().GpuStream(cfg, w)
+    g = full_shape_step(cfg, make_weights(cfg, seed=0), 4, seed=0)
+    assert g.ctx.state()[2] == (1 << 15) - 1
+
+
+def test_c3t1_full_shape_step():
+    """The paper's own Eq. 3 mode at the metric shape (configs[2] with ONE new frame per step,
+    P:121 "narrowing the prediction pipeline to only one frame"; C5's online model): 11 steps
+    fill the 10-frame memory, the 11th (720 queries x 7920 keys, the small-chunk attention
+    path) is compared stage by stage."""
+    cfg = CONFIGS["C3T1"].replace(layers=2)
+    g = full_shape_step(cfg, make_weights(cfg, seed=30), 11, seed=30)
+    assert g.ctx.state()[2] == (1 << 11) - 1
+
+
+def test_c3t1_full_shape_sensitive():
+    """C3T1 with logit-sensitive weights (memory-dependent output): 1 block, 11 steps."""
+    cfg = CONFIGS["C3T1"].replace(layers=1)
+    full_shape_step(cfg, make_weights(cfg, seed=31, variant="sensitive"), 11, seed=31, emulate=True)
+
+
+def test_c3_graph_replayed_8_block_step():
+    """The step bench.py times: BASELINE configs[2] in full (8 blocks), vi_run_step replaying
+    one captured CUDA graph per (ring state, buffers).  Its outputs are compared with the
+    oracle after the memory is full, and are bitwise equal to the eager path (vi_soft_split /
+    vi_memory_step x 8 / vi_soft_composite launched one by one)."""
+    from paper_2403_16161_b200 import vi
+    cfg = CONFIGS["C3"]
+    w = make_weights(cfg, seed=32)
+    ctx = vi.Context.from_synth(cfg)
+    ctx.set_weights(w)
+    eager = H().GpuStream(cfg, w)
     o = O.OracleStream(cfg, w)
     for i in range(4):
-        feats = make_features(cfg, 5, first_frame=5 * i, seed=0)
+        feats = make_features(cfg, 5, first_frame=5 * i, seed=32)
         o.push(5)
-        _, ost = o.step(feats)
-        _, gst = g.step(feats, stages=(i == 3))
-    assert g.ctx.state()[2] == (1 << 15) - 1
-    compare_step(cfg, ost, gst, 2e-2)
+        ref, _ = o.step(feats)
+        f = torch.from_numpy(feats).to(torch.bfloat16).cuda()
+        out = torch.empty_like(f)
+        ctx.run_step(f, 5, out)
+        ctx.sync()
+        ge, _ = eager.step(feats, stages=False)
+        assert torch.equal(out, ge), f"step {i}: graph replay differs from the eager launches"
+        if i >= 2:                   # memory full from step 2 on (15 slots)
+            assert_close(out, ref, 2e-2, f"step {i} out")
+    assert ctx.state()[2] == (1 << 15) - 1
+    # a replay of an already captured graph (same ring state and buffers) is deterministic too
+    assert ctx.launches() > 0
+
+
+def test_positional_embedding_bf16():
+    """pos_embed = 1 (reading Q8: an additive [P, D] table at the split, never temporal): the
+    oracle adds it in embed(); the GPU's embed GEMM epilogue adds it per token row."""
+    cfg = CONFIGS["C3S"].replace(layers=1, pos_embed=1)
+    w = make_weights(cfg, seed=33, variant="sensitive")
+    assert w["pos"] is not None
+    run_pair(cfg, w, steps=3, emulate=True)
+
+
+def test_positional_embedding_fp32():
+    cfg = CONFIGS["C1"].replace(pos_embed=1)
+    w = make_weights(cfg, seed=34)
+    run_pair(cfg, w, steps=4)
 
 
 def _run_steps(cfg, w, steps, seed):
@@ -386,15 +508,7 @@ def test_stream_k_headdim64_c3_shape():
     """Head dim 64 through the stream-K kernel (attn_sk2<64>): the C3 token grid (3600
     queries x 10800 keys, 60 units) with D = 256; the 4th step compared stage by stage."""
     cfg = CONFIGS["C3"].replace(layers=1, d_model=256)
-    w = make_weights(cfg, seed=23)
-    g = H().GpuStream(cfg, w)
-    o = O.OracleStream(cfg, w)
-    for i in range(4):
-        feats = make_features(cfg, 5, first_frame=5 * i, seed=23)
-        o.push(5)
-        _, ost = o.step(feats)
-        _, gst = g.step(feats, stages=(i == 3))
-    compare_step(cfg, ost, gst, 2e-2)
+    full_shape_step(cfg, make_weights(cfg, seed=23), 4, seed=23)
 
 
 def test_c2_full_shape_step():
@@ -403,16 +517,8 @@ def test_c2_full_shape_step():
     3 steps fill the memory, the 4th (720 queries x 2160 keys) is compared stage by stage,
     on masked frames."""
     cfg = CONFIGS["C2"]
-    w = make_weights(cfg, seed=0, variant="sensitive")
-    g = H().GpuStream(cfg, w)
-    o = O.OracleStream(cfg, w)
-    for i in range(4):
-        feats = make_features(cfg, 5, first_frame=5 * i, seed=0, masked=True)
-        o.push(5)
-        _, ost = o.step(feats)
-        _, gst = g.step(feats, stages=(i == 3))
+    g = full_shape_step(cfg, make_weights(cfg, seed=0, variant="sensitive"), 4, seed=0, masked=True, emulate=True)
     assert g.ctx.state()[2] == (1 << 15) - 1
-    compare_step(cfg, ost, gst, 2e-2)
 
 
 def test_reference_frames_bf16():
@@ -421,7 +527,7 @@ def test_reference_frames_bf16():
     (0 leaves again at frame 9) -- ring state bit-exact, every stage within the bf16 bar."""
     cfg = CONFIGS["C3S"].replace(layers=2, t_new=1, mem_frames=2, ref_rate=3, max_refs=2)
     w = make_weights(cfg, seed=8, variant="sensitive")
-    run_pair(cfg, w, steps=10, masked="moving")
+    run_pair(cfg, w, steps=10, masked="moving", emulate=True)
 
 
 def test_reference_frames_fp32_and_refine_commit():
@@ -459,7 +565,7 @@ def test_window_attention_c3s_ragged():
     (30 tokens, padded to 32 rows), ragged chunks, the memory wraps; every stage vs the oracle."""
     cfg = CONFIGS["C3S"].replace(t_new=3, win_h=5, win_w=6)
     w = make_weights(cfg, seed=12, variant="sensitive")
-    run_pair(cfg, w, steps=5, ns=[3, 1, 2, 3, 2])
+    run_pair(cfg, w, steps=5, ns=[3, 1, 2, 3, 2], emulate=True)
 
 
 def test_window_attention_with_reference_frames():
@@ -467,22 +573,14 @@ def test_window_attention_with_reference_frames():
     rows inside every window's key region (window-major memory); 10 one-frame steps."""
     cfg = CONFIGS["C3S"].replace(layers=2, t_new=1, mem_frames=2, ref_rate=3, max_refs=2, win_h=5, win_w=6)
     w = make_weights(cfg, seed=14, variant="sensitive")
-    run_pair(cfg, w, steps=10, masked="moving")
+    run_pair(cfg, w, steps=10, masked="moving", emulate=True)
 
 
 def test_window_attention_c4_full_shape_step():
     """BASELINE configs[3] shape (2 of its 16 blocks): 720 tokens/frame in 16 windows of 5 x 9,
     5 new frames over a 10-frame memory; the 4th step compared stage by stage."""
     cfg = CONFIGS["C4"].replace(layers=2)
-    w = make_weights(cfg, seed=13, variant="sensitive")
-    g = H().GpuStream(cfg, w)
-    o = O.OracleStream(cfg, w)
-    for i in range(4):
-        feats = make_features(cfg, 5, first_frame=5 * i, seed=13)
-        o.push(5)
-        _, ost = o.step(feats)
-        _, gst = g.step(feats, stages=(i == 3))
-    compare_step(cfg, ost, gst, 2e-2)
+    full_shape_step(cfg, make_weights(cfg, seed=13, variant="sensitive"), 4, seed=13, emulate=True)
 
 
 def test_run_step_async_pipelined_equals_run_step():

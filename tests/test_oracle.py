@@ -474,6 +474,57 @@ def test_round_bf16_is_rne():
     assert np.array_equal(round_bf16(x), ref)
 
 
+def test_rel_err_with_emulation_denominator_triangle():
+    """rel_err(g, e; den_ref=o) + rel_err(e, o) bounds rel_err(g, o) (the parity tests' bar)."""
+    rng = np.random.default_rng(5)
+    o = rng.standard_normal(1000)
+    e = o + 1e-3 * rng.standard_normal(1000)
+    g = e + 1e-3 * rng.standard_normal(1000)
+    assert O.rel_err(g, o) <= O.rel_err(g, e, den_ref=o) + O.rel_err(e, o) + 1e-15
+    assert O.rel_err(g, e, den_ref=e) == O.rel_err(g, e)
+
+
+def test_bf16_round_matches_torch_and_ties():
+    """The emulation's bf16 rounding (fp64 -> fp32 -> bf16, RNE) against torch's cast and hand
+    values: 1 + 2^-8 is a tie (rounds to even 1), 1 + 3 2^-8 a tie rounding up to 1 + 2^-6."""
+    x = np.array([1.0, 1.0 + 2 ** -8, 1.0 + 3 * 2 ** -8, -2.5, 0.1, -7.77e-3, 1e30], np.float64)
+    ref = torch.from_numpy(x.astype(np.float32)).to(torch.bfloat16).to(torch.float64).numpy()
+    assert np.array_equal(O.bf16_round(x), ref)
+    assert O.bf16_round(np.array([1.0 + 2 ** -8]))[0] == 1.0
+    assert O.bf16_round(np.array([1.0 + 3 * 2 ** -8]))[0] == 1.0 + 2 ** -6
+    big = np.random.default_rng(1).standard_normal(4096) * 3
+    assert np.array_equal(O.bf16_round(big), torch.from_numpy(big.astype(np.float32)).to(torch.bfloat16).double().numpy())
+
+
+def test_bf16_storage_emulation_rounds_the_stored_tensors():
+    """emulate_bf16_storage: LN1's output h is the oracle's rounded to bf16, Q/K/V are the exact
+    projection of that h rounded to bf16, O and g are bf16 values; the embedding (x0) is
+    unchanged; the result differs from the oracle only by that storage rounding."""
+    cfg = CONFIGS["C1"].replace(layers=2, mem_frames=2)
+    w = make_weights(cfg, seed=3, variant="sharp")
+    o, e = O.OracleStream(cfg, w), O.emulate_bf16_storage(cfg, w)
+    feats = make_features(cfg, 1, seed=3)
+    o.push(1); e.push(1)
+    _, so = o.step(feats)
+    _, se = e.step(feats)
+    assert np.array_equal(so["x0"], se["x0"])
+    l0o, l0e = so["layers"][0], se["layers"][0]
+    assert np.array_equal(l0e["h1"], O.bf16_round(l0o["h1"]))          # LN1 output (GEMM operand)
+    Q, K, V = (O.bf16_round(O.linear(l0e["h1"], w["wqkv"][0], w["bqkv"][0])[:, i * 64:(i + 1) * 64]) for i in range(3))
+    for k, ref in (("q", Q), ("k", K), ("v", V)):
+        assert np.array_equal(l0e[k], ref)                         # rounded after the exact projection
+        assert not np.array_equal(l0e[k], l0o[k])
+    assert np.array_equal(l0e["o"], O.bf16_round(l0e["o"]))
+    assert np.array_equal(l0e["g"], O.bf16_round(l0e["g"]))
+    assert 0 < O.rel_err(se["out"], so["out"]) < 0.2
+    # and the K/V a later step attends to are the rounded ones (re-projected from cached inputs)
+    f2 = make_features(cfg, 1, first_frame=1, seed=3)
+    o.push(1); e.push(1)
+    o.step(f2); e.step(f2)
+    Ke, Ve = e.frame_kv(1, 0)
+    assert np.array_equal(Ke, O.bf16_round(Ke)) and np.array_equal(Ve, O.bf16_round(Ve))
+
+
 # ---------------------------------------------------------------- reference frames (Eq. 3 M_{1,r})
 
 def _select_memory(f, s, r, R):
