@@ -12,7 +12,7 @@
 #include "kernels.h"
 
 // SK2_EXPERIMENT (micro-benchmark builds only): 1 = softmax warps skip the math (MMA + TMA
-// pipeline alone), 2 = no MMAs issued (softmax chain alone)
+// pipeline alone), 2 = no MMAs issued (softmax chain alone), 3 = no K / V loads, 4 = 1 + 3
 #ifndef SK2_EXPERIMENT
 #define SK2_EXPERIMENT 0
 #endif
@@ -21,14 +21,15 @@
 #ifndef SK2_TRACE
 #define SK2_TRACE 0
 #endif
-// exp2 pairs k with k % MOD >= GE go to the degree-3 polynomial on the FMA pipe, the rest
-// to MUFU (C3 micro, same box: 5 of 16 pairs (3/2) 80.8 us, 4/16 (4/3) 81.4, 6/16 (5/3) 81.7,
-// none 82.9, 8/16 85.8; 3/2 moved one bf16-bar test to 2.04 % > 2 %: 4/3 kept)
+// exp2 pairs k with k % MOD >= GE go to the degree-3 polynomial on the FMA pipe (max rel.
+// error 7.5e-5, far below the bf16 rounding of P), the rest to MUFU.  Round 2 A/B (C3 micro,
+// one box, 3 alternations): 5 of 16 pairs (3/2) 80.7 us, 4/16 (4/3) 81.2, 6/16 (8/5) 83.3,
+// none 83.0 (profiles/r02_attn_ab.md)
 #ifndef SK2_POLY_MOD
-#define SK2_POLY_MOD 4
+#define SK2_POLY_MOD 3
 #endif
 #ifndef SK2_POLY_GE
-#define SK2_POLY_GE 3
+#define SK2_POLY_GE 2
 #endif
 
 namespace vi {
@@ -48,9 +49,13 @@ struct AttnSk2Smem {
   static constexpr int XCH_OFF = STG_OFF + 16 * 32 * 48;        // [2 phases][2 tiles][2 halves][128] fp32
   static constexpr int LSE_OFF = XCH_OFF + 2 * 2 * 2 * 128 * 4;   // [2 halves][2 piece parities][256] fp32 (merge)
   static constexpr int TOTAL = LSE_OFF + 2 * 2 * 256 * 4 + 1024;
-  // owner merge: 32 KB chunk buffers over the idle Q / K / V smem, NBH per O column half
+  // owner merge: 32 KB chunk buffers over the idle Q / K / V smem, NBH per O column half; a
+  // piece (a split unit's normalised partial O, bf16 [HD/8][256 rows] x 8 columns) arrives in
+  // chunks of PCOL columns of one O half
   static constexpr int NBH = (3 * 512 * HD / 32768) / 2 > 3 ? 3 : (3 * 512 * HD / 32768) / 2;
-  static constexpr int CPP = HD / 64;                           // 32-column chunks per piece half
+  static constexpr int PCOL = HD / 2 < 64 ? HD / 2 : 64;
+  static constexpr int CPP = (HD / 2) / PCOL;                   // chunks per piece half
+  static constexpr uint32_t CHUNK = 256u * PCOL * 2u;           // bytes
 };
 
 __device__ __forceinline__ void sk2_key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
@@ -176,8 +181,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(&s_full[t], 1);
-      mbar_init(&p_full[2 * t], 128);
-      mbar_init(&p_full[2 * t + 1], 128);
+      mbar_init(&p_full[2 * t], 4);        // one elected arrive per softmax warp of the key half
+      mbar_init(&p_full[2 * t + 1], 4);
       mbar_init(&o_final[t], 1);
       mbar_init(&o_free[t], 256);
     }
@@ -223,6 +228,14 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         const int st = jg % ST;
         const uint32_t par = ((jg / ST) & 1) ^ 1;
         if (jg >= ST) mbar_wait(&k_empty[st], par);
+        if (SK2_EXPERIMENT >= 3) {   // micro only: no K / V traffic (operands stale)
+          if (elect_one()) mbar_arrive(&k_full[st]);
+          __syncwarp();
+          if (jg >= ST) mbar_wait(&v_empty[st], par);
+          if (elect_one()) mbar_arrive(&v_full[st]);
+          __syncwarp();
+          continue;
+        }
         if (elect_one()) {
           uint8_t* sk = smem + L::K_OFF + st * L::KB;
           mbar_arrive_expect_tx(&k_full[st], L::KB);
@@ -280,11 +293,11 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             if (i >= L::NBH) mbar_wait(&merge_empty[hf * 3 + b], ((i / L::NBH) - 1) & 1);
             if (lane == 0) {
               uint64_t* bar = &merge_full[hf * 3 + b];
-              mbar_arrive_expect_tx(bar, 32768u + (cc == 0 ? 1024u : 0u));
+              mbar_arrive_expect_tx(bar, L::CHUNK + (cc == 0 ? 1024u : 0u));
               bulk_g2s(smem + (size_t)(hf * L::NBH + b) * 32768,
                        reinterpret_cast<const uint8_t*>(a.spart) +
-                           ((size_t)c * (HD / 4) * 256 + (size_t)((hf * (HD / 2) + cc * 32) / 4) * 256) * 16,
-                       32768u, bar);
+                           ((size_t)c * (HD / 8) * 256 + (size_t)((hf * (HD / 2) + cc * L::PCOL) / 8) * 256) * 16,
+                       L::CHUNK, bar);
               if (cc == 0)
                 bulk_g2s(smem + L::LSE_OFF + (hf * 2 + ((i / L::CPP) & 1)) * 1024, a.slse + (size_t)c * 256, 1024u, bar);
             }
@@ -407,13 +420,13 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int nq = WIN ? a.win_nq : a.Nq;       // query rows of the unit's row space
       // all 32 rows of this warp past Nq (a tail pair): keep the barrier phases, skip the math
       // (their P / O lanes hold garbage that only reaches rows never stored)
-      const bool dead = q0 + t * 128 + qd * 32 >= nq || SK2_EXPERIMENT == 1;
+      const bool dead = q0 + t * 128 + qd * 32 >= nq || SK2_EXPERIMENT == 1 || SK2_EXPERIMENT == 4;
       float m_use = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         const int g = jg + j;
         mbar_wait(&s_full[t], g & 1);
         if (dead) {
-          mbar_arrive(&p_full[2 * t + hf]);
+          if (lane == 0) mbar_arrive(&p_full[2 * t + hf]);
           continue;
         }
         int row0, nv, nskip;
@@ -499,7 +512,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         tmem_wait_st();
         tc_fence_before();
-        mbar_arrive(&p_full[2 * t + hf]);
+        __syncwarp();                                  // every lane's P stores are complete ...
+        if (lane == 0) mbar_arrive(&p_full[2 * t + hf]);   // ... then one arrive per warp
         if (tr) trc[g * 32 + 4 + t * 8 + hf * 4 + qd] = clock64();
         const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
         l = l * alpha + (s01.x + s01.y);
@@ -538,17 +552,20 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         __syncwarp();
       };
       if (ta > 0) {
-        // continuation piece: normalised partial -> this CTA's slot, then raise the flag
+        // continuation piece: normalised partial (bf16: half the bytes the owner pulls in at
+        // the end of the launch) -> this CTA's slot, then raise the flag
         const float inv = 1.f / l;
-        float4* dst = reinterpret_cast<float4*>(a.spart) + (size_t)cta * (HD / 4) * 256 + r256;
+        uint4* dst = reinterpret_cast<uint4*>(a.spart) + (size_t)cta * (HD / 8) * 256 + r256;
 #pragma unroll 1
         for (int c = 0; c < OH; c += 32) {
           float f[32];
           tmem_ld32(TOh + c, reinterpret_cast<uint32_t*>(f));
           tmem_wait_ld();
 #pragma unroll
-          for (int k = 0; k < 32; k += 4)
-            dst[((hf * OH + c + k) / 4) * 256] = make_float4(f[k] * inv, f[k + 1] * inv, f[k + 2] * inv, f[k + 3] * inv);
+          for (int k = 0; k < 32; k += 8)
+            dst[((hf * OH + c + k) / 8) * 256] =
+                make_uint4(pack_bf16(f[k] * inv, f[k + 1] * inv), pack_bf16(f[k + 2] * inv, f[k + 3] * inv),
+                           pack_bf16(f[k + 4] * inv, f[k + 5] * inv), pack_bf16(f[k + 6] * inv, f[k + 7] * inv));
         }
         tc_fence_before();
         mbar_arrive(&o_free[t]);
@@ -585,26 +602,34 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             wsum = wsum * am + wk;
             m = mn;
           }
-          const float4* stage = reinterpret_cast<const float4*>(smem + (size_t)(hf * L::NBH + b) * 32768);
-          float f[32];
-          tmem_ld32(TOh + cc * 32, reinterpret_cast<uint32_t*>(f));
-          tmem_wait_ld();
+          const uint4* stage = reinterpret_cast<const uint4*>(smem + (size_t)(hf * L::NBH + b) * 32768);
+          const bool last_piece = i + L::CPP >= items;
+#pragma unroll 1
+          for (int sub = 0; sub < L::PCOL / 32; ++sub) {
+            const int col = cc * L::PCOL + sub * 32;    // within the O half
+            float f[32];
+            tmem_ld32(TOh + col, reinterpret_cast<uint32_t*>(f));
+            tmem_wait_ld();
 #pragma unroll
-          for (int q4 = 0; q4 < 8; ++q4) {
-            const float4 v = stage[q4 * 256 + r256];
-            f[4 * q4] = f[4 * q4] * alpha + wk * v.x;
-            f[4 * q4 + 1] = f[4 * q4 + 1] * alpha + wk * v.y;
-            f[4 * q4 + 2] = f[4 * q4 + 2] * alpha + wk * v.z;
-            f[4 * q4 + 3] = f[4 * q4 + 3] * alpha + wk * v.w;
+            for (int q8 = 0; q8 < 4; ++q8) {
+              const uint4 v = stage[(sub * 4 + q8) * 256 + r256];
+              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+              for (int e = 0; e < 4; ++e) {
+                const float2 p2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
+                f[8 * q8 + 2 * e] = f[8 * q8 + 2 * e] * alpha + wk * p2.x;
+                f[8 * q8 + 2 * e + 1] = f[8 * q8 + 2 * e + 1] * alpha + wk * p2.y;
+              }
+            }
+            if (last_piece) {                          // last piece: normalise and write out
+              write_out16(col, f, 1.f / wsum);
+              write_out16(col + 16, f + 16, 1.f / wsum);
+            } else {
+              tmem_st32(TOh + col, reinterpret_cast<uint32_t*>(f));
+              tmem_wait_st();
+            }
           }
           mbar_arrive(&merge_empty[hf * 3 + b]);       // chunk buffer (and lse slot reads) done
-          if (i + L::CPP >= items) {                   // last piece: normalise and write out
-            write_out16(cc * 32, f, 1.f / wsum);
-            write_out16(cc * 32 + 16, f + 16, 1.f / wsum);
-          } else {
-            tmem_st32(TOh + cc * 32, reinterpret_cast<uint32_t*>(f));
-            tmem_wait_st();
-          }
         }
         if (ct && warp == 0 && lane == 0) ct[13] = (long long)globaltimer();
         tc_fence_before();

@@ -1,9 +1,11 @@
-// Standalone timing of the stream-K memory attention (attn_sk3.cu / attn_sk2.cu) at the C3 shape:
+// Standalone timing of the stream-K memory attention (attn_sk2.cu) at the C3 shape:
 // 3600 queries x 10800 keys (15 full ring slots of 720 tokens), 4 heads, d = 128.
 //
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo --expt-relaxed-constexpr \
-//        -I include -I paper_2403_16161_b200/csrc tools/micro/attn_micro.cu -lcuda -o /tmp/attn_micro
-//   /tmp/attn_micro [iters] [t(race)|x] [grid (0 = auto)] [kernel version 2|3]
+//        -I include -I paper_2403_16161_b200/csrc [-DATTN_SRC='"/path/attn_sk2.cu"'] \
+//        tools/micro/attn_micro.cu -lcuda -o /tmp/attn_micro
+//   /tmp/attn_micro [iters] [t(race)|x] [grid (0 = auto)] [2] [w(indow shape)]
+// (tools/micro/ab_attn.sh builds two sources and alternates them on one GPU)
 //
 // Prints the mean launch time, TFLOP/s (4 Nq Nk D valid-key FLOPs) and, with `trace`, the
 // clock64 timeline of CTA 0's first key tiles (the kernel's VI_SK_TRACE stamps).
@@ -15,8 +17,11 @@
 #ifndef SK2_TRACE
 #define SK2_TRACE 1   // per-CTA / per-tile stamps compiled in (-DSK2_TRACE=0 for the library's code)
 #endif
-#include "../../paper_2403_16161_b200/csrc/kernels/attn_sk2.cu"
-#include "../../paper_2403_16161_b200/csrc/kernels/attn_sk3.cu"
+#ifndef ATTN_SRC
+#define ATTN_SRC "../../paper_2403_16161_b200/csrc/kernels/attn_sk2.cu"
+#endif
+#include ATTN_SRC
+#include "../../paper_2403_16161_b200/csrc/kernels/setup.cu"
 using namespace vi;
 
 typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -52,7 +57,7 @@ int main(int argc, char** argv) {
   const int iters = argc > 1 ? atoi(argv[1]) : 50;
   const bool trace = argc > 2 && argv[2][0] == 't';
   const int grid_override = argc > 3 ? atoi(argv[3]) : 0;
-  const int ver = argc > 4 ? atoi(argv[4]) : 3;
+  const int ver = 2;
   // argv[5] == 'w': the C4 window shape (16 windows of 5 x 9 tokens, window-major rows,
   // 225 queries and 675 keys per window, key regions padded to 680 rows)
   const bool win = argc > 5 && argv[5][0] == 'w';
@@ -71,7 +76,7 @@ int main(int argc, char** argv) {
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   CUtensorMap tq = tmap(q, D, Nq, 64, 128), tk = tmap(k, D, SP, 64, 128), tv = tmap(vt, vt_ld, D, 64, HD);
   auto launch = [&](const AttnTC& aa, int gr, cudaStream_t s_) {
-    return ver == 2 ? launch_attn_sk2(tq, tk, tv, aa, gr, s_) : launch_attn_sk3(tq, tk, tv, aa, gr, s_);
+    return launch_attn_sk2(tq, tk, tv, aa, gr, s_);
   };
   AttnTC a;
   memset(&a, 0, sizeof(a));
@@ -101,7 +106,7 @@ int main(int argc, char** argv) {
   a.sk_tail = (ver == 2 && rem > 0 && rem <= 128 && !win) ? 1 : 0;
   a.sk_tail_w = a.sk_tail && getenv("VI_SK_TAIL_W") ? atoi(getenv("VI_SK_TAIL_W")) : 16;
   a.sk_wfull = (long long)(a.npairs - a.sk_tail) * H * a.segs.tile0[1];
-  a.sk_ucost = getenv("VI_SK_UNIT_COST") ? atoi(getenv("VI_SK_UNIT_COST")) : 0;
+  a.sk_ucost = getenv("VI_SK_UNIT_COST") ? atoi(getenv("VI_SK_UNIT_COST")) : (win ? 0 : 56);
   int grid = int(work < nsm ? work : nsm);
   if (grid_override > 0) grid = grid_override;
   cudaStream_t st;
