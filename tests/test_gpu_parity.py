@@ -50,7 +50,8 @@ def log_parity(tag, errs, bars, emu=None):
         return
     worst = max(errs, key=lambda k: errs[k] / bars[k])
     rec = {"test": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "tag": tag,
-           "worst_stage": worst, "err": errs[worst], "bar": bars[worst], "ratio": errs[worst] / bars[worst]}
+           "worst_stage": worst, "err": errs[worst], "bar": bars[worst], "ratio": errs[worst] / bars[worst],
+           "stages": {k: round(v, 6) for k, v in errs.items()}}
     if emu:
         we = max(emu, key=emu.get)
         rec["vs_emulation"] = {"stage": we, "err": emu[we]}
