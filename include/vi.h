@@ -114,6 +114,16 @@ typedef struct vi_config {
    * bf16 path; head sharding with tp_size <= heads; no refine commits or memory reads (the
    * memory is window-major). */
   int win_h, win_w;
+  /* Refined memory M-bar of Eq. 4 (SPEC select_refined S:467-475; reading Q22):
+   * with refined_mem = 1 the memory also keeps the refining inpainter's results for frames
+   * that have left the online span: the frames t-s'..t (refined_span s' >= 0; t = the newest
+   * frame a refine commit has been applied for, the watermark) in s'+1 refined-span slots,
+   * and, with refined_rate r' > 0, the max_refined_refs newest refined frames whose id is a
+   * multiple of r' (refined references; the oldest leaves first).  The online span M keeps
+   * its own frames (an online frame with a refined entry holds it in its online slot:
+   * refined wins).  Slots in total: mem_frames + max_new_frames + max_ref_frames
+   * + (s'+1) + max_refined_refs <= 64.  0 = off: commits only overwrite online frames. */
+  int refined_mem, refined_span, refined_rate, max_refined_refs;
 } vi_config;
 
 /* Weights, host fp32 pointers in nn.Linear layout (y = x W^T + b); converted to the
@@ -217,12 +227,16 @@ vi_status vi_tp_local_allgather(vi_ctx* const* ctxs, int n);
  * out[y][x][c] = sum of the patch entries landing on (y,x) / cover count (IEEE div). */
 vi_status vi_soft_composite(vi_ctx* ctx, const void* in, int n, void* feat, int project);
 
-/* Refine commit (Eq. 4's refined memory M-bar): overwrite the memory
- * entries of a past, resident frame for every block with k, v = [L][P][D] (host or
- * device, ctx dtype; a head-sharded context keeps only its heads' columns).  Queued and applied at the next vi_memory_push, so a frame is
- * never torn across blocks; a later commit for the same frame replaces an earlier one.
- * The payload is copied before return (buffers may be reused).  Thread-safe w.r.t.
- * the context's other calls.  VI_E_PROTOCOL / VI_NOT_RESIDENT as vi_memory_evict. */
+/* Refine commit (Eq. 4's refined memory M-bar): the refined memory entries of a
+ * past frame for every block, k, v = [L][P][D] (host or device, ctx dtype; a head-sharded
+ * context keeps only its heads' columns).  Queued and applied at the next vi_memory_push,
+ * so a frame is never torn across blocks; a later commit for the same frame replaces an
+ * earlier one.  A frame still resident is overwritten in place (refined wins); with
+ * vi_config.refined_mem a frame that has left the online span lands in the refined memory
+ * if Eq. 4 selects it at that push (within s' of the watermark, or a refined reference),
+ * else it is dropped.  The payload is copied before return (buffers may be reused).
+ * Thread-safe w.r.t. the context's other calls.  VI_E_PROTOCOL for a future frame or the
+ * current chunk before its step finished; VI_NOT_RESIDENT if it can no longer be used. */
 vi_status vi_refine_commit(vi_ctx* ctx, int64_t frame_id, const void* k, const void* v);
 
 /* Read the memory entries of a resident past frame for every block into k, v =
@@ -233,8 +247,12 @@ vi_status vi_refine_commit(vi_ctx* ctx, int64_t frame_id, const void* k, const v
  * VI_NOT_RESIDENT if the frame left the memory. */
 vi_status vi_memory_read(vi_ctx* ctx, int64_t frame_id, void* k, void* v);
 
+/* Eq. 4's watermark t of a context with refined memory (-1: no refined frame yet). */
+int64_t vi_refined_watermark(vi_ctx* ctx);
+
 /* Host snapshot of the ring: slot_id[N] (-1 = empty), refined[N] (0/1), N = vi_num_slots
- * (the S = mem_frames + max_new_frames span slots, then the reference slots), valid bitmask
+ * (the S = mem_frames + max_new_frames span slots, then the reference slots, then the refined
+ * span and refined reference slots of Eq. 4), valid bitmask
  * (bit s = slot s holds a resident frame).  Any pointer may be NULL. */
 vi_status vi_memory_state(vi_ctx* ctx, int64_t* slot_id, uint8_t* refined, uint64_t* valid_mask);
 
@@ -306,6 +324,12 @@ vi_status vi_ring_create(vi_ring** out, int mem_frames, int max_new_frames);
 /* With reference frames (see vi_config.ref_rate / max_ref_frames). */
 vi_status vi_ring_create_ex(vi_ring** out, int mem_frames, int max_new_frames, int ref_rate,
                             int max_ref_frames);
+/* With Eq. 4's refined memory (see vi_config.refined_mem; refined_mem = 1 implied). */
+vi_status vi_ring_create_refined(vi_ring** out, int mem_frames, int max_new_frames, int ref_rate,
+                                 int max_ref_frames, int refined_span, int refined_rate,
+                                 int max_refined_refs);
+/* Eq. 4's watermark t: the newest frame id a refine commit has been applied for (-1: none). */
+int64_t vi_ring_watermark(const vi_ring* r);
 vi_status vi_ring_destroy(vi_ring* r);
 vi_status vi_ring_push(vi_ring* r, int n, int64_t* first_id, int64_t* evicted, int* n_evicted);
 vi_status vi_ring_evict(vi_ring* r, int64_t frame_id);

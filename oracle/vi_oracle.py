@@ -338,9 +338,21 @@ def joint_forward(feats: np.ndarray, w, cfg, mode: str = "causal",
 # ----------------------------------------------------------------------------------
 
 class OracleMemory:
-    """Resident-set bookkeeping + per-(layer, frame) cache, no slots, no arrays of slots."""
+    """Resident-set bookkeeping + per-(layer, frame) cache, no arrays of slots (the slot
+    numbers of ``state()`` follow the documented mapping, for comparison with the GPU ring).
 
-    def __init__(self, mem_frames: int, max_new: int, ref_rate: int = 0, max_refs: int = 0):
+    Regions (all plain sets of frame ids):
+      * online span: the frames f-M .. f-1 of Eq. 3 (span s = M, P:127-130) and the chunk;
+      * Eq. 3 references M_{1,r}^{f-1} (reading Q12): multiples of r that left the span, the R
+        newest kept;
+      * Eq. 4's refined memory M-bar (reading Q22; SPEC select_refined S:467-475):
+        refined frames t-s' .. t (refined span; t = the newest frame whose refine commit has
+        been applied, the watermark) and the R' newest refined frames with id a multiple of r'
+        (refined references), each frame at most once (an online-span frame with a refined
+        entry stays there: refined wins)."""
+
+    def __init__(self, mem_frames: int, max_new: int, ref_rate: int = 0, max_refs: int = 0,
+                 refined_span: Optional[int] = None, refined_rate: int = 0, max_refined_refs: int = 0):
         self.M = mem_frames
         self.T_max = max_new
         # Eq. 3's reference frames M_{1,r}^{f-1} (P:127-130): multiples of r stay after they
@@ -348,56 +360,127 @@ class OracleMemory:
         self.r = ref_rate if max_refs > 0 else 0
         self.R = max_refs if ref_rate > 0 else 0
         self.refs: Dict[int, int] = {}     # reference frame id -> its slot (S .. S+R-1)
+        # Eq. 4's refined memory (None: off)
+        self.refd = refined_span is not None
+        self.sr = refined_span if self.refd else 0
+        self.rr = refined_rate if (self.refd and max_refined_refs > 0) else 0
+        self.RR = max_refined_refs if (self.refd and refined_rate > 0) else 0
+        self.t = -1                        # watermark
+        self.online: set = set()
+        self.rspan: set = set()            # refined span frames (not in the online span)
+        self.rrefs: Dict[int, int] = {}    # refined reference id -> its slot
         self.next_id = 0
         self.cur_first = 0     # first id of the chunk pushed last
         self.cur_n = 0
-        self.resident: set = set()
         self.refined: set = set()
         self.pending: Dict[int, object] = {}
         self.stepped = False   # has the chunk pushed last gone through all blocks?
+
+    @property
+    def resident(self) -> set:
+        return self.online | set(self.refs) | self.rspan | set(self.rrefs)
 
     def mark_stepped(self):
         self.stepped = True
 
     @property
+    def S(self) -> int:
+        return self.M + self.T_max
+
+    @property
+    def SR(self) -> int:
+        return self.sr + 1 if self.refd else 0
+
+    @property
     def slots(self) -> int:
-        return self.M + self.T_max + self.R
+        return self.S + self.R + self.SR + self.RR
+
+    def _ref_cand(self, j: int) -> bool:
+        return self.RR > 0 and self.rr > 0 and j % self.rr == 0
 
     def push(self, n: int, on_evict=None, on_commit=None) -> Tuple[int, List[int]]:
         if n < 1 or n > self.T_max:
             raise ValueError("push: n out of range")
         f = self.next_id
-        S = self.M + self.T_max
+        S = self.S
         evicted = []
+        before = set(self.resident)    # a frame can only be reported evicted if it was resident
+        tn = max([self.t] + list(self.pending)) if self.refd else self.t
 
         def drop(j):
-            self.resident.discard(j)
+            self.online.discard(j)
+            self.rspan.discard(j)
+            self.refs.pop(j, None)
+            self.rrefs.pop(j, None)
             self.refined.discard(j)
             self.pending.pop(j, None)
-            evicted.append(j)
+            if j in before:
+                evicted.append(j)
             if on_evict:
                 on_evict(j)
-        for j in sorted(j for j in self.resident if j < f - self.M and j not in self.refs):
+
+        def keep_refined_ref(j) -> bool:
+            """Give j a refined-reference slot: the lowest free one, else the oldest
+            reference's if j is newer (the oldest leaves); False: j is not kept."""
+            b = S + self.R + self.SR
+            free = [k for k in range(b, b + self.RR) if k not in self.rrefs.values()]
+            if free:
+                self.rrefs[j] = min(free)
+                return True
+            if not self.rrefs or min(self.rrefs) > j:
+                return False
+            oldest = min(self.rrefs)
+            slot = self.rrefs[oldest]
+            drop(oldest)
+            self.rrefs[j] = slot
+            return True
+
+        # 1. refined span frames below t - s' (t: the watermark after this push's commits)
+        for j in sorted(x for x in self.rspan if x < tn - self.sr):
+            self.rspan.discard(j)
+            if not (self._ref_cand(j) and keep_refined_ref(j)):
+                self.rspan.add(j)
+                drop(j)
+        # 2. frames leaving the online span
+        for j in sorted(x for x in self.online if x < f - self.M):
+            self.online.discard(j)
+            has_refined = j in self.refined or j in self.pending
+            if self.refd and has_refined and j >= tn - self.sr:
+                self.rspan.add(j)
+                continue
+            if self.refd and has_refined and self._ref_cand(j) and keep_refined_ref(j):
+                continue
             if self.r > 0 and j % self.r == 0:
                 free = [k for k in range(S, S + self.R) if k not in self.refs.values()]
                 if free:
                     slot = min(free)
                 else:
                     oldest = min(self.refs)
-                    slot = self.refs.pop(oldest)
+                    slot = self.refs[oldest]
                     drop(oldest)
                 self.refs[j] = slot
             else:
+                self.online.add(j)
                 drop(j)
-        evicted.sort()
+        # 3. queued commits: resident frames are overwritten; with the refined memory, others
+        # land in it when Eq. 4 selects them
         for j in sorted(self.pending):
-            if j in self.resident:
+            land = j in self.resident
+            if not land and self.refd:
+                if j >= tn - self.sr:
+                    self.rspan.add(j)
+                    land = True
+                elif self._ref_cand(j):
+                    land = keep_refined_ref(j)
+            if land:
                 self.refined.add(j)
                 if on_commit:
                     on_commit(j, self.pending[j])
         self.pending.clear()
+        self.t = tn
+        evicted.sort()
         for j in range(f, f + n):
-            self.resident.add(j)
+            self.online.add(j)
         self.next_id = f + n
         self.cur_first, self.cur_n = f, n
         self.stepped = False
@@ -414,11 +497,24 @@ class OracleMemory:
             return VI_NOT_RESIDENT
         return VI_OK
 
+    def _may_land(self, fid: int) -> bool:
+        """A past, non-resident frame's refine commit can still be used (refined memory on):
+        it is within s' of the watermark the commit would raise it to, or a refined-reference
+        candidate newer than the oldest refined reference held (or a slot is free)."""
+        if not self.refd:
+            return False
+        tw = max([self.t, fid] + list(self.pending))
+        if fid >= tw - self.sr:
+            return True
+        return self._ref_cand(fid) and (len(self.rrefs) < self.RR or fid > min(self.rrefs))
+
     def evict(self, fid: int, on_evict=None) -> int:
         st = self._check_past(fid)
         if st == VI_OK:
+            self.online.discard(fid)
+            self.rspan.discard(fid)
             self.refs.pop(fid, None)
-            self.resident.discard(fid)
+            self.rrefs.pop(fid, None)
             self.refined.discard(fid)
             self.pending.pop(fid, None)
             if on_evict:
@@ -427,20 +523,31 @@ class OracleMemory:
 
     def commit(self, fid: int, payload) -> int:
         st = self._check_past(fid)
+        if st == VI_NOT_RESIDENT and self._may_land(fid):
+            st = VI_OK
         if st == VI_OK:
             self.pending[fid] = payload
         return st
 
     def window(self) -> List[int]:
-        """Memory frames the current chunk attends to, in temporal order."""
+        """Memory frames the current chunk attends to, in temporal order (Eq. 3 / Eq. 4)."""
         return sorted(j for j in self.resident if j < self.cur_first)
 
     def state(self) -> Tuple[List[int], List[int], int]:
-        """(slot_id[S], refined[S], valid mask) under slot = id mod S."""
-        S = self.M + self.T_max
+        """(slot_id[slots], refined[slots], valid mask): online span slot = id mod S (SURVEY
+        §8(c)), then the reference slots, refined span slot = S + R + id mod (s'+1), then the
+        refined reference slots."""
+        S = self.S
         slot_id, ref, mask = [-1] * self.slots, [0] * self.slots, 0
         for j in self.resident:
-            s = self.refs[j] if j in self.refs else j % S
+            if j in self.refs:
+                s = self.refs[j]
+            elif j in self.rrefs:
+                s = self.rrefs[j]
+            elif j in self.rspan:
+                s = S + self.R + j % self.SR
+            else:
+                s = j % S
             assert slot_id[s] == -1, "two resident frames share a slot"
             slot_id[s] = j
             ref[s] = int(j in self.refined)
@@ -455,7 +562,10 @@ class OracleStream:
         self.cfg = cfg
         self.w = w
         self.store = store     # None: the oracle; a rounding function: the bf16-storage emulation
-        self.mem = OracleMemory(cfg.mem_frames, cfg.t_new, getattr(cfg, "ref_rate", 0), getattr(cfg, "max_refs", 0))
+        self.mem = OracleMemory(cfg.mem_frames, cfg.t_new, getattr(cfg, "ref_rate", 0), getattr(cfg, "max_refs", 0),
+                                refined_span=(cfg.refined_span if getattr(cfg, "refined_mem", 0) else None),
+                                refined_rate=getattr(cfg, "refined_rate", 0),
+                                max_refined_refs=getattr(cfg, "max_refined_refs", 0))
         self.chunk_causal = chunk_causal
         # (layer, frame id) -> ("x", block input [P, D]) or ("kv", K [P, D], V [P, D])
         self.entries: Dict[Tuple[int, int], tuple] = {}

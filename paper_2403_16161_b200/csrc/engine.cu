@@ -396,8 +396,12 @@ static vi_status validate(const vi_config* k, std::string* why) {
   if (k->layers < 1 || k->heads < 1 || k->d_model < 1 || k->mem_frames < 0 || k->max_new_frames < 1)
     return bad("layers, heads, d_model, max_new_frames must be >= 1 and mem_frames >= 0");
   if (k->ref_rate < 0 || k->max_ref_frames < 0) return bad("ref_rate and max_ref_frames must be >= 0");
-  if (k->mem_frames + k->max_new_frames + (k->ref_rate > 0 ? k->max_ref_frames : 0) > 64)
-    return bad("mem_frames + max_new_frames + max_ref_frames must be <= 64");
+  if (k->refined_mem && (k->refined_span < 0 || k->refined_rate < 0 || k->max_refined_refs < 0))
+    return bad("refined_span, refined_rate and max_refined_refs must be >= 0");
+  if (k->mem_frames + k->max_new_frames + (k->ref_rate > 0 ? k->max_ref_frames : 0) +
+          (k->refined_mem ? k->refined_span + 1 + (k->refined_rate > 0 ? k->max_refined_refs : 0) : 0) > 64)
+    return bad("mem_frames + max_new_frames + max_ref_frames + refined slots must be <= 64");
+  if (k->refined_mem && k->win_h > 0) return bad("refined memory: not built for window attention (no refine commits)");
   if (k->d_model % k->heads) return bad("d_model must be divisible by heads");
   const int hd = k->d_model / k->heads;
   if (k->dtype != VI_DTYPE_BF16 && k->dtype != VI_DTYPE_FP32) return bad("dtype must be 0 (bf16) or 1 (fp32)");
@@ -504,7 +508,9 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->cfg = *cfg;
   c->L = cfg->layers; c->H = cfg->heads; c->D = cfg->d_model; c->hd = c->D / c->H;
   c->P = cfg->tokens_per_frame; c->M = cfg->mem_frames; c->Tmax = cfg->max_new_frames; c->S = c->M + c->Tmax;
-  c->ST = c->S + (cfg->ref_rate > 0 ? cfg->max_ref_frames : 0);
+  c->ring = Ring(c->M, c->Tmax, cfg->ref_rate, cfg->max_ref_frames, cfg->refined_mem, cfg->refined_span,
+                 cfg->refined_rate, cfg->max_refined_refs);
+  c->ST = c->ring.slots();
   c->F = cfg->ffn_hidden; c->Pd = cfg->kh * cfg->kw * cfg->feat_c;
   if (cfg->win_h > 0) {
     const int oh = (cfg->feat_h + 2 * cfg->ph - cfg->kh) / cfg->sh + 1, ow = (cfg->feat_w + 2 * cfg->pw - cfg->kw) / cfg->sw + 1;
@@ -523,7 +529,6 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   }
   c->vt_ld = (c->KR + 63) / 64 * 64;
   c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
-  c->ring = Ring(c->M, c->Tmax, cfg->ref_rate, cfg->max_ref_frames);
   {
     const int G = cfg->tp_size < 1 ? 1 : cfg->tp_size;
     c->sharded = G > 1 || cfg->nccl_id != nullptr;
@@ -1523,6 +1528,11 @@ extern "C" vi_status vi_memory_footprint(const vi_ctx* c, int64_t* slab_bytes, i
   return VI_OK;
 }
 extern "C" int vi_num_slots(const vi_ctx* c) { return c ? c->ST : 0; }
+extern "C" int64_t vi_refined_watermark(vi_ctx* c) {
+  if (!c) return -1;
+  std::lock_guard<std::mutex> lk(c->mu);
+  return c->ring.t;
+}
 extern "C" void* vi_stream(const vi_ctx* c) { return c ? (void*)c->stream : nullptr; }
 extern "C" const char* vi_version(void) { return "vi-memstep 0.1 (sm_100a)"; }
 

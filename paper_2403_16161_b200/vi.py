@@ -34,7 +34,8 @@ EXPORTS = ["vi_config_default", "vi_create", "vi_create_ex", "vi_destroy", "vi_s
            "vi_stream", "vi_debug_read", "vi_ring_create", "vi_ring_destroy", "vi_ring_push", "vi_ring_evict",
            "vi_ring_commit", "vi_ring_mark_stepped", "vi_ring_state", "vi_version", "vi_memory_step_attn",
            "vi_memory_step_ffn", "vi_tp_layout", "vi_tp_unique_id", "vi_tp_local_allgather", "vi_memory_footprint",
-           "vi_memory_read", "vi_ring_create_ex", "vi_run_step_async"]
+           "vi_memory_read", "vi_ring_create_ex", "vi_run_step_async", "vi_ring_create_refined", "vi_ring_watermark",
+           "vi_refined_watermark"]
 
 
 class ViConfig(C.Structure):
@@ -43,7 +44,8 @@ class ViConfig(C.Structure):
         "feat_h", "feat_w", "feat_c", "kh", "kw", "sh", "sw", "ph", "pw",
         "ffn_hidden", "ffn_kind", "dtype", "pos_embed", "device")] + [("stream", C.c_void_p)] + [
         ("tp_size", C.c_int), ("tp_rank", C.c_int), ("nccl_id", C.c_void_p), ("stream_priority", C.c_int),
-        ("ref_rate", C.c_int), ("max_ref_frames", C.c_int), ("win_h", C.c_int), ("win_w", C.c_int)]
+        ("ref_rate", C.c_int), ("max_ref_frames", C.c_int), ("win_h", C.c_int), ("win_w", C.c_int),
+        ("refined_mem", C.c_int), ("refined_span", C.c_int), ("refined_rate", C.c_int), ("max_refined_refs", C.c_int)]
 
 
 WEIGHT_FIELDS = ("embed_w", "embed_b", "pos", "ln1_g", "ln1_b", "wqkv", "bqkv", "wo", "bo", "ln2_g", "ln2_b",
@@ -79,6 +81,9 @@ _sig = {
     "vi_debug_read": (C.c_int32, [_P, C.c_int, C.c_int, C.c_int, _P, C.c_size_t]),
     "vi_ring_create": (C.c_int32, [C.POINTER(_P), C.c_int, C.c_int]),
     "vi_ring_create_ex": (C.c_int32, [C.POINTER(_P), C.c_int, C.c_int, C.c_int, C.c_int]),
+    "vi_ring_create_refined": (C.c_int32, [C.POINTER(_P)] + [C.c_int] * 7),
+    "vi_ring_watermark": (C.c_int64, [_P]),
+    "vi_refined_watermark": (C.c_int64, [_P]),
     "vi_ring_destroy": (C.c_int32, [_P]),
     "vi_ring_push": (C.c_int32, [_P, C.c_int, _I64P, _I64P, C.POINTER(C.c_int)]),
     "vi_ring_evict": (C.c_int32, [_P, C.c_int64]),
@@ -131,13 +136,25 @@ def _ptr(x) -> Optional[int]:
 class Ring:
     """vi_ring_*: the integer ring bookkeeping every context uses, without a GPU."""
 
-    def __init__(self, mem_frames: int, max_new_frames: int, ref_rate: int = 0, max_refs: int = 0):
+    def __init__(self, mem_frames: int, max_new_frames: int, ref_rate: int = 0, max_refs: int = 0,
+                 refined_span: Optional[int] = None, refined_rate: int = 0, max_refined_refs: int = 0):
+        """refined_span = None: no refined memory; s' >= 0: Eq. 4's refined memory."""
         h = _P()
-        st = _lib.vi_ring_create_ex(C.byref(h), mem_frames, max_new_frames, ref_rate, max_refs)
+        if refined_span is None:
+            st = _lib.vi_ring_create_ex(C.byref(h), mem_frames, max_new_frames, ref_rate, max_refs)
+        else:
+            st = _lib.vi_ring_create_refined(C.byref(h), mem_frames, max_new_frames, ref_rate, max_refs,
+                                             refined_span, refined_rate, max_refined_refs)
         if st != VI_OK:
-            raise ViError(st, "vi_ring_create_ex")
+            raise ViError(st, "vi_ring_create")
         self._h = h
         self.S = mem_frames + max_new_frames + (max_refs if ref_rate > 0 and max_refs > 0 else 0)
+        if refined_span is not None:
+            self.S += refined_span + 1 + (max_refined_refs if refined_rate > 0 else 0)
+
+    @property
+    def watermark(self) -> int:
+        return _lib.vi_ring_watermark(self._h)
 
     def __del__(self):
         if getattr(self, "_h", None):
@@ -237,7 +254,9 @@ class Context:
                    device=device, stream=stream, tp_size=tp_size, tp_rank=tp_rank, nccl_id=nccl_id,
                    stream_priority=stream_priority, ref_rate=getattr(c, "ref_rate", 0),
                    max_ref_frames=getattr(c, "max_refs", 0), win_h=getattr(c, "win_h", 0),
-                   win_w=getattr(c, "win_w", 0))
+                   win_w=getattr(c, "win_w", 0), refined_mem=getattr(c, "refined_mem", 0),
+                   refined_span=getattr(c, "refined_span", 0), refined_rate=getattr(c, "refined_rate", 0),
+                   max_refined_refs=getattr(c, "max_refined_refs", 0))
 
     def close(self):
         if getattr(self, "_h", None):
@@ -341,6 +360,10 @@ class Context:
 
     def stream(self) -> int:
         return _lib.vi_stream(self._h)
+
+    def refined_watermark(self) -> int:
+        """Eq. 4's watermark t (vi_refined_watermark; -1: no refined frame yet)."""
+        return _lib.vi_refined_watermark(self._h)
 
     def debug_read(self, what: str, dst, layer: int = 0, slot: int = 0):
         nbytes = dst.numel() * dst.element_size() if hasattr(dst, "numel") else dst.nbytes

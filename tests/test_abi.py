@@ -151,3 +151,59 @@ def test_ring_reference_golden_spec(V):
     sid, _, _ = r.state()
     assert sorted(x for x in sid if x >= 0) == [0, 10, 13, 14, 15, 16, 17, 18]
     assert sid[6:] in ([0, 10], [10, 0])          # the two reference slots follow the 6 span slots
+
+
+# ---------------------------------------------------------------- Eq. 4's refined memory M-bar
+
+def test_ring_refined_matches_oracle_random_traces(V):
+    """Eq. 4's refined memory (reading Q22): slot table, refined bits, watermark, commit codes
+    and evictions bit-exact against the oracle's set model over random traces of pushes,
+    explicit evictions and refine commits (resident, landing in the refined span or the
+    refined references, or useless), with and without Eq. 3 references alongside."""
+    rnd = random.Random(4242)
+    for trial in range(400):
+        M, T = rnd.randint(0, 6), rnd.randint(1, 3)
+        sr, rrt, RR = rnd.randint(0, 5), rnd.randint(0, 5), rnd.randint(0, 3)
+        rr, R = (rnd.randint(1, 5), rnd.randint(1, 3)) if rnd.random() < 0.3 else (0, 0)
+        r = V.Ring(M, T, rr, R, refined_span=sr, refined_rate=rrt, max_refined_refs=RR)
+        m = O.OracleMemory(M, T, ref_rate=rr, max_refs=R, refined_span=sr, refined_rate=rrt, max_refined_refs=RR)
+        for step in range(70):
+            x = rnd.random()
+            if x < 0.35:
+                n = rnd.randint(1, T)
+                assert r.push(n) == m.push(n), (trial, step)
+                r.mark_stepped(); m.mark_stepped()
+            elif x < 0.45:
+                fid = rnd.randint(-1, m.next_id + 1)
+                assert r.evict(fid) == m.evict(fid), (trial, step, fid)
+            else:
+                fid = rnd.randint(max(-1, m.next_id - 3 * (M + sr + 2)), m.next_id + 1)
+                assert r.commit(fid) == m.commit(fid, None), (trial, step, fid)
+            assert r.state() == tuple(m.state()), (trial, step)
+            assert r.watermark == m.t
+
+
+def test_ring_refined_golden_spec_select_refined(V):
+    """SPEC S:473 (Fig. 3 caption): select_refined(f=18, t=14, s=s'=3, r'=10) -> online
+    {15, 16, 17}, refined {11..14}, refined references {0, 10}.  The online inpainter has shown
+    frames 0..17 (span 3); the refiner has committed its results for frames 0..14 (t = 14);
+    at frame 18's push the memory holds exactly those sets."""
+    r = V.Ring(3, 1, refined_span=3, refined_rate=10, max_refined_refs=2)
+    m = O.OracleMemory(3, 1, refined_span=3, refined_rate=10, max_refined_refs=2)
+    for f in range(18):
+        for x in (r, m):
+            x.push(1)
+            x.mark_stepped()
+    codes = [r.commit(j) for j in range(15)]
+    assert codes == [m.commit(j, None) for j in range(15)]
+    assert all(c == V.VI_OK for c in codes)
+    r.push(1); m.push(1)
+    sid, ref, _ = r.state()
+    S = 3 + 1
+    online = sorted(x for x in sid[:S] if 0 <= x < 18)
+    refined_span = sorted(x for x in sid[S:S + 4] if x >= 0)
+    refined_refs = sorted(x for x in sid[S + 4:] if x >= 0)
+    assert (online, refined_span, refined_refs) == ([15, 16, 17], [11, 12, 13, 14], [0, 10])
+    assert r.watermark == 14 and m.window() == [0, 10, 11, 12, 13, 14, 15, 16, 17]
+    assert all(ref[i] for i in range(len(sid)) if sid[i] in (0, 10, 11, 12, 13, 14))
+    assert r.state() == tuple(m.state())

@@ -115,3 +115,68 @@ def test_memory_read_roundtrip_and_protocol():
     assert ctx.read_kv(10, kh, vh) == vi.VI_E_PROTOCOL               # future frame
     ctx.run_step(f[0:1], 1, o[0:1])                                  # frame 4: frame 0 leaves (M = 3)
     assert ctx.read_kv(0, kh, vh) == vi.VI_NOT_RESIDENT
+
+
+# ---------------------------------------------------------------- Eq. 4's refined memory M-bar
+
+def _refined_stream(cfg, w, steps, commits, seed, tol):
+    """Free-running oracle (+ bf16-storage emulation on the bf16 path) and GPU streams with
+    refine commits of arbitrary K/V (commits[i] = frame ids committed before push i); every step
+    compared stage by stage, ring state (slots, refined bits) and commit codes bit-exact."""
+    import gpu_harness
+    from test_gpu_parity import check_attention_kernel, compare_step
+    from vi_synth import make_kv
+    g = gpu_harness.GpuStream(cfg, w)
+    o = O.OracleStream(cfg, w)
+    e = O.emulate_bf16_storage(cfg, w) if cfg.dtype == "bf16" else None
+    for i in range(steps):
+        for fid in commits.get(i, ()):
+            K, V = make_kv(cfg, seed + 100, fid, scale=0.5)        # bf16-representable on the bf16 path
+            if cfg.dtype == "bf16":                                 # the payload is in the ctx dtype
+                Kg, Vg = (torch.from_numpy(a).to(torch.bfloat16).contiguous() for a in (K, V))
+            else:
+                Kg, Vg = K, V
+            codes = [g.ctx.commit(fid, Kg, Vg), o.commit(fid, K, V)]
+            if e is not None:
+                codes.append(e.commit(fid, K, V))
+            assert len(set(codes)) == 1, (i, fid, codes)
+        feats = make_features(cfg, 1, first_frame=i, seed=seed, masked="moving")
+        o.push(1)
+        _, ost = o.step(feats)
+        est = None
+        if e is not None:
+            e.push(1)
+            _, est = e.step(feats)
+        _, gst = g.step(feats)
+        assert g.ctx.state() == tuple(o.mem.state()), f"step {i}: ring state differs"
+        compare_step(cfg, ost, gst, tol, tag=f"step {i}: ", est=est)
+        if cfg.dtype == "bf16":
+            fids = o.mem.window() + [o.mem.cur_first]
+            check_attention_kernel(g, cfg, gst["layers"][-1], cfg.layers - 1, fids, tol, tag=f"step {i}: ")
+    return g, o
+
+
+# a refiner lagging the online stream: at frame i it hands over frames up to i - 3 (some still
+# in the online span: overwritten in place; older ones land in the refined span or, multiples
+# of r' = 3, in the refined references; the oldest are useless and rejected or dropped)
+_COMMITS = {4: [0, 1], 6: [1, 2, 3], 8: [3, 4, 5], 9: [6], 11: [6, 7, 8], 12: [9], 13: [0, 9, 10]}
+
+
+def test_refined_memory_bf16_matches_oracle():
+    """Eq. 4 on the bf16 tensor-core path: online span 2, refined span s' = 2,
+    refined references every r' = 3 frames (2 kept); 14 one-frame steps."""
+    cfg = CONFIGS["C3S"].replace(layers=2, t_new=1, mem_frames=2, refined_mem=1, refined_span=2, refined_rate=3,
+                                 max_refined_refs=2)
+    w = make_weights(cfg, seed=40, variant="sensitive")
+    g, o = _refined_stream(cfg, w, 14, _COMMITS, seed=40, tol=2e-2)
+    assert g.ctx.refined_watermark() == o.mem.t == 10
+    sid, ref, _ = g.ctx.state()
+    assert sum(1 for s in sid[cfg.mem_frames + 1:] if s >= 0) >= 3     # refined regions in use
+
+
+def test_refined_memory_fp32_matches_oracle():
+    """The same schedule on the fp32 SIMT path (BASELINE configs[0] shape) at 1e-4."""
+    cfg = CONFIGS["C1"].replace(layers=2, mem_frames=2, refined_mem=1, refined_span=2, refined_rate=3,
+                                max_refined_refs=2)
+    w = make_weights(cfg, seed=41, variant="sensitive")
+    _refined_stream(cfg, w, 14, _COMMITS, seed=41, tol=1e-4)

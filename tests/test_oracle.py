@@ -582,6 +582,109 @@ def test_reference_memory_step_equals_masked_joint_pass():
     assert np.abs(plain["out"][8] - joint["out"][8]).max() > 1e-6
 
 
+# ---------------------------------------------------------------- Eq. 4's refined memory M-bar
+
+def _select_refined(f, t, s, s2, r2, R2):
+    """SPEC select_refined (S:467-475), written out: online neighbours [max(0,f-s), f-1];
+    refined neighbours [max(0,t-s'), t] minus the online ones (store precedence: a frame is
+    held once); refined references = multiples of r' in [0, t] minus both, of which the
+    memory keeps the R' newest (reading Q22).  t < 0: no refined frame yet (select_memory)."""
+    online = set(range(max(0, f - s), f))
+    if t < 0:
+        return online, set(), set()
+    refined = set(range(max(0, t - s2), t + 1)) - online
+    refs = sorted(j for j in range(t + 1) if r2 > 0 and j % r2 == 0 and j not in online and j not in refined)
+    return online, refined, set(refs[-R2:] if R2 > 0 else [])
+
+
+def test_refined_golden_spec_select_refined():
+    """SPEC S:473 / Fig. 3 caption: f=18, t=14, s=s'=3, r'=10 -> online {15,16,17},
+    refined {11..14}, refined references {0, 10}."""
+    online, refined, refs = _select_refined(18, 14, 3, 3, 10, 4)
+    assert (online, refined, refs) == ({15, 16, 17}, {11, 12, 13, 14}, {0, 10})
+    m = O.OracleMemory(3, 1, refined_span=3, refined_rate=10, max_refined_refs=2)
+    for f in range(18):
+        m.push(1)
+        m.mark_stepped()
+    for j in range(15):
+        m.commit(j, None)
+    m.push(1)
+    assert m.window() == sorted(online | refined | refs) and m.t == 14
+    assert (m.rspan, set(m.rrefs)) == (refined, refs)
+
+
+def test_refined_window_matches_spec_sets_random():
+    """The set model's memory equals SPEC select_refined's sets for random (s, s', r', R') and
+    refiner schedules (the refiner commits every frame up to its lagging watermark t)."""
+    rnd = random.Random(77)
+    for trial in range(200):
+        s, s2, r2, R2 = rnd.randint(0, 5), rnd.randint(0, 5), rnd.randint(0, 6), rnd.randint(1, 3)
+        lag, every = rnd.randint(1, 6), rnd.randint(1, 4)
+        m = O.OracleMemory(s, 1, refined_span=s2, refined_rate=r2, max_refined_refs=R2)
+        t = -1
+        for f in range(40):
+            if f % every == 0 and f - lag > t and f - lag >= 0:
+                t = f - lag
+                for j in range(t + 1):
+                    m.commit(j, None)
+            m.push(1)
+            online, refined, refs = _select_refined(f, t, s, s2, r2, R2)
+            assert m.window() == sorted(online | refined | refs), (trial, f, t)
+            assert m.t == t
+            m.mark_stepped()
+
+
+def test_refined_memory_without_commits_is_the_memory_model():
+    """Degradation: no refine commit -> exactly Eq. 3's memory."""
+    a = O.OracleMemory(4, 2)
+    b = O.OracleMemory(4, 2, refined_span=3, refined_rate=5, max_refined_refs=2)
+    for n in (2, 1, 2, 2, 1, 2, 2):
+        assert a.push(n) == b.push(n)
+        assert a.window() == b.window()
+        a.mark_stepped(); b.mark_stepped()
+
+
+def test_refined_memory_step_equals_masked_joint_pass():
+    """Exact memoisation with Eq. 4's refined memory (invariant I3): an identity refiner (it
+    commits every frame's own per-block K/V once the frame is t = f - 2 old, every 3 frames)
+    makes T=1 memory steps with online span s, refined span s' and refined references every r'
+    frames equal one joint pass in which frame i's queries see exactly select_refined(i, t)
+    and itself (Eq. 4)."""
+    s, s2, r2, R2, n, lag, every = 1, 2, 3, 2, 13, 2, 3
+    cfg = CONFIGS["C1"].replace(layers=2, mem_frames=s, refined_mem=1, refined_span=s2, refined_rate=r2,
+                                max_refined_refs=R2)
+    w = make_weights(cfg, seed=17, variant="sensitive")
+    feats = make_features(cfg, n, seed=17)
+    st = O.OracleStream(cfg, w)
+    kv = {}
+    mask = np.zeros((n, n), bool)
+    t = -1
+    outs = []
+    for i in range(n):
+        if i % every == 0 and i - lag > t and i - lag >= 0:
+            t = i - lag
+            for j in range(t + 1):
+                K = np.stack([kv[(l, j)][0] for l in range(cfg.layers)])
+                V = np.stack([kv[(l, j)][1] for l in range(cfg.layers)])
+                st.commit(j, K, V)
+        st.push(1)
+        online, refined, refs = _select_refined(i, t, s, s2, r2, R2)
+        assert st.mem.window() == sorted(online | refined | refs)
+        for j in online | refined | refs | {i}:
+            mask[i, j] = True
+        out, _ = st.step(feats[i:i + 1])
+        outs.append(out[0])
+        for l in range(cfg.layers):
+            kv[(l, i)] = st.frame_kv(l, i)
+    joint = O.joint_forward(feats, w, cfg, mode="mask", frame_mask=mask)
+    for i in range(n):
+        np.testing.assert_allclose(outs[i], joint["out"][i], rtol=1e-9, atol=1e-11)
+    # the refined memory matters: Eq. 3 with the same span alone differs at the last frame
+    plain = O.joint_forward(feats, w, cfg, mode="mask",
+                            frame_mask=np.array([[i - s <= j <= i for j in range(n)] for i in range(n)]))
+    assert np.abs(plain["out"][n - 1] - joint["out"][n - 1]).max() > 1e-6
+
+
 # ---------------------------------------------------------------- window attention (BASELINE configs[3])
 
 def test_window_ids_partition_the_grid():

@@ -53,6 +53,10 @@ class Config:
     max_refs: int = 0      # reference slots kept (the oldest reference leaves first)
     win_h: int = 0         # window attention: win_h x win_w token windows (0 = global attention)
     win_w: int = 0
+    refined_mem: int = 0   # Eq. 4's refined memory M-bar (0 = off)
+    refined_span: int = 0  # s' of Eq. 4 (refined frames t-s'..t)
+    refined_rate: int = 0  # r' of Eq. 4 (refined reference frames, 0 = none)
+    max_refined_refs: int = 0
 
     @property
     def oh(self) -> int:
@@ -76,7 +80,9 @@ class Config:
 
     @property
     def slots(self) -> int:
-        return self.mem_frames + self.t_new + (self.max_refs if self.ref_rate > 0 else 0)
+        return (self.mem_frames + self.t_new + (self.max_refs if self.ref_rate > 0 else 0) +
+                ((self.refined_span + 1 + (self.max_refined_refs if self.refined_rate > 0 else 0))
+                 if self.refined_mem else 0))
 
     def replace(self, **kw) -> "Config":
         return dataclasses.replace(self, **kw)
