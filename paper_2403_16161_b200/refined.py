@@ -34,12 +34,22 @@ from . import vi
 class RefinedRun:
     def __init__(self, cfg, weights: Dict[str, np.ndarray], window: int = 20, every: int = 5,
                  device_online: int = 0, device_refiner: Optional[int] = None, refiner: bool = True,
-                 synchronous: bool = False):
+                 synchronous: bool = False, refined_span: Optional[int] = None, refined_rate: int = 0,
+                 max_refined_refs: int = 0):
+        """refined_span = s' (not None): the online memory also keeps Eq. 4's refined memory
+        M-bar_{t-s'}^{t} U M-bar_{1,r'}^{t} (refined_rate r', max_refined_refs kept), and the
+        refiner commits only the frames Eq. 4 can use (its window's frames still in the online
+        span, within s' of its newest frame, or multiples of r')."""
         assert cfg.t_new == 1, "the online inpainter processes one frame at a time (Eq. 3/4)"
         self.cfg, self.window, self.every = cfg, window, every
         self.refiner_on, self.synchronous = refiner, synchronous
+        self.sr, self.rr = refined_span, refined_rate
+        ocfg = cfg
+        if refined_span is not None:
+            ocfg = cfg.replace(refined_mem=1, refined_span=refined_span, refined_rate=refined_rate,
+                               max_refined_refs=max_refined_refs)
         # CUDA clamps the priority to the device's greatest (most negative) value
-        self.online = vi.Context.from_synth(cfg, device=device_online, stream_priority=-100)
+        self.online = vi.Context.from_synth(ocfg, device=device_online, stream_priority=-100)
         self.online.set_weights(weights)
         self.dev_ref = device_online if device_refiner is None else device_refiner
         self.ref = None
@@ -51,7 +61,7 @@ class RefinedRun:
             with torch.cuda.device(self.dev_ref):
                 self.kbuf = torch.empty(shape, dtype=torch.bfloat16, device=f"cuda:{self.dev_ref}")
                 self.vbuf = torch.empty_like(self.kbuf)
-        self.stats = dict(windows=0, commits=0, not_resident=0, refine_s=0.0, lag_frames=[])
+        self.stats = dict(windows=0, commits=0, not_resident=0, refine_s=0.0, lag_frames=[], watermark=-1)
         self._q: "queue.Queue" = queue.Queue()
         self._online_frame = -1
 
@@ -68,15 +78,20 @@ class RefinedRun:
         first = self.ref.run_step(self.ref_in[:n], n, ref_out[:n])
         self.ref.sync()
         for i in range(n):
+            fid = lo + i
+            if self.sr is not None and not (fid >= f - max(self.sr, self.cfg.mem_frames) or
+                                            (self.rr > 0 and fid % self.rr == 0)):
+                continue                             # Eq. 4 would not select it: not handed over
             if self.ref.read_kv(first + i, self.kbuf, self.vbuf) != vi.VI_OK:
                 continue
-            st = self.online.commit(lo + i, self.kbuf, self.vbuf)
+            st = self.online.commit(fid, self.kbuf, self.vbuf)
             if st == vi.VI_OK:
                 self.stats["commits"] += 1
             else:
                 self.stats["not_resident"] += 1
         self.stats["windows"] += 1
         self.stats["refine_s"] += time.perf_counter() - t0
+        self.stats["watermark"] = f
         self.stats["lag_frames"].append(self._online_frame - f)
 
     def _worker(self, feats_ref, ref_out):
