@@ -111,7 +111,8 @@ typedef struct vi_config {
   /* Window attention (E2FGVI-shaped, BASELINE configs[3]): a query sees only the keys of
    * its own win_h x win_w token window (non-overlapping, tiling the token grid), in every
    * frame of the memory and the chunk (reference frames included).  0 = global attention.
-   * bf16 path; head sharding with tp_size <= heads; no refine commits or memory reads (the
+   * bf16 path; head sharding (tp_size > heads: the tp_size/heads ranks of a head split its
+   * windows by window rows; they must divide the window rows); no refine commits or memory reads (the
    * memory is window-major). */
   int win_h, win_w;
   /* Refined memory M-bar of Eq. 4 (SPEC select_refined S:467-475; reading Q22):

@@ -136,6 +136,7 @@ struct vi_ctx {
   // head sharding (tp.h): Hl local heads, Q/K/V width Dl = Hl * hd; the attention writes
   // the rank's chunk of the gathered head-major buffer og [H][head_rows][hd]
   bool sharded = false;
+  bool win_split = false;         // windows + more ranks than heads: the head's windows split by window rows
   TpLayout tp;
   int Hl = 0, Dl = 0;
   void* comm = nullptr;           // ncclComm_t (NULL: unsharded, or exchange driven by the caller)
@@ -434,7 +435,11 @@ static vi_status validate(const vi_config* k, std::string* why) {
   if (k->win_h > 0) {
     if (k->dtype != VI_DTYPE_BF16) return bad("window attention: bf16 path only");
     if (oh % k->win_h || ow % k->win_w) return bad("window attention: windows must tile the token grid");
-    if (k->tp_size > k->heads) return bad("window attention: head sharding needs tp_size <= heads");
+    if (k->tp_size > k->heads) {   // q = tp_size / heads ranks per head split its windows by window rows
+      const int q = k->tp_size / k->heads;
+      if (k->tp_size % k->heads || (oh / k->win_h) % q || k->tokens_per_frame % q)
+        return bad("window attention with tp_size > heads: tp_size / heads must divide the window rows");
+    }
   }
   const int G = k->tp_size < 1 ? 1 : k->tp_size;
   if (G > 1 || k->nccl_id) {
@@ -535,6 +540,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     tp_layout(c->H, c->hd, c->Tmax * c->P, G, c->sharded ? cfg->tp_rank : 0, &c->tp);
     c->Hl = c->tp.nheads;
     c->Dl = c->Hl * c->hd;
+    c->win_split = c->sharded && cfg->win_h > 0 && c->tp.qparts > 1;
     c->cfg.nccl_id = nullptr;   // caller memory: only read here
   }
   const int oh = (cfg->feat_h + 2 * cfg->ph - cfg->kh) / cfg->sh + 1;
@@ -1057,10 +1063,19 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.Nq = c->win_n * a.win_qstride;   // rows of the KV-split partials (window-major)
   }
   if (c->sharded) {   // this rank's query rows, written head-major into its chunk of og
-    if (!c->win_n) {  // (windows: tp_size <= heads, every query row of the rank's heads)
+    if (!c->win_n) {
       a.q_row0 = c->tp.row0();
       a.Nq = c->tp.rows(M);
       if (a.Nq == 0) return VI_OK;   // a query part beyond a short chunk: nothing to attend
+    } else if (c->win_split) {
+      // q ranks per head: rank part p takes window rows [p*wr/q, (p+1)*wr/q) -- tokens
+      // [p*P/q, (p+1)*P/q) of every frame -- and writes them part-locally (frame-major)
+      const int q = c->tp.qparts, nw = c->win_n / q;
+      a.win_n = nw;
+      a.win0 = c->tp.qpart * nw;
+      a.win_split_rows = c->P / q;
+      a.win_part = c->tp.qpart;
+      a.Nq = nw * a.win_qstride;
     }
     a.o = static_cast<bf16*>(c->og) + (size_t)c->tp.rank * c->tp.chunk_elems;
     a.o_ld = c->hd;
@@ -1078,7 +1093,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   // window attention: sk2 over (head, window, query pair) units, stream-K split over up to
   // VI_WIN_SPLIT CTAs per unit (C4: 64 units of 6 key tiles; attn_tc2's KV split + combine
   // kernel measured 28 us/block)
-  const int win_units = c->win_n ? c->win_n * a.win_npw * a.H : 0;
+  const int win_units = c->win_n ? a.win_n * a.win_npw * a.H : 0;
   if (c->win_n && win_units <= c->num_sms) {
     a.npairs = a.win_npw;
     a.units = win_units;
@@ -1111,7 +1126,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     const int grid = int(work < c->num_sms ? work : c->num_sms);
     PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
   } else {   // small chunks (and windows beyond one wave): fixed KV split + combine kernel
-    const int units = c->win_n ? c->win_n * a.win_npw * a.H : ((a.Nq + 255) / 256) * a.H;
+    const int units = c->win_n ? a.win_n * a.win_npw * a.H : ((a.Nq + 255) / 256) * a.H;
     choose_split(units, ntiles, &a.nsplit, &a.tiles_per_split);
     a.nsplit = (ntiles + a.tiles_per_split - 1) / a.tiles_per_split;
     PLAUNCH(VI_PROF_ATTN, launch_attn_tc2(c->tm_q, c->tm_k, c->tm_vt, a, c->stream), "attention");
@@ -1135,17 +1150,23 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
       return c->fail(VI_E_NCCL, std::string("ncclAllGather: ") + nccl().error_string(r));
     }
   }
+  // window-split head sharding: the gathered parts back to token-major rows (O-proj's A)
+  if (c->win_split)
+    PLAUNCH(VI_PROF_ROW, launch_window_part_gather(c->og, c->o, M, c->P, c->H, c->hd, c->tp.qparts, c->tp.part_rows,
+                                                   c->stream),
+            "window part gather");
   // a7: output projection + residual
   Epi eo = epi_base(c, EPI_RESID, M, D, c->b_o + (size_t)l * D);
   eo.x_in = x_in; eo.x_out = x_out;
-  if (c->sharded) {   // A = concat_h(O_h) read head-major from the gathered buffer
+  if (c->sharded && !c->win_split) {   // A = concat_h(O_h) read head-major from the gathered buffer
     eo.a_hs = c->tp.head_rows;
     eo.a_kpb = c->hd / 64;
   }
   CUtensorMap tx_in, tx_out;
   const bool te = c->bf16 && make_tmap_out(&tx_in, x_in, true, D, M) && make_tmap_out(&tx_out, x_out, true, D, M);
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->sharded ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D, c->bn_o, eo, c->stream, 0,
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc((c->sharded && !c->win_split) ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D,
+                                         c->bn_o, eo, c->stream, 0,
                                          te ? &tx_out : nullptr, te ? &tx_in : nullptr),
             "o gemm");
   else
@@ -1577,7 +1598,7 @@ extern "C" vi_status vi_debug_read(vi_ctx* c, int what, int layer, int slot, voi
     for (size_t d = 0; d < Dl; ++d)
       for (int p = 0; p < c->P; ++p) std::memcpy(&tr[((size_t)p * Dl + d) * es], &tmp[(d * c->P + p) * es], es);
     CK(cudaMemcpy(dst, tr.data(), need, cudaMemcpyDefault), "debug copy V");
-  } else if (what == VI_DBG_O && c->sharded) {
+  } else if (what == VI_DBG_O && c->sharded && !c->win_split) {
     // gathered head-major [H][head_rows][hd] -> [rows][D]
     const size_t hr = c->tp.head_rows, hd = c->hd;
     std::vector<uint8_t> tmp((size_t)c->H * hr * hd * es), out(need);

@@ -64,7 +64,8 @@ __device__ __forceinline__ int win_out_row(const AttnTC& a, int w, int q) {
   const int t = q / a.win_pad, i = q - t * a.win_pad;
   if (i >= a.win_real) return -1;
   const int oy = (w / a.win_cols) * a.win_h + i / a.win_w, ox = (w % a.win_cols) * a.win_w + i % a.win_w;
-  return t * a.P + oy * a.ow + ox;
+  const int tok = oy * a.ow + ox;
+  return a.win_split_rows ? t * a.win_split_rows + tok - a.win_part * a.win_split_rows : t * a.P + tok;
 }
 
 __device__ __forceinline__ void key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
@@ -127,7 +128,8 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_final + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int win = a.win_n ? int(blockIdx.x) / a.win_npw : 0;                   // window (0 if global)
+  const int win_l = a.win_n ? int(blockIdx.x) / a.win_npw : 0;                 // window of this launch's range
+  const int win = a.win0 + win_l;                                                // window (0 if global)
   const int q0 = (a.win_n ? int(blockIdx.x) % a.win_npw : int(blockIdx.x)) * 256, h = blockIdx.y, z = blockIdx.z;
   const int wq = win * a.win_qstride, wk = win * a.win_kstride;                  // window row offsets
   const int ntiles = a.segs.tile0[a.segs.n];
@@ -341,7 +343,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     const int q = q0 + t * 128 + qd * 32 + lane;
     // output row (global: q itself; windows: the token row of (frame, window index), -1 = none)
     const int orow = a.win_n ? win_out_row(a, win, q) : (q < a.Nq ? q : -1);
-    const int qp = wq + q;                            // row of the KV-split partials
+    const int qp = win_l * a.win_qstride + q;         // row of the KV-split partials (launch-local windows)
     if (n > 0) {
       mbar_wait(&o_final[t], 0);
       tc_fence_after();
@@ -420,7 +422,7 @@ __global__ void attn_combine_kernel(const AttnTC a) {
     const size_t r = i / hd4;
     const int h = int(r % a.H);
     const int q = int(r / a.H);             // KV-split partial row (windows: window-major)
-    const int orow = a.win_n ? win_out_row(a, q / a.win_qstride, q % a.win_qstride) : q;
+    const int orow = a.win_n ? win_out_row(a, a.win0 + q / a.win_qstride, q % a.win_qstride) : q;
     if (orow < 0) continue;
     float mx = -INFINITY;
     for (int z = 0; z < a.nsplit; ++z) mx = fmaxf(mx, a.lse[((size_t)z * a.H + h) * a.Nq + q]);

@@ -104,8 +104,9 @@ __device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0
     const int per_h = a.win_n * a.win_npw;
     h = u / per_h;
     const int r = u - h * per_h;
-    win = r / a.win_npw;
-    q0 = (r - win * a.win_npw) * 256;
+    const int wl = r / a.win_npw;                 // window within this launch's range
+    win = a.win0 + wl;
+    q0 = (r - wl * a.win_npw) * 256;
     return;
   }
   const int full = a.npairs - a.sk_tail;     // full pairs per head
@@ -126,7 +127,8 @@ __device__ __forceinline__ int sk2_win_out_row(const AttnTC& a, int w, int q) {
   const int t = q / a.win_pad, i = q - t * a.win_pad;
   if (i >= a.win_real) return -1;
   const int oy = (w / a.win_cols) * a.win_h + i / a.win_w, ox = (w % a.win_cols) * a.win_w + i % a.win_w;
-  return t * a.P + oy * a.ow + ox;
+  const int tok = oy * a.ow + ox;
+  return a.win_split_rows ? t * a.win_split_rows + tok - a.win_part * a.win_split_rows : t * a.P + tok;
 }
 
 // WIN: window attention compiled in (a separate instantiation, so the global-attention kernel

@@ -137,7 +137,17 @@ struct AttnTC {
   // key segments (slot s at s * win_pad); rows with index % win_pad >= win_real are padding
   // (keys masked, queries not written); output row of (t, i) = t * P + token(w, i)
   int win_n, win_npw, win_qstride, win_kstride, win_pad, win_real, win_h, win_w, win_cols, ow, P, win_nq;
+  // windows [win0, win0 + win_n) of the win_cols-wide window grid (head sharding with more
+  // ranks than heads splits a head's windows between q ranks by window rows); with
+  // win_split_rows > 0 (= P / q) an output row goes to the rank's part-local row
+  // t * win_split_rows + (token - win_part * win_split_rows) instead of the token row
+  int win0, win_split_rows, win_part;
 };
+// Window-split head sharding: the gathered head outputs og [H][q][part_rows][d] (part p of
+// head h = that head's tokens [p*P/q, (p+1)*P/q) of every frame, frame-major) -> O [M][D]
+// token-major for the output projection
+cudaError_t launch_window_part_gather(const void* og, void* o, int M, int P, int H, int hd, int q, int part_rows,
+                                      cudaStream_t st);
 // two 128-query tiles per CTA, P kept in TMEM, fixed KV split (small chunks; attn.cu)
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                             cudaStream_t st);

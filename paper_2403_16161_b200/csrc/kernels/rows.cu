@@ -172,3 +172,36 @@ cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D,
 }
 
 }  // namespace vi
+
+namespace vi {
+
+// og [H][q][part_rows][hd] -> o [M][H*hd]: token m = t*P + i of head h comes from part
+// p = i / (P/q), row t*(P/q) + i - p*(P/q) (16-byte vectors; bf16)
+__global__ void window_part_gather_kernel(const uint4* __restrict__ og, uint4* __restrict__ o, int M, int P, int H,
+                                          int hd8, int q, int part_rows) {
+  griddep_wait();
+  griddep_launch();
+  const int split = P / q;
+  const size_t total = (size_t)M * H * hd8;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    const int c = int(idx % hd8);
+    const size_t r = idx / hd8;
+    const int h = int(r % H), m = int(r / H);
+    const int t = m / P, i = m - t * P, p = i / split;
+    const size_t src_row = ((size_t)h * q + p) * part_rows + (size_t)t * split + (i - p * split);
+    o[((size_t)m * H + h) * hd8 + c] = og[src_row * hd8 + c];
+  }
+}
+
+cudaError_t launch_window_part_gather(const void* og, void* o, int M, int P, int H, int hd, int q, int part_rows,
+                                      cudaStream_t st) {
+  if (hd % 8 || q < 1 || P % q) return cudaErrorInvalidValue;
+  const size_t total = (size_t)M * H * (hd / 8);
+  int blocks = int((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  pdl_launch(window_part_gather_kernel, dim3(blocks), dim3(256), 0, st, (const uint4*)og, (uint4*)o, M, P, H, hd / 8,
+             q, part_rows);
+  return cudaGetLastError();
+}
+
+}  // namespace vi

@@ -229,9 +229,19 @@ def test_split_phase_equals_memory_step_and_protocol():
     assert e.value.status == vi.VI_E_PROTOCOL
 
 
-@pytest.mark.parametrize("G", [2, 4])
+@pytest.mark.parametrize("G", [2, 4, 8])
 def test_head_sharded_window_attention(G):
     """Window attention (BASELINE configs[3]: heads sharded across GPUs with an all-gather of
-    the head outputs) on the reduced map: 10 x 18 tokens in 5 x 6 windows."""
+    the head outputs) on the reduced map: 10 x 18 tokens in 2 x 3 windows of 5 x 6.  G = 8 > H:
+    each head's windows are split between a rank pair by window rows (part-local outputs,
+    gathered back to token rows before the output projection)."""
     cfg = CONFIGS["C3S"].replace(win_h=5, win_w=6)
     _run_group(cfg, make_weights(cfg, seed=5, variant="sensitive"), G, ns=[2, 1, 2, 2])
+
+
+def test_head_sharded_window_attention_c4_shape_g8():
+    """BASELINE configs[3] ("heads sharded across 2/4/8 GPUs") at its full token shape (2 of
+    its 16 blocks): 720 tokens in 16 windows of 5 x 9, 5 new frames over a 10-frame memory,
+    8 ranks = 4 heads x 2 halves of the window rows."""
+    cfg = CONFIGS["C4"].replace(layers=2)
+    _run_group(cfg, make_weights(cfg, seed=6, variant="sensitive"), 8, ns=[5, 5, 5, 5])
