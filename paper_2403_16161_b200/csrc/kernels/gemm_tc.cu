@@ -40,7 +40,7 @@ struct GemmSmem {
   static constexpr int STG_OFF = STAGES * STAGE_BYTES;
   static constexpr int STG_BYTES = TE ? 8 * 2 * 4096 : 0;
   static constexpr int BAR_OFF = STG_OFF + STG_BYTES;
-  static constexpr int NBAR = 2 * STAGES + 4 + 8;                          // + [8] x_in tile loads
+  static constexpr int NBAR = 2 * STAGES + 4 + 16;                         // + [8 warps][2 buffers] x_in tile loads
   static constexpr int BIAS_OFF = BAR_OFF + NBAR * 8 + 16;                 // [2][BN] fp32
   static constexpr int TOTAL = BIAS_OFF + 2 * BN * 4 + 1024;              // +1024 alignment slack
 };
@@ -65,8 +65,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   uint64_t* empty = full + STAGES;
   uint64_t* tfull = empty + STAGES;     // [2] accumulator ready for the epilogue
   uint64_t* tempty = tfull + 2;         // [2] accumulator drained by the epilogue (leader's counts both CTAs)
-  uint64_t* xbar = tempty + 2;          // [8] per epilogue warp: x_in tile landed (TE, EPI_RESID)
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 8);
+  uint64_t* xbar = tempty + 2;          // [8 warps][2 staging buffers]: x_in tile landed (TE, EPI_RESID)
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(xbar + 16);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   if (threadIdx.x == 0) GTR(0);
@@ -94,7 +94,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       mbar_init(&tfull[b], 1);
       mbar_init(&tempty[b], PAIR ? 16 : 8);     // one elected arrive per epilogue warp (of both CTAs)
     }
-    for (int w = 0; w < 8; ++w) mbar_init(&xbar[w], 1);
+    for (int w = 0; w < 16; ++w) mbar_init(&xbar[w], 1);
     fence_barrier_init();
   }
   if (warp == 2) {
@@ -178,7 +178,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     float* bias_s = reinterpret_cast<float*>(smem + L::BIAS_OFF);
     uint8_t* stg = smem + L::STG_OFF + ew * 8192;
     int nchunk = 0;
-    uint32_t xphase = 0;
+    uint32_t xphase = 0;   // bit b: parity of staging buffer b's next x_in load
     int lt = 0;
     for (int st = cid; st < ntiles; st += ncl, ++lt) {
       const int acc = lt & 1;
@@ -188,6 +188,24 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         for (int i = etid; i < BN; i += 256) bs[i] = n0 + i < epi.N ? __ldg(epi.bias + n0 + i) : 0.f;
       }
       gemm_named_bar_sync(1, 256);
+      // residual epilogue: the x_in tiles of this warp's first two chunks are requested now,
+      // while the accumulator is still being computed (both staging buffers free: every
+      // earlier store has read them), so their latency overlaps the mainloop
+      const bool pre_x = TE && epi.kind == EPI_RESID;
+      if (pre_x) {
+        if (lane == 0) {
+          bulk_wait_read<0>();
+          for (int k = 0; k < 2; ++k) {
+            const int c = hc * (BN / 2) + k * 32;
+            if (c < (hc + 1) * (BN / 2) && n0 + c < epi.N) {
+              const int b = (nchunk + k) & 1;
+              mbar_arrive_expect_tx(&xbar[2 * ew + b], 4096);
+              tma_load_2d(stg + b * 4096, &tmX, &xbar[2 * ew + b], n0 + c, m0 + q * 32);
+            }
+          }
+        }
+        __syncwarp();
+      }
       mbar_wait(&tfull[acc], (lt >> 1) & 1);
       if (lt < 4 && ew == 0 && lane == 0) GTR(7 + lt);
       tc_fence_after();
@@ -199,17 +217,19 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         const bool resid = epi.kind == EPI_RESID, qkv = epi.kind == EPI_QKV;
         const int cw = (resid || epi.out_f32) ? 32 : 64;           // columns per 128-byte row
         const int sw = lane & 7;                                  // 128-byte swizzle phase of this row
+        int kc = 0;                             // chunk index within this tile
 #pragma unroll 1
-        for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += cw, ++nchunk) {
+        for (int c = hc * (BN / 2); c < (hc + 1) * (BN / 2); c += cw, ++nchunk, ++kc) {
           if (n0 + c >= epi.N) break;
-          uint8_t* buf = stg + (nchunk & 1) * 4096;
-          if (nchunk >= 2) {                    // the store that used this buffer has read it
+          const int bi = nchunk & 1;
+          uint8_t* buf = stg + bi * 4096;
+          if (nchunk >= 2 && !(pre_x && kc < 2)) {   // the store that used this buffer has read it
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
           }
-          if (resid && lane == 0) {
-            mbar_arrive_expect_tx(&xbar[ew], 4096);
-            tma_load_2d(buf, &tmX, &xbar[ew], n0 + c, m0 + q * 32);
+          if (resid && kc >= 2 && lane == 0) {  // (chunks 0, 1 were requested before the mainloop ended)
+            mbar_arrive_expect_tx(&xbar[2 * ew + bi], 4096);
+            tma_load_2d(buf, &tmX, &xbar[2 * ew + bi], n0 + c, m0 + q * 32);
           }
 #pragma unroll 1
           // QKV: a 64-column chunk lies in one of Q / K / V (D % 64 == 0); V leaves transposed
@@ -239,8 +259,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 *reinterpret_cast<bf16*>(vb + (h2 + i) * 16) = __float2bfloat16_rn(v[i]);
             } else if (resid || epi.out_f32) {
               if (resid) {
-                mbar_wait(&xbar[ew], xphase);
-                xphase ^= 1u;
+                mbar_wait(&xbar[2 * ew + bi], (xphase >> bi) & 1u);
+                xphase ^= 1u << bi;
               }
 #pragma unroll
               for (int j = 0; j < 8; ++j) {
