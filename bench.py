@@ -53,15 +53,31 @@ def gemm_flop_per_step(cfg):
 
 
 def patch_bytes_per_step(cfg):
-    """Algorithmic HBM bytes of the patch kernels of one step (bf16 features/tokens, fp32 Yp
-    and F3N hidden): split, composite and, for F3N, the fold/unfold of every block."""
+    """ALGORITHMIC HBM bytes of the patch kernels of one step (SURVEY §8(d) / §8(a) rows a1, a10,
+    a13: bf16 features, tokens, patch vectors and F3N hidden): split = read the map + write the
+    tokens; composite = read the patch vectors + write the map; F3N per block = read the hidden
+    (fold) + write the re-split hidden (unfold), the small fold map itself not counted.  C3:
+    66.6 MB per frame, 333 MB per 5-frame step."""
+    T, P, Pd = cfg.t_new, cfg.tokens, cfg.patch_dim
+    fmap = T * cfg.feat_h * cfg.feat_w * cfg.feat_c * 2
+    tok = T * P * Pd * 2
+    b = (fmap + tok) + (tok + fmap)
+    if cfg.ffn_kind == 1:
+        b += cfg.layers * 2 * (T * P * cfg.ffn_hidden * 2)
+    return float(b)
+
+
+def patch_bytes_implementation(cfg):
+    """The bytes this implementation's patch kernels move per step (the F3N hidden u and the
+    back-projection output Yp are kept fp32 for precision; the fold map read by
+    the unfold counted): reported beside the algorithmic figure."""
     T, P, Pd = cfg.t_new, cfg.tokens, cfg.patch_dim
     fmap = T * cfg.feat_h * cfg.feat_w * cfg.feat_c * 2
     b = fmap + T * P * Pd * 2                       # split: read features, write tokens
     b += T * P * Pd * 4 + fmap                      # composite: read fp32 Yp, write features
     if cfg.ffn_kind == 1:
         C = cfg.ffn_hidden // (cfg.kh * cfg.kw)
-        fold = T * cfg.feat_h * cfg.feat_w * C * 4
+        fold = T * cfg.feat_h * cfg.feat_w * C * 2
         b += cfg.layers * ((T * P * cfg.ffn_hidden * 4 + fold) + (fold + T * P * cfg.ffn_hidden * 2))
     return float(b)
 
@@ -397,7 +413,10 @@ def run_ours(args, cfg):
             "frac": gflop / (gemm_ms * 1e-3) / 1e12 / bf16_peak, "flop_per_step": gflop, "ms_per_step": gemm_ms},
         "patch kernels (soft split, F3N fold/unfold, soft composite; eager launches, CUDA events)": {
             "bound": "hbm", "achieved": pbytes / (patch_ms * 1e-3) / 1e9, "peak": hbm_peak, "unit": "GB/s",
-            "frac": pbytes / (patch_ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": pbytes, "ms_per_step": patch_ms}}
+            "frac": pbytes / (patch_ms * 1e-3) / 1e9 / hbm_peak, "bytes_per_step": pbytes,
+            "bytes": "algorithmic (SURVEY §8(d): bf16 intermediates)", "ms_per_step": patch_ms,
+            "implementation_bytes_per_step": patch_bytes_implementation(cfg),
+            "implementation_frac": patch_bytes_implementation(cfg) / (patch_ms * 1e-3) / 1e9 / hbm_peak}}
     line["deterministic"] = deterministic
     if os.environ.get("VI_PROFILE_MODE") == "2":
         line["profile_ms_per_step"] = {k: v[0] / args.steps for k, v in prof.items()}

@@ -166,7 +166,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   // o_final committed, 4 last epilogue start, 5 owner flags seen, 6 exit, 7 segments,
   // 8..11 MMA warp: each segment's o_final commit (first 4), 12 continuation piece
   // published, 13 owner's merge done
-  long long* const ct = (SK2_TRACE && a.cta_trace) ? a.cta_trace + (size_t)cta * 16 : nullptr;
+  long long* const ct = (SK2_TRACE && a.cta_trace) ? a.cta_trace + (size_t)cta * 24 : nullptr;
   if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
 
   if (warp == 16 && lane == 0) {
@@ -289,6 +289,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             while (ld_acquire_gpu(a.sflag + c) == 0) __nanosleep(32);
 #endif
             fence_proxy_async_global();                // the piece is read through the async proxy
+            if (ct && i + L::CPP >= items) ct[14] = (long long)globaltimer();   // last piece's flag seen
           }
           __syncwarp();
           for (int hf = 0; hf < 2; ++hf) {
@@ -595,6 +596,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         for (int i = 0; i < items; ++i) {
           const int cc = i % L::CPP, b = i % L::NBH;
           mbar_wait(&merge_full[hf * 3 + b], (i / L::NBH) & 1);
+          if (ct && warp == 0 && lane == 0 && i + L::CPP >= items && cc == 0)
+            ct[15] = (long long)globaltimer();          // last piece's first chunk landed
           if (cc == 0) {                               // a new piece: its weight, rescale A
             const float lk = reinterpret_cast<const float*>(smem + L::LSE_OFF + (hf * 2 + ((i / L::CPP) & 1)) * 1024)[r256];
             const float mn = fmaxf(m, lk);

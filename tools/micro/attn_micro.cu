@@ -20,8 +20,11 @@
 #ifndef ATTN_SRC
 #define ATTN_SRC "../../paper_2403_16161_b200/csrc/kernels/attn_sk2.cu"
 #endif
+#ifndef SETUP_SRC
+#define SETUP_SRC "../../paper_2403_16161_b200/csrc/kernels/setup.cu"
+#endif
 #include ATTN_SRC
-#include "../../paper_2403_16161_b200/csrc/kernels/setup.cu"
+#include SETUP_SRC
 using namespace vi;
 
 typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -75,8 +78,13 @@ int main(int argc, char** argv) {
   int nsm = 0;
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, 0);
   CUtensorMap tq = tmap(q, D, Nq, 64, 128), tk = tmap(k, D, SP, 64, 128), tv = tmap(vt, vt_ld, D, 64, HD);
+  CUtensorMap to = tmap(o, D, Nq, 64, 32);     // output rows (TMA-store epilogue)
   auto launch = [&](const AttnTC& aa, int gr, cudaStream_t s_) {
+#ifdef VI_SK2_HAS_OUT_MAP
+    return launch_attn_sk2(tq, tk, tv, aa, gr, s_, &to);
+#else
     return launch_attn_sk2(tq, tk, tv, aa, gr, s_);
+#endif
   };
   AttnTC a;
   memset(&a, 0, sizeof(a));
@@ -85,6 +93,9 @@ int main(int argc, char** argv) {
   a.segs.n = 1; a.segs.row0[0] = 0; a.segs.lead[0] = 0; a.segs.len[0] = SP; a.segs.tile0[0] = 0;
   a.segs.tile0[1] = (SP + 127) / 128;
   a.o = reinterpret_cast<bf16*>(o); a.o_ld = D; a.o_hs = HD; a.q_row0 = 0;
+#ifdef VI_SK2_HAS_OUT_MAP
+  a.o_tma = (argc > 5 && argv[5][0] == 'w') ? 0 : 1;
+#endif
   a.npairs = (Nq + 255) / 256;
   a.units = a.npairs * H;
   if (win) {
@@ -126,19 +137,19 @@ int main(int argc, char** argv) {
          cudaGetErrorString(err));
   if (getenv("CTA_TRACE")) {   // per-CTA globaltimer stamps of one launch
     long long* ctb;
-    cudaMalloc(&ctb, (size_t)grid * 16 * 8);
-    cudaMemset(ctb, 0, (size_t)grid * 16 * 8);
+    cudaMalloc(&ctb, (size_t)grid * 24 * 8);
+    cudaMemset(ctb, 0, (size_t)grid * 24 * 8);
     a.cta_trace = ctb;
     launch(a, grid, st);
     cudaStreamSynchronize(st);
     a.cta_trace = nullptr;
-    std::vector<long long> h((size_t)grid * 16);
+    std::vector<long long> h((size_t)grid * 24);
     cudaMemcpy(h.data(), ctb, h.size() * 8, cudaMemcpyDeviceToHost);
     long long t0 = LLONG_MAX;
-    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 16]);
+    for (int c = 0; c < grid; ++c) t0 = std::min(t0, h[c * 24]);
     printf("cta: entry setup firstQK lastOfinal lastEpi ownerFlags exit nseg | segment o_final (ns from first entry)\n");
     for (int c = 0; c < grid; ++c) {
-      const long long* e = &h[c * 16];
+      const long long* e = &h[c * 24];
       printf("%3d:", c);
       for (int i = 0; i < 7; ++i) printf(" %6lld", e[i] ? e[i] - t0 : -1);
       printf(" %lld |", e[7]);
