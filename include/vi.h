@@ -286,7 +286,8 @@ void* vi_stream(const vi_ctx* ctx);
 
 /* Device-side timing of the context's own kernels with CUDA events on its stream.
  * mode 0 = off, 1 = memory attention only (kernel self-timing, graph-safe),
- * 2 = every category (CUDA events; eager launches), 3 = attention + GEMMs (self-timing).  vi_profile_read waits for the stream, then returns per category
+ * 2 = every category (CUDA events; eager launches), 3 = attention, GEMMs and the patch
+ * kernels of the fixed 7x7 / stride-3 geometry (kernel self-timing inside the step graph).  vi_profile_read waits for the stream, then returns per category
  * the summed milliseconds and the number of timed launches and resets the counters.
  * Categories: VI_PROF_ATTN, VI_PROF_GEMM (all tensor-core / SIMT GEMMs),
  * VI_PROF_PATCH (soft split / composite / F3N fold-unfold), VI_PROF_ROW (LN, casts). */

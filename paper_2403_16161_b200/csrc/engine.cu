@@ -595,7 +595,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     c->lse = (float*)A((size_t)kMaxSplit * c->H * std::max(rows, (size_t)c->QR) * 4);
   }
   c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);
-  c->attn_timing = (unsigned long long*)A(2 * sizeof(KernelTiming));   // [0] attention, [1] GEMMs
+  c->attn_timing = (unsigned long long*)A(3 * sizeof(KernelTiming));   // [0] attention, [1] GEMMs, [2] patch
   c->num_sms = prop.multiProcessorCount;
   if (c->bf16) {
     c->sk_part = (float*)A((size_t)c->num_sms * 256 * c->hd * 4);
@@ -626,9 +626,9 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     return VI_E_CUDA;
   }
   {
-    KernelTiming kt[2];
+    KernelTiming kt[3];
     std::memset(kt, 0, sizeof(kt));
-    kt[0].tmin = kt[1].tmin = ~0ull;
+    kt[0].tmin = kt[1].tmin = kt[2].tmin = ~0ull;
     if (cudaMemcpy(c->attn_timing, kt, sizeof(kt), cudaMemcpyHostToDevice) != cudaSuccess) {
       delete c;
       return VI_E_CUDA;
@@ -933,6 +933,10 @@ extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refin
 
 // ------------------------------------------------------------------------------ compute
 
+// the patch kernels' self-timing slot (vi_profile mode 3) or NULL
+static unsigned long long* patch_timing(const vi_ctx* c) {
+  return c->prof_mode == 3 ? c->attn_timing + 2 * (sizeof(KernelTiming) / sizeof(unsigned long long)) : nullptr;
+}
 static Epi epi_base(const vi_ctx* c, int kind, int M, int N, const float* bias) {
   Epi e;
   std::memset(&e, 0, sizeof(e));
@@ -950,7 +954,7 @@ extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out
   if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_split: weights not set");
   const int dt = c->bf16 ? 0 : 1;
   void* tok = project ? c->tokens : out;
-  PLAUNCH(VI_PROF_PATCH, launch_unfold(feat, tok, n, c->g, dt, c->stream), "unfold");
+  PLAUNCH(VI_PROF_PATCH, launch_unfold(feat, tok, n, c->g, dt, c->stream, patch_timing(c)), "unfold");
   if (project) {
     const int M = n * c->P;
     Epi e = epi_base(c, EPI_STORE, M, c->D, c->b_embed);
@@ -1187,8 +1191,8 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
             "ffn1 gemm");
   if (f3n) {
     // g = GELU(unfold(fold(u))) = unfold(GELU(fold(u))): GELU once per folded cell
-    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, dt, n, c->gf, true, c->stream), "f3n fold");
-    PLAUNCH(VI_PROF_PATCH, launch_unfold(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream), "f3n unfold");
+    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, dt, n, c->gf, true, c->stream, patch_timing(c)), "f3n fold");
+    PLAUNCH(VI_PROF_PATCH, launch_unfold(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream, patch_timing(c)), "f3n unfold");
   }
   // a11: FFN2 + residual
   Epi e2 = epi_base(c, EPI_RESID, M, D, c->b_2 + (size_t)l * D);
@@ -1318,7 +1322,9 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
     }
     tok = c->bf16 ? c->yp32 : c->tokens;
   }
-  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, (project && c->bf16) ? 1 : dt, feat, dt, n, c->g, false, c->stream), "fold");
+  PLAUNCH(VI_PROF_PATCH, launch_fold(tok, (project && c->bf16) ? 1 : dt, feat, dt, n, c->g, false, c->stream,
+                                     patch_timing(c)),
+          "fold");
   return VI_OK;
 }
 
@@ -1510,15 +1516,17 @@ extern "C" vi_status vi_profile_read(vi_ctx* c, double* ms, int64_t* launches) {
   CK(cudaStreamSynchronize(c->stream), "profile sync");
   double acc[VI_PROF_N] = {0, 0, 0, 0};
   int64_t cnt[VI_PROF_N] = {0, 0, 0, 0};
-  {  // kernels' self-timing (mode 1; graph-safe): [0] attention, [1] GEMMs
-    KernelTiming kt[2];
+  {  // kernels' self-timing (modes 1, 3; graph-safe): [0] attention, [1] GEMMs, [2] patch kernels
+    KernelTiming kt[3];
     CK(cudaMemcpy(kt, c->attn_timing, sizeof(kt), cudaMemcpyDeviceToHost), "profile read");
     acc[VI_PROF_ATTN] += double(kt[0].total_ns) * 1e-6;
     cnt[VI_PROF_ATTN] += int64_t(kt[0].launches);
     acc[VI_PROF_GEMM] += double(kt[1].total_ns) * 1e-6;
     cnt[VI_PROF_GEMM] += int64_t(kt[1].launches);
+    acc[VI_PROF_PATCH] += double(kt[2].total_ns) * 1e-6;
+    cnt[VI_PROF_PATCH] += int64_t(kt[2].launches);
     std::memset(kt, 0, sizeof(kt));
-    kt[0].tmin = kt[1].tmin = ~0ull;
+    kt[0].tmin = kt[1].tmin = kt[2].tmin = ~0ull;
     CK(cudaMemcpy(c->attn_timing, kt, sizeof(kt), cudaMemcpyHostToDevice), "profile reset");
   }
   for (auto& r : c->prof_recs) {

@@ -41,11 +41,13 @@ struct Geom {
 
 // ---- patch gather kernels (HBM-bound) -------------------
 // soft split: in [n][H][W][C] -> out [n][P][kh*kw*C]; dtype 0 = bf16, 1 = fp32.
-cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st);
+// timing (optional): KernelTiming the launch folds its first-CTA-start / last-CTA-end into (profile mode 3)
+cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st,
+                          unsigned long long* timing = nullptr);
 // fold with cover-count division: in [n][P][kh*kw*C] (in_dtype) -> out [n][H][W][C] (out_dtype),
 // optionally GELU of the folded value (Fusion-FFN).  Requires ceil(k/s) <= 3 per dimension.
 cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g, bool gelu,
-                        cudaStream_t st);
+                        cudaStream_t st, unsigned long long* timing = nullptr);
 
 // ---- row kernels -------------------------------------------------------------------
 // LayerNorm over D (eps 1e-5), fp32 in, out dtype 0 bf16 / 1 fp32.

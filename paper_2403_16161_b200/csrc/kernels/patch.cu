@@ -150,9 +150,10 @@ __global__ void __launch_bounds__(256) fold_kernel(const Tin* __restrict__ in, T
 // Same results as the generic kernels above; all index divisions are by constants.
 template <typename T, int VEC, int CV, int KH, int KW>
 __global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g,
-                                                           int ntok) {
+                                                           int ntok, unsigned long long* timing) {
   griddep_wait();
   griddep_launch();
+  if (timing && threadIdx.x == 0) time_begin(timing);
   constexpr int KK = KH * KW, PER = KK * CV;
   const int P = g.oh * g.ow;
   const int total = ntok * PER;
@@ -174,13 +175,18 @@ __global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__
         *reinterpret_cast<float4*>(d) = __ldg(reinterpret_cast<const float4*>(src));
     }
   }
+  if (timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) time_end(timing, gridDim.x);
+  }
 }
 
 template <typename Tin, typename Tout, int VEC, int CV, int KH, int KW, int SH, int SW, bool GELU>
 __global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g,
-                                                         int ncell) {
+                                                         int ncell, unsigned long long* timing) {
   griddep_wait();
   griddep_launch();
+  if (timing && threadIdx.x == 0) time_begin(timing);
   constexpr int KK = KH * KW, C = CV * VEC;
   constexpr int MAXC = (KH + SH - 1) / SH > (KW + SW - 1) / SW ? (KH + SH - 1) / SH : (KW + SW - 1) / SW;
   const int P = g.oh * g.ow;
@@ -228,6 +234,10 @@ __global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__
     }
     Vec<Tout, VEC>::st(out + (size_t)cell * C + cv * VEC, acc);
   }
+  if (timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) time_end(timing, gridDim.x);
+  }
 }
 
 template <> struct Vec<bf16, 4> {
@@ -247,14 +257,15 @@ static int grid_cap(long long total, int per_block = 256) {
   return int(b < 148 * 32 ? (b ? b : 1) : 148 * 32);
 }
 
-cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st) {
+cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st,
+                          unsigned long long* timing) {
   const int ntok = n * g.oh * g.ow;
   if (g.kh == 7 && g.kw == 7) {
     const int CV = g.C / (dtype == 0 ? 8 : 4);
     const long long total = (long long)ntok * 49 * CV;
 #define UF(T, V, CVV)                                                                                     \
     if (CV == CVV) {                                                                                      \
-      pdl_launch(unfold_fixed_kernel<T, V, CVV, 7, 7>, dim3(grid_cap(total)), dim3(256), 0, st, (const T*)in, (T*)out, g, ntok); \
+      pdl_launch(unfold_fixed_kernel<T, V, CVV, 7, 7>, dim3(grid_cap(total)), dim3(256), 0, st, (const T*)in, (T*)out, g, ntok, timing); \
       return cudaGetLastError();                                                                          \
     }
     if (dtype == 0) { UF(bf16, 8, 16) UF(bf16, 8, 5) UF(bf16, 8, 32) }
@@ -272,7 +283,7 @@ cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int d
 }
 
 cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, int n, const Geom& g, bool gelu,
-                        cudaStream_t st) {
+                        cudaStream_t st, unsigned long long* timing) {
   const int blocks = n * g.H;
   if (g.kh == 7 && g.kw == 7 && g.sh == 3 && g.sw == 3) {
     const int ncell = n * g.H * g.W;
@@ -280,9 +291,9 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
     if (g.C == CVV * V) {                                                                                     \
       const long long total = (long long)ncell * CVV;                                                        \
       if (gelu)                                                                                               \
-        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell); \
+        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell, timing); \
       else                                                                                                    \
-        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell); \
+        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell, timing); \
       return cudaGetLastError();                                                                              \
     }
     if (in_dtype == 1 && out_dtype == 0) { FF(float, bf16, 4, 10) FF(float, bf16, 4, 32) }
