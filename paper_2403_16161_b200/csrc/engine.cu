@@ -193,6 +193,7 @@ struct vi_ctx {
   int prof_mode = 0;
   unsigned long long* attn_timing = nullptr;   // KernelTiming (device), used in profile mode 1
   int num_sms = 148;
+  float* skws = nullptr;   // split-K GEMM partials: <= num_sms work items of 128 x 128 fp32
   float *sk_part = nullptr, *sk_lse = nullptr;  // stream-K partial slots [num_sms][256][hd], [num_sms][256]
   int* sk_flag = nullptr;                       // [num_sms], zero between launches
   // CUDA graphs of whole steps (vi_run_step), keyed by everything baked into the launches
@@ -291,6 +292,12 @@ static int sk_unit_cost() {
   // 56 -> 81.7, 58-60 -> 81.5, 62 -> 83.0, 64 -> 83.0 (partition-dependent steps)
   const int b = e ? atoi(e) : 56;
   return b < 0 ? 0 : (b > 4096 ? 4096 : b);
+}
+// VI_SPLITK=0: no split-K for the small-M residual GEMMs (A/B measurements; read per launch
+// so a test can compare both paths in one process)
+static bool splitk_enabled() {
+  const char* e = getenv("VI_SPLITK");
+  return !(e && e[0] == '0');
 }
 static void debug_wait(vi_ctx* c, const char* where) {
   for (int i = 0; i < 20000; ++i) {
@@ -601,6 +608,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     c->sk_part = (float*)A((size_t)c->num_sms * 256 * c->hd * 4);
     c->sk_lse = (float*)A((size_t)c->num_sms * 256 * 4);
     c->sk_flag = (int*)A((size_t)c->num_sms * 4);
+    c->skws = (float*)A((size_t)c->num_sms * 128 * 128 * 4);
   }
   if (!ok) {
     delete c;
@@ -946,6 +954,43 @@ static Epi epi_base(const vi_ctx* c, int kind, int M, int N, const float* bias) 
   return e;
 }
 
+// Split-K plan for a residual GEMM [M x N] += A[M x K] W^T with single-CTA 128 x 128 tiles:
+// when the output has at most num_sms / 2 tiles (one frame per chunk, the paper's T = 1 mode)
+// most SMs would idle, so every tile's k-blocks are cut into ks consecutive ranges, one work
+// item each (<= num_sms items: the workspace holds num_sms 128 x 128 fp32 partials).
+// Returns ks (0 = do not split).
+static int splitk_plan(const vi_ctx* c, int M, int N, int K) {
+  if (!splitk_enabled() || !c->bf16 || !c->skws || N % 128) return 0;
+  const int out = (M + 127) / 128 * (N / 128), nk = (K + 63) / 64;
+  if (out * 2 > c->num_sms) return 0;
+  int ks = std::min(std::min(c->num_sms / out, 8), nk);
+  if (ks < 2) return 0;
+  const int kper = (nk + ks - 1) / ks;
+  ks = (nk + kper - 1) / kper;   // every split non-empty
+  return ks < 2 ? 0 : ks;
+}
+
+// x_out = x_in + bias + A W^T through ks split-K partials and the deterministic reduction
+// (which also writes LayerNorm(x_out) to h when ln_g != NULL)
+static vi_status splitk_resid(vi_ctx* c, int ks, const CUtensorMap& amap, const CUtensorMap& wmap, int brow0, int M,
+                              int N, int K, int a_hs, int a_kpb, const float* bias, const float* x_in, float* x_out,
+                              const float* ln_g, const float* ln_b, void* h, const char* where) {
+  const int kpad = (M + 127) / 128 * 128;
+  Epi e = epi_base(c, EPI_STORE, M, N, nullptr);
+  e.out = c->skws; e.ldo = N; e.out_f32 = 1;
+  e.ksplit = ks; e.kpad_rows = kpad;
+  e.a_hs = a_hs; e.a_kpb = a_kpb;
+  CUtensorMap tws;
+  if (!make_tmap_out(&tws, c->skws, true, N, (uint64_t)ks * kpad))
+    return c->fail(VI_E_CUDA, std::string(where) + ": split-K workspace map");
+  PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(amap, wmap, brow0, M, N, K, 128, e, c->stream, 0, &tws, nullptr), where);
+  PLAUNCH(VI_PROF_GEMM,
+          launch_splitk_resid(c->skws, ks, (size_t)kpad * N, bias, x_in, x_out, ln_g, ln_b, h, c->bf16 ? 0 : 1, M, N,
+                              c->stream, e.timing),
+          where);
+  return VI_OK;
+}
+
 extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out, int project) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
@@ -1168,7 +1213,14 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   }
   CUtensorMap tx_in, tx_out;
   const bool te = c->bf16 && make_tmap_out(&tx_in, x_in, true, D, M) && make_tmap_out(&tx_out, x_out, true, D, M);
-  if (c->bf16)
+  // small M: split-K partials, then one kernel for reduction + residual + LN2 (a7 + a8)
+  const int ks_o = te ? splitk_plan(c, M, D, D) : 0;
+  if (ks_o) {
+    const vi_status r = splitk_resid(c, ks_o, (c->sharded && !c->win_split) ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D,
+                                     D, eo.a_hs, eo.a_kpb, eo.bias, x_in, x_out, c->ln2_g + (size_t)l * D,
+                                     c->ln2_b + (size_t)l * D, c->h, "o gemm (split-K)");
+    if (r != VI_OK) return r;
+  } else if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc((c->sharded && !c->win_split) ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D, D,
                                          c->bn_o, eo, c->stream, 0,
                                          te ? &tx_out : nullptr, te ? &tx_in : nullptr),
@@ -1177,7 +1229,8 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
     PLAUNCH(VI_PROF_GEMM, launch_gemm_simt_f32((const float*)c->o, (const float*)c->w_o + (size_t)l * D * D, M, D, D, eo, c->stream),
             "o gemm");
   // a8: LN2
-  PLAUNCH(VI_PROF_ROW, launch_layernorm(x_out, c->ln2_g + (size_t)l * D, c->ln2_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln2");
+  if (!ks_o)
+    PLAUNCH(VI_PROF_ROW, launch_layernorm(x_out, c->ln2_g + (size_t)l * D, c->ln2_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln2");
   // a9 / a10: FFN1 (+ F3N fold/unfold) + GELU
   const bool f3n = c->cfg.ffn_kind == VI_FFN_F3N;
   Epi e1 = epi_base(c, f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
@@ -1199,7 +1252,12 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   e2.x_in = x_out; e2.x_out = x_out;
   // FFN2 (K = F = 1960) on CTA-pair tiles 256 x 128 (tools/micro/gemm_micro: 16.9 vs 18.3 us)
   const bool pair2 = te;
-  if (c->bf16)
+  const int ks_2 = te ? splitk_plan(c, M, D, F) : 0;
+  if (ks_2) {
+    const vi_status r = splitk_resid(c, ks_2, c->tm_g, c->tm_w2, l * D, M, D, F, 0, 0, e2.bias, x_out, x_out, nullptr,
+                                     nullptr, nullptr, "ffn2 gemm (split-K)");
+    if (r != VI_OK) return r;
+  } else if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, pair2 ? c->tm_w2_pair : c->tm_w2, l * D, M, D, F, pair2 ? 128 : c->bn_2, e2,
                                          c->stream, pair2 ? 1 : 0, te ? &tx_out : nullptr, te ? &tx_out : nullptr),
             "ffn2 gemm");

@@ -162,6 +162,10 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // the set-up above overlaps the previous kernel's tail (programmatic dependent launch); the
+  // combine kernel may launch now (it waits for this grid's completion before reading)
+  griddep_wait();
+  griddep_launch();
   if (threadIdx.x == 0) time_begin(a.timing);
 
   if (warp == 8) {
@@ -401,7 +405,8 @@ static cudaError_t launch2_hd(const CUtensorMap& tq, const CUtensorMap& tk, cons
   cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(attn_tc2_kernel<HD>), L::TOTAL);
   if (e != cudaSuccess) return e;
   dim3 grid(a.win_n ? a.win_n * a.win_npw : (a.Nq + 255) / 256, a.H, a.nsplit);
-  attn_tc2_kernel<HD><<<grid, 384, L::TOTAL, st>>>(tq, tk, tvt, a);
+  e = pdl_launch(attn_tc2_kernel<HD>, grid, dim3(384), L::TOTAL, st, tq, tk, tvt, a);
+  if (e != cudaSuccess) return e;
   return cudaGetLastError();
 }
 
@@ -412,9 +417,14 @@ cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const 
   return cudaErrorInvalidValue;
 }
 
-// Merge KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), fixed order.
-__global__ void attn_combine_kernel(const AttnTC a) {
+// Merge KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), z in fixed order.
+// Thread = (query row, head, 4 columns); the split's lse values and partial rows are all
+// requested before the sums (kMaxZ <= 16 splits), so a thread waits for one round of loads.
+constexpr int kMaxZ = 16;
+__global__ void __launch_bounds__(256) attn_combine_kernel(const AttnTC a) {
+  griddep_wait();
   if (threadIdx.x == 0) time_begin(a.timing);
+  griddep_launch();
   const int hd4 = a.hd / 4;
   const size_t total = (size_t)a.Nq * a.H * hd4;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
@@ -424,31 +434,41 @@ __global__ void attn_combine_kernel(const AttnTC a) {
     const int q = int(r / a.H);             // KV-split partial row (windows: window-major)
     const int orow = a.win_n ? win_out_row(a, a.win0 + q / a.win_qstride, q % a.win_qstride) : q;
     if (orow < 0) continue;
+    float lz[kMaxZ];
+    float4 v[kMaxZ];
+#pragma unroll
+    for (int z = 0; z < kMaxZ; ++z) {
+      lz[z] = z < a.nsplit ? a.lse[((size_t)z * a.H + h) * a.Nq + q] : -INFINITY;
+      v[z] = z < a.nsplit ? *reinterpret_cast<const float4*>(a.opart + ((size_t)z * a.Nq + q) * a.D + h * a.hd + c4 * 4)
+                          : make_float4(0.f, 0.f, 0.f, 0.f);
+    }
     float mx = -INFINITY;
-    for (int z = 0; z < a.nsplit; ++z) mx = fmaxf(mx, a.lse[((size_t)z * a.H + h) * a.Nq + q]);
+#pragma unroll
+    for (int z = 0; z < kMaxZ; ++z) mx = fmaxf(mx, lz[z]);
     float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
-    for (int z = 0; z < a.nsplit; ++z) {
-      const float lz = a.lse[((size_t)z * a.H + h) * a.Nq + q];
-      if (lz == -INFINITY) continue;
-      const float w = exp2f(lz - mx);
+#pragma unroll
+    for (int z = 0; z < kMaxZ; ++z) {
+      if (lz[z] == -INFINITY) continue;
+      const float w = exp2f(lz[z] - mx);
       wsum += w;
-      const float4 v = *reinterpret_cast<const float4*>(a.opart + ((size_t)z * a.Nq + q) * a.D + h * a.hd + c4 * 4);
-      acc[0] += w * v.x; acc[1] += w * v.y; acc[2] += w * v.z; acc[3] += w * v.w;
+      acc[0] += w * v[z].x; acc[1] += w * v[z].y; acc[2] += w * v[z].z; acc[3] += w * v[z].w;
     }
     const float inv = 1.f / wsum;
     uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
     *dst = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   }
-  __syncthreads();
-  if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
+  if (a.timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
+  }
 }
 
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st) {
+  if (a.nsplit > kMaxZ) return cudaErrorInvalidValue;
   const size_t total = (size_t)a.Nq * a.H * (a.hd / 4);
   size_t blocks = (total + 255) / 256;
   if (blocks > 148 * 8) blocks = 148 * 8;
-  attn_combine_kernel<<<unsigned(blocks ? blocks : 1), 256, 0, st>>>(a);
-  return cudaGetLastError();
+  return pdl_launch(attn_combine_kernel, dim3(unsigned(blocks ? blocks : 1)), dim3(256), 0, st, a);
 }
 
 }  // namespace vi

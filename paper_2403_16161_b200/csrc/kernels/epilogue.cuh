@@ -43,6 +43,11 @@ struct Epi {
   // EPI_QKV through the TMA-store epilogue: rows of this layer's block in the K map (l * S * P)
   // and in the Vt map (l * D)
   int qkv_krow0, qkv_vrow0;
+  // split-K (small M: too few output tiles for the SMs): ksplit > 1 runs every tile as ksplit
+  // work items over consecutive k-block ranges, each storing its raw fp32 partial (EPI_STORE,
+  // out_f32, no bias) at rows split * kpad_rows + m of the workspace; splitk_reduce_kernel then
+  // sums the partials in split order and applies the real epilogue (deterministic)
+  int ksplit, kpad_rows;
 };
 
 // QKV destinations of row m (token p of chunk frame t): Q row and memory (K row / Vt column)

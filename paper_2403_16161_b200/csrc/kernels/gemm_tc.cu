@@ -74,8 +74,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   const bool leader = rank == 0;
   const int cid = PAIR ? blockIdx.x / 2 : blockIdx.x, ncl = PAIR ? gridDim.x / 2 : gridDim.x;
   const int tiles_m = (epi.M + TM - 1) / TM, tiles_n = (epi.N + BN - 1) / BN;
-  const int ntiles = tiles_m * tiles_n;
-  const int nk = (K + 63) / 64;
+  const int ks = epi.ksplit > 1 ? epi.ksplit : 1;
+  const int nout = tiles_m * tiles_n;          // output tiles
+  const int ntiles = nout * ks;                // work items: (split, tile), tile fastest
+  const int nk_all = (K + 63) / 64;
+  const int kper = (nk_all + ks - 1) / ks;     // k-blocks per split
   constexpr uint32_t TMEM_COLS = 2 * BN < 32 ? 32 : 2 * BN;
 
   if (warp == 0 && lane == 0) {
@@ -106,7 +109,26 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
   else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  // everything above overlaps the previous kernel's tail (programmatic dependent launch)
+  // B is always a weight matrix (constant during a step): the producer requests the first
+  // work item's first stages of B before waiting for the previous kernel, so those loads and
+  // everything above overlap its tail (programmatic dependent launch)
+  int npre = 0;
+  if (warp == 0 && lane == 0 && cid < ntiles) {
+    const int ot = cid % nout, kb0 = (cid / nout) * kper;
+    const int kb1 = kb0 + kper < nk_all ? kb0 + kper : nk_all;
+    const int bn0 = brow0 + (ot / tiles_m) * BN + (PAIR ? rank * (BN / 2) : 0);
+    npre = kb1 - kb0 < STAGES ? kb1 - kb0 : STAGES;
+    for (int j = 0; j < npre; ++j) {
+      uint8_t* sa = smem + j * L::STAGE_BYTES;
+      if (PAIR) {
+        if (leader) mbar_arrive_expect_tx(&full[j], 2 * L::STAGE_BYTES);   // both CTAs' A and B bytes
+        tma_load_2d_pair(sa + L::A_BYTES, &tmB, &full[j], (kb0 + j) * 64, bn0);
+      } else {
+        mbar_arrive_expect_tx(&full[j], L::STAGE_BYTES);
+        tma_load_2d(sa + L::A_BYTES, &tmB, &full[j], (kb0 + j) * 64, bn0);
+      }
+    }
+  }
   griddep_wait();
   griddep_launch();
   if (threadIdx.x == 0) GTR(1);
@@ -116,9 +138,11 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     if (lane == 0) {
       int it = 0;                               // global k-block counter (ring position)
       for (int st = cid; st < ntiles; st += ncl) {
-        const int m0 = (st % tiles_m) * TM + rank * 128, n0 = (st / tiles_m) * BN;
+        const int ot = st % nout, kb0 = (st / nout) * kper;
+        const int kb1 = kb0 + kper < nk_all ? kb0 + kper : nk_all;
+        const int m0 = (ot % tiles_m) * TM + rank * 128, n0 = (ot / tiles_m) * BN;
         const int bn0 = brow0 + n0 + (PAIR ? rank * (BN / 2) : 0);
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) & 1) ^ 1);
           uint8_t* sa = smem + s * L::STAGE_BYTES;
@@ -128,7 +152,10 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             ak = (kb - hh * epi.a_kpb) * 64;
             am = hh * epi.a_hs + m0;
           }
-          if (PAIR) {
+          if (it < npre) {            // B of this stage was requested before the wait
+            if (PAIR) tma_load_2d_pair(sa, &tmA, &full[s], ak, am);
+            else tma_load_2d(sa, &tmA, &full[s], ak, am);
+          } else if (PAIR) {
             if (leader) mbar_arrive_expect_tx(&full[s], 2 * L::STAGE_BYTES);   // both CTAs' bytes
             tma_load_2d_pair(sa, &tmA, &full[s], ak, am);
             tma_load_2d_pair(sa + L::A_BYTES, &tmB, &full[s], kb * 64, bn0);
@@ -146,10 +173,12 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
       int it = 0, lt = 0;
       for (int st = cid; st < ntiles; st += ncl, ++lt) {
         const int acc = lt & 1;
+        const int kb0 = (st / nout) * kper;
+        const int kb1 = kb0 + kper < nk_all ? kb0 + kper : nk_all;
         if (lt >= 2) mbar_wait(&tempty[acc], ((lt >> 1) & 1) ^ 1);
         tc_fence_after();
         const uint32_t d = tmem + acc * BN;
-        for (int kb = 0; kb < nk; ++kb, ++it) {
+        for (int kb = kb0; kb < kb1; ++kb, ++it) {
           const int s = it % STAGES;
           mbar_wait(&full[s], (it / STAGES) & 1);
           if (it == 0) GTR(2);
@@ -159,9 +188,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
 #pragma unroll
           for (int k = 0; k < 4; ++k) {
             if (PAIR)
-              umma_bf16_ss_pair(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
+              umma_bf16_ss_pair(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb != kb0) || k);
             else
-              umma_bf16_ss(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb | k) != 0);
+              umma_bf16_ss(d, sdesc_k_sw128(a + k * 32), sdesc_k_sw128(b + k * 32), idesc, (kb != kb0) || k);
           }
           if (PAIR) umma_commit_pair(&empty[s]);    // the stage is free in both CTAs
           else umma_commit(&empty[s]);
@@ -182,7 +211,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
     int lt = 0;
     for (int st = cid; st < ntiles; st += ncl, ++lt) {
       const int acc = lt & 1;
-      const int m0 = (st % tiles_m) * TM + rank * 128, n0 = (st / tiles_m) * BN;
+      const int ot = st % nout;
+      const int m0 = (ot % tiles_m) * TM + rank * 128, n0 = (ot / tiles_m) * BN;
+      const int srow0 = (st / nout) * epi.kpad_rows;   // split-K: this split's workspace rows
       float* bs = bias_s + acc * BN;
       if (epi.bias) {
         for (int i = etid; i < BN; i += 256) bs[i] = n0 + i < epi.N ? __ldg(epi.bias + n0 + i) : 0.f;
@@ -284,7 +315,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           __syncwarp();
           if (lane == 0) {
             if (region == 0) {
-              tma_store_2d(&tmO, buf, n0 + c, m0 + q * 32);
+              tma_store_2d(&tmO, buf, n0 + c, srow0 + m0 + q * 32);
             } else {
               // K rows / Vt columns of the frame's memory slot, 8 tokens at a time (P % 8 == 0:
               // a group never straddles two frames); rows past the chunk are not stored
@@ -352,7 +383,7 @@ static cudaError_t launch_cfg(const CUtensorMap& a, const CUtensorMap& b, int br
   cudaError_t err = ensure_kernel_setup(reinterpret_cast<const void*>(kfn), L::TOTAL, CS, 384, &max_clusters);
   if (err != cudaSuccess) return err;
   const int TM = PAIR ? 256 : 128;
-  const int ntiles = ((M + TM - 1) / TM) * ((N + BN - 1) / BN);
+  const int ntiles = ((M + TM - 1) / TM) * ((N + BN - 1) / BN) * (e.ksplit > 1 ? e.ksplit : 1);
   const int ncl = ntiles < max_clusters ? ntiles : max_clusters;
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(ncl * CS);
@@ -378,6 +409,12 @@ cudaError_t launch_gemm_tc(const CUtensorMap& a, const CUtensorMap& b, int brow0
     if (e.kind == EPI_NONE) return cudaErrorInvalidValue;
     if ((e.kind == EPI_RESID || e.kind == EPI_QKV) && !tmx) return cudaErrorInvalidValue;
     if (e.kind == EPI_QKV && (!tmv || e.out_f32 || e.win_pad || e.P % 8 || e.D % 64)) return cudaErrorInvalidValue;
+    if (e.ksplit > 1) {   // split-K partials: raw fp32 stores, every split non-empty, whole tiles per split
+      const int TM = pair ? 256 : 128, nk = (K + 63) / 64, kper = (nk + e.ksplit - 1) / e.ksplit;
+      if (e.kind != EPI_STORE || !e.out_f32 || e.bias || e.pos || e.win_pad || (e.ksplit - 1) * kper >= nk ||
+          e.kpad_rows < (M + TM - 1) / TM * TM)
+        return cudaErrorInvalidValue;
+    }
     if (pair) {
       switch (bn) {
         case 128: return launch_cfg<128, 6, true, true>(a, b, brow0, M, N, K, e, st, tmo, tmx, tmv);

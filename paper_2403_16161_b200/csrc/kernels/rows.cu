@@ -52,23 +52,15 @@ __global__ void layernorm_kernel(const float* __restrict__ x, const float* __res
 
 // Vectorised variant for D % 128 == 0 (D <= 1024): lane l owns float4 columns l, l+32, ...
 // so every load / store instruction of a warp covers one contiguous 512 B (256 B) span.
+// LayerNorm of one row held as float4 v[NV] by a warp (lane l owns float4 columns l, l+32, ...)
 template <typename Tout, int NV>
-__global__ void __launch_bounds__(256) layernorm_v4_kernel(const float4* __restrict__ x, const float4* __restrict__ g,
-                                                           const float4* __restrict__ b, Tout* __restrict__ out,
-                                                           int rows, int D) {
-  griddep_wait();
-  griddep_launch();
-  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
-  if (warp >= rows) return;
+__device__ __forceinline__ void ln_row_v4(const float4 (&v)[NV], const float4* __restrict__ g,
+                                          const float4* __restrict__ b, Tout* __restrict__ out, size_t row, int D,
+                                          int lane) {
   const int D4 = D / 4;
-  const float4* xr = x + (size_t)warp * D4;
-  float4 v[NV];
   float sm = 0.f;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    v[i] = xr[i * 32 + lane];
-    sm += (v[i].x + v[i].y) + (v[i].z + v[i].w);
-  }
+  for (int i = 0; i < NV; ++i) sm += (v[i].x + v[i].y) + (v[i].z + v[i].w);
 #pragma unroll
   for (int o = 16; o; o >>= 1) sm += __shfl_xor_sync(0xffffffffu, sm, o);
   const float mu = sm / D;
@@ -87,11 +79,96 @@ __global__ void __launch_bounds__(256) layernorm_v4_kernel(const float4* __restr
     const float o0 = (v[i].x - mu) * rstd * gg.x + bb.x, o1 = (v[i].y - mu) * rstd * gg.y + bb.y;
     const float o2 = (v[i].z - mu) * rstd * gg.z + bb.z, o3 = (v[i].w - mu) * rstd * gg.w + bb.w;
     if constexpr (sizeof(Tout) == 2) {
-      reinterpret_cast<uint2*>(out)[(size_t)warp * D4 + i * 32 + lane] = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
+      reinterpret_cast<uint2*>(out)[row * D4 + i * 32 + lane] = make_uint2(pack_bf16(o0, o1), pack_bf16(o2, o3));
     } else {
-      reinterpret_cast<float4*>(out)[(size_t)warp * D4 + i * 32 + lane] = make_float4(o0, o1, o2, o3);
+      reinterpret_cast<float4*>(out)[row * D4 + i * 32 + lane] = make_float4(o0, o1, o2, o3);
     }
   }
+}
+
+// Vectorised variant for D % 128 == 0 (D <= 1024): lane l owns float4 columns l, l+32, ...
+// so every load / store instruction of a warp covers one contiguous 512 B (256 B) span.
+template <typename Tout, int NV>
+__global__ void __launch_bounds__(256) layernorm_v4_kernel(const float4* __restrict__ x, const float4* __restrict__ g,
+                                                           const float4* __restrict__ b, Tout* __restrict__ out,
+                                                           int rows, int D) {
+  griddep_wait();
+  griddep_launch();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= rows) return;
+  const float4* xr = x + (size_t)warp * (D / 4);
+  float4 v[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) v[i] = xr[i * 32 + lane];
+  ln_row_v4<Tout, NV>(v, g, b, out, warp, D, lane);
+}
+
+// Split-K reduction (gemm_tc with Epi::ksplit > 1): row m of the residual output is
+// x_out = x_in + (bias + sum_s ws[s][m]) with the partials added in split order s = 0, 1, ...
+// (deterministic); LN (g != NULL) also writes LayerNorm(x_out) to h, i.e. the next pre-norm
+// (Q1) fused into the reduction.  One warp per row, D % 128 == 0, D <= 1024.
+template <typename Tout, int NV, bool LN>
+__global__ void __launch_bounds__(256) splitk_resid_kernel(const float4* __restrict__ ws, int ksplit, size_t split_ld4,
+                                                           const float4* __restrict__ bias, const float4* x_in,
+                                                           float4* x_out, const float4* __restrict__ g,
+                                                           const float4* __restrict__ b, Tout* __restrict__ h, int rows,
+                                                           int D, unsigned long long* timing) {
+  griddep_wait();
+  if (threadIdx.x == 0) time_begin(timing);
+  griddep_launch();
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp < rows) {   // (x_in may alias x_out: each element is read before it is written, by one thread)
+    const size_t r4 = (size_t)warp * (D / 4);
+    float4 v[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) v[i] = ws[r4 + i * 32 + lane];
+    for (int s = 1; s < ksplit; ++s) {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float4 p = ws[s * split_ld4 + r4 + i * 32 + lane];
+        v[i].x += p.x; v[i].y += p.y; v[i].z += p.z; v[i].w += p.w;
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float4 bb = __ldg(bias + i * 32 + lane), xi = x_in[r4 + i * 32 + lane];
+      v[i].x = xi.x + (v[i].x + bb.x); v[i].y = xi.y + (v[i].y + bb.y);
+      v[i].z = xi.z + (v[i].z + bb.z); v[i].w = xi.w + (v[i].w + bb.w);
+      x_out[r4 + i * 32 + lane] = v[i];
+    }
+    if constexpr (LN) ln_row_v4<Tout, NV>(v, g, b, h, warp, D, lane);
+  }
+  if (timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) time_end(timing, gridDim.x);
+  }
+}
+
+cudaError_t launch_splitk_resid(const float* ws, int ksplit, size_t split_ld, const float* bias, const float* x_in,
+                                float* x_out, const float* g, const float* b, void* h, int h_dtype, int rows, int D,
+                                cudaStream_t st, unsigned long long* timing) {
+  if (D % 128 || D > 1024 || ksplit < 1 || split_ld % 4) return cudaErrorInvalidValue;
+  const int blocks = (rows * 32 + 255) / 256;
+  const size_t ld4 = split_ld / 4;
+#define SKR(NV)                                                                                                    \
+  if (D == NV * 128) {                                                                                             \
+    if (!g)                                                                                                        \
+      pdl_launch(splitk_resid_kernel<bf16, NV, false>, dim3(blocks), dim3(256), 0, st, (const float4*)ws, ksplit,  \
+                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)nullptr,            \
+                 (const float4*)nullptr, (bf16*)nullptr, rows, D, timing);                                                 \
+    else if (h_dtype == 0)                                                                                         \
+      pdl_launch(splitk_resid_kernel<bf16, NV, true>, dim3(blocks), dim3(256), 0, st, (const float4*)ws, ksplit,   \
+                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)g,                  \
+                 (const float4*)b, (bf16*)h, rows, D, timing);                                                             \
+    else                                                                                                           \
+      pdl_launch(splitk_resid_kernel<float, NV, true>, dim3(blocks), dim3(256), 0, st, (const float4*)ws, ksplit,  \
+                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)g,                  \
+                 (const float4*)b, (float*)h, rows, D, timing);                                                            \
+    return cudaGetLastError();                                                                                     \
+  }
+  SKR(1) SKR(2) SKR(3) SKR(4) SKR(5) SKR(6) SKR(7) SKR(8)
+#undef SKR
+  return cudaErrorInvalidValue;
 }
 
 cudaError_t launch_layernorm(const float* x, const float* g, const float* b, void* out, int out_dtype, int rows,
