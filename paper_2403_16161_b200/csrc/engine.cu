@@ -156,7 +156,8 @@ struct vi_ctx {
   void *kslab = nullptr, *vtslab = nullptr;
   // workspaces
   void *tokens = nullptr, *yp32 = nullptr, *w_back2 = nullptr, *h = nullptr, *q = nullptr, *o = nullptr, *u = nullptr, *gbuf = nullptr, *xb = nullptr;
-  float *x_ws = nullptr, *fold_ws = nullptr, *opart = nullptr, *lse = nullptr;
+  float *x_ws = nullptr, *fold_ws = nullptr, *lse = nullptr;
+  vi::bf16* opart = nullptr;
   void *feat_in = nullptr, *feat_out = nullptr;
   // vi_run_step_async: copy streams (frames in / results out: one stream for both would order
   // step k+1's input copy behind step k's output copy, i.e. behind step k) and two staging slots
@@ -598,7 +599,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->x_ws = (float*)A(rows * D * 4);
   c->fold_ws = (float*)A((size_t)c->Tmax * cfg->feat_h * cfg->feat_w * std::max(c->gf.C, 1) * 4);
   if (c->bf16) {
-    c->opart = (float*)A((size_t)kMaxSplit * std::max(rows, (size_t)c->QR) * D * 4);
+    c->opart = (vi::bf16*)A((size_t)kMaxSplit * std::max(rows, (size_t)c->QR) * D * 2);
     c->lse = (float*)A((size_t)kMaxSplit * c->H * std::max(rows, (size_t)c->QR) * 4);
   }
   c->feat_in = A(fmap * es); c->feat_out = A(fmap * es);

@@ -107,7 +107,40 @@ struct Attn2Smem {
   static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
 };
 
+// Merge of the KV-split partials of partial row qp, head h, columns 4 c4 .. 4 c4 + 3:
+// O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), z in split order.  All loads are issued
+// before the sums (at most kMaxZ splits).
+constexpr int kMaxZ = 16;
+__device__ __forceinline__ void merge_partials4(const AttnTC& a, int qp, int h, int c4, bf16* dst) {
+  float lz[kMaxZ];
+  float4 v[kMaxZ];
+#pragma unroll
+  for (int z = 0; z < kMaxZ; ++z) {
+    lz[z] = z < a.nsplit ? __ldcg(a.lse + ((size_t)z * a.H + h) * a.Nq + qp) : -INFINITY;
+    uint2 u = make_uint2(0u, 0u);
+    if (z < a.nsplit) u = __ldcg(reinterpret_cast<const uint2*>(a.opart + ((size_t)z * a.Nq + qp) * a.D + h * a.hd) + c4);
+    const float2 v01 = unpack_bf16x2(u.x), v23 = unpack_bf16x2(u.y);
+    v[z] = make_float4(v01.x, v01.y, v23.x, v23.y);
+  }
+  float mx = -INFINITY;
+#pragma unroll
+  for (int z = 0; z < kMaxZ; ++z) mx = fmaxf(mx, lz[z]);
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+#pragma unroll
+  for (int z = 0; z < kMaxZ; ++z) {
+    if (lz[z] == -INFINITY) continue;
+    const float w = exp2f(lz[z] - mx);
+    wsum += w;
+    acc[0] += w * v[z].x; acc[1] += w * v[z].y; acc[2] += w * v[z].z; acc[3] += w * v[z].w;
+  }
+  const float inv = 1.f / wsum;
+  *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+}
+
 // One softmax warpgroup per Q tile (thread = row, all 128 keys).
+#ifndef TC2_TRACE
+#define TC2_TRACE 0   // per-CTA globaltimer stamps into AttnTC::cta_trace (micro-benchmarks only)
+#endif
 template <int HD>
 __global__ void __launch_bounds__(384, 1)
 attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
@@ -137,6 +170,11 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   int t_end = t_begin + a.tiles_per_split;
   if (t_end > ntiles) t_end = ntiles;
   const int n = t_end > t_begin ? t_end - t_begin : 0;
+  long long* const ct =
+      (TC2_TRACE && a.cta_trace)
+          ? a.cta_trace + (size_t)((blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x) * 8
+          : nullptr;
+  if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
 
   if (warp == 8 && lane == 0) {
     tma_prefetch(&tq);
@@ -167,6 +205,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   griddep_wait();
   griddep_launch();
   if (threadIdx.x == 0) time_begin(a.timing);
+  if (ct && threadIdx.x == 0) ct[1] = (long long)globaltimer();
 
   if (warp == 8) {
     if (lane == 0 && n > 0) {
@@ -262,6 +301,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       key_tile(a.segs, t_begin + jj, row0, nv, nskip);
       const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && jj < 32;
       mbar_wait(&s_full[t], jj & 1);
+      if (ct && jj == 0 && threadIdx.x == 0) ct[2] = (long long)globaltimer();
       if (tr) a.trace[jj * 32 + t * 12 + qd] = clock64();
       tc_fence_after();
       float s[128];
@@ -352,6 +392,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       mbar_wait(&o_final[t], 0);
       tc_fence_after();
     }
+    if (ct && threadIdx.x == 0) ct[3] = (long long)globaltimer();
     const float inv = n > 0 ? 1.f / l : 0.f;
     if (a.nsplit == 1) {
 #pragma unroll 1
@@ -369,33 +410,50 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
       }
     } else {
-      float* op = a.opart + ((size_t)z * a.Nq + qp) * a.D + h * HD;
+      // the normalised partial row (bf16, as attn_sk2's pieces) leaves through shared memory as
+      // one bulk copy (direct stores put 32 rows in every warp instruction and ran at one L2
+      // sector per clock: 4.5 us per CTA for fp32 rows).  Staging: tile t's rows at a padded
+      // pitch (a warp's 16-B stores cover 8 bank groups) in the Q / K buffers, free once
+      // o_final[t] is seen (the MMAs complete in issue order and QK(1, n-1) precedes the commit
+      // of O(0)).
+      constexpr int PITCH = HD * 2 + 16;
+      static_assert(2 * 128 * PITCH <= L::V_OFF, "partial staging exceeds the Q / K buffers");
+      uint8_t* srow = smem + (size_t)(t * 128 + qd * 32 + lane) * PITCH;
 #pragma unroll 1
       for (int c = 0; c < HD; c += 32) {
         uint32_t r[32];
         if (n > 0) {
           tmem_ld32(TO + c, r);
           tmem_wait_ld();
-        }
-        if (orow >= 0) {
-          float4* dst = reinterpret_cast<float4*>(op + c);
+        } else {
 #pragma unroll
-          for (int i = 0; i < 8; ++i)
-            dst[i] = n > 0 ? make_float4(__uint_as_float(r[4 * i]) * inv, __uint_as_float(r[4 * i + 1]) * inv,
-                                         __uint_as_float(r[4 * i + 2]) * inv, __uint_as_float(r[4 * i + 3]) * inv)
-                           : make_float4(0.f, 0.f, 0.f, 0.f);
+          for (int i = 0; i < 32; ++i) r[i] = 0u;
         }
+        const float* f = reinterpret_cast<const float*>(r);
+        uint4* dst = reinterpret_cast<uint4*>(srow + c * 2);
+#pragma unroll
+        for (int i = 0; i < 4; ++i)
+          dst[i] = make_uint4(pack_bf16(f[8 * i] * inv, f[8 * i + 1] * inv), pack_bf16(f[8 * i + 2] * inv, f[8 * i + 3] * inv),
+                              pack_bf16(f[8 * i + 4] * inv, f[8 * i + 5] * inv), pack_bf16(f[8 * i + 6] * inv, f[8 * i + 7] * inv));
       }
-      if (orow >= 0) a.lse[((size_t)z * a.H + h) * a.Nq + qp] = n > 0 ? m_use + __log2f(l) : -INFINITY;
+      if (orow >= 0) {
+        fence_proxy_async_smem();
+        bulk_s2g(a.opart + ((size_t)z * a.Nq + qp) * a.D + h * HD, srow, HD * 2);
+        bulk_commit();
+        a.lse[((size_t)z * a.H + h) * a.Nq + qp] = n > 0 ? m_use + __log2f(l) : -INFINITY;
+        bulk_wait_read<0>();
+      }
     }
+    if (ct && threadIdx.x == 0) ct[4] = (long long)globaltimer();
   }
   tc_fence_before();
   __syncthreads();
-  if (threadIdx.x == 0) time_end(a.timing, gridDim.x * gridDim.y * gridDim.z);
   if (warp == 10) {
     tc_fence_after();
     tmem_dealloc(tmem, 512);
   }
+  if (ct && threadIdx.x == 0) ct[5] = (long long)globaltimer();
+  if (threadIdx.x == 0) time_end(a.timing, gridDim.x * gridDim.y * gridDim.z);
 }
 
 template <int HD>
@@ -405,9 +463,7 @@ static cudaError_t launch2_hd(const CUtensorMap& tq, const CUtensorMap& tk, cons
   cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(attn_tc2_kernel<HD>), L::TOTAL);
   if (e != cudaSuccess) return e;
   dim3 grid(a.win_n ? a.win_n * a.win_npw : (a.Nq + 255) / 256, a.H, a.nsplit);
-  e = pdl_launch(attn_tc2_kernel<HD>, grid, dim3(384), L::TOTAL, st, tq, tk, tvt, a);
-  if (e != cudaSuccess) return e;
-  return cudaGetLastError();
+  return pdl_launch(attn_tc2_kernel<HD>, grid, dim3(384), L::TOTAL, st, tq, tk, tvt, a);
 }
 
 cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
@@ -417,45 +473,19 @@ cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const 
   return cudaErrorInvalidValue;
 }
 
-// Merge KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), z in fixed order.
-// Thread = (query row, head, 4 columns); the split's lse values and partial rows are all
-// requested before the sums (kMaxZ <= 16 splits), so a thread waits for one round of loads.
-constexpr int kMaxZ = 16;
+// Merge of the KV-split partials as a separate kernel (grids beyond one wave):
+// thread = (query row, head, 4 columns)
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnTC a) {
   griddep_wait();
   if (threadIdx.x == 0) time_begin(a.timing);
   griddep_launch();
   const int hd4 = a.hd / 4;
-  const size_t total = (size_t)a.Nq * a.H * hd4;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
-    const int c4 = int(i % hd4);
-    const size_t r = i / hd4;
-    const int h = int(r % a.H);
-    const int q = int(r / a.H);             // KV-split partial row (windows: window-major)
+  const int total = a.Nq * a.H * hd4;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
+    const int c4 = i % hd4, r = i / hd4;
+    const int h = r % a.H, q = r / a.H;     // KV-split partial row (windows: window-major)
     const int orow = a.win_n ? win_out_row(a, a.win0 + q / a.win_qstride, q % a.win_qstride) : q;
-    if (orow < 0) continue;
-    float lz[kMaxZ];
-    float4 v[kMaxZ];
-#pragma unroll
-    for (int z = 0; z < kMaxZ; ++z) {
-      lz[z] = z < a.nsplit ? a.lse[((size_t)z * a.H + h) * a.Nq + q] : -INFINITY;
-      v[z] = z < a.nsplit ? *reinterpret_cast<const float4*>(a.opart + ((size_t)z * a.Nq + q) * a.D + h * a.hd + c4 * 4)
-                          : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    float mx = -INFINITY;
-#pragma unroll
-    for (int z = 0; z < kMaxZ; ++z) mx = fmaxf(mx, lz[z]);
-    float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
-#pragma unroll
-    for (int z = 0; z < kMaxZ; ++z) {
-      if (lz[z] == -INFINITY) continue;
-      const float w = exp2f(lz[z] - mx);
-      wsum += w;
-      acc[0] += w * v[z].x; acc[1] += w * v[z].y; acc[2] += w * v[z].z; acc[3] += w * v[z].w;
-    }
-    const float inv = 1.f / wsum;
-    uint2* dst = reinterpret_cast<uint2*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
-    *dst = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
+    if (orow >= 0) merge_partials4(a, q, h, c4, a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
   }
   if (a.timing) {
     __syncthreads();

@@ -262,9 +262,9 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             mbar_arrive_expect_tx(&xbar[2 * ew + bi], 4096);
             tma_load_2d(buf, &tmX, &xbar[2 * ew + bi], n0 + c, m0 + q * 32);
           }
-#pragma unroll 1
           // QKV: a 64-column chunk lies in one of Q / K / V (D % 64 == 0); V leaves transposed
           const int region = qkv ? (n0 + c) / epi.D : 0;
+#pragma unroll 1
           for (int h2 = 0; h2 < cw; h2 += 32) {
             float v[32];
             tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c + h2, reinterpret_cast<uint32_t*>(v));

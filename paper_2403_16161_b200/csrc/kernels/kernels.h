@@ -114,7 +114,7 @@ struct AttnTC {
   float scale_log2;
   KeySegs segs;
   bf16* o;                  // [Nq][D] final (nsplit == 1)
-  float* opart;             // [nsplit][Nq][D] normalised partial outputs (nsplit > 1)
+  bf16* opart;              // [nsplit][Nq][D] normalised partial outputs, bf16 (nsplit > 1)
   float* lse;               // [nsplit][H][Nq] log2-sum-exp of the partials
   // stream-K (attn_sk_kernel): units = (query-tile pair, head), work = units x key tiles,
   // split evenly over the persistent grid; partial results of split units go through
