@@ -107,36 +107,6 @@ struct Attn2Smem {
   static constexpr int TOTAL = BAR_OFF + NBAR * 8 + 16 + 1024;
 };
 
-// Merge of the KV-split partials of partial row qp, head h, columns 4 c4 .. 4 c4 + 3:
-// O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), z in split order.  All loads are issued
-// before the sums (at most kMaxZ splits).
-constexpr int kMaxZ = 16;
-__device__ __forceinline__ void merge_partials4(const AttnTC& a, int qp, int h, int c4, bf16* dst) {
-  float lz[kMaxZ];
-  float4 v[kMaxZ];
-#pragma unroll
-  for (int z = 0; z < kMaxZ; ++z) {
-    lz[z] = z < a.nsplit ? __ldcg(a.lse + ((size_t)z * a.H + h) * a.Nq + qp) : -INFINITY;
-    uint2 u = make_uint2(0u, 0u);
-    if (z < a.nsplit) u = __ldcg(reinterpret_cast<const uint2*>(a.opart + ((size_t)z * a.Nq + qp) * a.D + h * a.hd) + c4);
-    const float2 v01 = unpack_bf16x2(u.x), v23 = unpack_bf16x2(u.y);
-    v[z] = make_float4(v01.x, v01.y, v23.x, v23.y);
-  }
-  float mx = -INFINITY;
-#pragma unroll
-  for (int z = 0; z < kMaxZ; ++z) mx = fmaxf(mx, lz[z]);
-  float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
-#pragma unroll
-  for (int z = 0; z < kMaxZ; ++z) {
-    if (lz[z] == -INFINITY) continue;
-    const float w = exp2f(lz[z] - mx);
-    wsum += w;
-    acc[0] += w * v[z].x; acc[1] += w * v[z].y; acc[2] += w * v[z].z; acc[3] += w * v[z].w;
-  }
-  const float inv = 1.f / wsum;
-  *reinterpret_cast<uint2*>(dst) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
-}
-
 // One softmax warpgroup per Q tile (thread = row, all 128 keys).
 #ifndef TC2_TRACE
 #define TC2_TRACE 0   // per-CTA globaltimer stamps into AttnTC::cta_trace (micro-benchmarks only)
@@ -473,19 +443,43 @@ cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const 
   return cudaErrorInvalidValue;
 }
 
-// Merge of the KV-split partials as a separate kernel (grids beyond one wave):
-// thread = (query row, head, 4 columns)
+// Merge of the KV-split partials: O = sum_z 2^(lse_z - M) O_z / sum_z 2^(lse_z - M), z in
+// split order (deterministic).  A group of hd / 4 lanes per (query row, head): lane z of the
+// group loads lse_z (broadcast by shuffles), every lane issues its <= kMaxZ partial loads
+// (4 bf16 columns each) before the sums.  Partial rows are window-major for windows.
+constexpr int kMaxZ = 16;
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnTC a) {
   griddep_wait();
   if (threadIdx.x == 0) time_begin(a.timing);
   griddep_launch();
-  const int hd4 = a.hd / 4;
-  const int total = a.Nq * a.H * hd4;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int c4 = i % hd4, r = i / hd4;
-    const int h = r % a.H, q = r / a.H;     // KV-split partial row (windows: window-major)
-    const int orow = a.win_n ? win_out_row(a, a.win0 + q / a.win_qstride, q % a.win_qstride) : q;
-    if (orow >= 0) merge_partials4(a, q, h, c4, a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c4 * 4);
+  const int G = a.hd / 4;                                   // lanes per row: 32 (d 128) or 16 (d 64)
+  const int sub = (threadIdx.x & 31) % G;
+  const int r = (blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const bool live = r < a.Nq * a.H;
+  const int h = live ? r % a.H : 0, q = live ? r / a.H : 0;
+  const float lme = (live && sub < a.nsplit) ? __ldcg(a.lse + ((size_t)sub * a.H + h) * a.Nq + q) : -INFINITY;
+  const uint2* src = reinterpret_cast<const uint2*>(a.opart + (size_t)q * a.D + h * a.hd) + sub;
+  const size_t zstride = (size_t)a.Nq * a.D / 4;            // one split's partials, in uint2
+  uint2 u[kMaxZ];
+#pragma unroll
+  for (int z = 0; z < kMaxZ; ++z) u[z] = (live && z < a.nsplit) ? __ldcg(src + z * zstride) : make_uint2(0u, 0u);
+  float mx = lme;
+  for (int o = G / 2; o; o >>= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o, G));
+  float acc[4] = {0.f, 0.f, 0.f, 0.f}, wsum = 0.f;
+#pragma unroll
+  for (int z = 0; z < kMaxZ; ++z) {
+    const float lz = __shfl_sync(0xffffffffu, lme, z, G);
+    if (lz == -INFINITY) continue;
+    const float w = exp2f(lz - mx);
+    const float2 v01 = unpack_bf16x2(u[z].x), v23 = unpack_bf16x2(u[z].y);
+    wsum += w;
+    acc[0] += w * v01.x; acc[1] += w * v01.y; acc[2] += w * v23.x; acc[3] += w * v23.y;
+  }
+  const int orow = !live ? -1 : a.win_n ? win_out_row(a, a.win0 + q / a.win_qstride, q % a.win_qstride) : q;
+  if (orow >= 0) {
+    const float inv = 1.f / wsum;
+    *reinterpret_cast<uint2*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + sub * 4) =
+        make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   }
   if (a.timing) {
     __syncthreads();
@@ -494,11 +488,10 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnTC a) {
 }
 
 cudaError_t launch_attn_combine(const AttnTC& a, cudaStream_t st) {
-  if (a.nsplit > kMaxZ) return cudaErrorInvalidValue;
-  const size_t total = (size_t)a.Nq * a.H * (a.hd / 4);
-  size_t blocks = (total + 255) / 256;
-  if (blocks > 148 * 8) blocks = 148 * 8;
-  return pdl_launch(attn_combine_kernel, dim3(unsigned(blocks ? blocks : 1)), dim3(256), 0, st, a);
+  if (a.nsplit > kMaxZ || (a.hd != 128 && a.hd != 64)) return cudaErrorInvalidValue;
+  const size_t threads = (size_t)a.Nq * a.H * (a.hd / 4);
+  const unsigned blocks = unsigned((threads + 255) / 256);
+  return pdl_launch(attn_combine_kernel, dim3(blocks ? blocks : 1), dim3(256), 0, st, a);
 }
 
 }  // namespace vi
