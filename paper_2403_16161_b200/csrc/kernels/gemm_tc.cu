@@ -46,7 +46,7 @@ struct GemmSmem {
 };
 
 #ifdef VI_GEMM_TRACE
-__device__ long long g_gemm_trace[24];
+__device__ long long g_gemm_trace[64];
 #define GTR(i) do { if (blockIdx.x == 0) g_gemm_trace[i] = (long long)globaltimer(); } while (0)
 #else
 #define GTR(i) do { } while (0)
@@ -254,6 +254,8 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
           if (n0 + c >= epi.N) break;
           const int bi = nchunk & 1;
           uint8_t* buf = stg + bi * 4096;
+          const bool gtr_c = lt == 0 && ew == 0 && lane == 0 && kc < 8;
+          if (gtr_c) GTR(16 + kc * 4);
           if (nchunk >= 2 && !(pre_x && kc < 2)) {   // the store that used this buffer has read it
             if (lane == 0) bulk_wait_read<1>();
             __syncwarp();
@@ -269,9 +271,14 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
             float v[32];
             tmem_ld32(tmem + acc * BN + (uint32_t(q * 32) << 16) + c + h2, reinterpret_cast<uint32_t*>(v));
             tmem_wait_ld();
+            if (gtr_c && h2 == 0) GTR(17 + kc * 4);
             if (epi.bias) {
+              const float4* b4 = reinterpret_cast<const float4*>(bs + c + h2);
 #pragma unroll
-              for (int i = 0; i < 32; ++i) v[i] += bs[c + h2 + i];
+              for (int i = 0; i < 8; ++i) {
+                const float4 bb = b4[i];
+                v[4 * i] += bb.x; v[4 * i + 1] += bb.y; v[4 * i + 2] += bb.z; v[4 * i + 3] += bb.w;
+              }
             }
             if (epi.kind == EPI_GELU) {
 #pragma unroll
@@ -311,6 +318,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                                pack_bf16(v[8 * j + 4], v[8 * j + 5]), pack_bf16(v[8 * j + 6], v[8 * j + 7]));
             }
           }
+          if (gtr_c) GTR(18 + kc * 4);
           fence_proxy_async_smem();
           __syncwarp();
           if (lane == 0) {
@@ -331,6 +339,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
               }
             }
             bulk_commit();
+            if (gtr_c) GTR(19 + kc * 4);
           }
         }
       } else {

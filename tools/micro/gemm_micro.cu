@@ -90,13 +90,17 @@ static void run(const char* name, int M, int N, int K, int bn, int kind, int pai
          N, K, bn, kind, pair, int(te), cudaGetErrorString(err), cudaGetErrorString(err2), us, tf, diff);
   fflush(stdout);
 #ifdef VI_GEMM_TRACE
-  long long tr[24];
+  long long tr[64];
   cudaMemcpyFromSymbol(tr, g_gemm_trace, sizeof(tr));
   printf("   CTA0 (ns from start): setup %lld first-data %lld | mma-done", tr[1] - tr[0], tr[2] - tr[0]);
   for (int i = 0; i < 4; ++i) printf(" %lld", tr[3 + i] > tr[0] ? tr[3 + i] - tr[0] : -1);
   printf(" | epi end");
   for (int i = 0; i < 4; ++i) printf(" %lld", tr[11 + i] > tr[0] ? tr[11 + i] - tr[0] : -1);
   printf(" | exit %lld\n", tr[15] - tr[0]);
+  printf("   epilogue warp 0, tile 0 chunks (start / tmem ld / smem written / store issued):");
+  for (int k = 0; k < 8 && tr[16 + 4 * k]; ++k)
+    printf(" [%lld %lld %lld %lld]", tr[16 + 4 * k] - tr[0], tr[17 + 4 * k] - tr[0], tr[18 + 4 * k] - tr[0], tr[19 + 4 * k] - tr[0]);
+  printf("\n");
   cudaMemset(g_gemm_trace_ptr(), 0, sizeof(tr));
 #endif
   cudaFree(A); cudaFree(W); cudaFree(O); cudaFree(bias); cudaFree(x);
