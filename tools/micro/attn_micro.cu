@@ -154,8 +154,9 @@ int main(int argc, char** argv) {
       for (int i = 0; i < 7; ++i) printf(" %6lld", e[i] ? e[i] - t0 : -1);
       printf(" %lld |", e[7]);
       for (int i = 0; i < e[7] && i < 4; ++i) printf(" %6lld", e[8 + i] - t0);
-      printf(" | piece published %6lld owner staged %6lld | direct %6lld %6lld", e[12] ? e[12] - t0 : -1, e[13] ? e[13] - t0 : -1,
-             e[14] ? e[14] - t0 : -1, e[15] ? e[15] - t0 : -1);
+      printf(" | piece published %6lld merged %6lld | lastflag %6lld lastland %6lld | go %6lld flag0 %6lld land0 %6lld merged0 %6lld",
+             e[12] ? e[12] - t0 : -1, e[13] ? e[13] - t0 : -1, e[14] ? e[14] - t0 : -1, e[15] ? e[15] - t0 : -1,
+             e[16] ? e[16] - t0 : -1, e[17] ? e[17] - t0 : -1, e[18] ? e[18] - t0 : -1, e[19] ? e[19] - t0 : -1);
       printf("\n");
     }
   }
