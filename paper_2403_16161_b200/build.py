@@ -32,6 +32,9 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "--expt-relaxed-constexpr", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
+# diagnostic builds only (e.g. VI_NVCC_EXTRA=-DVI_MBAR_TIMEOUT: barrier waits trap with a message
+# instead of hanging); the product build passes nothing
+FLAGS += os.environ.get("VI_NVCC_EXTRA", "").split()
 
 
 def _obj(src: str) -> str:

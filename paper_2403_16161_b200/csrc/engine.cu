@@ -1143,15 +1143,23 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   // window attention: sk2 over (head, window, query pair) units, stream-K split over up to
   // VI_WIN_SPLIT CTAs per unit (C4: 64 units of 6 key tiles; attn_tc2's KV split + combine
   // kernel measured 28 us/block)
+  // With one CTA per (head, window, 128-query tile) unit fitting in one wave (C4: 16 windows x
+  // 2 tiles x 4 heads = 128), units are single Q tiles and never split: no merge tail
+  // (each CTA's tile-1 warps idle).
+  // (VI_WIN_SPLIT > 1 or VI_WIN_PAIRS: the pair units with a stream-K split, A/B and tests)
+  const char* ws = getenv("VI_WIN_SPLIT");
+  const int single_units = c->win_n ? a.win_n * ((a.win_nq + 127) / 128) * a.H : 0;
+  const bool single = c->win_n && single_units <= c->num_sms && !getenv("VI_WIN_PAIRS") && !(ws && atoi(ws) > 1);
+  if (single) a.win_npw = (a.win_nq + 127) / 128;
   const int win_units = c->win_n ? a.win_n * a.win_npw * a.H : 0;
   if (c->win_n && win_units <= c->num_sms) {
     a.npairs = a.win_npw;
     a.units = win_units;
+    a.sk_single = single ? 1 : 0;
     a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
     a.sk_tail = 0; a.sk_tail_w = 16; a.sk_ucost = 0;
     a.sk_wfull = (long long)a.units * ntiles;
-    const char* ws = getenv("VI_WIN_SPLIT");
-    const int split = std::max(1, ws ? atoi(ws) : 2);
+    const int split = single ? 1 : std::max(1, ws ? atoi(ws) : 2);
     const long long work = (long long)a.units * ntiles;
     const int grid = int(std::min<long long>(std::min<long long>((long long)a.units * split, work), c->num_sms));
     PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");

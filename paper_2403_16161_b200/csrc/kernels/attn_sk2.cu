@@ -106,7 +106,7 @@ __device__ __forceinline__ void sk2_unit(const AttnTC& a, int u, int& h, int& q0
     const int r = u - h * per_h;
     const int wl = r / a.win_npw;                 // window within this launch's range
     win = a.win0 + wl;
-    q0 = (r - wl * a.win_npw) * 256;
+    q0 = (r - wl * a.win_npw) * (a.sk_single ? 128 : 256);
     return;
   }
   const int full = a.npairs - a.sk_tail;     // full pairs per head
@@ -200,6 +200,9 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  // single-tile window units are launched with programmatic dependent launch (no CTA waits on
+  // another): the set-up above overlaps the previous kernel's tail
+  griddep_wait();
   if (threadIdx.x == 0) time_begin(a.timing);
   if (ct && threadIdx.x == 0) ct[1] = (long long)globaltimer();
   // debug timeline (VI_SK_TRACE): CTA 0, first segment's first 32 key tiles, 32 clock64 stamps per tile
@@ -327,6 +330,9 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const int nq = WIN ? a.win_nq : a.Nq;
       const bool t1_live = q0 + 128 < nq && SK2_EXPERIMENT != 2;   // tile 1 of a tail pair: commits only
       const bool t0_live = SK2_EXPERIMENT != 2;
+      // single-tile units: tile 1 does not exist (no MMAs, no commits, no waits on its warps,
+      // which leave at once); the K / V stages are released with tile 0's MMAs
+      const int tl = a.sk_single ? 0 : 1;
       mbar_wait(q_full, sg & 1);
       auto issue_pv = [&](int t, int j) {          // O_t (+)= P_t(j) V(j), j local to the segment
         const int g = jg + j, st = g % ST;
@@ -345,7 +351,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
                 umma_bf16_ts(tmem + 256 + t * 128, tmem + t * 128 + hh * 64 + k4 * 8,
                              dv + uint64_t((hh * (HD * 128) + k4 * 32) >> 4), idesc_o, (j | hh | k4) != 0);
             }
-            if (hh == 1 && t == 1) umma_commit(&v_empty[st]);
+            if (hh == 1 && t == tl) umma_commit(&v_empty[st]);
           }
           __syncwarp();
         }
@@ -368,18 +374,18 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
           umma_commit(&s_full[t]);
           if (trc && g < 32) trc[g * 32 + 24 + t] = clock64();
           if (ct && g == 0 && t == 0) ct[2] = (long long)globaltimer();
-          if (t == 1) umma_commit(&k_empty[st]);
+          if (t == tl) umma_commit(&k_empty[st]);
         }
         __syncwarp();
       };
       for (int j = 0; j < n; ++j)
-        for (int t = 0; t < 2; ++t) {
+        for (int t = 0; t <= tl; ++t) {
           if (j > 0) issue_pv(t, j - 1);
           issue_qk(t, j);
         }
       if (elect_one()) umma_commit(q_empty);       // all QK of the segment issued: Q smem free when done
       __syncwarp();
-      for (int t = 0; t < 2; ++t) {
+      for (int t = 0; t <= tl; ++t) {
         issue_pv(t, n - 1);
         if (elect_one()) umma_commit(&o_final[t]);
         __syncwarp();
@@ -393,7 +399,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       jg += n;
       w += n;
     }
-  } else if (warp < 16) {
+  } else if (warp < 16 && !(a.sk_single && warp >= 8)) {   // (single-tile units: tile 1's warps idle)
     const int t = warp >> 3;                        // Q tile
     const int hf = (warp >> 2) & 1;                 // key half / O column half
     const int qd = warp & 3;                        // TMEM lane quadrant
@@ -673,6 +679,12 @@ static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, c
   using L = AttnSk2Smem<HD>;
   cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(attn_sk2_kernel<HD, WIN>), L::TOTAL);
   if (e != cudaSuccess) return e;
+  // single-tile units run one CTA per unit (their tile-1 warps leave at once, so no unit may be
+  // split): no CTA waits on another -> plain PDL launch
+  if (a.sk_single) {
+    if (grid != a.units) return cudaErrorInvalidValue;
+    return pdl_launch(attn_sk2_kernel<HD, WIN>, dim3(grid), dim3(576), L::TOTAL, st, tq, tk, tvt, a);
+  }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
   cfg.blockDim = dim3(576);

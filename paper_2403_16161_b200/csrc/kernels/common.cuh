@@ -1,6 +1,7 @@
 // Shared device helpers for the sm_100a kernels: bf16 packing, mbarriers, TMA,
 // tcgen05 (TMEM alloc / MMA / commit / ld / st) as thin inline-PTX wrappers.
 #pragma once
+#include <cstdio>
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>

@@ -126,6 +126,8 @@ struct AttnTC {
   // softmax quadrants past Nq are skipped); sk_wfull = work items of the full units.
   int sk_tail, sk_tail_w;
   int sk_ucost;              // attn_sk2 split cost of a unit's start (16 = one key tile of a pair)
+  int sk_single;             // attn_sk2 window units of ONE 128-query tile (tile 1 idle): with one
+                             // CTA per unit no unit is split, so no piece is merged
   long long sk_wfull;
   float* spart;             // [grid][256][hd]
   float* slse;              // [grid][256]

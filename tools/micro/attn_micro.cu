@@ -4,7 +4,7 @@
 //   nvcc -gencode arch=compute_100a,code=sm_100a -O3 -std=c++17 -lineinfo --expt-relaxed-constexpr \
 //        -I include -I paper_2403_16161_b200/csrc [-DATTN_SRC='"/path/attn_sk2.cu"'] \
 //        tools/micro/attn_micro.cu -lcuda -o /tmp/attn_micro
-//   /tmp/attn_micro [iters] [t(race)|x] [grid (0 = auto)] [2] [w(indow shape)]
+//   /tmp/attn_micro [iters] [t(race)|x] [grid (0 = auto)] [2] [w(indow shape)] [s(ingle-tile window units)]
 // (tools/micro/ab_attn.sh builds two sources and alternates them on one GPU)
 //
 // Prints the mean launch time, TFLOP/s (4 Nq Nk D valid-key FLOPs) and, with `trace`, the
@@ -25,6 +25,9 @@
 #endif
 #include ATTN_SRC
 #include SETUP_SRC
+namespace vi {
+int g_pdl = 1;   // (rows.cu's definition in the library)
+}
 using namespace vi;
 
 typedef CUresult (*PFN)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*, const cuuint64_t*,
@@ -106,6 +109,14 @@ int main(int argc, char** argv) {
     a.segs.tile0[1] = (15 * WREAL + 127) / 128;
     a.npairs = 1;
     a.units = WN * H;
+#ifndef VI_SK2_NO_SINGLE
+    if (argc > 6 && argv[6][0] == 's') {   // single 128-query tiles per unit (the engine's C4 default)
+      a.sk_single = 1;
+      a.win_npw = 2;
+      a.npairs = 2;
+      a.units = WN * 2 * H;
+    }
+#endif
   }
   cudaMalloc(&a.spart, (size_t)nsm * 2 * 256 * HD * 4);
   cudaMalloc(&a.slse, (size_t)nsm * 2 * 256 * 4);
