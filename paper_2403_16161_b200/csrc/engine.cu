@@ -182,6 +182,7 @@ struct vi_ctx {
 
   // tensor maps (bf16 path)
   CUtensorMap tm_tokens, tm_wembed, tm_h, tm_wqkv, tm_o, tm_wo, tm_w1, tm_g, tm_w2, tm_xb, tm_wback;
+  CUtensorMap tm_w1_128;   // W1 with 128-row boxes: FFN1 on 128-column tiles for small M
   CUtensorMap tm_w2_pair;    // W2 with a 64-row box: the CTA-pair FFN2 (256 x 128 tiles)
   CUtensorMap tm_q, tm_k, tm_vt, tm_og;
   CUtensorMap tm_u_out, tm_g_out, tm_yp_out;   // GEMM outputs through the TMA-store epilogue
@@ -480,6 +481,7 @@ static vi_status build_maps(vi_ctx* c) {
   ok &= make_tmap(&c->tm_o, c->o, c->D, rows, 64, 128);
   ok &= make_tmap(&c->tm_wo, c->w_o, c->D, (uint64_t)c->L * c->D, 64, c->bn_o);
   ok &= make_tmap(&c->tm_w1, c->w_1, c->D, (uint64_t)c->L * c->F, 64, c->bn_1);
+  ok &= make_tmap(&c->tm_w1_128, c->w_1, c->D, (uint64_t)c->L * c->F, 64, 128);
   ok &= make_tmap(&c->tm_g, c->gbuf, c->F, rows, 64, 128);
   ok &= make_tmap(&c->tm_w2, c->w_2, c->F, (uint64_t)c->L * c->D, 64, c->bn_2);
   ok &= make_tmap(&c->tm_w2_pair, c->w_2, c->F, (uint64_t)c->L * c->D, 64, 64);
@@ -1243,9 +1245,12 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   // a9 / a10: FFN1 (+ F3N fold/unfold) + GELU
   const bool f3n = c->cfg.ffn_kind == VI_FFN_F3N;
   Epi e1 = epi_base(c, f3n ? EPI_STORE : EPI_GELU, M, F, c->b_1 + (size_t)l * F);
+  const bool ffn1_small = c->bn_1 == 256 && ((M + 127) / 128) * ((F + 255) / 256) * 2 <= c->num_sms;
   e1.out = f3n ? c->u : c->gbuf; e1.ldo = F; e1.out_f32 = f3n ? 1 : 0;
   if (c->bf16)
-    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, c->tm_w1, l * F, M, F, D, c->bn_1, e1, c->stream, 0,
+    // small M (one frame): 128-column tiles, twice the CTAs of the 256-column ones
+    PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_h, ffn1_small ? c->tm_w1_128 : c->tm_w1, l * F, M, F, D,
+                                         ffn1_small ? 128 : c->bn_1, e1, c->stream, 0,
                                          f3n ? &c->tm_u_out : &c->tm_g_out),
             "ffn1 gemm");
   else
@@ -1432,7 +1437,8 @@ static vi_status step_graph(vi_ctx* c, const void* fin, int n, void* fout) {
     ce = cudaGraphInstantiate(&exec, graph, 0);
     cudaGraphDestroy(graph);
     if (ce != cudaSuccess) return c->cuda_fail(ce, "graph instantiate");
-    if (c->graphs.size() >= 32) {   // evict the least recently used
+    if (c->graphs.size() >= 64) {   // evict the least recently used (64: every (ring state, buffer)
+                                    // pair of a one-frame step cycling over 4 buffers stays cached)
       auto lru = std::min_element(c->graphs.begin(), c->graphs.end(),
                                   [](const vi_ctx::GraphEntry& a, const vi_ctx::GraphEntry& b) {
                                     return a.last_use < b.last_use;
