@@ -977,7 +977,7 @@ static int splitk_plan(const vi_ctx* c, int M, int N, int K) {
 // (which also writes LayerNorm(x_out) to h when ln_g != NULL)
 static vi_status splitk_resid(vi_ctx* c, int ks, const CUtensorMap& amap, const CUtensorMap& wmap, int brow0, int M,
                               int N, int K, int a_hs, int a_kpb, const float* bias, const float* x_in, float* x_out,
-                              const float* ln_g, const float* ln_b, void* h, const char* where) {
+                              const float* pos, const float* ln_g, const float* ln_b, void* h, const char* where) {
   const int kpad = (M + 127) / 128 * 128;
   Epi e = epi_base(c, EPI_STORE, M, N, nullptr);
   e.out = c->skws; e.ldo = N; e.out_f32 = 1;
@@ -988,7 +988,7 @@ static vi_status splitk_resid(vi_ctx* c, int ks, const CUtensorMap& amap, const 
     return c->fail(VI_E_CUDA, std::string(where) + ": split-K workspace map");
   PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(amap, wmap, brow0, M, N, K, 128, e, c->stream, 0, &tws, nullptr), where);
   PLAUNCH(VI_PROF_GEMM,
-          launch_splitk_resid(c->skws, ks, (size_t)kpad * N, bias, x_in, x_out, ln_g, ln_b, h, c->bf16 ? 0 : 1, M, N,
+          launch_splitk_resid(c->skws, ks, (size_t)kpad * N, bias, x_in, x_out, pos, c->P, ln_g, ln_b, h, c->bf16 ? 0 : 1, M, N,
                               c->stream, e.timing),
           where);
   return VI_OK;
@@ -1009,7 +1009,13 @@ extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out
     e.out = out; e.ldo = c->D; e.out_f32 = 1; e.pos = c->cfg.pos_embed ? c->pos : nullptr; e.P = c->P;
     CUtensorMap tmo;
     const bool te = c->bf16 && make_tmap_out(&tmo, out, true, c->D, M);
-    if (c->bf16)
+    // small M (one frame: 24 output tiles, K = 6272): split-K partials + one reduction kernel
+    const int ks = te && c->bn_embed == 128 ? splitk_plan(c, M, c->D, c->Pd) : 0;
+    if (ks) {
+      const vi_status r = splitk_resid(c, ks, c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, 0, 0, c->b_embed, nullptr,
+                                       static_cast<float*>(out), e.pos, nullptr, nullptr, nullptr, "embed gemm (split-K)");
+      if (r != VI_OK) return r;
+    } else if (c->bf16)
       PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, c->bn_embed, e, c->stream, 0,
                                            te ? &tmo : nullptr),
               "embed gemm");
@@ -1228,7 +1234,7 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   const int ks_o = te ? splitk_plan(c, M, D, D) : 0;
   if (ks_o) {
     const vi_status r = splitk_resid(c, ks_o, (c->sharded && !c->win_split) ? c->tm_og : c->tm_o, c->tm_wo, l * D, M, D,
-                                     D, eo.a_hs, eo.a_kpb, eo.bias, x_in, x_out, c->ln2_g + (size_t)l * D,
+                                     D, eo.a_hs, eo.a_kpb, eo.bias, x_in, x_out, nullptr, c->ln2_g + (size_t)l * D,
                                      c->ln2_b + (size_t)l * D, c->h, "o gemm (split-K)");
     if (r != VI_OK) return r;
   } else if (c->bf16)
@@ -1269,7 +1275,7 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   const int ks_2 = te ? splitk_plan(c, M, D, F) : 0;
   if (ks_2) {
     const vi_status r = splitk_resid(c, ks_2, c->tm_g, c->tm_w2, l * D, M, D, F, 0, 0, e2.bias, x_out, x_out, nullptr,
-                                     nullptr, nullptr, "ffn2 gemm (split-K)");
+                                     nullptr, nullptr, nullptr, "ffn2 gemm (split-K)");
     if (r != VI_OK) return r;
   } else if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, pair2 ? c->tm_w2_pair : c->tm_w2, l * D, M, D, F, pair2 ? 128 : c->bn_2, e2,

@@ -54,11 +54,12 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
 cudaError_t launch_layernorm(const float* x, const float* g, const float* b, void* out, int out_dtype, int rows,
                              int D, cudaStream_t st);
 // x fp32 [rows][D] -> [rows][2D] bf16 (hi | lo) for the extended-precision back projection
-// split-K reduction + residual (+ fused LayerNorm into h when g != NULL); ws partial s of row m
-// at ws + s * split_ld + m * D (fp32)
+// split-K reduction: out = x_in (NULL: none) + bias + sum of the partials (+ pos[m % P] when
+// pos != NULL), and LayerNorm(out) into h when g != NULL; ws partial s of row m at
+// ws + s * split_ld + m * D (fp32)
 cudaError_t launch_splitk_resid(const float* ws, int ksplit, size_t split_ld, const float* bias, const float* x_in,
-                                float* x_out, const float* g, const float* b, void* h, int h_dtype, int rows, int D,
-                                cudaStream_t st, unsigned long long* timing = nullptr);
+                                float* x_out, const float* pos, int P, const float* g, const float* b, void* h,
+                                int h_dtype, int rows, int D, cudaStream_t st, unsigned long long* timing = nullptr);
 cudaError_t launch_split_bf16(const float* x, void* out, int rows, int D, cudaStream_t st);
 // v [P][D] (row pitch src_ld elements) -> vt_slab[d][col0 + p] (row pitch ld)
 cudaError_t launch_transpose_to_slab(const void* v, void* vt_slab, int P, int D, size_t ld, size_t col0, int dtype,

@@ -103,16 +103,19 @@ __global__ void __launch_bounds__(256) layernorm_v4_kernel(const float4* __restr
   ln_row_v4<Tout, NV>(v, g, b, out, warp, D, lane);
 }
 
-// Split-K reduction (gemm_tc with Epi::ksplit > 1): row m of the residual output is
-// x_out = x_in + (bias + sum_s ws[s][m]) with the partials added in split order s = 0, 1, ...
-// (deterministic); LN (g != NULL) also writes LayerNorm(x_out) to h, i.e. the next pre-norm
-// (Q1) fused into the reduction.  One warp per row, D % 128 == 0, D <= 1024.
+// Split-K reduction (gemm_tc with Epi::ksplit > 1): row m of the output is
+// out = x_in + (bias + sum_s ws[s][m]) (x_in == NULL: no residual) with the partials added in
+// split order s = 0, 1, ... (deterministic), then + pos[m % P] when pos != NULL (the embedding's
+// positional table, the unsplit epilogue's order); LN (g != NULL) also writes LayerNorm(out)
+// to h, i.e. the next pre-norm (Q1) fused into the reduction.  One warp per row, D % 128 == 0,
+// D <= 1024.
 template <typename Tout, int NV, bool LN>
 __global__ void __launch_bounds__(256) splitk_resid_kernel(const float4* __restrict__ ws, int ksplit, size_t split_ld4,
                                                            const float4* __restrict__ bias, const float4* x_in,
-                                                           float4* x_out, const float4* __restrict__ g,
-                                                           const float4* __restrict__ b, Tout* __restrict__ h, int rows,
-                                                           int D, unsigned long long* timing) {
+                                                           float4* x_out, const float4* __restrict__ pos, int P,
+                                                           const float4* __restrict__ g, const float4* __restrict__ b,
+                                                           Tout* __restrict__ h, int rows, int D,
+                                                           unsigned long long* timing) {
   griddep_wait();
   if (threadIdx.x == 0) time_begin(timing);
   griddep_launch();
@@ -131,9 +134,16 @@ __global__ void __launch_bounds__(256) splitk_resid_kernel(const float4* __restr
     }
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      const float4 bb = __ldg(bias + i * 32 + lane), xi = x_in[r4 + i * 32 + lane];
-      v[i].x = xi.x + (v[i].x + bb.x); v[i].y = xi.y + (v[i].y + bb.y);
-      v[i].z = xi.z + (v[i].z + bb.z); v[i].w = xi.w + (v[i].w + bb.w);
+      const float4 bb = __ldg(bias + i * 32 + lane);
+      v[i].x += bb.x; v[i].y += bb.y; v[i].z += bb.z; v[i].w += bb.w;
+      if (x_in) {
+        const float4 xi = x_in[r4 + i * 32 + lane];
+        v[i].x = xi.x + v[i].x; v[i].y = xi.y + v[i].y; v[i].z = xi.z + v[i].z; v[i].w = xi.w + v[i].w;
+      }
+      if (pos) {
+        const float4 pp = __ldg(pos + (size_t)(warp % P) * (D / 4) + i * 32 + lane);
+        v[i].x += pp.x; v[i].y += pp.y; v[i].z += pp.z; v[i].w += pp.w;
+      }
       x_out[r4 + i * 32 + lane] = v[i];
     }
     if constexpr (LN) ln_row_v4<Tout, NV>(v, g, b, h, warp, D, lane);
@@ -145,25 +155,25 @@ __global__ void __launch_bounds__(256) splitk_resid_kernel(const float4* __restr
 }
 
 cudaError_t launch_splitk_resid(const float* ws, int ksplit, size_t split_ld, const float* bias, const float* x_in,
-                                float* x_out, const float* g, const float* b, void* h, int h_dtype, int rows, int D,
-                                cudaStream_t st, unsigned long long* timing) {
-  if (D % 128 || D > 1024 || ksplit < 1 || split_ld % 4) return cudaErrorInvalidValue;
+                                float* x_out, const float* pos, int P, const float* g, const float* b, void* h,
+                                int h_dtype, int rows, int D, cudaStream_t st, unsigned long long* timing) {
+  if (D % 128 || D > 1024 || ksplit < 1 || split_ld % 4 || (pos && P < 1)) return cudaErrorInvalidValue;
   const int blocks = (rows * 32 + 255) / 256;
   const size_t ld4 = split_ld / 4;
 #define SKR(NV)                                                                                                    \
   if (D == NV * 128) {                                                                                             \
     if (!g)                                                                                                        \
       pdl_launch(splitk_resid_kernel<bf16, NV, false>, dim3(blocks), dim3(256), 0, st, (const float4*)ws, ksplit,  \
-                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)nullptr,            \
-                 (const float4*)nullptr, (bf16*)nullptr, rows, D, timing);                                                 \
+                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)pos, P,             \
+                 (const float4*)nullptr, (const float4*)nullptr, (bf16*)nullptr, rows, D, timing);                 \
     else if (h_dtype == 0)                                                                                         \
       pdl_launch(splitk_resid_kernel<bf16, NV, true>, dim3(blocks), dim3(256), 0, st, (const float4*)ws, ksplit,   \
-                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)g,                  \
-                 (const float4*)b, (bf16*)h, rows, D, timing);                                                             \
+                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)pos, P,             \
+                 (const float4*)g, (const float4*)b, (bf16*)h, rows, D, timing);                                   \
     else                                                                                                           \
       pdl_launch(splitk_resid_kernel<float, NV, true>, dim3(blocks), dim3(256), 0, st, (const float4*)ws, ksplit,  \
-                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)g,                  \
-                 (const float4*)b, (float*)h, rows, D, timing);                                                            \
+                 ld4, (const float4*)bias, (const float4*)x_in, (float4*)x_out, (const float4*)pos, P,             \
+                 (const float4*)g, (const float4*)b, (float*)h, rows, D, timing);                                  \
     return cudaGetLastError();                                                                                     \
   }
   SKR(1) SKR(2) SKR(3) SKR(4) SKR(5) SKR(6) SKR(7) SKR(8)
