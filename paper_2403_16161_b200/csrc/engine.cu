@@ -142,6 +142,11 @@ struct vi_ctx {
   void* comm = nullptr;           // ncclComm_t (NULL: unsharded, or exchange driven by the caller)
   void* og = nullptr;
   int attn_layer = -1;            // layer whose _attn half ran last (its _ffn half pending)
+  // inside step_body (vi_run_step's own sequence of launches) a split-K reduction that
+  // produces a block input also writes that block's LN1 into h (fuse_ln1); h_ready = the
+  // layer whose LN1 is already in h (-1: none).  Never across public per-layer calls.
+  bool fuse_ln1 = false;
+  int h_ready = -1;
   cudaEvent_t ev_attn = nullptr, ev_gather = nullptr;   // vi_tp_local_allgather ordering
   Ring ring{0, 1};
   std::mutex mu;
@@ -1012,9 +1017,12 @@ extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out
     // small M (one frame: 24 output tiles, K = 6272): split-K partials + one reduction kernel
     const int ks = te && c->bn_embed == 128 ? splitk_plan(c, M, c->D, c->Pd) : 0;
     if (ks) {
+      const bool ln0 = c->fuse_ln1;   // block 0's LN1 in the same pass (inside vi_run_step only)
       const vi_status r = splitk_resid(c, ks, c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, 0, 0, c->b_embed, nullptr,
-                                       static_cast<float*>(out), e.pos, nullptr, nullptr, nullptr, "embed gemm (split-K)");
+                                       static_cast<float*>(out), e.pos, ln0 ? c->ln1_g : nullptr,
+                                       ln0 ? c->ln1_b : nullptr, ln0 ? c->h : nullptr, "embed gemm (split-K)");
       if (r != VI_OK) return r;
+      if (ln0) c->h_ready = 0;
     } else if (c->bf16)
       PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_tokens, c->tm_wembed, 0, M, c->D, c->Pd, c->bn_embed, e, c->stream, 0,
                                            te ? &tmo : nullptr),
@@ -1077,8 +1085,10 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   void* vl = static_cast<uint8_t*>(c->vtslab) + (size_t)l * c->vt_ld * Dl * es;
   const uint64_t valid = c->ring.valid_mask();
 
-  // a3: LN1
-  PLAUNCH(VI_PROF_ROW, launch_layernorm(x_in, c->ln1_g + (size_t)l * D, c->ln1_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln1");
+  // a3: LN1 (unless the reduction that produced x_in wrote it)
+  if (!(c->fuse_ln1 && c->h_ready == l))
+    PLAUNCH(VI_PROF_ROW, launch_layernorm(x_in, c->ln1_g + (size_t)l * D, c->ln1_b + (size_t)l * D, c->h, dt, M, D, c->stream), "ln1");
+  c->h_ready = -1;
   // a4: QKV projection + memory write
   Epi eq = epi_base(c, EPI_QKV, M, 3 * Dl, c->b_qkv + (size_t)l * 3 * Dl);
   eq.D = Dl; eq.q = c->q; eq.kslab = kl; eq.vtslab = vl; eq.first_slot = int(c->ring.cur_first % c->S);
@@ -1274,9 +1284,13 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
   const bool pair2 = te;
   const int ks_2 = te ? splitk_plan(c, M, D, F) : 0;
   if (ks_2) {
+    const bool ln_next = c->fuse_ln1 && l + 1 < c->L;   // the next block's LN1 in the same pass
     const vi_status r = splitk_resid(c, ks_2, c->tm_g, c->tm_w2, l * D, M, D, F, 0, 0, e2.bias, x_out, x_out, nullptr,
-                                     nullptr, nullptr, nullptr, "ffn2 gemm (split-K)");
+                                     ln_next ? c->ln1_g + (size_t)(l + 1) * D : nullptr,
+                                     ln_next ? c->ln1_b + (size_t)(l + 1) * D : nullptr, ln_next ? c->h : nullptr,
+                                     "ffn2 gemm (split-K)");
     if (r != VI_OK) return r;
+    if (ln_next) c->h_ready = l + 1;
   } else if (c->bf16)
     PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(c->tm_g, pair2 ? c->tm_w2_pair : c->tm_w2, l * D, M, D, F, pair2 ? 128 : c->bn_2, e2,
                                          c->stream, pair2 ? 1 : 0, te ? &tx_out : nullptr, te ? &tx_out : nullptr),
@@ -1407,12 +1421,20 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
 }
 
 // The device part of one step (split+embed, L blocks, back-projection+composite).
-static vi_status step_body(vi_ctx* c, const void* fin, int n, void* fout) {
+static vi_status step_body_seq(vi_ctx* c, const void* fin, int n, void* fout) {
   vi_status st;
   if ((st = vi_soft_split(c, fin, n, c->x_ws, 1)) != VI_OK) return st;
   for (int l = 0; l < c->L; ++l)
     if ((st = vi_memory_step(c, l, c->x_ws, c->x_ws)) != VI_OK) return st;
   return vi_soft_composite(c, c->x_ws, n, fout, 1);
+}
+static vi_status step_body(vi_ctx* c, const void* fin, int n, void* fout) {
+  c->fuse_ln1 = true;     // x_ws flows from block to block untouched: LN1 may ride on a reduction
+  c->h_ready = -1;
+  const vi_status st = step_body_seq(c, fin, n, fout);
+  c->fuse_ln1 = false;
+  c->h_ready = -1;
+  return st;
 }
 
 // Enqueue the device part of a step (after the push) on the ctx stream: replay of the step's

@@ -442,6 +442,32 @@ def test_c3_graph_replayed_8_block_step():
     assert ctx.launches() > 0
 
 
+def test_c3t1_run_step_equals_per_layer_calls():
+    """One frame per step (C3T1, 3 blocks): vi_run_step's graph, in which the split-K
+    reductions of the embedding and of FFN2 also write the next block's LN1, is bitwise equal
+    to the public per-layer calls (vi_soft_split / vi_memory_step / vi_soft_composite, no LN1
+    fusion across calls) on every step, and matches the oracle once the memory is full."""
+    from paper_2403_16161_b200 import vi
+    cfg = CONFIGS["C3T1"].replace(layers=3)
+    w = make_weights(cfg, seed=35)
+    ctx = vi.Context.from_synth(cfg)
+    ctx.set_weights(w)
+    eager = H().GpuStream(cfg, w)
+    o = O.OracleStream(cfg, w)
+    for i in range(12):
+        feats = make_features(cfg, 1, first_frame=i, seed=35)
+        f = torch.from_numpy(feats).to(torch.bfloat16).cuda()
+        out = torch.empty_like(f)
+        ctx.run_step(f, 1, out)
+        ctx.sync()
+        ge, _ = eager.step(feats, stages=False)
+        assert torch.equal(out, ge), f"step {i}: vi_run_step differs from the per-layer calls"
+        o.push(1)
+        ref, _ = o.step(feats)
+        if i >= 10:                  # memory full (10 frames + the new one)
+            assert_close(out, ref, 2e-2, f"step {i} out")
+
+
 def test_positional_embedding_bf16():
     """pos_embed = 1 (reading Q8: an additive [P, D] table at the split, never temporal): the
     oracle adds it in embed(); the GPU's embed GEMM epilogue adds it per token row."""
