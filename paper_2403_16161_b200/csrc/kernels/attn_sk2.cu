@@ -132,8 +132,10 @@ __device__ __forceinline__ int sk2_win_out_row(const AttnTC& a, int w, int q) {
 }
 
 // WIN: window attention compiled in (a separate instantiation, so the global-attention kernel
-// carries none of the window code: it measurably cost the C3 softmax loop registers)
-template <int HD, bool WIN>
+// carries none of the window code: it measurably cost the C3 softmax loop registers).
+// SINGLE (window units of one 128-query tile, AttnTC::sk_single): a third instantiation, so
+// the pair kernels' softmax loop carries none of its branches (they cost C3 2.5 %).
+template <int HD, bool WIN, bool SINGLE>
 __global__ void __launch_bounds__(576, 1)
 attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tk,
                const __grid_constant__ CUtensorMap tvt, const AttnTC a) {
@@ -202,7 +204,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   const uint32_t tmem = *tmem_slot;
   // single-tile window units are launched with programmatic dependent launch (no CTA waits on
   // another): the set-up above overlaps the previous kernel's tail
-  griddep_wait();
+  if (SINGLE) griddep_wait();
   if (threadIdx.x == 0) time_begin(a.timing);
   if (ct && threadIdx.x == 0) ct[1] = (long long)globaltimer();
   // debug timeline (VI_SK_TRACE): CTA 0, first segment's first 32 key tiles, 32 clock64 stamps per tile
@@ -332,7 +334,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       const bool t0_live = SK2_EXPERIMENT != 2;
       // single-tile units: tile 1 does not exist (no MMAs, no commits, no waits on its warps,
       // which leave at once); the K / V stages are released with tile 0's MMAs
-      const int tl = a.sk_single ? 0 : 1;
+      const int tl = SINGLE ? 0 : 1;
       mbar_wait(q_full, sg & 1);
       auto issue_pv = [&](int t, int j) {          // O_t (+)= P_t(j) V(j), j local to the segment
         const int g = jg + j, st = g % ST;
@@ -378,17 +380,77 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         __syncwarp();
       };
-      for (int j = 0; j < n; ++j)
-        for (int t = 0; t <= tl; ++t) {
-          if (j > 0) issue_pv(t, j - 1);
-          issue_qk(t, j);
+      if (SINGLE) {
+        // one Q tile, S double-buffered in the two S regions (S(j) in buffer j & 1, P(j) over
+        // it), O in tile 0's O: QK(j + 1) runs while the softmax works on S(j).  QK(j + 2)
+        // reuses buffer j & 1 after PV(j) in issue order (the tensor pipe completes in order).
+        // o_final[1] completes once per PV: the softmax's lazy O rescale at tile j waits for
+        // PV(j - 1) there.  One segment per CTA (the launch checks grid == units).
+        auto qk1 = [&](int j) {
+          const int g = jg + j, st = g % ST, b = j & 1;
+          mbar_wait(&k_full[st], (g / ST) & 1);
+          tc_fence_after();
+          const uint64_t dk = dk0 + uint64_t((st * L::KB) >> 4);
+          if (elect_one()) {
+            if (t0_live) {
+#pragma unroll
+              for (int kk = 0; kk < HD / 16; ++kk) {
+                const uint64_t off = uint64_t(((kk >> 2) * 16384 + (kk & 3) * 32) >> 4);
+                umma_bf16_ss(tmem + b * 128, dq0 + off, dk + off, idesc_s, kk > 0);
+              }
+            }
+            umma_commit(&s_full[b]);
+            if (ct && g == 0) ct[2] = (long long)globaltimer();
+            umma_commit(&k_empty[st]);
+          }
+          __syncwarp();
+        };
+        auto pv1 = [&](int j) {
+          const int g = jg + j, st = g % ST, b = j & 1;
+          mbar_wait(&v_full[st], (g / ST) & 1);
+          const uint64_t dv = dv0 + uint64_t((st * L::VB) >> 4);
+#pragma unroll
+          for (int hh = 0; hh < 2; ++hh) {
+            mbar_wait(&p_full[2 * b + hh], (j >> 1) & 1);
+            tc_fence_after();
+            if (elect_one()) {
+              if (t0_live) {
+#pragma unroll
+                for (int k4 = 0; k4 < 4; ++k4)
+                  umma_bf16_ts(tmem + 256, tmem + b * 128 + hh * 64 + k4 * 8,
+                               dv + uint64_t((hh * (HD * 128) + k4 * 32) >> 4), idesc_o, (j | hh | k4) != 0);
+              }
+              if (hh == 1) {
+                umma_commit(&v_empty[st]);
+                umma_commit(&o_final[1]);
+              }
+            }
+            __syncwarp();
+          }
+        };
+        qk1(0);
+        for (int j = 1; j < n; ++j) {
+          qk1(j);
+          pv1(j - 1);
         }
-      if (elect_one()) umma_commit(q_empty);       // all QK of the segment issued: Q smem free when done
-      __syncwarp();
-      for (int t = 0; t <= tl; ++t) {
-        issue_pv(t, n - 1);
-        if (elect_one()) umma_commit(&o_final[t]);
+        if (elect_one()) umma_commit(q_empty);
         __syncwarp();
+        pv1(n - 1);
+        if (elect_one()) umma_commit(&o_final[0]);
+        __syncwarp();
+      } else {
+        for (int j = 0; j < n; ++j)
+          for (int t = 0; t <= tl; ++t) {
+            if (j > 0) issue_pv(t, j - 1);
+            issue_qk(t, j);
+          }
+        if (elect_one()) umma_commit(q_empty);       // all QK of the segment issued: Q smem free when done
+        __syncwarp();
+        for (int t = 0; t <= tl; ++t) {
+          issue_pv(t, n - 1);
+          if (elect_one()) umma_commit(&o_final[t]);
+          __syncwarp();
+        }
       }
       if (ct && lane == 0) {
         const long long now = (long long)globaltimer();
@@ -399,14 +461,14 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       jg += n;
       w += n;
     }
-  } else if (warp < 16 && !(a.sk_single && warp >= 8)) {   // (single-tile units: tile 1's warps idle)
+  } else if (warp < 16 && !(SINGLE && warp >= 8)) {   // (single-tile units: tile 1's warps idle)
     const int t = warp >> 3;                        // Q tile
     const int hf = (warp >> 2) & 1;                 // key half / O column half
     const int qd = warp & 3;                        // TMEM lane quadrant
     const int row = qd * 32 + lane;                 // row within the Q tile
     const int pair_bar = 1 + t * 4 + qd;            // named barrier of warps (w, w ^ 4)
     const uint32_t lane_off = uint32_t(qd * 32) << 16;
-    const uint32_t TS = tmem + t * 128 + lane_off, TO = tmem + 256 + t * 128 + lane_off;
+    const uint32_t TO = tmem + 256 + t * 128 + lane_off;       // (S / P: TS per key tile below)
     constexpr int OH = HD / 2;                      // O columns of this half
     float* xch = reinterpret_cast<float*>(smem + L::XCH_OFF);
     const float2 cc = make_float2(a.scale_log2, a.scale_log2);
@@ -433,11 +495,14 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       float m_use = -INFINITY, l = 0.f;
       for (int j = 0; j < n; ++j) {
         const int g = jg + j;
-        mbar_wait(&s_full[t], g & 1);
+        // single-tile units: S(j) / P(j) in buffer j & 1 (see the MMA warp)
+        const int sb = SINGLE ? (g & 1) : t;
+        mbar_wait(&s_full[sb], SINGLE ? (g >> 1) & 1 : g & 1);
         if (dead) {
-          if (lane == 0) mbar_arrive(&p_full[2 * t + hf]);
+          if (lane == 0) mbar_arrive(&p_full[2 * sb + hf]);
           continue;
         }
+        const uint32_t TS = tmem + sb * 128 + lane_off;
         int row0, nv, nskip;
         sk2_key_tile(a.segs, ta + j, row0, nv, nskip);
         tc_fence_after();
@@ -506,6 +571,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         // The PV MMAs of EITHER key half accumulate into all O columns, so both warps of the
         // pair (same row maxima, same decision) finish their column half before either one
         // hands its P half over.  Rare (lazy threshold 2^8).
+        if (SINGLE && j > 0) mbar_wait(&o_final[1], (g - 1) & 1);   // PV(j - 1) done (every tile: phase order)
         if (__any_sync(0xffffffffu, grow) && j > 0) {
 #pragma unroll 1
           for (int c = 0; c < OH; c += 32) {
@@ -522,7 +588,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         tmem_wait_st();
         tc_fence_before();
         __syncwarp();                                  // every lane's P stores are complete ...
-        if (lane == 0) mbar_arrive(&p_full[2 * t + hf]);   // ... then one arrive per warp
+        if (lane == 0) mbar_arrive(&p_full[2 * sb + hf]);   // ... then one arrive per warp
         if (tr) trc[g * 32 + 4 + t * 8 + hf * 4 + qd] = clock64();
         const float2 s01 = fadd2(fadd2(sum[0], sum[1]), fadd2(sum[2], sum[3]));
         l = l * alpha + (s01.x + s01.y);
@@ -673,17 +739,18 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   }
 }
 
-template <int HD, bool WIN>
+template <int HD, bool WIN, bool SINGLE>
 static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
                                 const AttnTC& a, int grid, cudaStream_t st) {
   using L = AttnSk2Smem<HD>;
-  cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(attn_sk2_kernel<HD, WIN>), L::TOTAL);
+  auto kfn = attn_sk2_kernel<HD, WIN, SINGLE>;
+  cudaError_t e = ensure_kernel_setup(reinterpret_cast<const void*>(kfn), L::TOTAL);
   if (e != cudaSuccess) return e;
   // single-tile units run one CTA per unit (their tile-1 warps leave at once, so no unit may be
   // split): no CTA waits on another -> plain PDL launch
-  if (a.sk_single) {
+  if (SINGLE) {
     if (grid != a.units) return cudaErrorInvalidValue;
-    return pdl_launch(attn_sk2_kernel<HD, WIN>, dim3(grid), dim3(576), L::TOTAL, st, tq, tk, tvt, a);
+    return pdl_launch(kfn, dim3(grid), dim3(576), L::TOTAL, st, tq, tk, tvt, a);
   }
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = dim3(grid);
@@ -695,18 +762,24 @@ static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, c
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, attn_sk2_kernel<HD, WIN>, tq, tk, tvt, a);
+  return cudaLaunchKernelEx(&cfg, kfn, tq, tk, tvt, a);
 }
 
 cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,
                            int grid, cudaStream_t st) {
-  if (a.win_n) {
-    if (a.hd == 128) return launch_sk2_hd<128, true>(tq, tk, tvt, a, grid, st);
-    if (a.hd == 64) return launch_sk2_hd<64, true>(tq, tk, tvt, a, grid, st);
+  if (a.win_n && a.sk_single) {
+    if (a.hd == 128) return launch_sk2_hd<128, true, true>(tq, tk, tvt, a, grid, st);
+    if (a.hd == 64) return launch_sk2_hd<64, true, true>(tq, tk, tvt, a, grid, st);
     return cudaErrorInvalidValue;
   }
-  if (a.hd == 128) return launch_sk2_hd<128, false>(tq, tk, tvt, a, grid, st);
-  if (a.hd == 64) return launch_sk2_hd<64, false>(tq, tk, tvt, a, grid, st);
+  if (a.sk_single) return cudaErrorInvalidValue;   // (single-tile units exist for windows only)
+  if (a.win_n) {
+    if (a.hd == 128) return launch_sk2_hd<128, true, false>(tq, tk, tvt, a, grid, st);
+    if (a.hd == 64) return launch_sk2_hd<64, true, false>(tq, tk, tvt, a, grid, st);
+    return cudaErrorInvalidValue;
+  }
+  if (a.hd == 128) return launch_sk2_hd<128, false, false>(tq, tk, tvt, a, grid, st);
+  if (a.hd == 64) return launch_sk2_hd<64, false, false>(tq, tk, tvt, a, grid, st);
   return cudaErrorInvalidValue;
 }
 
