@@ -400,6 +400,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
               }
             }
             umma_commit(&s_full[b]);
+            if (trc && g < 32) trc[g * 32 + 24 + b] = clock64();
             if (ct && g == 0) ct[2] = (long long)globaltimer();
             umma_commit(&k_empty[st]);
           }

@@ -183,10 +183,11 @@ int main(int argc, char** argv) {
     const long long t0 = h[24];
     printf("per key tile j and Q tile t: S ready | row max exchanged | P written (half0 min..max, half1 min..max) | "
            "PV issue (half0, half1) | QK issued   (clk relative to the first QK)\n");
-    for (int j = 0; j < 32 && h[j * 32 + 24]; ++j) {
+    for (int j = 0; j < 32 && (h[j * 32 + 24] || h[j * 32 + 25]); ++j) {
       printf("%2d", j);
       for (int t = 0; t < 2; ++t) {
         const long long* e = &h[j * 32];
+        if (!e[24 + t]) continue;          // (single-tile units: tile j on warpgroup j % 2 only)
         long long pm[2][2];
         for (int hf = 0; hf < 2; ++hf) {
           pm[hf][0] = LLONG_MAX;
