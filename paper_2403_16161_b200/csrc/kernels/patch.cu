@@ -154,25 +154,32 @@ __global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__
   griddep_wait();
   griddep_launch();
   if (timing && threadIdx.x == 0) time_begin(timing);
-  constexpr int KK = KH * KW, PER = KK * CV;
+  constexpr int KK = KH * KW, PER = KK * CV, U = 4;   // U vectors per thread in flight
   const int P = g.oh * g.ow;
-  const int total = ntok * PER;
-  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
-    const int gt = i / PER, v = i - gt * PER;        // token, vector within the token
-    const int j = v / CV, cv = v - j * CV;
-    const int ky = j / KW, kx = j - ky * KW;
-    const int t = gt / P, tok = gt - t * P;
-    const int oy = tok / g.ow, ox = tok - oy * g.ow;
-    const int y = oy * g.sh - g.ph + ky, x = ox * g.sw - g.pw + kx;
-    T* d = out + (size_t)i * VEC;
-    if (y < 0 || y >= g.H || x < 0 || x >= g.W) {
-      Vec<T, VEC>::zero(d);
-    } else {
-      const T* src = in + (((size_t)t * g.H + y) * g.W + x) * (CV * VEC) + cv * VEC;
-      if constexpr (sizeof(T) == 2)
-        *reinterpret_cast<uint4*>(d) = __ldg(reinterpret_cast<const uint4*>(src));
-      else
-        *reinterpret_cast<float4*>(d) = __ldg(reinterpret_cast<const float4*>(src));
+  const int total = ntok * PER, stride = gridDim.x * blockDim.x;
+  for (int base = blockIdx.x * blockDim.x + threadIdx.x; base < total; base += U * stride) {
+    uint4 val[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * stride;
+      val[u] = make_uint4(0u, 0u, 0u, 0u);
+      if (i < total) {
+        const int gt = i / PER, v = i - gt * PER;        // token, vector within the token
+        const int j = v / CV, cv = v - j * CV;
+        const int ky = j / KW, kx = j - ky * KW;
+        const int t = gt / P, tok = gt - t * P;
+        const int oy = tok / g.ow, ox = tok - oy * g.ow;
+        const int y = oy * g.sh - g.ph + ky, x = ox * g.sw - g.pw + kx;
+        if (y >= 0 && y < g.H && x >= 0 && x < g.W) {
+          const T* src = in + (((size_t)t * g.H + y) * g.W + x) * (CV * VEC) + cv * VEC;
+          val[u] = __ldg(reinterpret_cast<const uint4*>(src));   // 16 B: 8 bf16 or 4 fp32
+        }
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int i = base + u * stride;
+      if (i < total) *reinterpret_cast<uint4*>(out + (size_t)i * VEC) = val[u];
     }
   }
   if (timing) {
@@ -263,9 +270,12 @@ cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int d
   if (g.kh == 7 && g.kw == 7) {
     const int CV = g.C / (dtype == 0 ? 8 : 4);
     const long long total = (long long)ntok * 49 * CV;
+    // 4 vectors per thread in flight when that still leaves >= 4 blocks per SM (C3: yes; one
+    // frame per step: no, there every vector gets its own thread)
+    const long long threads = (total + 3) / 4 >= 148LL * 4 * 256 ? (total + 3) / 4 : total;
 #define UF(T, V, CVV)                                                                                     \
     if (CV == CVV) {                                                                                      \
-      pdl_launch(unfold_fixed_kernel<T, V, CVV, 7, 7>, dim3(grid_cap(total)), dim3(256), 0, st, (const T*)in, (T*)out, g, ntok, timing); \
+      pdl_launch(unfold_fixed_kernel<T, V, CVV, 7, 7>, dim3(grid_cap(threads)), dim3(256), 0, st, (const T*)in, (T*)out, g, ntok, timing); \
       return cudaGetLastError();                                                                          \
     }
     if (dtype == 0) { UF(bf16, 8, 16) UF(bf16, 8, 5) UF(bf16, 8, 32) }
