@@ -614,8 +614,8 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   c->num_sms = prop.multiProcessorCount;
   if (c->bf16) {
     c->sk_part = (float*)A((size_t)c->num_sms * 256 * c->hd * 4);
-    c->sk_lse = (float*)A((size_t)c->num_sms * 256 * 4);
-    c->sk_flag = (int*)A((size_t)c->num_sms * 4);
+    c->sk_lse = (float*)A((size_t)2 * c->num_sms * 256 * 4);   // two piece slots per CTA
+    c->sk_flag = (int*)A((size_t)(c->num_sms + 1) * 8);   // (as [num_sms + 1] int64 slice starts)
     c->skws = (float*)A((size_t)c->num_sms * 128 * 128 * 4);
   }
   if (!ok) {
@@ -1174,7 +1174,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.npairs = a.win_npw;
     a.units = win_units;
     a.sk_single = single ? 1 : 0;
-    a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
+    a.spart = c->sk_part; a.slse = c->sk_lse; a.sbegin = reinterpret_cast<long long*>(c->sk_flag);
     a.sk_tail = 0; a.sk_tail_w = 16; a.sk_ucost = 0;
     a.sk_wfull = (long long)a.units * ntiles;
     const int split = single ? 1 : std::max(1, ws ? atoi(ws) : 2);
@@ -1187,7 +1187,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
     a.npairs = (a.Nq + 255) / 256;
     a.units = a.npairs * a.H;
-    a.spart = c->sk_part; a.slse = c->sk_lse; a.sflag = c->sk_flag;
+    a.spart = c->sk_part; a.slse = c->sk_lse; a.sbegin = reinterpret_cast<long long*>(c->sk_flag);
     const long long work = (long long)a.units * ntiles;
     // a last pair with an empty second tile (C3: 3600 = 14 x 256 + 16) skips tile 1's MMAs
     // and the dead softmax quadrants, but its key tiles still cost about a full pair's (the

@@ -170,6 +170,10 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   // published, 13 owner's merge done
   long long* const ct = (SK2_TRACE && a.cta_trace) ? a.cta_trace + (size_t)cta * 24 : nullptr;
   if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
+  if (!SINGLE && threadIdx.x == 0 && a.sbegin) {   // the slice starts, for sk2_combine_kernel
+    a.sbegin[cta] = w_begin;
+    if (cta == G - 1) a.sbegin[G] = w_end;
+  }
 
   if (warp == 16 && lane == 0) {
     tma_prefetch(&tq);
@@ -262,57 +266,6 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         __syncwarp();
       }
       w += tb - ta;
-    }
-    // Owner merge of a split unit (this CTA's last segment starts a unit it does not finish):
-    // once both Q tiles' last PVs are done (Q / K / V smem idle), bulk-load the pieces of CTAs
-    // cta+1 .. cta+np, LAST CTA first (its piece is that CTA's first segment, published long
-    // before the end), 32-column chunks per O half into NBH buffers each; a piece's first
-    // chunk also brings its 256 lse values.  The flag of a piece is acquired before its loads.
-    if (w_end > w_begin) {
-      const long long wl = w_end - 1;
-      const int u = int(wl / NT);
-      const long long ub = (long long)u * NT;
-      if (w_begin <= ub && w_end < ub + NT) {       // last segment = [ub, w_end): owner
-        // (not o_final: this warp may reach here before or after the MMA warp finishes either
-        // of the last two segments, and a parity wait cannot tell those phases apart)
-        mbar_wait(merge_go, 0);
-        int last = cta + 1;
-        while (last + 1 < G && sk2_begin(a, W, G, last + 1) < ub + NT) ++last;
-        const int np = last - cta, items = np * L::CPP;
-        for (int i = 0; i < items; ++i) {
-          const int c = cta + np - i / L::CPP, cc = i % L::CPP, b = i % L::NBH;
-          if (cc == 0 && lane == 0) {
-#ifdef VI_MBAR_TIMEOUT
-            for (long long it = 0; ld_acquire_gpu(a.sflag + c) == 0; ++it) {
-              __nanosleep(32);
-              if (it > (1ll << 22)) {
-                printf("[flag timeout] block %d waits for piece of CTA %d\n", cta, c);
-                __trap();
-              }
-            }
-#else
-            while (ld_acquire_gpu(a.sflag + c) == 0) __nanosleep(32);
-#endif
-            fence_proxy_async_global();                // the piece is read through the async proxy
-            if (ct && i + L::CPP >= items) ct[14] = (long long)globaltimer();   // last piece's flag seen
-          }
-          __syncwarp();
-          for (int hf = 0; hf < 2; ++hf) {
-            if (i >= L::NBH) mbar_wait(&merge_empty[hf * 3 + b], ((i / L::NBH) - 1) & 1);
-            if (lane == 0) {
-              uint64_t* bar = &merge_full[hf * 3 + b];
-              mbar_arrive_expect_tx(bar, L::CHUNK + (cc == 0 ? 1024u : 0u));
-              bulk_g2s(smem + (size_t)(hf * L::NBH + b) * 32768,
-                       reinterpret_cast<const uint8_t*>(a.spart) +
-                           ((size_t)c * (HD / 8) * 256 + (size_t)((hf * (HD / 2) + cc * L::PCOL) / 8) * 256) * 16,
-                       L::CHUNK, bar);
-              if (cc == 0)
-                bulk_g2s(smem + L::LSE_OFF + (hf * 2 + ((i / L::CPP) & 1)) * 1024, a.slse + (size_t)c * 256, 1024u, bar);
-            }
-            __syncwarp();
-          }
-        }
-      }
     }
   } else if (warp == 17) {
     // The whole warp walks the schedule (warp-uniform control flow keeps the descriptors in
@@ -627,11 +580,13 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         __syncwarp();
       };
-      if (ta > 0) {
-        // continuation piece: normalised partial (bf16: half the bytes the owner pulls in at
-        // the end of the launch) -> this CTA's slot, then raise the flag
+      if (ta > 0 || tb < NT) {
+        // part of a split unit: its normalised partial (bf16) + lse -> the CTA's piece slot
+        // (2c: its first segment, 2c + 1: its last); sk2_combine_kernel merges a unit's pieces
+        // after the launch (every CTA finishes its own work: no CTA waits on another)
         const float inv = 1.f / l;
-        uint4* dst = reinterpret_cast<uint4*>(a.spart) + (size_t)cta * (HD / 8) * 256 + r256;
+        const int slot = 2 * cta + (sg == 0 ? 0 : 1);
+        uint4* dst = reinterpret_cast<uint4*>(a.spart) + (size_t)slot * (HD / 8) * 256 + r256;
 #pragma unroll 1
         for (int c = 0; c < OH; c += 32) {
           float f[32];
@@ -645,75 +600,8 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         }
         tc_fence_before();
         mbar_arrive(&o_free[t]);
-        if (hf == 0) a.slse[(size_t)cta * 256 + r256] = lse_own;
-        sk2_bar_sync(9, 512);                         // every row of the slot written (CTA scope) ...
-        if (threadIdx.x == 0) {                      // ... then one cumulative gpu-scope release
-          __threadfence();
-          atomicExch(&a.sflag[cta], 1);
-          if (ct) ct[12] = (long long)globaltimer();
-        }
-      } else if (tb < NT) {
-        // owner of a split unit (always the last segment of this CTA): the producer warp
-        // streams the pieces in (see above); online-rescaled merge in that order: A <- A
-        // 2^(m - m') + 2^(lse_k - m') O_k, W likewise, out = A / W (own O enters normalised)
-        const long long unit_end = (long long)(u + 1) * NT;
-        int last = cta + 1;
-        while (last + 1 < G && sk2_begin(a, W, G, last + 1) < unit_end) ++last;
-        const int np = last - cta;
-        const int items = np * L::CPP;
-        mbar_arrive(merge_go);                       // this tile's MMAs are done: smem free for the pieces
-        if (ct && warp == 0 && lane == 0) ct[5] = (long long)globaltimer();
-        float m = lse_own, wsum = 1.f, alpha = 1.f, wk = 0.f;
-        const float sfirst = 1.f / l;
-#pragma unroll 1
-        for (int i = 0; i < items; ++i) {
-          const int cc = i % L::CPP, b = i % L::NBH;
-          mbar_wait(&merge_full[hf * 3 + b], (i / L::NBH) & 1);
-          if (ct && warp == 0 && lane == 0 && i + L::CPP >= items && cc == 0)
-            ct[15] = (long long)globaltimer();          // last piece's first chunk landed
-          if (cc == 0) {                               // a new piece: its weight, rescale A
-            const float lk = reinterpret_cast<const float*>(smem + L::LSE_OFF + (hf * 2 + ((i / L::CPP) & 1)) * 1024)[r256];
-            const float mn = fmaxf(m, lk);
-            const float am = ex2(m - mn);
-            alpha = am * (i == 0 ? sfirst : 1.f);
-            wk = ex2(lk - mn);
-            wsum = wsum * am + wk;
-            m = mn;
-          }
-          const uint4* stage = reinterpret_cast<const uint4*>(smem + (size_t)(hf * L::NBH + b) * 32768);
-          const bool last_piece = i + L::CPP >= items;
-#pragma unroll 1
-          for (int sub = 0; sub < L::PCOL / 32; ++sub) {
-            const int col = cc * L::PCOL + sub * 32;    // within the O half
-            float f[32];
-            tmem_ld32(TOh + col, reinterpret_cast<uint32_t*>(f));
-            tmem_wait_ld();
-#pragma unroll
-            for (int q8 = 0; q8 < 4; ++q8) {
-              const uint4 v = stage[(sub * 4 + q8) * 256 + r256];
-              const uint32_t w[4] = {v.x, v.y, v.z, v.w};
-#pragma unroll
-              for (int e = 0; e < 4; ++e) {
-                const float2 p2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&w[e]));
-                f[8 * q8 + 2 * e] = f[8 * q8 + 2 * e] * alpha + wk * p2.x;
-                f[8 * q8 + 2 * e + 1] = f[8 * q8 + 2 * e + 1] * alpha + wk * p2.y;
-              }
-            }
-            if (last_piece) {                          // last piece: normalise and write out
-              write_out16(col, f, 1.f / wsum);
-              write_out16(col + 16, f + 16, 1.f / wsum);
-            } else {
-              tmem_st32(TOh + col, reinterpret_cast<uint32_t*>(f));
-              tmem_wait_st();
-            }
-          }
-          mbar_arrive(&merge_empty[hf * 3 + b]);       // chunk buffer (and lse slot reads) done
-        }
-        if (ct && warp == 0 && lane == 0) ct[13] = (long long)globaltimer();
-        tc_fence_before();
-        mbar_arrive(&o_free[t]);
-        sk2_bar_sync(11, 512);                       // every row has read the slots
-        for (int k = threadIdx.x; k < np; k += 512) a.sflag[cta + 1 + k] = 0;
+        if (hf == 0) a.slse[(size_t)slot * 256 + r256] = lse_own;
+        if (ct && threadIdx.x == 0) ct[12] = (long long)globaltimer();
       } else {
         const float inv = 1.f / l;
 #pragma unroll 1
@@ -740,6 +628,92 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   }
 }
 
+// Merge of the split units (units whose key tiles several CTAs shared): every part wrote its
+// normalised partial (bf16) + lse to its CTA's piece slot; out = sum_k 2^(lse_k - M) O_k /
+// sum_k 2^(lse_k - M), online-rescaled over the parts in CTA order (deterministic); units
+// covered by one CTA were written by the attention.  The parts of a unit come from the slice
+// starts the attention's CTAs wrote (a.sbegin).  Block = (unit, 32 rows, 8 column groups),
+// thread = (row, 8 columns): lane = row, so a warp reads 512 contiguous bytes of a piece
+// ([HD/8][256 rows] x 16 B).
+template <int HD, bool WIN>
+__global__ void __launch_bounds__(256) sk2_combine_kernel(const AttnTC a, int G) {
+  griddep_wait();
+  if (threadIdx.x == 0) time_begin(a.timing);
+  griddep_launch();
+  constexpr int C8 = HD / 8;                    // 8-column groups per row
+  const int NT = a.segs.tile0[a.segs.n];
+  const int u = blockIdx.x;
+  const long long ub = (long long)u * NT, ue = ub + NT;
+  __shared__ int s_slot[32];
+  __shared__ int s_np;
+  __shared__ long long sb[257];                 // slice starts of the attention's CTAs ([G] = W)
+  for (int c = threadIdx.x; c <= G && c < 257; c += blockDim.x) sb[c] = __ldcg(a.sbegin + c);
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int lo = 0, hi = G - 1;                     // the CTA whose slice holds the unit's first tile
+    while (lo < hi) {
+      const int mid = (lo + hi + 1) >> 1;
+      if (sb[mid] <= ub) lo = mid;
+      else hi = mid - 1;
+    }
+    int np = 0;
+    for (int c = lo; c < G && sb[c] < ue && np < 32; ++c)
+      s_slot[np++] = 2 * c + (sb[c] >= ub ? 0 : 1);   // first / last segment of c
+    s_np = np;
+  }
+  __syncthreads();
+  const int np = s_np;
+  if (np > 1) {
+    const int r = blockIdx.y * 32 + (threadIdx.x & 31), c8 = blockIdx.z * 8 + (threadIdx.x >> 5);
+    int h, q0, win;
+    sk2_unit<WIN>(a, u, h, q0, win);
+    const int orow = WIN ? sk2_win_out_row(a, win, q0 + r) : (q0 + r < a.Nq ? q0 + r : -1);
+    if (orow >= 0) {
+      // online rescale over the parts in CTA order; each group of up to 4 parts has all its
+      // loads issued before the sums
+      const uint4* sp = reinterpret_cast<const uint4*>(a.spart);
+      float m = -INFINITY, wsum = 0.f, acc[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+      for (int k0 = 0; k0 < np; k0 += 4) {
+        float lk[4];
+        uint4 v[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          lk[k] = -INFINITY;
+          v[k] = make_uint4(0u, 0u, 0u, 0u);
+          if (k0 + k < np) {
+            const int slot = s_slot[k0 + k];
+            lk[k] = __ldcg(a.slse + (size_t)slot * 256 + r);
+            v[k] = __ldcg(sp + ((size_t)slot * C8 + c8) * 256 + r);
+          }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          if (k0 + k >= np) break;
+          const float mn = fmaxf(m, lk[k]);
+          const float sc = ex2(m - mn), w = ex2(lk[k] - mn);   // (sc = 0 for the first part)
+          wsum = wsum * sc + w;
+          const uint32_t wv[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+          for (int e = 0; e < 4; ++e) {
+            const float2 p2 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&wv[e]));
+            acc[2 * e] = acc[2 * e] * sc + w * p2.x;
+            acc[2 * e + 1] = acc[2 * e + 1] * sc + w * p2.y;
+          }
+          m = mn;
+        }
+      }
+      const float inv = 1.f / wsum;
+      *reinterpret_cast<uint4*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + c8 * 8) =
+          make_uint4(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv),
+                     pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
+    }
+  }
+  if (a.timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) time_end(a.timing, gridDim.x * gridDim.y * gridDim.z);
+  }
+}
+
 template <int HD, bool WIN, bool SINGLE>
 static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt,
                                 const AttnTC& a, int grid, cudaStream_t st) {
@@ -763,7 +737,11 @@ static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, c
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kfn, tq, tk, tvt, a);
+  e = cudaLaunchKernelEx(&cfg, kfn, tq, tk, tvt, a);
+  if (e != cudaSuccess) return e;
+  // the split units' pieces -> output rows
+  if (!a.sbegin || grid > 256) return cudaErrorInvalidValue;
+  return pdl_launch(sk2_combine_kernel<HD, WIN>, dim3(a.units, 8, HD / 64), dim3(256), 0, st, a, grid);
 }
 
 cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,

@@ -133,6 +133,7 @@ struct AttnTC {
   float* spart;             // [grid][256][hd]
   float* slse;              // [grid][256]
   int* sflag;               // [grid], 0 between launches
+  long long* sbegin;        // attn_sk2: [grid + 1] work-slice starts, written by the attention for the combine
   long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
   long long* cta_trace;     // attn_sk2: [grid][16] globaltimer stamps per CTA (micro-benchmarks; NULL = off)
   unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves

@@ -122,6 +122,9 @@ int main(int argc, char** argv) {
   cudaMalloc(&a.slse, (size_t)nsm * 2 * 256 * 4);
   cudaMalloc(&a.sflag, (size_t)(nsm * 2 + a.units + 8) * 4);
   cudaMemset(a.sflag, 0, (size_t)(nsm * 2 + a.units + 8) * 4);
+#ifndef VI_SK2_BASE
+  a.sbegin = reinterpret_cast<long long*>(a.sflag);   // (nsm + 1 int64 fit in the flag buffer)
+#endif
   const long long work = (long long)a.units * a.segs.tile0[1];
   // sk2 tail ordering (engine.cu): the last pair of each head has an empty second tile
   const int rem = Nq % 256;
@@ -146,6 +149,17 @@ int main(int argc, char** argv) {
   const double flop = 4.0 * Nq * (win ? 15.0 * WREAL : double(SP)) * D, us = 1e3 * ms / iters;
   printf("attn_sk%d C3: grid %d, %.2f us/launch, %.1f TFLOP/s (%s)\n", ver, grid, us, flop / (us * 1e-6) / 1e12,
          cudaGetErrorString(err));
+#ifndef VI_SK2_BASE
+  if (getenv("COMB_ONLY") && !win) {   // the split-unit combine kernel alone, back to back
+    cudaEventRecord(e0, st);
+    for (int i = 0; i < iters; ++i) sk2_combine_kernel<128, false><<<dim3(a.units, 8, 2), 256, 0, st>>>(a, grid);
+    cudaEventRecord(e1, st);
+    cudaStreamSynchronize(st);
+    float cms = 0.f;
+    cudaEventElapsedTime(&cms, e0, e1);
+    printf("combine alone: %.2f us/launch (%s)\n", 1e3 * cms / iters, cudaGetErrorString(cudaGetLastError()));
+  }
+#endif
   if (getenv("CTA_TRACE")) {   // per-CTA globaltimer stamps of one launch
     long long* ctb;
     cudaMalloc(&ctb, (size_t)grid * 24 * 8);
