@@ -202,7 +202,8 @@ struct vi_ctx {
   int num_sms = 148;
   float* skws = nullptr;   // split-K GEMM partials: <= num_sms work items of 128 x 128 fp32
   float *sk_part = nullptr, *sk_lse = nullptr;  // stream-K partial slots [num_sms][256][hd], [num_sms][256]
-  int* sk_flag = nullptr;                       // [num_sms], zero between launches
+  int* sk_flag = nullptr;                       // attn_sk2 unit parts [2][sk_units_cap]
+  int sk_units_cap = 0;
   // CUDA graphs of whole steps (vi_run_step), keyed by everything baked into the launches
   struct GraphEntry {
     std::vector<uint64_t> key;
@@ -615,7 +616,8 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   if (c->bf16) {
     c->sk_part = (float*)A((size_t)c->num_sms * 256 * c->hd * 4);
     c->sk_lse = (float*)A((size_t)2 * c->num_sms * 256 * 4);   // two piece slots per CTA
-    c->sk_flag = (int*)A((size_t)(c->num_sms + 1) * 8);   // (as [num_sms + 1] int64 slice starts)
+    c->sk_units_cap = ((c->QR + 255) / 256 + c->win_n + 1) * c->H;
+    c->sk_flag = (int*)A((size_t)2 * c->sk_units_cap * 4);   // stream-K unit parts [2][units]
     c->skws = (float*)A((size_t)c->num_sms * 128 * 128 * 4);
   }
   if (!ok) {
@@ -1174,12 +1176,13 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.npairs = a.win_npw;
     a.units = win_units;
     a.sk_single = single ? 1 : 0;
-    a.spart = c->sk_part; a.slse = c->sk_lse; a.sbegin = reinterpret_cast<long long*>(c->sk_flag);
+    a.spart = c->sk_part; a.slse = c->sk_lse; a.uparts = c->sk_flag;
     a.sk_tail = 0; a.sk_tail_w = 16; a.sk_ucost = 0;
     a.sk_wfull = (long long)a.units * ntiles;
     const int split = single ? 1 : std::max(1, ws ? atoi(ws) : 2);
     const long long work = (long long)a.units * ntiles;
     const int grid = int(std::min<long long>(std::min<long long>((long long)a.units * split, work), c->num_sms));
+    if (a.units > c->sk_units_cap) return c->fail(VI_E_ARG, "attention: more stream-K units than the context holds");
     PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
     return VI_OK;
   }
@@ -1187,7 +1190,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     // persistent stream-K: one CTA per SM over (query-tile pair, head) x key tiles
     a.npairs = (a.Nq + 255) / 256;
     a.units = a.npairs * a.H;
-    a.spart = c->sk_part; a.slse = c->sk_lse; a.sbegin = reinterpret_cast<long long*>(c->sk_flag);
+    a.spart = c->sk_part; a.slse = c->sk_lse; a.uparts = c->sk_flag;
     const long long work = (long long)a.units * ntiles;
     // a last pair with an empty second tile (C3: 3600 = 14 x 256 + 16) skips tile 1's MMAs
     // and the dead softmax quadrants, but its key tiles still cost about a full pair's (the
@@ -1200,6 +1203,7 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
     a.sk_ucost = sk_unit_cost();
     a.sk_wfull = (long long)(a.npairs - a.sk_tail) * a.H * ntiles;
     const int grid = int(work < c->num_sms ? work : c->num_sms);
+    if (a.units > c->sk_units_cap) return c->fail(VI_E_ARG, "attention: more stream-K units than the context holds");
     PLAUNCH(VI_PROF_ATTN, launch_attn_sk2(c->tm_q, c->tm_k, c->tm_vt, a, grid, c->stream), "attention");
   } else {   // small chunks (and windows beyond one wave): fixed KV split + combine kernel
     const int units = c->win_n ? a.win_n * a.win_npw * a.H : ((a.Nq + 255) / 256) * a.H;

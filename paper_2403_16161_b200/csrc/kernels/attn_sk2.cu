@@ -170,9 +170,15 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   // published, 13 owner's merge done
   long long* const ct = (SK2_TRACE && a.cta_trace) ? a.cta_trace + (size_t)cta * 24 : nullptr;
   if (ct && threadIdx.x == 0) ct[0] = (long long)globaltimer();
-  if (!SINGLE && threadIdx.x == 0 && a.sbegin) {   // the slice starts, for sk2_combine_kernel
-    a.sbegin[cta] = w_begin;
-    if (cta == G - 1) a.sbegin[G] = w_end;
+  if (!SINGLE && threadIdx.x == 0 && a.uparts && w_end > w_begin) {
+    // for sk2_combine_kernel: this CTA is the first part of the units starting in its slice
+    // (flag: the slice starts exactly there) and the last part of the units ending in it
+    const int NT_ = a.segs.tile0[a.segs.n];
+    for (long long uu = w_begin / NT_; uu * NT_ < w_end; ++uu) {
+      const long long ub_ = uu * NT_;
+      if (ub_ >= w_begin) a.uparts[uu] = cta | ((ub_ == w_begin ? 1 : 0) << 16);
+      if (ub_ + NT_ - 1 >= w_begin && ub_ + NT_ - 1 < w_end) a.uparts[a.units + uu] = cta;
+    }
   }
 
   if (warp == 16 && lane == 0) {
@@ -631,38 +637,20 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
 // Merge of the split units (units whose key tiles several CTAs shared): every part wrote its
 // normalised partial (bf16) + lse to its CTA's piece slot; out = sum_k 2^(lse_k - M) O_k /
 // sum_k 2^(lse_k - M), online-rescaled over the parts in CTA order (deterministic); units
-// covered by one CTA were written by the attention.  The parts of a unit come from the slice
-// starts the attention's CTAs wrote (a.sbegin).  Block = (unit, 32 rows, 8 column groups),
+// covered by one CTA were written by the attention.  The parts of a unit come from the first
+// and last CTAs the attention's CTAs recorded (a.uparts).  Block = (unit, 32 rows, 8 column groups),
 // thread = (row, 8 columns): lane = row, so a warp reads 512 contiguous bytes of a piece
 // ([HD/8][256 rows] x 16 B).
 template <int HD, bool WIN>
-__global__ void __launch_bounds__(256) sk2_combine_kernel(const AttnTC a, int G) {
+__global__ void __launch_bounds__(256) sk2_combine_kernel(const AttnTC a) {
   griddep_wait();
   if (threadIdx.x == 0) time_begin(a.timing);
   griddep_launch();
   constexpr int C8 = HD / 8;                    // 8-column groups per row
-  const int NT = a.segs.tile0[a.segs.n];
   const int u = blockIdx.x;
-  const long long ub = (long long)u * NT, ue = ub + NT;
-  __shared__ int s_slot[32];
-  __shared__ int s_np;
-  __shared__ long long sb[257];                 // slice starts of the attention's CTAs ([G] = W)
-  for (int c = threadIdx.x; c <= G && c < 257; c += blockDim.x) sb[c] = __ldcg(a.sbegin + c);
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    int lo = 0, hi = G - 1;                     // the CTA whose slice holds the unit's first tile
-    while (lo < hi) {
-      const int mid = (lo + hi + 1) >> 1;
-      if (sb[mid] <= ub) lo = mid;
-      else hi = mid - 1;
-    }
-    int np = 0;
-    for (int c = lo; c < G && sb[c] < ue && np < 32; ++c)
-      s_slot[np++] = 2 * c + (sb[c] >= ub ? 0 : 1);   // first / last segment of c
-    s_np = np;
-  }
-  __syncthreads();
-  const int np = s_np;
+  const int p0 = __ldcg(a.uparts + u), c1 = __ldcg(a.uparts + a.units + u);
+  const int c0 = p0 & 0xffff, b0 = p0 >> 16;     // first / last CTA of the unit
+  const int np = c1 - c0 + 1;                     // parts: c0 (its first segment iff b0), c0+1 .. c1
   if (np > 1) {
     const int r = blockIdx.y * 32 + (threadIdx.x & 31), c8 = blockIdx.z * 8 + (threadIdx.x >> 5);
     int h, q0, win;
@@ -681,7 +669,7 @@ __global__ void __launch_bounds__(256) sk2_combine_kernel(const AttnTC a, int G)
           lk[k] = -INFINITY;
           v[k] = make_uint4(0u, 0u, 0u, 0u);
           if (k0 + k < np) {
-            const int slot = s_slot[k0 + k];
+            const int slot = k0 + k == 0 ? 2 * c0 + (b0 ? 0 : 1) : 2 * (c0 + k0 + k);
             lk[k] = __ldcg(a.slse + (size_t)slot * 256 + r);
             v[k] = __ldcg(sp + ((size_t)slot * C8 + c8) * 256 + r);
           }
@@ -740,8 +728,8 @@ static cudaError_t launch_sk2_hd(const CUtensorMap& tq, const CUtensorMap& tk, c
   e = cudaLaunchKernelEx(&cfg, kfn, tq, tk, tvt, a);
   if (e != cudaSuccess) return e;
   // the split units' pieces -> output rows
-  if (!a.sbegin || grid > 256) return cudaErrorInvalidValue;
-  return pdl_launch(sk2_combine_kernel<HD, WIN>, dim3(a.units, 8, HD / 64), dim3(256), 0, st, a, grid);
+  if (!a.uparts || grid > 65535) return cudaErrorInvalidValue;   // (CTA index in 16 bits)
+  return pdl_launch(sk2_combine_kernel<HD, WIN>, dim3(a.units, 8, HD / 64), dim3(256), 0, st, a);
 }
 
 cudaError_t launch_attn_sk2(const CUtensorMap& tq, const CUtensorMap& tk, const CUtensorMap& tvt, const AttnTC& a,

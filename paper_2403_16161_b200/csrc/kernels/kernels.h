@@ -133,7 +133,8 @@ struct AttnTC {
   float* spart;             // [grid][256][hd]
   float* slse;              // [grid][256]
   int* sflag;               // [grid], 0 between launches
-  long long* sbegin;        // attn_sk2: [grid + 1] work-slice starts, written by the attention for the combine
+  int* uparts;              // attn_sk2 -> combine: [units] first CTA of each unit (| 1 << 16: its slice starts
+                            // at the unit) and [units] last CTA, written by the attention
   long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
   long long* cta_trace;     // attn_sk2: [grid][16] globaltimer stamps per CTA (micro-benchmarks; NULL = off)
   unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves

@@ -123,7 +123,7 @@ int main(int argc, char** argv) {
   cudaMalloc(&a.sflag, (size_t)(nsm * 2 + a.units + 8) * 4);
   cudaMemset(a.sflag, 0, (size_t)(nsm * 2 + a.units + 8) * 4);
 #ifndef VI_SK2_BASE
-  a.sbegin = reinterpret_cast<long long*>(a.sflag);   // (nsm + 1 int64 fit in the flag buffer)
+  a.uparts = a.sflag;   // (2 x units ints fit in the flag buffer)
 #endif
   const long long work = (long long)a.units * a.segs.tile0[1];
   // sk2 tail ordering (engine.cu): the last pair of each head has an empty second tile
@@ -152,7 +152,7 @@ int main(int argc, char** argv) {
 #ifndef VI_SK2_BASE
   if (getenv("COMB_ONLY") && !win) {   // the split-unit combine kernel alone, back to back
     cudaEventRecord(e0, st);
-    for (int i = 0; i < iters; ++i) sk2_combine_kernel<128, false><<<dim3(a.units, 8, 2), 256, 0, st>>>(a, grid);
+    for (int i = 0; i < iters; ++i) sk2_combine_kernel<128, false><<<dim3(a.units, 8, 2), 256, 0, st>>>(a);
     cudaEventRecord(e1, st);
     cudaStreamSynchronize(st);
     float cms = 0.f;
