@@ -455,6 +455,9 @@ def main():
     ap.add_argument("--tp", action="store_true",
                     help="one stream with its heads sharded over the N ranks (NCCL all-gather per block)")
     args = ap.parse_args()
+    if os.environ.get("VI_BENCH_WATCHDOG"):   # debugging: dump every thread's stack, then exit
+        import faulthandler
+        faulthandler.dump_traceback_later(float(os.environ["VI_BENCH_WATCHDOG"]), exit=True)
     from vi_synth import CONFIGS
     cfg = CONFIGS[args.config]
     if args.impl == "reference":

@@ -270,7 +270,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       int row0, nv, nskip;
       key_tile(a.segs, t_begin + jj, row0, nv, nskip);
       const bool tr = a.trace && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && lane == 0 && jj < 32;
-      mbar_wait(&s_full[t], jj & 1);
+      mbar_wait_warp(&s_full[t], jj & 1);
       if (ct && jj == 0 && threadIdx.x == 0) ct[2] = (long long)globaltimer();
       if (tr) a.trace[jj * 32 + t * 12 + qd] = clock64();
       tc_fence_after();
@@ -359,7 +359,7 @@ attn_tc2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
     const int orow = a.win_n ? win_out_row(a, win, q) : (q < a.Nq ? q : -1);
     const int qp = win_l * a.win_qstride + q;         // row of the KV-split partials (launch-local windows)
     if (n > 0) {
-      mbar_wait(&o_final[t], 0);
+      mbar_wait_warp(&o_final[t], 0);
       tc_fence_after();
     }
     if (ct && threadIdx.x == 0) ct[3] = (long long)globaltimer();

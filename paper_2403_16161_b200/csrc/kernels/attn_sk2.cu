@@ -68,10 +68,13 @@ __device__ __forceinline__ void sk2_key_tile(const KeySegs& s, int g, int& row0,
   nskip = off == 0 ? s.lead[i] : 0;
 }
 
+// bar.sync is .aligned: every lane of the warp must arrive converged
 __device__ __forceinline__ void sk2_named_bar_sync(int id, int n) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 __device__ __forceinline__ void sk2_bar_sync(int id, int n) {
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
@@ -229,7 +232,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       int h, q0, win;
       sk2_unit<WIN>(a, u, h, q0, win);
       const int wq = win * a.win_qstride, wk = win * a.win_kstride;   // window row offsets
-      if (sg > 0) mbar_wait(q_empty, (sg - 1) & 1);
+      if (sg > 0) mbar_wait_warp(q_empty, (sg - 1) & 1);
       if (elect_one()) {
         mbar_arrive_expect_tx(q_full, 2 * L::QB);
 #pragma unroll
@@ -244,11 +247,11 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         sk2_key_tile(a.segs, j, row0, nv, nskip);
         const int st = jg % ST;
         const uint32_t par = ((jg / ST) & 1) ^ 1;
-        if (jg >= ST) mbar_wait(&k_empty[st], par);
+        if (jg >= ST) mbar_wait_warp(&k_empty[st], par);
         if (SK2_EXPERIMENT >= 3) {   // micro only: no K / V traffic (operands stale)
           if (elect_one()) mbar_arrive(&k_full[st]);
           __syncwarp();
-          if (jg >= ST) mbar_wait(&v_empty[st], par);
+          if (jg >= ST) mbar_wait_warp(&v_empty[st], par);
           if (elect_one()) mbar_arrive(&v_full[st]);
           __syncwarp();
           continue;
@@ -261,7 +264,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
             tma_load_2d(sk + at * 16384, &tk, &k_full[st], h * HD + at * 64, a.krow_base + wk + row0);
         }
         __syncwarp();
-        if (jg >= ST) mbar_wait(&v_empty[st], par);
+        if (jg >= ST) mbar_wait_warp(&v_empty[st], par);
         if (elect_one()) {
           uint8_t* sv = smem + L::V_OFF + st * L::VB;
           mbar_arrive_expect_tx(&v_full[st], L::VB);
@@ -294,15 +297,15 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       // single-tile units: tile 1 does not exist (no MMAs, no commits, no waits on its warps,
       // which leave at once); the K / V stages are released with tile 0's MMAs
       const int tl = SINGLE ? 0 : 1;
-      mbar_wait(q_full, sg & 1);
+      mbar_wait_warp(q_full, sg & 1);
       auto issue_pv = [&](int t, int j) {          // O_t (+)= P_t(j) V(j), j local to the segment
         const int g = jg + j, st = g % ST;
-        if (t == 0) mbar_wait(&v_full[st], (g / ST) & 1);
-        if (j == 0 && sg > 0) mbar_wait(&o_free[t], (sg - 1) & 1);   // previous segment's O read out
+        if (t == 0) mbar_wait_warp(&v_full[st], (g / ST) & 1);
+        if (j == 0 && sg > 0) mbar_wait_warp(&o_free[t], (sg - 1) & 1);   // previous segment's O read out
         const uint64_t dv = dv0 + uint64_t((st * L::VB) >> 4);
 #pragma unroll
         for (int hh = 0; hh < 2; ++hh) {
-          mbar_wait(&p_full[2 * t + hh], g & 1);
+          mbar_wait_warp(&p_full[2 * t + hh], g & 1);
           tc_fence_after();
           if (elect_one()) {
             if (trc && g < 32) trc[g * 32 + 20 + hh * 6 + t] = clock64();
@@ -320,7 +323,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       auto issue_qk = [&](int t, int j) {          // S_t = Q_t K(j)^T
         const int g = jg + j, st = g % ST;
         if (t == 0) {
-          mbar_wait(&k_full[st], (g / ST) & 1);
+          mbar_wait_warp(&k_full[st], (g / ST) & 1);
           tc_fence_after();
         }
         const uint64_t dk = dk0 + uint64_t((st * L::KB) >> 4), dq = dq0 + uint64_t((t * L::QB) >> 4);
@@ -347,7 +350,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         // PV(j - 1) there.  One segment per CTA (the launch checks grid == units).
         auto qk1 = [&](int j) {
           const int g = jg + j, st = g % ST, b = j & 1;
-          mbar_wait(&k_full[st], (g / ST) & 1);
+          mbar_wait_warp(&k_full[st], (g / ST) & 1);
           tc_fence_after();
           const uint64_t dk = dk0 + uint64_t((st * L::KB) >> 4);
           if (elect_one()) {
@@ -367,11 +370,11 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         };
         auto pv1 = [&](int j) {
           const int g = jg + j, st = g % ST, b = j & 1;
-          mbar_wait(&v_full[st], (g / ST) & 1);
+          mbar_wait_warp(&v_full[st], (g / ST) & 1);
           const uint64_t dv = dv0 + uint64_t((st * L::VB) >> 4);
 #pragma unroll
           for (int hh = 0; hh < 2; ++hh) {
-            mbar_wait(&p_full[2 * b + hh], (j >> 1) & 1);
+            mbar_wait_warp(&p_full[2 * b + hh], (j >> 1) & 1);
             tc_fence_after();
             if (elect_one()) {
               if (t0_live) {
@@ -457,7 +460,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         const int g = jg + j;
         // single-tile units: S(j) / P(j) in buffer j & 1 (see the MMA warp)
         const int sb = SINGLE ? (g & 1) : t;
-        mbar_wait(&s_full[sb], SINGLE ? (g >> 1) & 1 : g & 1);
+        mbar_wait_warp(&s_full[sb], SINGLE ? (g >> 1) & 1 : g & 1);
         if (dead) {
           if (lane == 0) mbar_arrive(&p_full[2 * sb + hf]);
           continue;
@@ -531,7 +534,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         // The PV MMAs of EITHER key half accumulate into all O columns, so both warps of the
         // pair (same row maxima, same decision) finish their column half before either one
         // hands its P half over.  Rare (lazy threshold 2^8).
-        if (SINGLE && j > 0) mbar_wait(&o_final[1], (g - 1) & 1);   // PV(j - 1) done (every tile: phase order)
+        if (SINGLE && j > 0) mbar_wait_warp(&o_final[1], (g - 1) & 1);   // PV(j - 1) done (every tile: phase order)
         if (__any_sync(0xffffffffu, grow) && j > 0) {
 #pragma unroll 1
           for (int c = 0; c < OH; c += 32) {
@@ -554,7 +557,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
         l = l * alpha + (s01.x + s01.y);
       }
       // ---- segment epilogue: each warp owns O columns [hf*64, +64) of its 32 rows
-      mbar_wait(&o_final[t], sg & 1);
+      mbar_wait_warp(&o_final[t], sg & 1);
       tc_fence_after();
       if (ct && warp == 0 && lane == 0) ct[4] = (long long)globaltimer();
       l += exchange(l);                             // row sum over both key halves

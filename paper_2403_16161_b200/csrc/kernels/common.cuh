@@ -48,6 +48,7 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  // (one thread; a whole warp waits with mbar_wait_warp)
   const uint32_t a = smem_u32(bar);
 #ifdef VI_MBAR_TIMEOUT
   // debug builds (micro-benchmarks of new kernels): trap instead of hanging the GPU
@@ -57,20 +58,35 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
         "{\n\t.reg .pred p;\n\t"
         "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
         "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(a), "r"(parity) : "memory");
-    if (n > (1ll << 21)) {
-      printf("[mbar timeout] block %d warp %d lane %d smem %u parity %u\n", blockIdx.x, threadIdx.x >> 5,
-             threadIdx.x & 31, a, parity);
-      __trap();
-    }
+    // every thread still waiting after 2^21 polls reports once (the whole wait cycle shows up),
+    // the kernel traps after 2^23
+    if (n == (1ll << 21) && (threadIdx.x & 31) == 0)
+      printf("[mbar timeout] grid %d block %d of %d threads, warp %d smem %u parity %u\n", gridDim.x,
+             blockIdx.x, blockDim.x, threadIdx.x >> 5, a, parity);
+    if (n > (1ll << 23)) __trap();
   }
 #else
-  asm volatile(
-      "{\n\t.reg .pred p;\n"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n}" ::"r"(a), "r"(parity)
-      : "memory");
+  uint32_t done;
+  do {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n}" : "=r"(done) : "r"(a), "r"(parity) : "memory");
+  } while (!done);
 #endif
+}
+// A whole warp waits for a phase: every lane polls, and the warp meets (full-mask __syncwarp)
+// before and after.  Without the meetings the lanes could fall out of step: one lane saw the
+// phase complete and ran ahead alone (into the next .aligned tcgen05.ld / bar.sync and the
+// next phase) while its siblings still polled -- and once the barrier had moved on by another
+// phase they polled for a parity that looked incomplete forever.  cuda-gdb on a hung C3 step
+// (the stream-K attention, ~1 in 10^4 steps) showed exactly that: a softmax warp with lane 0
+// past the S wait and lanes 1-31 still in it.  (Polling by lane 0 alone also cured it, but
+// put a wake-up on the softmax's critical path: C3 attention 0.60 -> 0.36 of peak.)
+__device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
+  __syncwarp();
+  mbar_wait(bar, parity);
+  __syncwarp();
 }
 
 // ------------------------------------------------------------------ TMA

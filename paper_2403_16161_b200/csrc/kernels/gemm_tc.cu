@@ -26,7 +26,8 @@
 
 namespace vi {
 
-__device__ __forceinline__ void gemm_named_bar_sync(int id, int n) {
+__device__ __forceinline__ void gemm_named_bar_sync(int id, int n) {   // (.aligned: converged warps)
+  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
@@ -237,7 +238,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
         }
         __syncwarp();
       }
-      mbar_wait(&tfull[acc], (lt >> 1) & 1);
+      mbar_wait_warp(&tfull[acc], (lt >> 1) & 1);
       if (lt < 4 && ew == 0 && lane == 0) GTR(7 + lt);
       tc_fence_after();
       const int m = m0 + q * 32 + lane;
@@ -297,7 +298,7 @@ gemm_tc_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ 
                 *reinterpret_cast<bf16*>(vb + (h2 + i) * 16) = __float2bfloat16_rn(v[i]);
             } else if (resid || epi.out_f32) {
               if (resid) {
-                mbar_wait(&xbar[2 * ew + bi], (xphase >> bi) & 1u);
+                mbar_wait_warp(&xbar[2 * ew + bi], (xphase >> bi) & 1u);
                 xphase ^= 1u << bi;
               }
 #pragma unroll

@@ -4,10 +4,14 @@
 // vector of token (oy, ox) is ordered (ky, kx, c); feature maps are channels-last.
 //   unfold: Tp[t][oy*ow+ox][(ky*kw+kx)*C + c] = F[t][oy*sh-ph+ky][ox*sw-pw+kx][c] (0 if outside)
 //   fold:   out[t][y][x][c] = (sum over windows covering (y,x), in token order) / count
-// Both are written as GATHERS with one thread per 16-byte vector of the output, so
-// every output byte is written once, coalesced, without atomics (deterministic), and
-// the overlapping reads (each input cell is read by up to 9 windows) hit L1/L2.
+// Both are written as GATHERS, so every output byte is written once, coalesced, without
+// atomics (deterministic), and the overlapping reads (each input cell is read by up to 9
+// windows) hit L1/L2: the 7x7 unfold with one warp per token (its patch vector is kh runs of
+// kw*C contiguous input elements; 8 16-byte loads per lane in flight before the stores), the
+// fold with one thread per 16-byte vector of an output cell.
 // The fold sums in fp32 and divides with IEEE round-to-nearest (no fast-math).
+#include <cstdlib>
+
 #include "kernels.h"
 
 namespace vi {
@@ -247,6 +251,52 @@ __global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__
   }
 }
 
+// ---- warp-per-token unfold (7x7 patches) --------------------------------------------------
+// One warp per token: the token's patch vector is KH runs (one per kernel row ky) of KW
+// consecutive input cells, i.e. KH contiguous spans of KW*C elements of the input row y; the
+// warp issues all its 16-B loads (R per lane) before any store.  Same bytes as unfold_fixed.
+template <typename T, int CV, int KH, int KW, int R>
+__global__ void __launch_bounds__(256) unfold_warp_kernel(const T* __restrict__ in, T* __restrict__ out, Geom g,
+                                                          int ntok, unsigned long long* timing) {
+  griddep_wait();
+  griddep_launch();
+  if (timing && threadIdx.x == 0) time_begin(timing);
+  constexpr int PER = KH * KW * CV, VEC = 16 / sizeof(T);
+  const int gt = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (gt < ntok) {
+    const int P = g.oh * g.ow, t = gt / P, tok = gt - t * P;
+    const int oy = tok / g.ow, ox = tok - oy * g.ow;
+    const int ybase = oy * g.sh - g.ph, xbase = ox * g.sw - g.pw;
+    const T* in_t = in + (size_t)t * g.H * g.W * (CV * VEC);
+    uint4* dst = reinterpret_cast<uint4*>(out + (size_t)gt * PER * VEC);
+#pragma unroll 1
+    for (int v0 = 0; v0 < PER; v0 += 32 * R) {
+      uint4 val[R];
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int v = v0 + r * 32 + lane;
+        val[r] = make_uint4(0u, 0u, 0u, 0u);
+        if (v < PER) {
+          const int j = v / CV, cv = v - j * CV;
+          const int ky = j / KW, kx = j - ky * KW;
+          const int y = ybase + ky, x = xbase + kx;
+          if (y >= 0 && y < g.H && x >= 0 && x < g.W)
+            val[r] = __ldg(reinterpret_cast<const uint4*>(in_t + ((size_t)y * g.W + x) * (CV * VEC)) + cv);
+        }
+      }
+#pragma unroll
+      for (int r = 0; r < R; ++r) {
+        const int v = v0 + r * 32 + lane;
+        if (v < PER) dst[v] = val[r];
+      }
+    }
+  }
+  if (timing) {
+    __syncthreads();
+    if (threadIdx.x == 0) time_end(timing, gridDim.x);
+  }
+}
+
 template <> struct Vec<bf16, 4> {
   static __device__ __forceinline__ void ld(const bf16* p, float* f) {
     uint2 u = *reinterpret_cast<const uint2*>(p);
@@ -264,9 +314,31 @@ static int grid_cap(long long total, int per_block = 256) {
   return int(b < 148 * 32 ? (b ? b : 1) : 148 * 32);
 }
 
+// VI_PATCH_V=0 (A/B only): the 7x7 unfold as per-vector gathers (unfold_fixed_kernel) instead
+// of one warp per token (tests/test_gpu_patch_variants.py: bitwise equal)
+static int patch_variant() {
+  static const int v = [] {
+    const char* e = getenv("VI_PATCH_V");
+    return e && e[0] == '0' ? 0 : 1;
+  }();
+  return v;
+}
+
 cudaError_t launch_unfold(const void* in, void* out, int n, const Geom& g, int dtype, cudaStream_t st,
                           unsigned long long* timing) {
   const int ntok = n * g.oh * g.ow;
+  if (g.kh == 7 && g.kw == 7 && patch_variant() == 1) {
+    const int CV = g.C / (dtype == 0 ? 8 : 4);
+    const int blocks = (ntok + 7) / 8;   // 8 warps (tokens) per block
+#define UW(T, CVV)                                                                                        \
+    if (CV == CVV) {                                                                                      \
+      pdl_launch(unfold_warp_kernel<T, CVV, 7, 7, 8>, dim3(blocks), dim3(256), 0, st, (const T*)in, (T*)out, g, ntok, timing); \
+      return cudaGetLastError();                                                                          \
+    }
+    if (dtype == 0) { UW(bf16, 16) UW(bf16, 5) }
+    else { UW(float, 10) UW(float, 32) }
+#undef UW
+  }
   if (g.kh == 7 && g.kw == 7) {
     const int CV = g.C / (dtype == 0 ? 8 : 4);
     const long long total = (long long)ntok * 49 * CV;
