@@ -414,6 +414,9 @@ def run_ours(args, cfg):
     # the fixed 7x7 / stride-3 kernels) when every patch launch of the step was timed, else the
     # CUDA events around eager launches (mode 2: includes each launch's ramp without overlap)
     n_patch = 2 + (2 * cfg.layers if cfg.ffn_kind == 1 else 0)
+    if os.environ.get("VI_PATCH_TIME_ONLY"):   # one patch kernel kind self-timed (engine.cu patch_timing)
+        print(f"patch kind {os.environ['VI_PATCH_TIME_ONLY']}: {sub[3]['patch'][0] / extra_steps:.4f} ms/step "
+              f"({sub[3]['patch'][1] / extra_steps:.0f} launches)", file=sys.stderr)
     self_timed = sub[3]["patch"][1] == n_patch * extra_steps
     patch_ms = max((sub[3] if self_timed else sub[2])["patch"][0] / extra_steps, 1e-9)
     patch_ms_events = sub[2]["patch"][0] / extra_steps

@@ -550,6 +550,7 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
   }
   c->vt_ld = (c->KR + 63) / 64 * 64;
   c->bf16 = cfg->dtype == VI_DTYPE_BF16; c->es = c->bf16 ? 2 : 4;
+
   {
     const int G = cfg->tp_size < 1 ? 1 : cfg->tp_size;
     c->sharded = G > 1 || cfg->nccl_id != nullptr;
@@ -951,9 +952,15 @@ extern "C" vi_status vi_memory_state(vi_ctx* c, int64_t* slot_id, uint8_t* refin
 
 // ------------------------------------------------------------------------------ compute
 
-// the patch kernels' self-timing slot (vi_profile mode 3) or NULL
-static unsigned long long* patch_timing(const vi_ctx* c) {
-  return c->prof_mode == 3 ? c->attn_timing + 2 * (sizeof(KernelTiming) / sizeof(unsigned long long)) : nullptr;
+// the patch kernels' self-timing slot (vi_profile mode 3) or NULL; VI_PATCH_TIME_ONLY=<kind>
+// (s split, f F3N fold, u F3N unfold, c composite) times that kernel alone (breakdowns)
+static unsigned long long* patch_timing(const vi_ctx* c, char kind) {
+  static const char only = [] {
+    const char* e = getenv("VI_PATCH_TIME_ONLY");
+    return e && e[0] ? e[0] : '\0';
+  }();
+  if (c->prof_mode != 3 || (only && only != kind)) return nullptr;
+  return c->attn_timing + 2 * (sizeof(KernelTiming) / sizeof(unsigned long long));
 }
 static Epi epi_base(const vi_ctx* c, int kind, int M, int N, const float* bias) {
   Epi e;
@@ -1009,7 +1016,7 @@ extern "C" vi_status vi_soft_split(vi_ctx* c, const void* feat, int n, void* out
   if (project && !c->have_weights) return c->fail(VI_E_PROTOCOL, "vi_soft_split: weights not set");
   const int dt = c->bf16 ? 0 : 1;
   void* tok = project ? c->tokens : out;
-  PLAUNCH(VI_PROF_PATCH, launch_unfold(feat, tok, n, c->g, dt, c->stream, patch_timing(c)), "unfold");
+  PLAUNCH(VI_PROF_PATCH, launch_unfold(feat, tok, n, c->g, dt, c->stream, patch_timing(c, 's')), "unfold");
   if (project) {
     const int M = n * c->P;
     Epi e = epi_base(c, EPI_STORE, M, c->D, c->b_embed);
@@ -1278,8 +1285,8 @@ static vi_status step_ffn(vi_ctx* c, int l, const float* x_in, float* x_out) {
             "ffn1 gemm");
   if (f3n) {
     // g = GELU(unfold(fold(u))) = unfold(GELU(fold(u))): GELU once per folded cell
-    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, dt, n, c->gf, true, c->stream, patch_timing(c)), "f3n fold");
-    PLAUNCH(VI_PROF_PATCH, launch_unfold(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream, patch_timing(c)), "f3n unfold");
+    PLAUNCH(VI_PROF_PATCH, launch_fold(c->u, 1, c->fold_ws, dt, n, c->gf, true, c->stream, patch_timing(c, 'f')), "f3n fold");
+    PLAUNCH(VI_PROF_PATCH, launch_unfold(c->fold_ws, c->gbuf, n, c->gf, dt, c->stream, patch_timing(c, 'u')), "f3n unfold");
   }
   // a11: FFN2 + residual
   Epi e2 = epi_base(c, EPI_RESID, M, D, c->b_2 + (size_t)l * D);
@@ -1419,7 +1426,7 @@ extern "C" vi_status vi_soft_composite(vi_ctx* c, const void* in, int n, void* f
     tok = c->bf16 ? c->yp32 : c->tokens;
   }
   PLAUNCH(VI_PROF_PATCH, launch_fold(tok, (project && c->bf16) ? 1 : dt, feat, dt, n, c->g, false, c->stream,
-                                     patch_timing(c)),
+                                     patch_timing(c, 'c')),
           "fold");
   return VI_OK;
 }

@@ -68,13 +68,8 @@ __device__ __forceinline__ void sk2_key_tile(const KeySegs& s, int g, int& row0,
   nskip = off == 0 ? s.lead[i] : 0;
 }
 
-// bar.sync is .aligned: every lane of the warp must arrive converged
+// (bar.sync is .aligned: callers are converged -- every wait ends in a full-warp meeting)
 __device__ __forceinline__ void sk2_named_bar_sync(int id, int n) {
-  __syncwarp();
-  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
-}
-__device__ __forceinline__ void sk2_bar_sync(int id, int n) {
-  __syncwarp();
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 

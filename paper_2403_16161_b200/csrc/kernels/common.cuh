@@ -75,16 +75,16 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
   } while (!done);
 #endif
 }
-// A whole warp waits for a phase: every lane polls, and the warp meets (full-mask __syncwarp)
-// before and after.  Without the meetings the lanes could fall out of step: one lane saw the
-// phase complete and ran ahead alone (into the next .aligned tcgen05.ld / bar.sync and the
-// next phase) while its siblings still polled -- and once the barrier had moved on by another
-// phase they polled for a parity that looked incomplete forever.  cuda-gdb on a hung C3 step
-// (the stream-K attention, ~1 in 10^4 steps) showed exactly that: a softmax warp with lane 0
-// past the S wait and lanes 1-31 still in it.  (Polling by lane 0 alone also cured it, but
-// put a wake-up on the softmax's critical path: C3 attention 0.60 -> 0.36 of peak.)
+// A whole warp waits for a phase: every lane polls, then the 32 lanes meet (full-mask
+// __syncwarp) before any of them goes on.  Without the meeting the lanes could fall out of
+// step: one lane saw the phase complete and ran ahead alone (through .aligned tcgen05.ld / st
+// and bar.sync, and its own arrive) into the next phase while its siblings still polled -- and
+// once the barrier had moved on by another phase they polled for a parity that looked
+// incomplete forever.  cuda-gdb on a hung C3 step (the stream-K attention, ~1 in 10^4 steps)
+// showed exactly that: a softmax warp with lane 0 past the S wait and lanes 1-31 still in it
+// (profiles/r02_hang.md).  No phase can complete twice while a warp is inside one of its
+// waits: every barrier a warp waits on needs that warp's own progress for its next phase.
 __device__ __forceinline__ void mbar_wait_warp(uint64_t* bar, uint32_t parity) {
-  __syncwarp();
   mbar_wait(bar, parity);
   __syncwarp();
 }
