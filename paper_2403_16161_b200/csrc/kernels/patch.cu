@@ -192,30 +192,42 @@ __global__ void __launch_bounds__(256) unfold_fixed_kernel(const T* __restrict__
   }
 }
 
-template <typename Tin, typename Tout, int VEC, int CV, int KH, int KW, int SH, int SW, bool GELU>
-__global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g,
+// (4 CTAs of 256 threads per SM: all 9 window loads of a thread stay in flight.  Capping the
+// registers for 6 or 8 CTAs per SM, no spills, made the compiler serialise the loads: the F3N
+// fold 0.057 -> 0.145 / 0.217 ms per C3 step)
+// HH, WW > 0: the output map is HH x WW with padding (KH - 1) / 2 (the memory step's shapes:
+// 60 x 108, 7x7 / 3 / 3 -> 20 x 36 tokens) -- every index division is by a constant and the
+// input offsets are 32-bit (the launcher checks the tensor fits); the same arithmetic in the
+// same order as the runtime-geometry instantiation (bitwise equal results)
+template <typename Tin, typename Tout, int VEC, int CV, int KH, int KW, int SH, int SW, bool GELU, int HH = 0, int WW = 0>
+__global__ void __launch_bounds__(256, 4) fold_fixed_kernel(const Tin* __restrict__ in, Tout* __restrict__ out, Geom g,
                                                          int ncell, unsigned long long* timing) {
   griddep_wait();
   griddep_launch();
   if (timing && threadIdx.x == 0) time_begin(timing);
   constexpr int KK = KH * KW, C = CV * VEC;
   constexpr int MAXC = (KH + SH - 1) / SH > (KW + SW - 1) / SW ? (KH + SH - 1) / SH : (KW + SW - 1) / SW;
-  const int P = g.oh * g.ow;
+  constexpr bool CG = HH > 0 && WW > 0;
+  constexpr int CPH = (KH - 1) / 2, CPW = (KW - 1) / 2;
+  constexpr int COH = CG ? (HH + 2 * CPH - KH) / SH + 1 : 1, COW = CG ? (WW + 2 * CPW - KW) / SW + 1 : 1;
+  const int H = CG ? HH : g.H, W = CG ? WW : g.W, ph = CG ? CPH : g.ph, pw = CG ? CPW : g.pw;
+  const int oh = CG ? COH : g.oh, ow = CG ? COW : g.ow;
+  const int P = oh * ow;
   const int total = ncell * CV;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
     const int cell = i / CV, cv = i - cell * CV;
-    const int tw = cell / g.W, x = cell - tw * g.W;
-    const int t = tw / g.H, y = tw - t * g.H;
-    const int yy = y + g.ph, xx = x + g.pw;
+    const int tw = cell / W, x = cell - tw * W;
+    const int t = tw / H, y = tw - t * H;
+    const int yy = y + ph, xx = x + pw;
     int oy0 = yy - KH + 1;
     oy0 = oy0 <= 0 ? 0 : (oy0 + SH - 1) / SH;
     int oy1 = yy / SH;
-    oy1 = oy1 < g.oh - 1 ? oy1 : g.oh - 1;
+    oy1 = oy1 < oh - 1 ? oy1 : oh - 1;
     int ox0 = xx - KW + 1;
     ox0 = ox0 <= 0 ? 0 : (ox0 + SW - 1) / SW;
     int ox1 = xx / SW;
-    ox1 = ox1 < g.ow - 1 ? ox1 : g.ow - 1;
-    const Tin* in_t = in + (size_t)t * P * KK * C + cv * VEC;
+    ox1 = ox1 < ow - 1 ? ox1 : ow - 1;
+    const Tin* in_t = in + (CG ? (size_t)(unsigned)(t * P * KK * C) : (size_t)t * P * KK * C) + cv * VEC;
     float acc[VEC];
 #pragma unroll
     for (int k = 0; k < VEC; ++k) acc[k] = 0.f;
@@ -227,7 +239,10 @@ __global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__
         if (oy0 + a <= oy1 && ox0 + b <= ox1) {
           const int oy = oy0 + a, ox = ox0 + b;
           const int ky = yy - oy * SH, kx = xx - ox * SW;
-          Vec<Tin, VEC>::ld(in_t + ((size_t)(oy * g.ow + ox) * KK + ky * KW + kx) * C, f[a][b]);
+          if constexpr (CG)
+            Vec<Tin, VEC>::ld(in_t + (unsigned)(((oy * ow + ox) * KK + ky * KW + kx) * C), f[a][b]);
+          else
+            Vec<Tin, VEC>::ld(in_t + ((size_t)(oy * ow + ox) * KK + ky * KW + kx) * C, f[a][b]);
         }
 #pragma unroll
     for (int a = 0; a < MAXC; ++a)
@@ -243,7 +258,10 @@ __global__ void __launch_bounds__(256) fold_fixed_kernel(const Tin* __restrict__
       acc[k] = __fdiv_rn(acc[k], c);
       if (GELU) acc[k] = gelu_erf(acc[k]);
     }
-    Vec<Tout, VEC>::st(out + (size_t)cell * C + cv * VEC, acc);
+    if constexpr (CG)
+      Vec<Tout, VEC>::st(out + (unsigned)(cell * C + cv * VEC), acc);
+    else
+      Vec<Tout, VEC>::st(out + (size_t)cell * C + cv * VEC, acc);
   }
   if (timing) {
     __syncthreads();
@@ -315,7 +333,8 @@ static int grid_cap(long long total, int per_block = 256) {
 }
 
 // VI_PATCH_V=0 (A/B only): the 7x7 unfold as per-vector gathers (unfold_fixed_kernel) instead
-// of one warp per token (tests/test_gpu_patch_variants.py: bitwise equal)
+// of one warp per token, and the fold with runtime geometry instead of the compile-time
+// 60 x 108 map (tests/test_gpu_patch_variants.py: bitwise equal)
 static int patch_variant() {
   static const int v = [] {
     const char* e = getenv("VI_PATCH_V");
@@ -369,10 +388,17 @@ cudaError_t launch_fold(const void* in, int in_dtype, void* out, int out_dtype, 
   const int blocks = n * g.H;
   if (g.kh == 7 && g.kw == 7 && g.sh == 3 && g.sw == 3) {
     const int ncell = n * g.H * g.W;
+    // the memory step's map (60 x 108, padding 3): compile-time geometry, 32-bit offsets
+    const bool c3 = g.H == 60 && g.W == 108 && g.ph == 3 && g.pw == 3 && g.oh == 20 && g.ow == 36 &&
+                    (long long)n * g.oh * g.ow * 49 * g.C < (1ll << 31) && patch_variant() == 1;
 #define FF(TI, TO, V, CVV)                                                                                    \
     if (g.C == CVV * V) {                                                                                     \
       const long long total = (long long)ncell * CVV;                                                        \
-      if (gelu)                                                                                               \
+      if (c3 && gelu)                                                                                         \
+        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true, 60, 108>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell, timing); \
+      else if (c3)                                                                                            \
+        pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false, 60, 108>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell, timing); \
+      else if (gelu)                                                                                          \
         pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, true>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell, timing); \
       else                                                                                                    \
         pdl_launch(fold_fixed_kernel<TI, TO, V, CVV, 7, 7, 3, 3, false>, dim3(grid_cap(total)), dim3(256), 0, st, (const TI*)in, (TO*)out, g, ncell, timing); \
