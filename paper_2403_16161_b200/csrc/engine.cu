@@ -1162,9 +1162,10 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   a.opart = c->opart; a.lse = c->lse;
   a.timing = (c->prof_mode == 1 || c->prof_mode == 3) ? c->attn_timing : nullptr;
   // Stream-K needs enough (query-pair, head) units: with few units (a chunk of one frame:
-  // 720 queries -> 12 units for 148 SMs) every unit splits ~12 ways and its owner merges the
-  // pieces serially, so small chunks take the fixed KV split + parallel combine kernel
-  // (C3, T = 1: 28 us vs 60 us per block; T = 5: stream-K 84 us vs ~93 us).
+  // 720 queries -> 12 units for 148 SMs) every unit splits ~12 ways, so small chunks take the
+  // fixed KV split + parallel combine kernel (round 1, owner merge: C3T1 28 vs 60 us per block;
+  // round 2, PDL-launched stream-K + combine kernel: C3T1 step 0.603 vs 0.598 ms, C2 0.436 vs
+  // 0.441 -- mixed, the KV split stays).
   const int sk_units = ((a.Nq + 255) / 256) * a.H;
   const bool small = sk_units * 4 < c->num_sms;
   // window attention: sk2 over (head, window, query pair) units, stream-K split over up to
