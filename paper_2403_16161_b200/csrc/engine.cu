@@ -200,7 +200,8 @@ struct vi_ctx {
   int prof_mode = 0;
   unsigned long long* attn_timing = nullptr;   // KernelTiming (device), used in profile mode 1
   int num_sms = 148;
-  float* skws = nullptr;   // split-K GEMM partials: <= num_sms work items of 128 x 128 fp32
+  float* skws = nullptr;   // split-K GEMM partials (splitk_plan)
+  size_t skws_floats = 0;
   float *sk_part = nullptr, *sk_lse = nullptr;  // stream-K partial slots [num_sms][256][hd], [num_sms][256]
   int* sk_flag = nullptr;                       // attn_sk2 unit parts [2][sk_units_cap]
   int sk_units_cap = 0;
@@ -619,7 +620,9 @@ extern "C" vi_status vi_create_ex(vi_ctx** out, const vi_config* cfg) {
     c->sk_lse = (float*)A((size_t)2 * c->num_sms * 256 * 4);   // two piece slots per CTA
     c->sk_units_cap = ((c->QR + 255) / 256 + c->win_n + 1) * c->H;
     c->sk_flag = (int*)A((size_t)2 * c->sk_units_cap * 4);   // stream-K unit parts [2][units]
-    c->skws = (float*)A((size_t)c->num_sms * 128 * 128 * 4);
+    // split-K partials: num_sms 128 x 128 tiles, or two k-halves of a CTA-pair-tiled chunk
+    c->skws_floats = std::max((size_t)c->num_sms * 128 * 128, (size_t)2 * ((rows + 255) / 256 * 256) * D);
+    c->skws = (float*)A(c->skws_floats * 4);
   }
   if (!ok) {
     delete c;
@@ -971,15 +974,27 @@ static Epi epi_base(const vi_ctx* c, int kind, int M, int N, const float* bias) 
   return e;
 }
 
-// Split-K plan for a residual GEMM [M x N] += A[M x K] W^T with single-CTA 128 x 128 tiles:
-// when the output has at most num_sms / 2 tiles (one frame per chunk, the paper's T = 1 mode)
-// most SMs would idle, so every tile's k-blocks are cut into ks consecutive ranges, one work
-// item each (<= num_sms items: the workspace holds num_sms 128 x 128 fp32 partials).
-// Returns ks (0 = do not split).
+// Split-K plan for a residual GEMM [M x N] += A[M x K] W^T.
+//  * single-CTA 128 x 128 tiles: when the output has at most num_sms / 2 tiles (one frame per
+//    chunk, the paper's T = 1 mode) most SMs would idle, so every tile's k-blocks are cut into
+//    ks consecutive ranges, one work item each (<= num_sms items).
+//  * CTA-pair 256 x 256 tiles, ks = 2 (returned with kSplitPair set): the patch embedding at
+//    full chunks (K = 6272; C3: 15 x 2 pair tiles -> 60 work items on 74 SM pairs).  A 256 x 256
+//    pair tile runs the MMA at the full per-SM rate where 128 x 128 tiles are operand-bound at
+//    about half of it (tools/micro/gemm_splitk: embedding + LN 41.0 -> 33.3 us); block 0's LN1
+//    rides on the reduction.  (FFN2, K = 1960, measured no faster in the step.)
+// Returns 0 (do not split), ks, or ks | kSplitPair.
+static constexpr int kSplitPair = 1 << 8;
 static int splitk_plan(const vi_ctx* c, int M, int N, int K) {
   if (!splitk_enabled() || !c->bf16 || !c->skws || N % 128) return 0;
   const int out = (M + 127) / 128 * (N / 128), nk = (K + 63) / 64;
-  if (out * 2 > c->num_sms) return 0;
+  if (out * 2 > c->num_sms) {
+    const int pair_tiles = (M + 255) / 256 * (N / 256);
+    if (N % 256 || K < 4096 || 2 * pair_tiles > c->num_sms / 2 ||
+        (size_t)2 * ((M + 255) / 256 * 256) * N > c->skws_floats)
+      return 0;
+    return 2 | kSplitPair;
+  }
   int ks = std::min(std::min(c->num_sms / out, 8), nk);
   if (ks < 2) return 0;
   const int kper = (nk + ks - 1) / ks;
@@ -988,11 +1003,14 @@ static int splitk_plan(const vi_ctx* c, int M, int N, int K) {
 }
 
 // x_out = x_in + bias + A W^T through ks split-K partials and the deterministic reduction
-// (which also writes LayerNorm(x_out) to h when ln_g != NULL)
-static vi_status splitk_resid(vi_ctx* c, int ks, const CUtensorMap& amap, const CUtensorMap& wmap, int brow0, int M,
+// (which also writes LayerNorm(x_out) to h when ln_g != NULL).  plan = splitk_plan's value;
+// with kSplitPair the partials come from CTA-pair 256 x 256 tiles (wmap's box: 64 x 128).
+static vi_status splitk_resid(vi_ctx* c, int plan, const CUtensorMap& amap, const CUtensorMap& wmap, int brow0, int M,
                               int N, int K, int a_hs, int a_kpb, const float* bias, const float* x_in, float* x_out,
                               const float* pos, const float* ln_g, const float* ln_b, void* h, const char* where) {
-  const int kpad = (M + 127) / 128 * 128;
+  const bool pair = plan & kSplitPair;
+  const int ks = plan & (kSplitPair - 1);
+  const int kpad = pair ? (M + 255) / 256 * 256 : (M + 127) / 128 * 128;
   Epi e = epi_base(c, EPI_STORE, M, N, nullptr);
   e.out = c->skws; e.ldo = N; e.out_f32 = 1;
   e.ksplit = ks; e.kpad_rows = kpad;
@@ -1000,7 +1018,8 @@ static vi_status splitk_resid(vi_ctx* c, int ks, const CUtensorMap& amap, const 
   CUtensorMap tws;
   if (!make_tmap_out(&tws, c->skws, true, N, (uint64_t)ks * kpad))
     return c->fail(VI_E_CUDA, std::string(where) + ": split-K workspace map");
-  PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(amap, wmap, brow0, M, N, K, 128, e, c->stream, 0, &tws, nullptr), where);
+  PLAUNCH(VI_PROF_GEMM, launch_gemm_tc(amap, wmap, brow0, M, N, K, pair ? 256 : 128, e, c->stream, pair ? 1 : 0, &tws, nullptr),
+          where);
   PLAUNCH(VI_PROF_GEMM,
           launch_splitk_resid(c->skws, ks, (size_t)kpad * N, bias, x_in, x_out, pos, c->P, ln_g, ln_b, h, c->bf16 ? 0 : 1, M, N,
                               c->stream, e.timing),
