@@ -44,18 +44,10 @@ struct AttnSk2Smem {
   static constexpr int K_OFF = 2 * QB;
   static constexpr int V_OFF = K_OFF + ST * KB;
   static constexpr int BAR_OFF = V_OFF + ST * VB;
-  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2 + 12 + 1;   // + merge_full / merge_empty [2][3], merge_go
+  static constexpr int NBAR = 2 + 4 * ST + 2 + 4 + 2 + 2;
   static constexpr int STG_OFF = (BAR_OFF + NBAR * 8 + 16 + 127) / 128 * 128;   // [16 warps][32 rows][48 B] output staging
   static constexpr int XCH_OFF = STG_OFF + 16 * 32 * 48;        // [2 phases][2 tiles][2 halves][128] fp32
-  static constexpr int LSE_OFF = XCH_OFF + 2 * 2 * 2 * 128 * 4;   // [2 halves][2 piece parities][256] fp32 (merge)
-  static constexpr int TOTAL = LSE_OFF + 2 * 2 * 256 * 4 + 1024;
-  // owner merge: 32 KB chunk buffers over the idle Q / K / V smem, NBH per O column half; a
-  // piece (a split unit's normalised partial O, bf16 [HD/8][256 rows] x 8 columns) arrives in
-  // chunks of PCOL columns of one O half
-  static constexpr int NBH = (3 * 512 * HD / 32768) / 2 > 3 ? 3 : (3 * 512 * HD / 32768) / 2;
-  static constexpr int PCOL = HD / 2 < 64 ? HD / 2 : 64;
-  static constexpr int CPP = (HD / 2) / PCOL;                   // chunks per piece half
-  static constexpr uint32_t CHUNK = 256u * PCOL * 2u;           // bytes
+  static constexpr int TOTAL = XCH_OFF + 2 * 2 * 2 * 128 * 4 + 1024;
 };
 
 __device__ __forceinline__ void sk2_key_tile(const KeySegs& s, int g, int& row0, int& nvalid, int& nskip) {
@@ -152,10 +144,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
   uint64_t* p_full = s_full + 2;      // [2 tiles][2 key halves]
   uint64_t* o_final = p_full + 4;     // [2] all PV of a segment done
   uint64_t* o_free = o_final + 2;     // [2] O read out by the epilogue
-  uint64_t* merge_full = o_free + 2;  // [2 halves][3 buffers] bulk loads of a split unit's pieces
-  uint64_t* merge_empty = merge_full + 6;   // [2 halves][3 buffers] chunk consumed (256 arrivals)
-  uint64_t* merge_go = merge_empty + 6;     // the owner's 512 softmax threads are past both tiles' last PV
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(merge_go + 1);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(o_free + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int NT = a.segs.tile0[a.segs.n];
@@ -198,11 +187,6 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
       mbar_init(&o_final[t], 1);
       mbar_init(&o_free[t], 256);
     }
-    for (int b = 0; b < 6; ++b) {
-      mbar_init(&merge_full[b], 1);
-      mbar_init(&merge_empty[b], 256);
-    }
-    mbar_init(merge_go, 512);
     fence_barrier_init();
   }
   if (warp == 17) tmem_alloc(tmem_slot, 512);
