@@ -20,3 +20,16 @@ def test_reference_arm_json_line():
     assert line["cpu_baseline"]["kind"] == "oracle" and line["cpu_baseline"]["cores"] >= 1
     assert line["e2e"]["h2d_bytes_per_step"] == 0
     assert "workload" in line["config"]
+
+
+def test_oracle_timing_tool_c1():
+    """tools/oracle_timing.py (SURVEY §8(d) oracle timing): one JSON line per (config, cores),
+    the 1-core line really pinned to one BLAS thread."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "tools", "oracle_timing.py"), "--configs", "C1", "--steps", "1"],
+                       capture_output=True, text=True, timeout=300, cwd=ROOT)
+    assert r.returncode == 0, r.stderr[-2000:]
+    lines = [json.loads(s) for s in r.stdout.strip().splitlines()]
+    assert len(lines) == 2 and all(l["config"] == "C1" for l in lines)
+    assert lines[0]["cores"] >= 1 and lines[1]["cores"] == 1
+    for l in lines:
+        assert l["frames_per_s"] > 0 and l["steps"] == 1 and l["kind"].startswith("oracle")
