@@ -245,3 +245,23 @@ def test_head_sharded_window_attention_c4_shape_g8():
     8 ranks = 4 heads x 2 halves of the window rows."""
     cfg = CONFIGS["C4"].replace(layers=2)
     _run_group(cfg, make_weights(cfg, seed=6, variant="sensitive"), 8, ns=[5, 5, 5, 5])
+
+
+def test_bench_tp_one_rank_json_line():
+    """`bench.py --tp` (the strong-scaling head-sharded run: NCCL all-gather inside every block)
+    launched as the driver launches N = 1: one JSON line with the contract's keys, scaling
+    "strong", the NCCL parallelism named, and the kernels counted."""
+    import json
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "bench.py"), "--tp", "--config", "C3T1", "--steps", "5",
+                        "--warmup", "3", "--no-cpu-baseline"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stderr[-3000:]
+    line = json.loads(r.stdout.strip().splitlines()[-1])
+    for k in ("metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better", "scaling",
+              "dtype", "config", "e2e", "gpu_launches", "roofline", "clocks"):
+        assert k in line, k
+    assert line["scaling"] == "strong" and line["value"] > 0 and line["gpu_launches"] > 0
+    assert "NCCL" in line["config"]["parallelism"]
