@@ -287,7 +287,10 @@ void* vi_stream(const vi_ctx* ctx);
 /* Device-side timing of the context's own kernels with CUDA events on its stream.
  * mode 0 = off, 1 = memory attention only (kernel self-timing, graph-safe),
  * 2 = every category (CUDA events; eager launches), 3 = attention, GEMMs and the patch
- * kernels of the fixed 7x7 / stride-3 geometry (kernel self-timing inside the step graph).  vi_profile_read waits for the stream, then returns per category
+ * kernels of the fixed 7x7 / stride-3 geometry (kernel self-timing inside the step graph),
+ * 4 = as 1 but the attention kernel alone (the split-merge kernel that follows it untimed).
+ * Modes 1 and 3 time the attention as its kernel's window plus the split-merge kernel's.
+ * vi_profile_read waits for the stream, then returns per category
  * the summed milliseconds and the number of timed launches and resets the counters.
  * Categories: VI_PROF_ATTN, VI_PROF_GEMM (all tensor-core / SIMT GEMMs),
  * VI_PROF_PATCH (soft split / composite / F3N fold-unfold), VI_PROF_ROW (LN, casts). */

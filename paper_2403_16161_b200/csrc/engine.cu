@@ -1179,7 +1179,8 @@ static vi_status step_attn(vi_ctx* c, int l, const float* x_in) {
   }
   const int ntiles = a.segs.tile0[a.segs.n];
   a.opart = c->opart; a.lse = c->lse;
-  a.timing = (c->prof_mode == 1 || c->prof_mode == 3) ? c->attn_timing : nullptr;
+  a.timing = (c->prof_mode == 1 || c->prof_mode == 3 || c->prof_mode == 4) ? c->attn_timing : nullptr;
+  a.combine_timing = c->prof_mode == 4 ? nullptr : a.timing;   // mode 4: the attention kernel alone
   // Stream-K needs enough (query-pair, head) units: with few units (a chunk of one frame:
   // 720 queries -> 12 units for 148 SMs) every unit splits ~12 ways, so small chunks take the
   // fixed KV split + parallel combine kernel (round 1, owner merge: C3T1 28 vs 60 us per block;
@@ -1637,7 +1638,7 @@ extern "C" vi_status vi_sync(vi_ctx* c) {
 extern "C" vi_status vi_profile(vi_ctx* c, int mode) {
   LIVE(c);
   DeviceGuard dg_(c->cfg.device);
-  if (mode < 0 || mode > 3) return VI_E_ARG;
+  if (mode < 0 || mode > 4) return VI_E_ARG;
   c->prof_mode = mode;
   return VI_OK;
 }

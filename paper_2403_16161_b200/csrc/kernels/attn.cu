@@ -450,7 +450,7 @@ cudaError_t launch_attn_tc2(const CUtensorMap& tq, const CUtensorMap& tk, const 
 constexpr int kMaxZ = 16;
 __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnTC a) {
   griddep_wait();
-  if (threadIdx.x == 0) time_begin(a.timing);
+  if (threadIdx.x == 0) time_begin(a.combine_timing);
   griddep_launch();
   const int G = a.hd / 4;                                   // lanes per row: 32 (d 128) or 16 (d 64)
   const int sub = (threadIdx.x & 31) % G;
@@ -481,9 +481,9 @@ __global__ void __launch_bounds__(256) attn_combine_kernel(const AttnTC a) {
     *reinterpret_cast<uint2*>(a.o + (size_t)orow * a.o_ld + (size_t)h * a.o_hs + sub * 4) =
         make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv), pack_bf16(acc[2] * inv, acc[3] * inv));
   }
-  if (a.timing) {
+  if (a.combine_timing) {
     __syncthreads();
-    if (threadIdx.x == 0) time_end(a.timing, gridDim.x);
+    if (threadIdx.x == 0) time_end(a.combine_timing, gridDim.x);
   }
 }
 

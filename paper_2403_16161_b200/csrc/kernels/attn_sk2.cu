@@ -626,7 +626,7 @@ attn_sk2_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ 
 template <int HD, bool WIN>
 __global__ void __launch_bounds__(256) sk2_combine_kernel(const AttnTC a) {
   griddep_wait();
-  if (threadIdx.x == 0) time_begin(a.timing);
+  if (threadIdx.x == 0) time_begin(a.combine_timing);
   griddep_launch();
   constexpr int C8 = HD / 8;                    // 8-column groups per row
   const int u = blockIdx.x;
@@ -678,9 +678,9 @@ __global__ void __launch_bounds__(256) sk2_combine_kernel(const AttnTC a) {
                      pack_bf16(acc[4] * inv, acc[5] * inv), pack_bf16(acc[6] * inv, acc[7] * inv));
     }
   }
-  if (a.timing) {
+  if (a.combine_timing) {
     __syncthreads();
-    if (threadIdx.x == 0) time_end(a.timing, gridDim.x * gridDim.y * gridDim.z);
+    if (threadIdx.x == 0) time_end(a.combine_timing, gridDim.x * gridDim.y * gridDim.z);
   }
 }
 

@@ -138,6 +138,8 @@ struct AttnTC {
   long long* trace;         // debug timeline of CTA (0,0,0) (NULL = off)
   long long* cta_trace;     // attn_sk2: [grid][16] globaltimer stamps per CTA (micro-benchmarks; NULL = off)
   unsigned long long* timing;   // KernelTiming (device) or NULL: the kernels time themselves
+  unsigned long long* combine_timing;   // the same for the split-merge kernels (sk2_combine,
+                                        // attn_combine); NULL = untimed (vi_profile mode 4)
   int H;
   // stream-K kernels (attn_sk, attn_sk2): query rows start at row q_row0 of the Q map;
   // output row i of local head h goes to o + i * o_ld + h * o_hs (unsharded: o_ld = D,
