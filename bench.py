@@ -271,7 +271,11 @@ def run_ours(args, cfg):
     time.sleep(0.3)
     starts = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ends = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    ctx.profile(int(os.environ.get("VI_PROFILE_MODE", "1")))   # attention kernels timed with events
+    # the timed steps run uninstrumented (profile mode 0): the kernels' self-timing (one
+    # atomic per CTA, ~960 CTAs per split-merge launch) lengthened the C3 step by ~20 us
+    # (1.301 vs 1.282 ms, same box); the attention's device time comes from an instrumented
+    # 20-step sub-run of the same workload below (profile modes 1 and 4)
+    ctx.profile(int(os.environ.get("VI_PROFILE_MODE", "0")))
     # untimed: records + uploads this profile mode's step graphs, one per (ring state, input
     # buffer) pair, so that no graph is captured inside the timed region (C3T1: 11 x 4)
     for k in range(nchunks * (cfg.mem_frames + T)):
@@ -323,7 +327,7 @@ def run_ours(args, cfg):
     # eager launches), and two replays of one step compared bitwise (no atomics anywhere)
     extra_steps = 20
     sub = {}
-    for mode in (3, 2, 4):
+    for mode in (3, 2, 4, 1):
         ctx.profile(mode)
         ctx.profile_read()
         for k in range(extra_steps):
@@ -354,8 +358,16 @@ def run_ours(args, cfg):
     value = streams.aggregate_fps(T * args.steps, n_streams, total_ms / 1e3)
     e2e_value = streams.aggregate_fps(T * e2e_steps, n_streams, e2e_s)
     bf16_peak, hbm_peak, peak_src = peaks()
-    attn_ms, attn_recs = prof["attention"]
-    per_block_ms = attn_ms / (args.steps * cfg.layers) if attn_ms > 0 else float("nan")
+    # attention device time per step: from the timed region when it ran instrumented
+    # (VI_PROFILE_MODE=1), else from the instrumented sub-run (profile mode 1, same workload)
+    if prof["attention"][0] > 0:
+        attn_step_ms, attn_src = prof["attention"][0] / args.steps, "kernel self-timing inside the timed steps"
+    else:
+        attn_step_ms = sub[1]["attention"][0] / extra_steps
+        attn_src = (f"kernel self-timing in an instrumented {extra_steps}-step sub-run (profile mode 1; "
+                    "the timed steps run uninstrumented)")
+    attn_ms = attn_step_ms * args.steps
+    per_block_ms = attn_step_ms / cfg.layers if attn_step_ms > 0 else float("nan")
     nq, nk = T * P, cfg.slots * (cfg.win_h * cfg.win_w if cfg.win_h else P)   # keys a query sees
     attn_flop = 4.0 * nq * nk * D / (world if args.tp else 1)   # this rank's share when head-sharded
     achieved = attn_flop / (per_block_ms * 1e-3) / 1e12 if attn_ms > 0 else float("nan")
@@ -389,7 +401,7 @@ def run_ours(args, cfg):
                      "frac": achieved / bf16_peak, "traffic": traffic,
                      "flop_per_launch": attn_flop, "avg_launch_ms": per_block_ms,
                      "peak_source": f"{peak_src} bf16 dense (burst)",
-                     "share_of_step": attn_ms / total_ms},
+                     "share_of_step": attn_ms / total_ms, "timing": attn_src},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": host_in[0].numel() * 2,
                 "d2h_bytes_per_step": host_out[0].numel() * 2,
                 "api": "vi_run_step_async (pinned host buffers; copies overlap neighbouring steps)"},

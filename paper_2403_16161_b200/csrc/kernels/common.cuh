@@ -430,21 +430,25 @@ __device__ __forceinline__ unsigned long long globaltimer() {
   return t;
 }
 // kernel self-timing (see KernelTiming in kernels.h): call time_begin at CTA start and
-// time_end when the CTA is done (thread 0 only).
+// time_end when the CTA is done (thread 0 only).  The launch window is [CTA (0,0,0)'s start,
+// the last CTA's end]: CTA (0,0,0) is dispatched first and, with every caller placing
+// time_begin after griddepcontrol.wait, starts with the first wave; each CTA then pays ONE
+// atomic at its end (the former per-CTA atomicMin + atomicMax + fence + atomicAdd on shared
+// counters cost the C3 step ~30 us, most of it in the 960-CTA split-merge kernels).
 __device__ __forceinline__ void time_begin(unsigned long long* tm) {
-  if (tm) atomicMin(&tm[0], globaltimer());
+  if (tm && blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0) {
+    atomicExch(&tm[0], globaltimer());
+    __threadfence();   // ordered before this CTA's own end count
+  }
 }
 __device__ __forceinline__ void time_end(unsigned long long* tm, unsigned int nctas) {
   if (!tm) return;
-  atomicMax(&tm[1], globaltimer());
-  __threadfence();
-  if (atomicAdd(&tm[2], 1ull) == nctas - 1) {
+  if (atomicAdd(&tm[2], 1ull) == nctas - 1) {   // the last CTA to finish
+    const unsigned long long t1 = globaltimer();
     __threadfence();
-    const unsigned long long t0 = atomicAdd(&tm[0], 0ull), t1 = atomicAdd(&tm[1], 0ull);
+    const unsigned long long t0 = atomicAdd(&tm[0], 0ull);
     atomicAdd(&tm[3], t1 - t0);
     atomicAdd(&tm[4], 1ull);
-    atomicExch(&tm[0], ~0ull);
-    atomicExch(&tm[1], 0ull);
     atomicExch(&tm[2], 0ull);
   }
 }

@@ -91,9 +91,9 @@ struct KeySegs {            // contiguous runs of valid ring slots, as slab row 
   int tile0[33];            // prefix count of 128-key tiles per segment
 };
 
-// Device-side self-timing of a sequence of stream-ordered launches (graph-safe): every CTA
-// folds its start / end globaltimer into [tmin, tmax]; the last CTA to finish adds
-// tmax - tmin to total_ns, counts the launch and resets the window.
+// Device-side self-timing of a sequence of stream-ordered launches (graph-safe): CTA (0,0,0)
+// stores its start globaltimer in tmin, every CTA counts itself done, and the last CTA to
+// finish adds (its end - tmin) to total_ns, counts the launch and resets the count (tmax unused).
 struct KernelTiming {
   unsigned long long tmin, tmax, done, total_ns, launches, pad[3];
 };
